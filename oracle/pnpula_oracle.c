@@ -1,0 +1,512 @@
+/*
+ * pnpula_oracle.c -- plain, slow, obviously-correct CPU oracle for the
+ * distributed PnP-ULA sampler of arXiv 2511.00870 (PAPER.md, "P:n" = line n).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference leg may load this library.
+ * It shares no code, header, table or constant generator with the CUDA path
+ * (paper_2511_00870_b200/csrc); neither includes the other.
+ *
+ * Arithmetic: IEEE binary64 throughout; plain nested loops in the paper's
+ * order; no blocking, fusion or reordering.  Optional "bf16 emulation" rounds
+ * CNN weights / the CNN input / inter-layer activations to bfloat16 (RNE) at the
+ * points where the GPU path stores bf16 (reading R26), still
+ * accumulating in fp64.
+ *
+ * What each function follows:
+ *   or_partition        eq:subsets_cartesian_partition P:473-482 (0-based, reading R4)
+ *   or_philox4x32_10    Philox4x32-10 (Salmon et al. 2011, Random123 constants) -- reading R9
+ *   or_normal           Box-Muller of Philox words, counter keyed on (seed, t+1, i, j, stream) R9/R10
+ *   or_conv_fwd/adj     H1 = same-size true convolution with zero boundary and its adjoint
+ *                       (readings R1/R2/R7); mask operator P:697-713
+ *   or_dncnn_residual   G_eps = T_K o ... o T_1 (eq:feedforward_cnn P:346-351,
+ *                       eq:cnn:convolution P:358-363, DnCNN example P:366-375)
+ *   or_run              Algorithm 1: x-update eq:sgs_pnp_ula_psgla:pnp_ula,
+ *                       z-update eq:sgs_pnp_ula_psgla:psgla, online moments
+ *   or_run (tiles>1)    same chain, every tile computed from its own padded copy S_b x
+ *                       (Def. prop:localselection P:135-152, ghost regions P:494-498)
+ *   or_check_stepsizes  eq:stepsize_cond P:581-587 (reading R11: ||H2||^2 -> ||H2||^2/rho)
+ *
+ * Parity pins for each function live in tests/test_oracle_*.py (see DESIGN.md
+ * section "Oracle pins").
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define OR_OK 0
+#define OR_E_INVALID 1
+#define OR_E_STATS_EMPTY 5
+
+/* ------------------------------------------------------------------ */
+/* Partition: 0-based form of eq:subsets_cartesian_partition:
+ * block p of n items split in `parts` covers [floor(p n/parts), floor((p+1) n/parts)). */
+void or_partition(int64_t n, int64_t parts, int64_t p, int64_t *lo, int64_t *hi) {
+  *lo = (p * n) / parts;
+  *hi = ((p + 1) * n) / parts;
+}
+
+/* ------------------------------------------------------------------ */
+/* Philox4x32-10 (Random123).  10 rounds; key schedule bumped between rounds. */
+static void or_mulhilo(uint32_t a, uint32_t b, uint32_t *hi, uint32_t *lo) {
+  uint64_t p = (uint64_t)a * (uint64_t)b;
+  *hi = (uint32_t)(p >> 32);
+  *lo = (uint32_t)p;
+}
+
+void or_philox4x32_10(const uint32_t ctr_in[4], const uint32_t key_in[2], uint32_t out[4]) {
+  uint32_t c0 = ctr_in[0], c1 = ctr_in[1], c2 = ctr_in[2], c3 = ctr_in[3];
+  uint32_t k0 = key_in[0], k1 = key_in[1];
+  for (int r = 0; r < 10; r++) {
+    if (r > 0) {
+      k0 += 0x9E3779B9u;
+      k1 += 0xBB67AE85u;
+    }
+    uint32_t hi0, lo0, hi1, lo1;
+    or_mulhilo(0xD2511F53u, c0, &hi0, &lo0);
+    or_mulhilo(0xCD9E8D57u, c2, &hi1, &lo1);
+    uint32_t n0 = hi1 ^ c1 ^ k0;
+    uint32_t n1 = lo1;
+    uint32_t n2 = hi0 ^ c3 ^ k1;
+    uint32_t n3 = lo0;
+    c0 = n0; c1 = n1; c2 = n2; c3 = n3;
+  }
+  out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+/* Standard normal at global pixel (i, j), iteration index t1 = t+1, stream s
+ * (0 = xi for x, 1 = zeta for z).  Reading R9: counter = (j>>2, i, t1, s),
+ * key = (seed lo, seed hi); lane = j & 3.  Box-Muller in fp64:
+ *   u_k = (U_k + 0.5) 2^-32,  rho = sqrt(-2 ln u_0),  theta = 2 pi u_1,
+ *   lanes 0,1 = rho cos(theta), rho sin(theta); lanes 2,3 likewise from (U_2, U_3). */
+double or_normal(uint64_t seed, uint32_t t1, int64_t i, int64_t j, uint32_t stream) {
+  uint32_t ctr[4] = {(uint32_t)((uint64_t)j >> 2), (uint32_t)i, t1, stream};
+  uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+  uint32_t w[4];
+  or_philox4x32_10(ctr, key, w);
+  int lane = (int)(j & 3);
+  int pair = lane >> 1;
+  double u0 = ((double)w[2 * pair] + 0.5) * 0x1p-32;
+  double u1 = ((double)w[2 * pair + 1] + 0.5) * 0x1p-32;
+  double rho = sqrt(-2.0 * log(u0));
+  double theta = 2.0 * M_PI * u1;
+  return (lane & 1) ? rho * sin(theta) : rho * cos(theta);
+}
+
+void or_normal_field(uint64_t seed, uint32_t t1, int32_t ny, int32_t nx, uint32_t stream, double *out) {
+  for (int64_t i = 0; i < ny; i++)
+    for (int64_t j = 0; j < nx; j++) out[i * nx + j] = or_normal(seed, t1, i, j, stream);
+}
+
+/* ------------------------------------------------------------------ */
+/* H1 = same-size true convolution, zero boundary (readings R1, R2):
+ *   (Hx)[i,j] = sum_{p=-ry..ry} sum_{q=-rx..rx} k[p+ry][q+rx] x[i-p][j-q]      */
+void or_conv_fwd(const double *x, int32_t ny, int32_t nx, const double *k, int32_t kh, int32_t kw,
+                 double *out) {
+  int ry = kh / 2, rx = kw / 2;
+  for (int i = 0; i < ny; i++)
+    for (int j = 0; j < nx; j++) {
+      double s = 0.0;
+      for (int p = -ry; p <= ry; p++)
+        for (int q = -rx; q <= rx; q++) {
+          int ii = i - p, jj = j - q;
+          if (ii < 0 || ii >= ny || jj < 0 || jj >= nx) continue;
+          s += k[(p + ry) * kw + (q + rx)] * x[(int64_t)ii * nx + jj];
+        }
+      out[(int64_t)i * nx + j] = s;
+    }
+}
+
+/* Adjoint H1^T: correlation with the same kernel, zero boundary:
+ *   (H^T r)[i,j] = sum_{p,q} k[p+ry][q+rx] r[i+p][j+q]                            */
+void or_conv_adj(const double *r, int32_t ny, int32_t nx, const double *k, int32_t kh, int32_t kw,
+                 double *out) {
+  int ry = kh / 2, rx = kw / 2;
+  for (int i = 0; i < ny; i++)
+    for (int j = 0; j < nx; j++) {
+      double s = 0.0;
+      for (int p = -ry; p <= ry; p++)
+        for (int q = -rx; q <= rx; q++) {
+          int ii = i + p, jj = j + q;
+          if (ii < 0 || ii >= ny || jj < 0 || jj >= nx) continue;
+          s += k[(p + ry) * kw + (q + rx)] * r[(int64_t)ii * nx + jj];
+        }
+      out[(int64_t)i * nx + j] = s;
+    }
+}
+
+/* ------------------------------------------------------------------ */
+/* bfloat16 round-to-nearest-even of a double, via fp32 (the GPU stores fp32
+ * values converted with __float2bfloat16_rn). */
+static double or_bf16(double v) {
+  float f = (float)v;
+  uint32_t u;
+  memcpy(&u, &f, 4);
+  if ((u & 0x7f800000u) == 0x7f800000u) return (double)f; /* inf/nan passthrough */
+  uint32_t lsb = (u >> 16) & 1u;
+  u += 0x7fffu + lsb;
+  u &= 0xffff0000u;
+  memcpy(&f, &u, 4);
+  return (double)f;
+}
+
+/* Number of weights / biases of a DnCNN-style net with n_layers 3x3 layers,
+ * C image channels and P features: C->P, (K-2) x P->P, P->C. */
+int64_t or_dncnn_param_count(int32_t n_layers, int32_t P, int32_t C) {
+  int64_t w = (int64_t)C * P * 9 + (int64_t)(n_layers - 2) * P * P * 9 + (int64_t)P * C * 9;
+  int64_t b = (int64_t)P * (n_layers - 1) + C;
+  return w + b;
+}
+
+/* CNN residual G_eps(x) for C = 1 (D_eps = Id - G_eps).
+ * Layer k: a^k_{c'}[i,j] = eta_k( b_k[c'] + sum_c sum_{u,v=-1..1} W_k[c'][c][u+1][v+1] a^{k-1}_c[i+u][j+v] )
+ * (PyTorch conv2d cross-correlation, half padding, reading R2/R8: zero outside
+ * the image at every layer input); eta = ReLU for k < K, identity for k = K.
+ * weights: fp32 OIHW, layers concatenated; biases: per layer, concatenated.     */
+int or_dncnn_residual(const double *x, int32_t ny, int32_t nx, int32_t n_layers, int32_t P,
+                      const float *weights, const float *biases, int32_t bf16_emulate, double *G) {
+  if (n_layers < 2 || P < 1) return OR_E_INVALID;
+  int64_t npx = (int64_t)ny * nx;
+  double *a = (double *)calloc((size_t)(npx * P), sizeof(double));
+  double *b = (double *)calloc((size_t)(npx * P), sizeof(double));
+  if (!a || !b) { free(a); free(b); return OR_E_INVALID; }
+  /* a^0 = x (one channel) */
+  for (int64_t n = 0; n < npx; n++) a[n] = bf16_emulate ? or_bf16(x[n]) : x[n];
+  int cin = 1;
+  const float *w = weights;
+  const float *bb = biases;
+  for (int k = 1; k <= n_layers; k++) {
+    int cout = (k == n_layers) ? 1 : P;
+    for (int co = 0; co < cout; co++)
+      for (int i = 0; i < ny; i++)
+        for (int j = 0; j < nx; j++) {
+          double s = 0.0;
+          for (int ci = 0; ci < cin; ci++)
+            for (int u = -1; u <= 1; u++)
+              for (int v = -1; v <= 1; v++) {
+                int ii = i + u, jj = j + v;
+                if (ii < 0 || ii >= ny || jj < 0 || jj >= nx) continue;
+                double wt = (double)w[((co * cin + ci) * 3 + (u + 1)) * 3 + (v + 1)];
+                if (bf16_emulate) wt = or_bf16(wt);
+                s += wt * a[(int64_t)ci * npx + (int64_t)ii * nx + jj];
+              }
+          s += (double)bb[co];
+          if (k < n_layers) {
+            if (s < 0.0) s = 0.0;                 /* ReLU */
+            if (bf16_emulate) s = or_bf16(s);     /* GPU stores activations as bf16 */
+          }
+          b[(int64_t)co * npx + (int64_t)i * nx + j] = s;
+        }
+    w += (int64_t)cout * cin * 9;
+    bb += cout;
+    double *t = a; a = b; b = t;
+    cin = cout;
+  }
+  for (int64_t n = 0; n < npx; n++) G[n] = a[n];
+  free(a);
+  free(b);
+  return OR_OK;
+}
+
+/* ------------------------------------------------------------------ */
+/* Step-size conditions eq:stepsize_cond, with ||H2||^2 read as
+ * ||H2||^2/rho (reading R11).  Returns bit 0 set if the first inequality fails,
+ * bit 1 if the second fails.  h2_over_rho = ||H2||^2/rho (0 when AXDA is off). */
+int or_check_stepsizes(double L, double h2_over_rho, double alpha, double eps, double L_D,
+                       double lambda, double gamma) {
+  int bad = 0;
+  double prior = (alpha > 0.0 && L_D > 0.0) ? alpha * L_D / (eps * eps) : 0.0;
+  double lhs1 = 2.0 * (L + h2_over_rho) + prior;
+  if (!(lhs1 <= 1.0 / (2.0 * lambda))) bad |= 1;
+  double lhs2 = 3.0 * gamma * (L + h2_over_rho + 1.0 / lambda + prior);
+  if (!(lhs2 < 1.0)) bad |= 2;
+  return bad;
+}
+
+/* ------------------------------------------------------------------ */
+typedef struct {
+  int32_t ny, nx;
+  int32_t op;                    /* 0 = convolution H1, 1 = mask H1 = diag(m) */
+  const float *kernel;           /* kh x kw true-convolution kernel, or NULL when separable given */
+  const float *ksep_y;           /* optional separable factors: k[p][q] = ksep_y[p] * ksep_x[q] */
+  const float *ksep_x;
+  int32_t kh, kw;
+  const uint8_t *mask;           /* ny*nx, op = 1 */
+  const float *y;                /* ny*nx observations */
+  double sigma2;
+  int32_t n_layers, channels;    /* 0 layers = no CNN prior */
+  const float *weights, *biases;
+  double alpha, eps;
+  int32_t bf16_emulate;
+  double lambda, c_lo, c_hi;     /* Moreau box term, lambda <= 0 = off */
+  double rho, kappa, z_lo, z_hi; /* AXDA z-block (H2 = I, f2 = indicator of [z_lo,z_hi]); rho <= 0 = off */
+  double gamma;
+  const float *x0;               /* NULL = zeros */
+  int64_t n_iter, burn_in;
+  uint64_t seed;
+  int32_t tiles_y, tiles_x;      /* <= 1 means untiled */
+} or_config;
+
+static void or_kernel2d(const or_config *c, double *k) {
+  for (int p = 0; p < c->kh; p++)
+    for (int q = 0; q < c->kw; q++)
+      k[p * c->kw + q] = c->ksep_y ? (double)c->ksep_y[p] * (double)c->ksep_x[q]
+                                   : (double)c->kernel[p * c->kw + q];
+}
+
+/* One untiled iteration of Algorithm 1 (lines 5-13) on global arrays. */
+static int or_step_global(const or_config *c, const double *k, const double *yd, uint64_t t,
+                          const double *x, const double *z, double *xn, double *zn,
+                          double *r, double *g, double *G) {
+  int ny = c->ny, nx = c->nx;
+  int64_t npx = (int64_t)ny * nx;
+  /* line 6: u1 = H1^T grad f1(H1 x),  f1(v) = ||y - v||^2/(2 sigma^2) (eq:potential_gaussian_likelihood) */
+  if (c->op == 0) {
+    or_conv_fwd(x, ny, nx, k, c->kh, c->kw, r);
+    for (int64_t n = 0; n < npx; n++) r[n] -= yd[n];
+    or_conv_adj(r, ny, nx, k, c->kh, c->kw, g);
+  } else {
+    for (int64_t n = 0; n < npx; n++) {
+      double m = c->mask[n] ? 1.0 : 0.0;
+      g[n] = m * (m * x[n] - yd[n]);
+    }
+  }
+  for (int64_t n = 0; n < npx; n++) g[n] /= c->sigma2;
+  /* line 8: D_eps(x) - x = -G_eps(x) */
+  int use_cnn = c->n_layers > 0 && c->alpha != 0.0;
+  if (use_cnn) {
+    int e = or_dncnn_residual(x, ny, nx, c->n_layers, c->channels, c->weights, c->biases,
+                              c->bf16_emulate, G);
+    if (e) return e;
+  }
+  double sq2g = sqrt(2.0 * c->gamma);
+  for (int64_t i = 0; i < ny; i++)
+    for (int64_t j = 0; j < nx; j++) {
+      int64_t n = i * nx + j;
+      /* line 10 / eq:sgs_pnp_ula_psgla:pnp_ula */
+      double v = x[n] - c->gamma * g[n];
+      if (c->rho > 0.0) v -= (c->gamma / c->rho) * (x[n] - z[n]);
+      if (use_cnn) v += (c->alpha * c->gamma / (c->eps * c->eps)) * (-G[n]);
+      if (c->lambda > 0.0) {
+        double pc = x[n] < c->c_lo ? c->c_lo : (x[n] > c->c_hi ? c->c_hi : x[n]);
+        v += (c->gamma / c->lambda) * (pc - x[n]);
+      }
+      v += sq2g * or_normal(c->seed, (uint32_t)(t + 1), i, j, 0);
+      xn[n] = v;
+    }
+  if (c->rho > 0.0) {
+    double sq2k = sqrt(2.0 * c->kappa);
+    for (int64_t i = 0; i < ny; i++)
+      for (int64_t j = 0; j < nx; j++) {
+        int64_t n = i * nx + j;
+        /* lines 12-13 / eq:sgs_pnp_ula_psgla:psgla with H2 = I, prox = projection onto [z_lo,z_hi] */
+        double v = z[n] - (c->kappa / c->rho) * (z[n] - xn[n]) +
+                   sq2k * or_normal(c->seed, (uint32_t)(t + 1), i, j, 1);
+        zn[n] = v < c->z_lo ? c->z_lo : (v > c->z_hi ? c->z_hi : v);
+      }
+  }
+  return OR_OK;
+}
+
+/* One tiled iteration: every tile b computes its block of x^{t+1}, z^{t+1}
+ * from S_b x only (the tile plus a ghost frame of width h, zero outside the
+ * image), exactly as worker b of Algorithm 1 would after line 5. */
+static int or_step_tiled(const or_config *c, const double *k, const double *yd, uint64_t t,
+                         const double *x, const double *z, double *xn, double *zn) {
+  int ny = c->ny, nx = c->nx;
+  int ry = c->kh / 2, rx = c->kw / 2;
+  int use_cnn = c->n_layers > 0 && c->alpha != 0.0;
+  int hr = (c->op == 0) ? 2 * (ry > rx ? ry : rx) : 0;
+  int h = use_cnn && c->n_layers > hr ? c->n_layers : hr;
+  for (int ty = 0; ty < c->tiles_y; ty++)
+    for (int tx = 0; tx < c->tiles_x; tx++) {
+      int64_t i0, i1, j0, j1;
+      or_partition(ny, c->tiles_y, ty, &i0, &i1);
+      or_partition(nx, c->tiles_x, tx, &j0, &j1);
+      int th = (int)(i1 - i0), tw = (int)(j1 - j0);
+      if (th < h || tw < h) return OR_E_INVALID;
+      int ph = th + 2 * h, pw = tw + 2 * h;
+      /* S_b x: padded local copy (ghost frame from neighbours, zero outside the image) */
+      double *xp = (double *)calloc((size_t)ph * pw, sizeof(double));
+      double *rp = (double *)calloc((size_t)ph * pw, sizeof(double));
+      double *gl = (double *)calloc((size_t)th * tw, sizeof(double));
+      double *Gl = (double *)calloc((size_t)th * tw, sizeof(double));
+      if (!xp || !rp || !gl || !Gl) { free(xp); free(rp); free(gl); free(Gl); return OR_E_INVALID; }
+      for (int a = 0; a < ph; a++)
+        for (int b = 0; b < pw; b++) {
+          int64_t gi = i0 - h + a, gj = j0 - h + b;
+          if (gi >= 0 && gi < ny && gj >= 0 && gj < nx) xp[(int64_t)a * pw + b] = x[gi * nx + gj];
+        }
+      if (c->op == 0) {
+        /* residual on tile (+) r, zero outside the image (reading R7) */
+        for (int a = h - ry; a < h + th + ry; a++)
+          for (int b = h - rx; b < h + tw + rx; b++) {
+            int64_t gi = i0 - h + a, gj = j0 - h + b;
+            if (gi < 0 || gi >= ny || gj < 0 || gj >= nx) continue;
+            double s = 0.0;
+            for (int p = -ry; p <= ry; p++)
+              for (int q = -rx; q <= rx; q++) {
+                int64_t ii = gi - p, jj = gj - q;
+                if (ii < 0 || ii >= ny || jj < 0 || jj >= nx) continue;
+                s += k[(p + ry) * c->kw + (q + rx)] * xp[(a - p) * (int64_t)pw + (b - q)];
+              }
+            rp[(int64_t)a * pw + b] = s - yd[gi * nx + gj];
+          }
+        for (int a = 0; a < th; a++)
+          for (int b = 0; b < tw; b++) {
+            int64_t gi = i0 + a, gj = j0 + b;
+            double s = 0.0;
+            for (int p = -ry; p <= ry; p++)
+              for (int q = -rx; q <= rx; q++) {
+                int64_t ii = gi + p, jj = gj + q;
+                if (ii < 0 || ii >= ny || jj < 0 || jj >= nx) continue;
+                s += k[(p + ry) * c->kw + (q + rx)] * rp[(a + h + p) * (int64_t)pw + (b + h + q)];
+              }
+            gl[(int64_t)a * tw + b] = s;
+          }
+      } else {
+        for (int a = 0; a < th; a++)
+          for (int b = 0; b < tw; b++) {
+            int64_t n = (i0 + a) * nx + (j0 + b);
+            double m = c->mask[n] ? 1.0 : 0.0;
+            gl[(int64_t)a * tw + b] = m * (m * xp[(int64_t)(a + h) * pw + (b + h)] - yd[n]);
+          }
+      }
+      for (int64_t n = 0; n < (int64_t)th * tw; n++) gl[n] /= c->sigma2;
+      if (use_cnn) {
+        /* receptive-field strategy: layer k is evaluated on tile (+) (K-k),
+         * activations outside the image are zero at every layer input (reading R8). */
+        int K = c->n_layers, P = c->channels;
+        double *A = (double *)calloc((size_t)ph * pw * P, sizeof(double));
+        double *B = (double *)calloc((size_t)ph * pw * P, sizeof(double));
+        if (!A || !B) { free(A); free(B); free(xp); free(rp); free(gl); free(Gl); return OR_E_INVALID; }
+        int64_t plane = (int64_t)ph * pw;
+        for (int64_t n = 0; n < plane; n++) A[n] = c->bf16_emulate ? or_bf16(xp[n]) : xp[n];
+        const float *w = c->weights;
+        const float *bb = c->biases;
+        int cin = 1;
+        for (int kk = 1; kk <= K; kk++) {
+          int cout = (kk == K) ? 1 : P;
+          int ext = K - kk;
+          memset(B, 0, sizeof(double) * (size_t)plane * P);
+          for (int co = 0; co < cout; co++)
+            for (int a = h - ext; a < h + th + ext; a++)
+              for (int b = h - ext; b < h + tw + ext; b++) {
+                int64_t gi = i0 - h + a, gj = j0 - h + b;
+                if (gi < 0 || gi >= ny || gj < 0 || gj >= nx) continue; /* stays 0 */
+                double s = 0.0;
+                for (int ci = 0; ci < cin; ci++)
+                  for (int u = -1; u <= 1; u++)
+                    for (int v = -1; v <= 1; v++) {
+                      int64_t ii = gi + u, jj = gj + v;
+                      if (ii < 0 || ii >= ny || jj < 0 || jj >= nx) continue;
+                      double wt = (double)w[((co * cin + ci) * 3 + (u + 1)) * 3 + (v + 1)];
+                      if (c->bf16_emulate) wt = or_bf16(wt);
+                      s += wt * A[(int64_t)ci * plane + (int64_t)(a + u) * pw + (b + v)];
+                    }
+                s += (double)bb[co];
+                if (kk < K) {
+                  if (s < 0.0) s = 0.0;
+                  if (c->bf16_emulate) s = or_bf16(s);
+                }
+                B[(int64_t)co * plane + (int64_t)a * pw + b] = s;
+              }
+          w += (int64_t)cout * cin * 9;
+          bb += cout;
+          double *tt = A; A = B; B = tt;
+          cin = cout;
+        }
+        for (int a = 0; a < th; a++)
+          for (int b = 0; b < tw; b++) Gl[(int64_t)a * tw + b] = A[(int64_t)(a + h) * pw + (b + h)];
+        free(A);
+        free(B);
+      }
+      double sq2g = sqrt(2.0 * c->gamma);
+      for (int a = 0; a < th; a++)
+        for (int b = 0; b < tw; b++) {
+          int64_t gi = i0 + a, gj = j0 + b, n = gi * nx + gj;
+          double xv = xp[(int64_t)(a + h) * pw + (b + h)];
+          double v = xv - c->gamma * gl[(int64_t)a * tw + b];
+          if (c->rho > 0.0) v -= (c->gamma / c->rho) * (xv - z[n]);
+          if (use_cnn) v += (c->alpha * c->gamma / (c->eps * c->eps)) * (-Gl[(int64_t)a * tw + b]);
+          if (c->lambda > 0.0) {
+            double pc = xv < c->c_lo ? c->c_lo : (xv > c->c_hi ? c->c_hi : xv);
+            v += (c->gamma / c->lambda) * (pc - xv);
+          }
+          v += sq2g * or_normal(c->seed, (uint32_t)(t + 1), gi, gj, 0);
+          xn[n] = v;
+          if (c->rho > 0.0) {
+            double zv = z[n] - (c->kappa / c->rho) * (z[n] - v) +
+                        sqrt(2.0 * c->kappa) * or_normal(c->seed, (uint32_t)(t + 1), gi, gj, 1);
+            zn[n] = zv < c->z_lo ? c->z_lo : (zv > c->z_hi ? c->z_hi : zv);
+          }
+        }
+      free(xp);
+      free(rp);
+      free(gl);
+      free(Gl);
+    }
+  return OR_OK;
+}
+
+/* Full chain.  Outputs (each ny*nx, any may be NULL): final x, final z,
+ * MMSE mean and variance (M2/(n-1), reading R15) of x^{(t)}, t = burn_in+1..n_iter
+ * (reading R14), accumulated with Welford's update (P:839 footnote). */
+int or_run(const or_config *c, double *x_out, double *z_out, double *mean_out, double *var_out,
+           int64_t *n_samples) {
+  if (c->ny <= 0 || c->nx <= 0 || c->gamma <= 0.0 || c->sigma2 <= 0.0) return OR_E_INVALID;
+  if (c->op == 0 && (c->kh % 2 == 0 || c->kw % 2 == 0)) return OR_E_INVALID;
+  if (c->rho > 0.0 && !(c->kappa > 0.0 && c->kappa < c->rho)) return OR_E_INVALID;
+  int64_t npx = (int64_t)c->ny * c->nx;
+  double *k = (double *)calloc((size_t)(c->kh > 0 ? c->kh * c->kw : 1), sizeof(double));
+  double *yd = (double *)malloc(sizeof(double) * (size_t)npx);
+  double *x = (double *)calloc((size_t)npx, sizeof(double));
+  double *xn = (double *)calloc((size_t)npx, sizeof(double));
+  double *z = (double *)calloc((size_t)npx, sizeof(double));
+  double *zn = (double *)calloc((size_t)npx, sizeof(double));
+  double *r = (double *)calloc((size_t)npx, sizeof(double));
+  double *g = (double *)calloc((size_t)npx, sizeof(double));
+  double *G = (double *)calloc((size_t)npx, sizeof(double));
+  double *mu = (double *)calloc((size_t)npx, sizeof(double));
+  double *m2 = (double *)calloc((size_t)npx, sizeof(double));
+  int err = OR_OK;
+  if (!k || !yd || !x || !xn || !z || !zn || !r || !g || !G || !mu || !m2) { err = OR_E_INVALID; goto done; }
+  if (c->op == 0) or_kernel2d(c, k);
+  for (int64_t n = 0; n < npx; n++) {
+    yd[n] = (double)c->y[n];
+    x[n] = c->x0 ? (double)c->x0[n] : 0.0;   /* x^0 */
+  }                                           /* z^0 = 0 */
+  int64_t cnt = 0;
+  for (int64_t t = 0; t < c->n_iter; t++) {
+    if (c->tiles_y > 1 || c->tiles_x > 1)
+      err = or_step_tiled(c, k, yd, (uint64_t)t, x, z, xn, zn);
+    else
+      err = or_step_global(c, k, yd, (uint64_t)t, x, z, xn, zn, r, g, G);
+    if (err) goto done;
+    if (t + 1 > c->burn_in) {
+      cnt++;
+      for (int64_t n = 0; n < npx; n++) {
+        double d = xn[n] - mu[n];
+        mu[n] += d / (double)cnt;
+        m2[n] += d * (xn[n] - mu[n]);
+      }
+    }
+    double *tt = x; x = xn; xn = tt;
+    if (c->rho > 0.0) { tt = z; z = zn; zn = tt; }
+  }
+  if (x_out) memcpy(x_out, x, sizeof(double) * (size_t)npx);
+  if (z_out) memcpy(z_out, z, sizeof(double) * (size_t)npx);
+  if (n_samples) *n_samples = cnt;
+  if (mean_out) {
+    if (cnt < 1) { err = OR_E_STATS_EMPTY; goto done; }
+    memcpy(mean_out, mu, sizeof(double) * (size_t)npx);
+  }
+  if (var_out) {
+    if (cnt < 2) { err = OR_E_STATS_EMPTY; goto done; }
+    for (int64_t n = 0; n < npx; n++) var_out[n] = m2[n] / (double)(cnt - 1);
+  }
+done:
+  free(k); free(yd); free(x); free(xn); free(z); free(zn); free(r); free(g); free(G); free(mu); free(m2);
+  return err;
+}
