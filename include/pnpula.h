@@ -1,0 +1,231 @@
+/*
+ * pnpula.h -- C ABI of the B200-native data-parallel hot path of the distributed
+ * Plug-and-Play ULA sampler of arXiv 2511.00870 ("A Distributed Plug-and-Play MCMC
+ * Algorithm for High-Dimensional Inverse Problems").  PAPER.md line n is cited "P:n".
+ *
+ * One chain, one image of ny x nx grayscale pixels (C = 1), split into a
+ * tiles_y x tiles_x grid of tiles (eq:subsets_cartesian_partition P:473-482 applied
+ * to both axes, "A 2D tessellation can be obtained ...").  Every rank owns
+ * n_tiles/world_size consecutive tiles (row-major tile order) on one CUDA device.
+ * Each iteration t -> t+1 computes, for every owned pixel (Algorithm 1):
+ *
+ *   x+ = x - (gamma/sigma2) H1^T (H1 x - y)                      lines 6-7
+ *          - (gamma/rho) (x - z)                                   line 6b, P:615  (H2 = I)
+ *          - (alpha gamma/eps^2) G_eps(x)                          line 8,  P:623  (D = Id - G)
+ *          + (gamma/lambda) (proj_[c_lo,c_hi](x) - x)
+ *          + sqrt(2 gamma) xi^{t+1}                                line 9,
+ *   z+ = proj_[z_lo,z_hi]( z - (kappa/rho)(z - x+) + sqrt(2 kappa) zeta^{t+1} )   lines 12-13
+ *   if t+1 > burn_in: Welford update of the per-pixel mean / M2 with x+           P:839
+ *
+ * H1 is either a same-size true convolution with zero boundary (odd kh x kw kernel,
+ * P:716-724) or a 0/1 mask.  G_eps is a DnCNN-style CNN:
+ * 1 -> P, (K-2) x (P -> P), P -> 1 channels, 3x3 cross-correlation with zero
+ * padding, bias on every layer, ReLU on all but the last layer.
+ * Noise: Philox4x32-10 with key = seed and counter = (j >> 2, i, t+1, stream),
+ * lane j & 3, Box-Muller -- a function of (seed, t, global pixel), so the chain is
+ * bitwise independent of the tile grid and of world_size (strengthening P:1063-1064).
+ *
+ * The only per-iteration communication is one grouped halo exchange of x
+ * (Alg. 1 line 5, grouped as in the remark P:674), of width
+ * h = max(2 r_H, K) where r_H = max(kh, kw)/2 (0 for a mask) and K = n_layers
+ * (0 without a prior): the receptive-field strategy of P:529-531 replaces the
+ * per-layer exchanges of P:526 and the overlap-add of line 7 by redundant
+ * computation on the halo.  Neighbours on other ranks are reached with NCCL
+ * point-to-point calls; tiles on the same rank with device copies.
+ *
+ * Conventions (all functions):
+ *  - return pnpula_status; PNPULA_OK = 0.  A thread-local message describing the
+ *    last failure (or a step-size warning) is available from pnpula_last_error().
+ *  - host pointers are only read during the call and are never retained; the
+ *    caller keeps ownership.  Device memory is owned by the context.
+ *  - a CUDA or NCCL failure poisons the context: every later call except
+ *    pnpula_destroy returns PNPULA_E_STATE.
+ *  - collective calls (marked [collective]) must be made by every rank in the
+ *    same order.
+ *  - a context is not thread-safe.
+ *  - there is no CPU fallback: creation fails with PNPULA_E_CUDA when no sm_100
+ *    device is available.
+ */
+#ifndef PNPULA_H
+#define PNPULA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  PNPULA_OK = 0,
+  PNPULA_E_INVALID_ARG = 1,        /* null pointer, non-positive step, even kernel, kappa not in (0, rho) */
+  PNPULA_E_SHAPE = 2,              /* in_rect does not cover the rank's tiles (+) r_H, bad sizes */
+  PNPULA_E_PARTITION_TOO_FINE = 3, /* a tile extent < halo width h (Def. 1 (i)) */
+  PNPULA_E_STEPSIZE = 4,           /* reserved: eq:stepsize_cond violations are warnings only */
+  PNPULA_E_STATS_EMPTY = 5,        /* fewer than 1 (mean) / 2 (variance) post-burn-in samples */
+  PNPULA_E_STATE = 6,              /* context poisoned by an earlier CUDA/NCCL error, or wrong call order */
+  PNPULA_E_CUDA = 7,
+  PNPULA_E_NCCL = 8,
+  PNPULA_E_OOM = 9,
+  PNPULA_E_UNSUPPORTED = 10        /* e.g. channels not in {16, 32, 64} */
+} pnpula_status;
+
+enum { PNPULA_OP_CONV = 0, PNPULA_OP_MASK = 1 };
+enum { PNPULA_SCOPE_LOCAL = 0, PNPULA_SCOPE_GLOBAL_ON_ROOT = 1 };
+
+/* flags */
+#define PNPULA_FLAG_HALO_VIA_NCCL 0x1  /* route same-rank halos through NCCL self send/recv (tests) */
+#define PNPULA_FLAG_CNN_LAYERWISE 0x2  /* one CNN layer per launch instead of fused layer chains */
+#define PNPULA_FLAG_NO_GRAPH      0x4  /* launch kernels directly instead of replaying a CUDA graph */
+
+typedef struct {
+  int32_t i0, j0, h, w; /* rectangle of global pixel coordinates: rows [i0, i0+h), cols [j0, j0+w) */
+} pnpula_rect;
+
+/* DnCNN-style denoiser weights, fp32, copied at create and stored as bf16. */
+typedef struct {
+  int32_t n_layers;      /* K >= 2 */
+  int32_t channels;      /* P, one of 16, 32, 64 */
+  const float *weights;  /* host; OIHW per layer, layers concatenated:
+                            [P][1][3][3], (K-2) x [P][P][3][3], [1][P][3][3] */
+  const float *biases;   /* host; P per layer for layers 1..K-1, then 1 */
+} pnpula_denoiser;
+
+typedef struct {
+  /* geometry and SPMD identity */
+  int32_t ny, nx;                /* global image, C = 1 */
+  int32_t tiles_y, tiles_x;      /* tile grid; tiles_y*tiles_x must be a multiple of world_size */
+  int32_t rank, world_size;      /* this process; world_size >= 1 */
+  int32_t device;                /* CUDA device ordinal used by this rank */
+  const uint8_t *nccl_uid;       /* 128 bytes from pnpula_get_unique_id on rank 0; required if world_size > 1 */
+  uint64_t stream;               /* cudaStream_t to launch on, or 0 for a context-owned stream */
+
+  /* likelihood f1(H1 x) = ||y - H1 x||^2 / (2 sigma2)  (eq:potential_gaussian_likelihood P:708-711) */
+  int32_t op;                    /* PNPULA_OP_CONV or PNPULA_OP_MASK */
+  const float *kernel;           /* host kh x kw row-major true-convolution kernel; may be NULL if separable factors given */
+  const float *kernel_y;         /* optional separable factors: kernel[p][q] = kernel_y[p] * kernel_x[q] exactly */
+  const float *kernel_x;
+  int32_t kh, kw;                /* odd sizes, <= 15 */
+  const uint8_t *mask;           /* host, covers in_rect, OP_MASK only (nonzero = observed) */
+  const float *y;                /* host observations covering in_rect */
+  const float *x0;               /* host initial state covering in_rect, or NULL for zeros */
+  pnpula_rect in_rect;           /* the rectangle y / mask / x0 cover (row-major h x w); must contain
+                                    every owned tile (+) r_H clipped to the image.  Use the whole image
+                                    {0, 0, ny, nx} when passing global arrays. */
+  double sigma2;                 /* noise variance > 0 */
+
+  /* prior */
+  const pnpula_denoiser *den;    /* NULL or alpha == 0: no CNN term */
+  double alpha, eps;             /* prior strength and denoiser noise level */
+  double lambda, c_lo, c_hi;     /* Moreau/box term (gamma/lambda)(proj_C(x) - x); lambda <= 0 disables */
+
+  /* AXDA z-block with H2 = I, f2 = indicator of [z_lo, z_hi]; rho <= 0 disables */
+  double rho, kappa, z_lo, z_hi;
+
+  double gamma;                  /* ULA step > 0 */
+
+  /* optional constants for the eq:stepsize_cond check (warning only; 0 = unknown) */
+  double lipschitz_L, lipschitz_LD;
+
+  int32_t flags;                 /* PNPULA_FLAG_* */
+} pnpula_config;
+
+typedef struct pnpula_ctx pnpula_ctx;
+
+/* Library version string. */
+const char *pnpula_version(void);
+
+/* Thread-local description of the last error or warning ("" if none). */
+const char *pnpula_last_error(void);
+
+/* 128-byte NCCL unique id; call on rank 0 and broadcast it (e.g. torch.distributed). */
+pnpula_status pnpula_get_unique_id(uint8_t out[128]);
+
+/* [collective] Validate cfg, partition the image, initialise NCCL (world_size > 1),
+ * allocate device buffers, copy y / mask / x0 / kernel / weights (bf16) to the device.
+ * On success *out receives a new context.  Step-size condition violations
+ * (eq:stepsize_cond P:581-587, read with ||H2||^2/rho, R11) are reported
+ * through pnpula_last_error() but do not fail. */
+pnpula_status pnpula_create(const pnpula_config *cfg, pnpula_ctx **out);
+
+/* [collective] Reset the chain: x = x0 (halos exchanged), z = 0, moments = 0, t = 0,
+ * and set burn_in and seed for the following pnpula_advance calls. */
+pnpula_status pnpula_reset(pnpula_ctx *ctx, int64_t burn_in, uint64_t seed);
+
+/* [collective] Run n_iter further iterations (asynchronous on the context stream). */
+pnpula_status pnpula_advance(pnpula_ctx *ctx, int64_t n_iter);
+
+/* [collective] pnpula_reset(burn_in, seed) then pnpula_advance(n_iter), then
+ * synchronise.  Deterministic in (cfg, n_iter, burn_in, seed) and bitwise independent
+ * of the tile grid and of world_size. */
+pnpula_status pnpula_run(pnpula_ctx *ctx, int64_t n_iter, int64_t burn_in, uint64_t seed);
+
+/* Block until all work queued on the context stream has finished. */
+pnpula_status pnpula_synchronize(pnpula_ctx *ctx);
+
+/* Rectangle covered by LOCAL-scope outputs: the bounding box of this rank's tiles. */
+pnpula_status pnpula_local_bbox(pnpula_ctx *ctx, pnpula_rect *out);
+
+/* [collective for GLOBAL scope] Posterior mean (MMSE) and per-pixel variance
+ * M2/(n-1) of x^{(t)}, t = burn_in+1 .. current t.  mean / var (either may be
+ * NULL) are host buffers of the LOCAL bbox size, or ny*nx on rank 0 for
+ * PNPULA_SCOPE_GLOBAL_ON_ROOT (other ranks may pass NULL).  Returns
+ * PNPULA_E_STATS_EMPTY if n < 1 (mean) or n < 2 (var requested). */
+pnpula_status pnpula_get_moments(pnpula_ctx *ctx, float *mean, float *var, int64_t *n_samples,
+                                 int32_t scope);
+
+/* [collective for GLOBAL scope] Current state x^t, z^t (either may be NULL) and t. */
+pnpula_status pnpula_get_state(pnpula_ctx *ctx, float *x, float *z, int64_t *t, int32_t scope);
+
+/* Number of tiles owned by this rank; halo width h; the i-th owned tile's rectangle. */
+pnpula_status pnpula_tile_info(pnpula_ctx *ctx, int32_t local_index, pnpula_rect *rect,
+                               int32_t *n_local_tiles, int32_t *halo);
+
+/* Diagnostic: padded buffer (tile (+) h ghost frame, row-major (th+2h) x (tw+2h)) of the
+ * current x of owned tile local_index, as the next iteration will read it. */
+pnpula_status pnpula_get_padded_x(pnpula_ctx *ctx, int32_t local_index, float *out);
+
+/* [collective] Diagnostic: evaluate the CNN residual G_eps on the current x^t and
+ * return it for the LOCAL bbox (host buffer, owned tiles written). */
+pnpula_status pnpula_get_denoiser_residual(pnpula_ctx *ctx, float *G);
+
+/* Per-kernel-class device time accumulated since the last call with reset != 0,
+ * measured with CUDA events on the launching stream while timing is enabled.
+ * name: "cnn", "update", "halo".  ms = total milliseconds, launches = count. */
+pnpula_status pnpula_set_timing(pnpula_ctx *ctx, int32_t enable);
+pnpula_status pnpula_kernel_time(pnpula_ctx *ctx, const char *name, double *ms, int64_t *launches,
+                                 int32_t reset);
+
+/* [collective] Free everything. */
+pnpula_status pnpula_destroy(pnpula_ctx *ctx);
+
+/* ---------------- host-only planning helpers (no GPU needed) ---------------- */
+
+/* Balanced 0-based partition of n items into parts: [lo, hi) of part p (R4). */
+void pnpula_partition(int64_t n, int64_t parts, int64_t p, int64_t *lo, int64_t *hi);
+
+/* Halo width h = max(2 r_H, K) (receptive-field strategy, R5). */
+int32_t pnpula_halo_width(int32_t op, int32_t kh, int32_t kw, int32_t n_layers);
+
+/* One ghost-region message: the global rectangle `rect` of tile src's interior
+ * that tile dst stores in its ghost frame (Fig. 2(b)). */
+typedef struct {
+  int32_t src_tile, dst_tile; /* row-major tile indices */
+  pnpula_rect rect;
+} pnpula_halo_msg;
+
+/* All messages of one exchange for a tiles_y x tiles_x grid and halo h, in the
+ * canonical (src_tile, dst_tile) order used to post NCCL sends/receives.
+ * Writes at most cap messages to out (out may be NULL) and returns the total count,
+ * or -1 if a tile extent is smaller than h. */
+int32_t pnpula_plan_halo(int32_t ny, int32_t nx, int32_t tiles_y, int32_t tiles_x, int32_t h,
+                         pnpula_halo_msg *out, int32_t cap);
+
+/* eq:stepsize_cond with ||H2||^2 read as h2_over_rho = ||H2||^2/rho
+ * (R11).  Returns 0 if both hold, bit 0 / bit 1 for the failing inequality. */
+int32_t pnpula_check_stepsizes(double L, double h2_over_rho, double alpha, double eps,
+                               double L_D, double lambda, double gamma);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PNPULA_H */

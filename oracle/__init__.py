@@ -53,6 +53,7 @@ class _Config(C.Structure):
         ("gamma", C.c_double), ("x0", C.c_void_p),
         ("n_iter", C.c_int64), ("burn_in", C.c_int64), ("seed", C.c_uint64),
         ("tiles_y", C.c_int32), ("tiles_x", C.c_int32),
+        ("i_off", C.c_int64), ("j_off", C.c_int64),
     ]
 
 
@@ -180,7 +181,9 @@ class Problem:
 
 
 def run(pb: Problem, n_iter: int, burn_in: int, seed: int, tiles=(1, 1), bf16_emulate=False,
-        want_var: bool = True) -> dict:
+        want_var: bool = True, origin=(0, 0)) -> dict:
+    """Run the chain.  origin = global coordinates of pixel (0, 0) when pb is a crop of a
+    larger image (only the noise indexing uses it)."""
     lib = _load()
     y = _f32(pb.y)
     ny, nx = y.shape
@@ -220,6 +223,7 @@ def run(pb: Problem, n_iter: int, burn_in: int, seed: int, tiles=(1, 1), bf16_em
         cfg.x0 = x0.ctypes.data
     cfg.n_iter, cfg.burn_in, cfg.seed = n_iter, burn_in, seed
     cfg.tiles_y, cfg.tiles_x = tiles
+    cfg.i_off, cfg.j_off = origin
     x = np.zeros((ny, nx)); z = np.zeros((ny, nx))
     mean = np.zeros((ny, nx)); var = np.zeros((ny, nx))
     n = C.c_int64()

@@ -246,6 +246,9 @@ typedef struct {
   int64_t n_iter, burn_in;
   uint64_t seed;
   int32_t tiles_y, tiles_x;      /* <= 1 means untiled */
+  int64_t i_off, j_off;          /* global coordinates of pixel (0,0) of this (cropped) image:
+                                    the noise is indexed by global pixel (reading R9), so a crop
+                                    of a larger image draws the same xi/zeta at the same pixel */
 } or_config;
 
 static void or_kernel2d(const or_config *c, double *k) {
@@ -292,7 +295,7 @@ static int or_step_global(const or_config *c, const double *k, const double *yd,
         double pc = x[n] < c->c_lo ? c->c_lo : (x[n] > c->c_hi ? c->c_hi : x[n]);
         v += (c->gamma / c->lambda) * (pc - x[n]);
       }
-      v += sq2g * or_normal(c->seed, (uint32_t)(t + 1), i, j, 0);
+      v += sq2g * or_normal(c->seed, (uint32_t)(t + 1), i + c->i_off, j + c->j_off, 0);
       xn[n] = v;
     }
   if (c->rho > 0.0) {
@@ -302,7 +305,7 @@ static int or_step_global(const or_config *c, const double *k, const double *yd,
         int64_t n = i * nx + j;
         /* lines 12-13 / eq:sgs_pnp_ula_psgla:psgla with H2 = I, prox = projection onto [z_lo,z_hi] */
         double v = z[n] - (c->kappa / c->rho) * (z[n] - xn[n]) +
-                   sq2k * or_normal(c->seed, (uint32_t)(t + 1), i, j, 1);
+                   sq2k * or_normal(c->seed, (uint32_t)(t + 1), i + c->i_off, j + c->j_off, 1);
         zn[n] = v < c->z_lo ? c->z_lo : (v > c->z_hi ? c->z_hi : v);
       }
   }
@@ -434,11 +437,11 @@ static int or_step_tiled(const or_config *c, const double *k, const double *yd, 
             double pc = xv < c->c_lo ? c->c_lo : (xv > c->c_hi ? c->c_hi : xv);
             v += (c->gamma / c->lambda) * (pc - xv);
           }
-          v += sq2g * or_normal(c->seed, (uint32_t)(t + 1), gi, gj, 0);
+          v += sq2g * or_normal(c->seed, (uint32_t)(t + 1), gi + c->i_off, gj + c->j_off, 0);
           xn[n] = v;
           if (c->rho > 0.0) {
             double zv = z[n] - (c->kappa / c->rho) * (z[n] - v) +
-                        sqrt(2.0 * c->kappa) * or_normal(c->seed, (uint32_t)(t + 1), gi, gj, 1);
+                        sqrt(2.0 * c->kappa) * or_normal(c->seed, (uint32_t)(t + 1), gi + c->i_off, gj + c->j_off, 1);
             zn[n] = zv < c->z_lo ? c->z_lo : (zv > c->z_hi ? c->z_hi : zv);
           }
         }

@@ -1,0 +1,97 @@
+// internal.h -- device-side parameter blocks shared by the host runtime
+// (pnpula_host.cpp) and the sm_100a kernels (*.cu).  Not part of the C ABI.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace pnpula {
+
+constexpr int kMaxTaps = 15;      // max kernel extent (odd), radius <= 7
+constexpr int kMaxChunk = 8;      // max CNN layers fused in one launch
+
+// Padded per-tile geometry: padded(r, c) holds global (i0 - h + r, j0 - hx + c).
+struct TileGeom {
+  int i0, j0, th, tw;   // interior rectangle (global)
+  int h;                // halo width (rows and columns)
+  int hx;               // padded column of interior column 0; (hx - j0) % 4 == 0 (mod 4 alignment)
+  int ph;               // padded rows = th + 2h
+  int pitch;            // floats per padded row (multiple of 32)
+};
+
+// K7: fused data-fidelity stencil + Moreau box + AXDA coupling + ULA update +
+// Philox/Box-Muller noise + z PSGLA step + Welford moments, one tile.
+struct UpdateParams {
+  const float *x;       // padded x^t (halo filled)
+  float *xn;            // padded x^{t+1} (interior written)
+  const float *y;       // padded y (valid on tile (+) r_H, zero outside the image)
+  const uint8_t *mask;  // padded mask (OP_MASK)
+  const float *G;       // padded CNN residual (interior), or nullptr
+  float *z;             // padded z (interior), in place, or nullptr
+  float *mean, *m2;     // padded moments (interior), in place
+  TileGeom g;
+  int ny, nx;
+  int op;               // 0 conv, 1 mask
+  int ry, rx;           // kernel radii
+  int separable;
+  float k2d[kMaxTaps * kMaxTaps];
+  float ky[kMaxTaps], kx[kMaxTaps];
+  // coefficients (fp64 on host, rounded once)
+  float a_g, a_rho, a_d, a_lam, a_xi;
+  float c_lo, c_hi;
+  float b_rho, b_zeta, z_lo, z_hi;
+  int has_z, has_G, has_box;
+  uint32_t seed_lo, seed_hi, t1;   // Philox key and iteration index t+1
+  int accumulate;                  // t+1 > burn_in
+  float inv_n;                     // 1 / (t+1 - burn_in)
+};
+
+// One rectangular copy between pitched fp32 buffers (halo exchange, pack/unpack).
+struct CopyJob {
+  const float *src;
+  float *dst;
+  int src_pitch, dst_pitch;   // floats
+  int rows, cols;
+};
+
+// Moments finalisation: var = M2 / (n - 1), packed interior -> contiguous.
+struct FinalizeParams {
+  const float *mean, *m2;
+  float *out_mean, *out_var;   // contiguous th x tw (either may be nullptr)
+  TileGeom g;
+  float inv_nm1;
+};
+
+// CNN chain: layers [l0, l0+nl) of the DnCNN-style net in one launch (see cnn_kernels.cu).
+struct CnnChunkParams {
+  int P;                 // features
+  int nl;                // layers in this launch
+  int first_is_input;    // layer l0 == 1: input is x (fp32, 1 channel)
+  int last_is_output;    // layer l0+nl-1 == K: output is G (fp32, 1 channel, no ReLU)
+  const uint16_t *w[kMaxChunk];   // packed bf16 B-operand images, one per layer
+  const float *b[kMaxChunk];      // fp32 biases per layer
+  // input: x (padded fp32) or activation buffer
+  const float *x; TileGeom xg;
+  const uint16_t *ain; int a_i0, a_j0, a_rows, a_cols;   // activation region (global origin, extent)
+  // output region (global) for the chunk's last layer
+  int oi0, oj0, oh, ow;
+  uint16_t *aout; int o_i0, o_j0, o_rows, o_cols;        // activation output buffer region
+  float *G; TileGeom gg;                                  // G output (padded geometry)
+  int ny, nx;
+  int strips;            // column strips
+  int rows_per_unit;     // output rows per work unit
+  int units;             // strips * row blocks
+  int *err;              // device error flag (watchdog)
+};
+
+// Launchers (return cudaGetLastError()).
+cudaError_t launch_update(const UpdateParams &p, cudaStream_t s);
+cudaError_t launch_copy_jobs(const CopyJob *d_jobs, int njobs, int max_rows, cudaStream_t s);
+cudaError_t launch_fill(float *p, float v, size_t n, cudaStream_t s);
+cudaError_t launch_finalize(const FinalizeParams &p, cudaStream_t s);
+cudaError_t launch_cnn_chunk(const CnnChunkParams &p, int num_sms, cudaStream_t s);
+size_t cnn_chunk_smem_bytes(int P, int nl, int first_is_input, int last_is_output);
+// Pack host fp32 OIHW weights of one layer into the device B-operand image (host side).
+void cnn_pack_layer(const float *w, int cout, int cin, uint16_t *out);
+size_t cnn_packed_layer_elems(int cout, int cin);
+
+}  // namespace pnpula

@@ -1,0 +1,992 @@
+// pnpula_host.cpp -- host runtime of libpnpula: validation, Cartesian tiling with
+// ghost frames (Def. 1), device buffer ownership, NCCL halo
+// exchange (Alg. 1 line 5, grouped as in P:674), the iteration loop of
+// Algorithm 1 and moment gathering.  Implements include/pnpula.h.
+#include "pnpula.h"
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+using namespace pnpula;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+void set_error(const char *fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+}
+
+int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+
+struct TileDev {
+  int index;               // global row-major tile index
+  TileGeom g;
+  float *x[2] = {nullptr, nullptr};
+  float *x0 = nullptr;     // padded x0 (interior), ghost frame zero
+  float *y = nullptr;
+  uint8_t *mask = nullptr;
+  float *z = nullptr, *mean = nullptr, *m2 = nullptr, *G = nullptr;
+  uint16_t *act[2] = {nullptr, nullptr};   // inter-chunk activations
+};
+
+struct CnnChunk {
+  int l0, nl;               // first layer (1-based), number of layers
+  int ext;                  // output region = tile (+) ext
+};
+
+struct Timer {
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+  size_t used = 0;
+  double ms = 0.0;
+  int64_t launches = 0;
+};
+
+}  // namespace
+
+struct pnpula_ctx {
+  // configuration (host copies of scalars)
+  int ny = 0, nx = 0, tiles_y = 1, tiles_x = 1, rank = 0, world = 1, device = 0;
+  int op = 0, kh = 0, kw = 0, ry = 0, rx = 0, separable = 0;
+  std::vector<float> k2d, ky, kx;
+  double sigma2 = 1, alpha = 0, eps = 1, lambda = 0, c_lo = 0, c_hi = 1, rho = 0, kappa = 0,
+         z_lo = 0, z_hi = 0, gamma = 0;
+  int flags = 0;
+  int n_layers = 0, channels = 0;   // 0 layers = no CNN
+  int h = 0;
+
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  ncclComm_t comm = nullptr;
+  int num_sms = 148;
+  int *d_err = nullptr;
+
+  int ntiles = 0, n_local = 0, first_tile = 0;
+  std::vector<TileDev> tiles;
+  pnpula_rect bbox{};
+
+  // CNN
+  std::vector<CnnChunk> chunks;
+  std::vector<uint16_t *> d_w;      // per layer packed weights
+  std::vector<float *> d_b;         // per layer biases
+
+  // halo plan
+  std::vector<pnpula_halo_msg> msgs;
+  CopyJob *d_local_jobs[2] = {nullptr, nullptr};
+  int n_local_jobs = 0, max_local = 0;
+  CopyJob *d_pack_jobs[2] = {nullptr, nullptr}, *d_unpack_jobs[2] = {nullptr, nullptr};
+  int n_pack = 0, n_unpack = 0, max_pack = 0, max_unpack = 0;
+  float *d_sendbuf = nullptr, *d_recvbuf = nullptr;
+  struct PeerMsg { int peer; size_t off, count; };
+  std::vector<PeerMsg> sends, recvs;
+
+  // chain state
+  int cur = 0;
+  int64_t t = 0, burn_in = 0;
+  uint64_t seed = 0;
+  bool have_reset = false;
+  bool poisoned = false;
+
+  // timing
+  bool timing = false;
+  Timer tm_cnn, tm_update, tm_halo;
+};
+
+namespace {
+
+pnpula_status fail_cuda(pnpula_ctx *c, cudaError_t e, const char *what, int line) {
+  set_error("CUDA error %s (%d) in %s (pnpula_host.cpp:%d)", cudaGetErrorString(e), (int)e, what, line);
+  if (c) c->poisoned = true;
+  return PNPULA_E_CUDA;
+}
+pnpula_status fail_nccl(pnpula_ctx *c, ncclResult_t e, const char *what, int line) {
+  set_error("NCCL error %s (%d) in %s (pnpula_host.cpp:%d)", ncclGetErrorString(e), (int)e, what, line);
+  if (c) c->poisoned = true;
+  return PNPULA_E_NCCL;
+}
+
+#define CU(c, expr)                                                       \
+  do {                                                                    \
+    cudaError_t _e = (expr);                                              \
+    if (_e != cudaSuccess) return fail_cuda((c), _e, #expr, __LINE__);   \
+  } while (0)
+#define NC(c, expr)                                                       \
+  do {                                                                    \
+    ncclResult_t _e = (expr);                                             \
+    if (_e != ncclSuccess) return fail_nccl((c), _e, #expr, __LINE__);    \
+  } while (0)
+
+void timer_begin(pnpula_ctx *c, Timer &t, cudaEvent_t *end_out) {
+  *end_out = nullptr;
+  if (!c->timing) return;
+  if (t.used == t.ev.size()) {
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    t.ev.push_back({a, b});
+  }
+  cudaEventRecord(t.ev[t.used].first, c->stream);
+  *end_out = t.ev[t.used].second;
+  t.used++;
+}
+void timer_end(pnpula_ctx *c, cudaEvent_t end) {
+  if (end) cudaEventRecord(end, c->stream);
+}
+void timer_collect(Timer &t) {
+  for (size_t i = 0; i < t.used; ++i) {
+    float ms = 0.f;
+    cudaEventSynchronize(t.ev[i].second);
+    cudaEventElapsedTime(&ms, t.ev[i].first, t.ev[i].second);
+    t.ms += ms;
+    t.launches++;
+  }
+  t.used = 0;
+}
+
+TileGeom make_geom(int i0, int j0, int th, int tw, int h) {
+  TileGeom g;
+  g.i0 = i0; g.j0 = j0; g.th = th; g.tw = tw; g.h = h;
+  g.hx = (int)round_up(std::max(h, 1), 4) + (j0 & 3);
+  g.ph = th + 2 * h;
+  g.pitch = (int)round_up(g.hx + tw + std::max(h, 4), 32);
+  return g;
+}
+
+size_t geom_elems(const TileGeom &g) { return (size_t)g.ph * g.pitch; }
+
+void tile_rect(int ny, int nx, int ty_n, int tx_n, int tile, pnpula_rect *r) {
+  int64_t a, b, c, d;
+  pnpula_partition(ny, ty_n, tile / tx_n, &a, &b);
+  pnpula_partition(nx, tx_n, tile % tx_n, &c, &d);
+  r->i0 = (int)a; r->h = (int)(b - a); r->j0 = (int)c; r->w = (int)(d - c);
+}
+
+pnpula_status check_ctx(pnpula_ctx *c) {
+  if (!c) { set_error("null context"); return PNPULA_E_INVALID_ARG; }
+  if (c->poisoned) { set_error("context poisoned by an earlier CUDA/NCCL error"); return PNPULA_E_STATE; }
+  return PNPULA_OK;
+}
+
+// copy a host rectangle (row-major, rect r of in_rect) into padded device buffer rows
+template <typename T>
+pnpula_status upload_padded(pnpula_ctx *c, T *dst, const TileGeom &g, const T *host,
+                            const pnpula_rect &in, int i0, int j0, int hgt, int wid) {
+  // region [i0, i0+hgt) x [j0, j0+wid) (global), clipped to the image and to in_rect
+  int a0 = std::max({i0, 0, in.i0}), a1 = std::min({i0 + hgt, c->ny, in.i0 + in.h});
+  int b0 = std::max({j0, 0, in.j0}), b1 = std::min({j0 + wid, c->nx, in.j0 + in.w});
+  if (a0 >= a1 || b0 >= b1) return PNPULA_OK;
+  const T *src = host + (size_t)(a0 - in.i0) * in.w + (b0 - in.j0);
+  T *d = dst + (size_t)(a0 - (g.i0 - g.h)) * g.pitch + (b0 - (g.j0 - g.hx));
+  CU(c, cudaMemcpy2DAsync(d, (size_t)g.pitch * sizeof(T), src, (size_t)in.w * sizeof(T),
+                          (size_t)(b1 - b0) * sizeof(T), (size_t)(a1 - a0), cudaMemcpyHostToDevice, c->stream));
+  return PNPULA_OK;
+}
+
+pnpula_status run_cnn(pnpula_ctx *c, int buf) {
+  for (auto &td : c->tiles) {
+    for (size_t ci = 0; ci < c->chunks.size(); ++ci) {
+      const CnnChunk &ch = c->chunks[ci];
+      CnnChunkParams p{};
+      p.P = c->channels;
+      p.nl = ch.nl;
+      p.first_is_input = ch.l0 == 1;
+      p.last_is_output = ch.l0 + ch.nl - 1 == c->n_layers;
+      for (int l = 0; l < ch.nl; ++l) {
+        p.w[l] = c->d_w[ch.l0 - 1 + l];
+        p.b[l] = c->d_b[ch.l0 - 1 + l];
+      }
+      const TileGeom &g = td.g;
+      p.x = td.x[buf];
+      p.xg = g;
+      const int ein = ch.ext + ch.nl;
+      if (!p.first_is_input) {
+        p.ain = td.act[(ci + 1) & 1];
+        p.a_i0 = g.i0 - ein; p.a_j0 = g.j0 - ein;
+        p.a_rows = g.th + 2 * ein; p.a_cols = g.tw + 2 * ein;
+      }
+      p.oi0 = g.i0 - ch.ext; p.oj0 = g.j0 - ch.ext;
+      p.oh = g.th + 2 * ch.ext; p.ow = g.tw + 2 * ch.ext;
+      if (!p.last_is_output) {
+        p.aout = td.act[ci & 1];
+        p.o_i0 = p.oi0; p.o_j0 = p.oj0; p.o_rows = p.oh; p.o_cols = p.ow;
+      } else {
+        p.G = td.G;
+        p.gg = g;
+      }
+      p.ny = c->ny; p.nx = c->nx;
+      p.err = c->d_err;
+      cudaEvent_t end;
+      timer_begin(c, c->tm_cnn, &end);
+      CU(c, launch_cnn_chunk(p, c->num_sms, c->stream));
+      timer_end(c, end);
+    }
+  }
+  return PNPULA_OK;
+}
+
+pnpula_status exchange(pnpula_ctx *c, int buf) {
+  cudaEvent_t end;
+  timer_begin(c, c->tm_halo, &end);
+  if (c->n_local_jobs) CU(c, launch_copy_jobs(c->d_local_jobs[buf], c->n_local_jobs, c->max_local, c->stream));
+  if (!c->sends.empty() || !c->recvs.empty()) {
+    if (c->n_pack) CU(c, launch_copy_jobs(c->d_pack_jobs[buf], c->n_pack, c->max_pack, c->stream));
+    NC(c, ncclGroupStart());
+    for (auto &m : c->sends) NC(c, ncclSend(c->d_sendbuf + m.off, m.count, ncclFloat32, m.peer, c->comm, c->stream));
+    for (auto &m : c->recvs) NC(c, ncclRecv(c->d_recvbuf + m.off, m.count, ncclFloat32, m.peer, c->comm, c->stream));
+    NC(c, ncclGroupEnd());
+    if (c->n_unpack) CU(c, launch_copy_jobs(c->d_unpack_jobs[buf], c->n_unpack, c->max_unpack, c->stream));
+  }
+  timer_end(c, end);
+  return PNPULA_OK;
+}
+
+UpdateParams make_update_params(pnpula_ctx *c, TileDev &td, int buf) {
+  UpdateParams p{};
+  p.x = td.x[buf];
+  p.xn = td.x[buf ^ 1];
+  p.y = td.y;
+  p.mask = td.mask;
+  p.G = (c->n_layers > 0) ? td.G : nullptr;
+  p.z = td.z;
+  p.mean = td.mean;
+  p.m2 = td.m2;
+  p.g = td.g;
+  p.ny = c->ny; p.nx = c->nx;
+  p.op = c->op;
+  p.ry = c->ry; p.rx = c->rx;
+  p.separable = c->separable;
+  if (c->op == PNPULA_OP_CONV) {
+    for (size_t i = 0; i < c->k2d.size(); ++i) p.k2d[i] = c->k2d[i];
+    for (size_t i = 0; i < c->ky.size(); ++i) p.ky[i] = c->ky[i];
+    for (size_t i = 0; i < c->kx.size(); ++i) p.kx[i] = c->kx[i];
+  }
+  p.a_g = (float)(c->gamma / c->sigma2);
+  p.has_z = c->rho > 0;
+  p.a_rho = p.has_z ? (float)(c->gamma / c->rho) : 0.f;
+  p.has_G = c->n_layers > 0;
+  p.a_d = p.has_G ? (float)(c->alpha * c->gamma / (c->eps * c->eps)) : 0.f;
+  p.has_box = c->lambda > 0;
+  p.a_lam = p.has_box ? (float)(c->gamma / c->lambda) : 0.f;
+  p.c_lo = (float)c->c_lo; p.c_hi = (float)c->c_hi;
+  p.a_xi = (float)std::sqrt(2.0 * c->gamma);
+  p.b_rho = p.has_z ? (float)(c->kappa / c->rho) : 0.f;
+  p.b_zeta = p.has_z ? (float)std::sqrt(2.0 * c->kappa) : 0.f;
+  p.z_lo = (float)c->z_lo; p.z_hi = (float)c->z_hi;
+  p.seed_lo = (uint32_t)c->seed;
+  p.seed_hi = (uint32_t)(c->seed >> 32);
+  return p;
+}
+
+pnpula_status step(pnpula_ctx *c) {
+  const int buf = c->cur;
+  if (c->n_layers > 0) {
+    pnpula_status s = run_cnn(c, buf);
+    if (s) return s;
+  }
+  const uint64_t t1 = (uint64_t)c->t + 1;
+  const bool acc = (int64_t)t1 > c->burn_in;
+  const double k = acc ? (double)((int64_t)t1 - c->burn_in) : 1.0;
+  for (auto &td : c->tiles) {
+    UpdateParams p = make_update_params(c, td, buf);
+    p.t1 = (uint32_t)t1;
+    p.accumulate = acc;
+    p.inv_n = (float)(1.0 / k);
+    cudaEvent_t end;
+    timer_begin(c, c->tm_update, &end);
+    CU(c, launch_update(p, c->stream));
+    timer_end(c, end);
+  }
+  pnpula_status s = exchange(c, buf ^ 1);
+  if (s) return s;
+  c->cur ^= 1;
+  c->t += 1;
+  return PNPULA_OK;
+}
+
+pnpula_status build_halo_plan(pnpula_ctx *c) {
+  int n = pnpula_plan_halo(c->ny, c->nx, c->tiles_y, c->tiles_x, c->h, nullptr, 0);
+  if (n < 0) { set_error("tile extent smaller than halo width %d", c->h); return PNPULA_E_PARTITION_TOO_FINE; }
+  c->msgs.resize(n);
+  pnpula_plan_halo(c->ny, c->nx, c->tiles_y, c->tiles_x, c->h, c->msgs.data(), n);
+  const int per_rank = c->ntiles / c->world;
+  auto owner = [&](int tile) { return tile / per_rank; };
+  auto local = [&](int tile) -> TileDev * {
+    int li = tile - c->first_tile;
+    return (li >= 0 && li < c->n_local) ? &c->tiles[li] : nullptr;
+  };
+  const bool force_nccl = (c->flags & PNPULA_FLAG_HALO_VIA_NCCL) != 0;
+  std::vector<CopyJob> lj[2], pj[2], uj[2];
+  size_t soff = 0, roff = 0;
+  for (auto &m : c->msgs) {
+    TileDev *src = local(m.src_tile), *dst = local(m.dst_tile);
+    if (!src && !dst) continue;
+    const pnpula_rect &r = m.rect;
+    const size_t cnt = (size_t)r.h * r.w;
+    auto off = [](const TileGeom &g, int gi, int gj) {
+      return (size_t)(gi - (g.i0 - g.h)) * g.pitch + (gj - (g.j0 - g.hx));
+    };
+    if (src && dst && !force_nccl) {
+      for (int b = 0; b < 2; ++b)
+        lj[b].push_back({src->x[b] + off(src->g, r.i0, r.j0), dst->x[b] + off(dst->g, r.i0, r.j0),
+                         src->g.pitch, dst->g.pitch, r.h, r.w});
+      c->max_local = std::max(c->max_local, (int)cnt);
+      continue;
+    }
+    if (src) {
+      for (int b = 0; b < 2; ++b)
+        pj[b].push_back({src->x[b] + off(src->g, r.i0, r.j0), nullptr, src->g.pitch, r.w, r.h, r.w});
+      c->sends.push_back({owner(m.dst_tile), soff, cnt});
+      soff += cnt;
+      c->max_pack = std::max(c->max_pack, (int)cnt);
+    }
+    if (dst) {
+      for (int b = 0; b < 2; ++b)
+        uj[b].push_back({nullptr, dst->x[b] + off(dst->g, r.i0, r.j0), r.w, dst->g.pitch, r.h, r.w});
+      c->recvs.push_back({owner(m.src_tile), roff, cnt});
+      roff += cnt;
+      c->max_unpack = std::max(c->max_unpack, (int)cnt);
+    }
+  }
+  if (soff) CU(c, cudaMalloc(&c->d_sendbuf, soff * sizeof(float)));
+  if (roff) CU(c, cudaMalloc(&c->d_recvbuf, roff * sizeof(float)));
+  for (int b = 0; b < 2; ++b) {
+    size_t so = 0, ro = 0;
+    for (size_t i = 0; i < pj[b].size(); ++i) { pj[b][i].dst = c->d_sendbuf + so; so += (size_t)pj[b][i].rows * pj[b][i].cols; }
+    for (size_t i = 0; i < uj[b].size(); ++i) { uj[b][i].src = c->d_recvbuf + ro; ro += (size_t)uj[b][i].rows * uj[b][i].cols; }
+  }
+  c->n_local_jobs = (int)lj[0].size();
+  c->n_pack = (int)pj[0].size();
+  c->n_unpack = (int)uj[0].size();
+  for (int b = 0; b < 2; ++b) {
+    if (c->n_local_jobs) {
+      CU(c, cudaMalloc(&c->d_local_jobs[b], lj[b].size() * sizeof(CopyJob)));
+      CU(c, cudaMemcpy(c->d_local_jobs[b], lj[b].data(), lj[b].size() * sizeof(CopyJob), cudaMemcpyHostToDevice));
+    }
+    if (c->n_pack) {
+      CU(c, cudaMalloc(&c->d_pack_jobs[b], pj[b].size() * sizeof(CopyJob)));
+      CU(c, cudaMemcpy(c->d_pack_jobs[b], pj[b].data(), pj[b].size() * sizeof(CopyJob), cudaMemcpyHostToDevice));
+    }
+    if (c->n_unpack) {
+      CU(c, cudaMalloc(&c->d_unpack_jobs[b], uj[b].size() * sizeof(CopyJob)));
+      CU(c, cudaMemcpy(c->d_unpack_jobs[b], uj[b].data(), uj[b].size() * sizeof(CopyJob), cudaMemcpyHostToDevice));
+    }
+  }
+  return PNPULA_OK;
+}
+
+// CNN chunking: greedy, as many consecutive layers per launch as shared memory allows.
+void plan_cnn_chunks(pnpula_ctx *c) {
+  c->chunks.clear();
+  const int K = c->n_layers;
+  const size_t budget = 227 * 1024;
+  int l = 1;
+  while (l <= K) {
+    int best = 1;
+    const int maxnl = (c->flags & PNPULA_FLAG_CNN_LAYERWISE) ? 1 : kMaxChunk;
+    for (int nl = 1; nl <= std::min(maxnl, K - l + 1); ++nl) {
+      if (cnn_chunk_smem_bytes(c->channels, nl, l == 1, l + nl - 1 == K) <= budget) best = nl;
+    }
+    c->chunks.push_back({l, best, K - (l + best - 1)});
+    l += best;
+  }
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+extern "C" {
+
+const char *pnpula_version(void) { return "pnpula-b200 0.1 (sm_100a)"; }
+
+const char *pnpula_last_error(void) { return g_last_error.c_str(); }
+
+void pnpula_partition(int64_t n, int64_t parts, int64_t p, int64_t *lo, int64_t *hi) {
+  *lo = (p * n) / parts;
+  *hi = ((p + 1) * n) / parts;
+}
+
+int32_t pnpula_halo_width(int32_t op, int32_t kh, int32_t kw, int32_t n_layers) {
+  int r = (op == PNPULA_OP_CONV) ? std::max(kh, kw) / 2 : 0;
+  return std::max(2 * r, std::max(n_layers, 0));
+}
+
+int32_t pnpula_plan_halo(int32_t ny, int32_t nx, int32_t tiles_y, int32_t tiles_x, int32_t h,
+                         pnpula_halo_msg *out, int32_t cap) {
+  const int nt = tiles_y * tiles_x;
+  std::vector<pnpula_rect> rects(nt);
+  for (int t = 0; t < nt; ++t) {
+    tile_rect(ny, nx, tiles_y, tiles_x, t, &rects[t]);
+    if (rects[t].h < h || rects[t].w < h) return -1;
+  }
+  if (h == 0) return 0;
+  int count = 0;
+  for (int s = 0; s < nt; ++s) {
+    for (int d = 0; d < nt; ++d) {
+      if (s == d) continue;
+      const pnpula_rect &rs = rects[s], &rd = rects[d];
+      // ghost frame of d = (rd (+) h) \ rd, clipped to the image; intersect with interior of s
+      int a0 = std::max(rs.i0, std::max(rd.i0 - h, 0));
+      int a1 = std::min(rs.i0 + rs.h, std::min(rd.i0 + rd.h + h, ny));
+      int b0 = std::max(rs.j0, std::max(rd.j0 - h, 0));
+      int b1 = std::min(rs.j0 + rs.w, std::min(rd.j0 + rd.w + h, nx));
+      if (a0 >= a1 || b0 >= b1) continue;
+      if (out && count < cap) out[count] = {s, d, {a0, b0, a1 - a0, b1 - b0}};
+      count++;
+    }
+  }
+  return count;
+}
+
+int32_t pnpula_check_stepsizes(double L, double h2_over_rho, double alpha, double eps, double L_D,
+                               double lambda, double gamma) {
+  int32_t bad = 0;
+  const double prior = (alpha > 0 && L_D > 0) ? alpha * L_D / (eps * eps) : 0.0;
+  if (!(2.0 * (L + h2_over_rho) + prior <= 0.5 / lambda)) bad |= 1;
+  if (!(3.0 * gamma * (L + h2_over_rho + 1.0 / lambda + prior) < 1.0)) bad |= 2;
+  return bad;
+}
+
+pnpula_status pnpula_get_unique_id(uint8_t out[128]) {
+  if (!out) { set_error("null output"); return PNPULA_E_INVALID_ARG; }
+  ncclUniqueId id;
+  ncclResult_t e = ncclGetUniqueId(&id);
+  if (e != ncclSuccess) return fail_nccl(nullptr, e, "ncclGetUniqueId", __LINE__);
+  static_assert(sizeof(id) == 128, "nccl id size");
+  memcpy(out, &id, 128);
+  return PNPULA_OK;
+}
+
+pnpula_status pnpula_destroy(pnpula_ctx *c);
+
+pnpula_status pnpula_create(const pnpula_config *cfg, pnpula_ctx **out) {
+  g_last_error.clear();
+  if (!cfg || !out) { set_error("null argument"); return PNPULA_E_INVALID_ARG; }
+  *out = nullptr;
+  const pnpula_config &f = *cfg;
+  if (f.ny <= 0 || f.nx <= 0) { set_error("image size must be positive"); return PNPULA_E_SHAPE; }
+  if (f.tiles_y <= 0 || f.tiles_x <= 0 || f.tiles_y > f.ny || f.tiles_x > f.nx) {
+    set_error("invalid tile grid %dx%d", f.tiles_y, f.tiles_x); return PNPULA_E_PARTITION_TOO_FINE;
+  }
+  const int ntiles = f.tiles_y * f.tiles_x;
+  if (f.world_size <= 0 || ntiles % f.world_size != 0 || f.rank < 0 || f.rank >= f.world_size) {
+    set_error("world_size must divide the tile count and rank be in range"); return PNPULA_E_INVALID_ARG;
+  }
+  if (!(f.gamma > 0) || !(f.sigma2 > 0)) { set_error("gamma and sigma2 must be > 0"); return PNPULA_E_INVALID_ARG; }
+  if (!f.y) { set_error("y is required"); return PNPULA_E_INVALID_ARG; }
+  if (f.op != PNPULA_OP_CONV && f.op != PNPULA_OP_MASK) { set_error("unknown op"); return PNPULA_E_INVALID_ARG; }
+  if (f.op == PNPULA_OP_CONV) {
+    if (f.kh <= 0 || f.kw <= 0 || f.kh % 2 == 0 || f.kw % 2 == 0 || f.kh > kMaxTaps || f.kw > kMaxTaps) {
+      set_error("kernel sizes must be odd and <= %d", kMaxTaps); return PNPULA_E_INVALID_ARG;
+    }
+    if (!f.kernel && !(f.kernel_y && f.kernel_x)) { set_error("kernel required"); return PNPULA_E_INVALID_ARG; }
+  } else if (!f.mask) {
+    set_error("mask required for OP_MASK"); return PNPULA_E_INVALID_ARG;
+  }
+  if (f.rho > 0 && !(f.kappa > 0 && f.kappa < f.rho)) { set_error("kappa must lie in (0, rho)"); return PNPULA_E_INVALID_ARG; }
+  const bool use_cnn = f.den && f.alpha != 0.0;
+  if (use_cnn) {
+    if (f.den->n_layers < 2 || !f.den->weights || !f.den->biases) { set_error("denoiser needs >= 2 layers and weights"); return PNPULA_E_INVALID_ARG; }
+    if (f.den->channels != 16 && f.den->channels != 32 && f.den->channels != 64) {
+      set_error("denoiser channels must be 16, 32 or 64"); return PNPULA_E_UNSUPPORTED;
+    }
+    if (!(f.eps > 0)) { set_error("eps must be > 0"); return PNPULA_E_INVALID_ARG; }
+  }
+  const pnpula_rect in = f.in_rect;
+
+  pnpula_ctx *c = new pnpula_ctx();
+  c->ny = f.ny; c->nx = f.nx; c->tiles_y = f.tiles_y; c->tiles_x = f.tiles_x;
+  c->rank = f.rank; c->world = f.world_size; c->device = f.device;
+  c->op = f.op; c->flags = f.flags;
+  c->sigma2 = f.sigma2; c->alpha = f.alpha; c->eps = f.eps; c->lambda = f.lambda;
+  c->c_lo = f.c_lo; c->c_hi = f.c_hi; c->rho = f.rho; c->kappa = f.kappa;
+  c->z_lo = f.z_lo; c->z_hi = f.z_hi; c->gamma = f.gamma;
+  if (f.op == PNPULA_OP_CONV) {
+    c->kh = f.kh; c->kw = f.kw; c->ry = f.kh / 2; c->rx = f.kw / 2;
+    c->separable = (f.kernel_y && f.kernel_x) ? 1 : 0;
+    if (c->separable) {
+      c->ky.assign(f.kernel_y, f.kernel_y + f.kh);
+      c->kx.assign(f.kernel_x, f.kernel_x + f.kw);
+    } else {
+      c->k2d.assign(f.kernel, f.kernel + f.kh * f.kw);
+    }
+  }
+  if (use_cnn) { c->n_layers = f.den->n_layers; c->channels = f.den->channels; }
+  c->h = pnpula_halo_width(f.op, f.kh, f.kw, c->n_layers);
+  c->ntiles = ntiles;
+  c->n_local = ntiles / f.world_size;
+  c->first_tile = f.rank * c->n_local;
+
+  // step-size check (warning only)
+  {
+    double L = f.lipschitz_L;
+    if (L <= 0) {
+      double s = 0;
+      if (f.op == PNPULA_OP_CONV) {
+        if (c->separable) {
+          double a = 0, b = 0;
+          for (float v : c->ky) a += std::fabs(v);
+          for (float v : c->kx) b += std::fabs(v);
+          s = a * b;
+        } else {
+          for (float v : c->k2d) s += std::fabs(v);
+        }
+      } else {
+        s = 1;
+      }
+      L = s * s / f.sigma2;   // ||H||^2 <= ||k||_1^2 (Young)
+    }
+    const double lam = f.lambda > 0 ? f.lambda : 1e300;
+    int32_t bad = pnpula_check_stepsizes(L, f.rho > 0 ? 1.0 / f.rho : 0.0, use_cnn ? f.alpha : 0.0,
+                                         use_cnn ? f.eps : 1.0, f.lipschitz_LD, lam, f.gamma);
+    if (bad) set_error("warning: eq:stepsize_cond violated (mask %d) -- continuing", bad);
+  }
+
+  // tiles and validation of in_rect coverage
+  const int rH = std::max(c->ry, c->rx);
+  pnpula_rect bb{INT32_MAX, INT32_MAX, 0, 0};
+  int bi1 = INT32_MIN, bj1 = INT32_MIN;
+  for (int li = 0; li < c->n_local; ++li) {
+    pnpula_rect r;
+    tile_rect(f.ny, f.nx, f.tiles_y, f.tiles_x, c->first_tile + li, &r);
+    if (r.h < c->h || r.w < c->h) {
+      set_error("tile %dx%d smaller than halo width %d", r.h, r.w, c->h);
+      delete c;
+      return PNPULA_E_PARTITION_TOO_FINE;
+    }
+    int need_i0 = std::max(r.i0 - rH, 0), need_i1 = std::min(r.i0 + r.h + rH, f.ny);
+    int need_j0 = std::max(r.j0 - rH, 0), need_j1 = std::min(r.j0 + r.w + rH, f.nx);
+    if (need_i0 < in.i0 || need_j0 < in.j0 || need_i1 > in.i0 + in.h || need_j1 > in.j0 + in.w) {
+      set_error("in_rect {%d,%d,%d,%d} does not cover tile (+) r_H", in.i0, in.j0, in.h, in.w);
+      delete c;
+      return PNPULA_E_SHAPE;
+    }
+    TileDev td;
+    td.index = c->first_tile + li;
+    td.g = make_geom(r.i0, r.j0, r.h, r.w, c->h);
+    c->tiles.push_back(td);
+    bb.i0 = std::min(bb.i0, r.i0); bb.j0 = std::min(bb.j0, r.j0);
+    bi1 = std::max(bi1, r.i0 + r.h); bj1 = std::max(bj1, r.j0 + r.w);
+  }
+  bb.h = bi1 - bb.i0; bb.w = bj1 - bb.j0;
+  c->bbox = bb;
+
+  std::string warn = g_last_error;
+  auto bail = [&](pnpula_status s) { pnpula_destroy(c); return s; };
+  cudaError_t e = cudaSetDevice(f.device);
+  if (e != cudaSuccess) { fail_cuda(nullptr, e, "cudaSetDevice", __LINE__); return bail(PNPULA_E_CUDA); }
+  cudaDeviceProp prop;
+  e = cudaGetDeviceProperties(&prop, f.device);
+  if (e != cudaSuccess) { fail_cuda(nullptr, e, "cudaGetDeviceProperties", __LINE__); return bail(PNPULA_E_CUDA); }
+  if (prop.major != 10 || prop.minor != 0) {
+    set_error("device %d is sm_%d%d; this library is built for sm_100a only", f.device, prop.major, prop.minor);
+    return bail(PNPULA_E_CUDA);
+  }
+  c->num_sms = prop.multiProcessorCount;
+  if (f.stream) {
+    c->stream = (cudaStream_t)(uintptr_t)f.stream;
+  } else {
+    e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) { fail_cuda(nullptr, e, "cudaStreamCreate", __LINE__); return bail(PNPULA_E_CUDA); }
+    c->own_stream = true;
+  }
+#define CUB(expr)                                                              \
+  do {                                                                         \
+    cudaError_t _e = (expr);                                                   \
+    if (_e != cudaSuccess) { fail_cuda(nullptr, _e, #expr, __LINE__);          \
+      return bail(_e == cudaErrorMemoryAllocation ? PNPULA_E_OOM : PNPULA_E_CUDA); } \
+  } while (0)
+  CUB(cudaMalloc(&c->d_err, sizeof(int)));
+  CUB(cudaMemsetAsync(c->d_err, 0, sizeof(int), c->stream));
+
+  if (f.world_size > 1) {
+    if (!f.nccl_uid) { set_error("nccl_uid required when world_size > 1"); return bail(PNPULA_E_INVALID_ARG); }
+    ncclUniqueId id;
+    memcpy(&id, f.nccl_uid, 128);
+    ncclResult_t r = ncclCommInitRank(&c->comm, f.world_size, id, f.rank);
+    if (r != ncclSuccess) { fail_nccl(nullptr, r, "ncclCommInitRank", __LINE__); return bail(PNPULA_E_NCCL); }
+  } else if (c->flags & PNPULA_FLAG_HALO_VIA_NCCL) {
+    int dev = f.device;
+    ncclResult_t r = ncclCommInitAll(&c->comm, 1, &dev);
+    if (r != ncclSuccess) { fail_nccl(nullptr, r, "ncclCommInitAll", __LINE__); return bail(PNPULA_E_NCCL); }
+  }
+
+  // device buffers
+  for (auto &td : c->tiles) {
+    const size_t n = geom_elems(td.g);
+    for (int b = 0; b < 2; ++b) {
+      CUB(cudaMalloc(&td.x[b], n * sizeof(float)));
+      CUB(cudaMemsetAsync(td.x[b], 0, n * sizeof(float), c->stream));
+    }
+    CUB(cudaMalloc(&td.x0, n * sizeof(float)));
+    CUB(cudaMemsetAsync(td.x0, 0, n * sizeof(float), c->stream));
+    CUB(cudaMalloc(&td.y, n * sizeof(float)));
+    CUB(cudaMemsetAsync(td.y, 0, n * sizeof(float), c->stream));
+    CUB(cudaMalloc(&td.mean, n * sizeof(float)));
+    CUB(cudaMalloc(&td.m2, n * sizeof(float)));
+    if (c->rho > 0) CUB(cudaMalloc(&td.z, n * sizeof(float)));
+    if (c->op == PNPULA_OP_MASK) {
+      CUB(cudaMalloc(&td.mask, n));
+      CUB(cudaMemsetAsync(td.mask, 0, n, c->stream));
+    }
+    if (c->n_layers > 0) {
+      CUB(cudaMalloc(&td.G, n * sizeof(float)));
+      CUB(cudaMemsetAsync(td.G, 0, n * sizeof(float), c->stream));
+    }
+    const TileGeom &g = td.g;
+    pnpula_status s;
+    s = upload_padded<float>(c, td.y, g, f.y, in, g.i0 - rH, g.j0 - rH, g.th + 2 * rH, g.tw + 2 * rH);
+    if (s) return bail(s);
+    if (f.x0) {
+      s = upload_padded<float>(c, td.x0, g, f.x0, in, g.i0, g.j0, g.th, g.tw);
+      if (s) return bail(s);
+    }
+    if (c->op == PNPULA_OP_MASK) {
+      s = upload_padded<uint8_t>(c, td.mask, g, f.mask, in, g.i0, g.j0, g.th, g.tw);
+      if (s) return bail(s);
+    }
+  }
+  // CNN weights
+  if (c->n_layers > 0) {
+    plan_cnn_chunks(c);
+    const int K = c->n_layers, P = c->channels;
+    const float *w = f.den->weights;
+    const float *b = f.den->biases;
+    int cin = 1;
+    for (int l = 1; l <= K; ++l) {
+      const int cout = (l == K) ? 1 : P;
+      std::vector<uint16_t> packed(cnn_packed_layer_elems(cout, cin));
+      cnn_pack_layer(w, cout, cin, packed.data());
+      uint16_t *dw = nullptr;
+      float *db = nullptr;
+      CUB(cudaMalloc(&dw, packed.size() * sizeof(uint16_t)));
+      CUB(cudaMemcpy(dw, packed.data(), packed.size() * sizeof(uint16_t), cudaMemcpyHostToDevice));
+      CUB(cudaMalloc(&db, cout * sizeof(float)));
+      CUB(cudaMemcpy(db, b, cout * sizeof(float), cudaMemcpyHostToDevice));
+      c->d_w.push_back(dw);
+      c->d_b.push_back(db);
+      w += (size_t)cout * cin * 9;
+      b += cout;
+      cin = cout;
+    }
+    size_t maxact = 0;
+    for (auto &ch : c->chunks) {
+      if (ch.l0 + ch.nl - 1 == K) continue;
+      for (auto &td : c->tiles)
+        maxact = std::max(maxact, (size_t)(td.g.th + 2 * ch.ext) * (td.g.tw + 2 * ch.ext) * P);
+    }
+    if (maxact) {
+      for (auto &td : c->tiles)
+        for (int b2 = 0; b2 < 2; ++b2) {
+          CUB(cudaMalloc(&td.act[b2], maxact * sizeof(uint16_t)));
+          CUB(cudaMemsetAsync(td.act[b2], 0, maxact * sizeof(uint16_t), c->stream));
+        }
+    }
+  }
+  {
+    pnpula_status s = build_halo_plan(c);
+    if (s) return bail(s);
+  }
+  CUB(cudaStreamSynchronize(c->stream));
+  g_last_error = warn;
+  *out = c;
+  return PNPULA_OK;
+#undef CUB
+}
+
+pnpula_status pnpula_reset(pnpula_ctx *c, int64_t burn_in, uint64_t seed) {
+  pnpula_status s = check_ctx(c);
+  if (s) return s;
+  if (burn_in < 0) { set_error("burn_in must be >= 0"); return PNPULA_E_INVALID_ARG; }
+  CU(c, cudaSetDevice(c->device));
+  for (auto &td : c->tiles) {
+    const size_t n = geom_elems(td.g) * sizeof(float);
+    CU(c, cudaMemcpyAsync(td.x[0], td.x0, n, cudaMemcpyDeviceToDevice, c->stream));
+    CU(c, cudaMemcpyAsync(td.x[1], td.x0, n, cudaMemcpyDeviceToDevice, c->stream));
+    if (td.z) CU(c, cudaMemsetAsync(td.z, 0, n, c->stream));
+    CU(c, cudaMemsetAsync(td.mean, 0, n, c->stream));
+    CU(c, cudaMemsetAsync(td.m2, 0, n, c->stream));
+  }
+  c->cur = 0;
+  c->t = 0;
+  c->burn_in = burn_in;
+  c->seed = seed;
+  c->have_reset = true;
+  return exchange(c, 0);
+}
+
+pnpula_status pnpula_advance(pnpula_ctx *c, int64_t n_iter) {
+  pnpula_status s = check_ctx(c);
+  if (s) return s;
+  if (!c->have_reset) { set_error("pnpula_reset must precede pnpula_advance"); return PNPULA_E_STATE; }
+  if (n_iter < 0) { set_error("n_iter must be >= 0"); return PNPULA_E_INVALID_ARG; }
+  CU(c, cudaSetDevice(c->device));
+  for (int64_t i = 0; i < n_iter; ++i) {
+    s = step(c);
+    if (s) return s;
+  }
+  CU(c, cudaGetLastError());
+  return PNPULA_OK;
+}
+
+pnpula_status pnpula_synchronize(pnpula_ctx *c) {
+  pnpula_status s = check_ctx(c);
+  if (s) return s;
+  CU(c, cudaStreamSynchronize(c->stream));
+  int err = 0;
+  CU(c, cudaMemcpy(&err, c->d_err, sizeof(int), cudaMemcpyDeviceToHost));
+  if (err) {
+    set_error("device watchdog fired (code %d): a CNN pipeline barrier timed out", err);
+    c->poisoned = true;
+    return PNPULA_E_CUDA;
+  }
+  if (c->comm) {
+    ncclResult_t ae;
+    NC(c, ncclCommGetAsyncError(c->comm, &ae));
+    if (ae != ncclSuccess) return fail_nccl(c, ae, "async", __LINE__);
+  }
+  return PNPULA_OK;
+}
+
+pnpula_status pnpula_run(pnpula_ctx *c, int64_t n_iter, int64_t burn_in, uint64_t seed) {
+  pnpula_status s = pnpula_reset(c, burn_in, seed);
+  if (s) return s;
+  s = pnpula_advance(c, n_iter);
+  if (s) return s;
+  return pnpula_synchronize(c);
+}
+
+pnpula_status pnpula_local_bbox(pnpula_ctx *c, pnpula_rect *out) {
+  pnpula_status s = check_ctx(c);
+  if (s) return s;
+  if (!out) { set_error("null output"); return PNPULA_E_INVALID_ARG; }
+  *out = c->bbox;
+  return PNPULA_OK;
+}
+
+pnpula_status pnpula_tile_info(pnpula_ctx *c, int32_t li, pnpula_rect *rect, int32_t *n_local, int32_t *halo) {
+  pnpula_status s = check_ctx(c);
+  if (s) return s;
+  if (n_local) *n_local = c->n_local;
+  if (halo) *halo = c->h;
+  if (rect) {
+    if (li < 0 || li >= c->n_local) { set_error("tile index out of range"); return PNPULA_E_INVALID_ARG; }
+    const TileGeom &g = c->tiles[li].g;
+    *rect = {g.i0, g.j0, g.th, g.tw};
+  }
+  return PNPULA_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+// Gather per-tile contiguous fields (count per tile = th*tw*nf floats) into host
+// buffers covering `dst_rect`; remote tiles travel to root over NCCL.
+pnpula_status gather_fields(pnpula_ctx *c, const std::vector<float *> &d_tile_bufs, int nf,
+                            const std::vector<float *> &host_out, const pnpula_rect &dst_rect, bool global) {
+  const int per_rank = c->ntiles / c->world;
+  auto place = [&](const pnpula_rect &r, const std::vector<float> &h) {
+    for (int f = 0; f < nf; ++f) {
+      float *o = host_out[f];
+      if (!o) continue;
+      for (int a = 0; a < r.h; ++a)
+        memcpy(o + (size_t)(r.i0 - dst_rect.i0 + a) * dst_rect.w + (r.j0 - dst_rect.j0),
+               h.data() + (size_t)f * r.h * r.w + (size_t)a * r.w, (size_t)r.w * sizeof(float));
+    }
+  };
+  for (int li = 0; li < c->n_local; ++li) {
+    const TileGeom &g = c->tiles[li].g;
+    std::vector<float> h((size_t)g.th * g.tw * nf);
+    CU(c, cudaMemcpyAsync(h.data(), d_tile_bufs[li], h.size() * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+    CU(c, cudaStreamSynchronize(c->stream));
+    if (!global || c->rank == 0) place({g.i0, g.j0, g.th, g.tw}, h);
+  }
+  if (!global || c->world == 1) return PNPULA_OK;
+  // remote tiles -> rank 0
+  if (c->rank == 0) {
+    for (int t = per_rank; t < c->ntiles; ++t) {
+      pnpula_rect r;
+      tile_rect(c->ny, c->nx, c->tiles_y, c->tiles_x, t, &r);
+      size_t cnt = (size_t)r.h * r.w * nf;
+      float *d = nullptr;
+      CU(c, cudaMalloc(&d, cnt * sizeof(float)));
+      NC(c, ncclRecv(d, cnt, ncclFloat32, t / per_rank, c->comm, c->stream));
+      std::vector<float> h(cnt);
+      CU(c, cudaMemcpyAsync(h.data(), d, cnt * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+      CU(c, cudaStreamSynchronize(c->stream));
+      CU(c, cudaFree(d));
+      place(r, h);
+    }
+  } else {
+    for (int li = 0; li < c->n_local; ++li) {
+      const TileGeom &g = c->tiles[li].g;
+      NC(c, ncclSend(d_tile_bufs[li], (size_t)g.th * g.tw * nf, ncclFloat32, 0, c->comm, c->stream));
+    }
+    CU(c, cudaStreamSynchronize(c->stream));
+  }
+  return PNPULA_OK;
+}
+
+pnpula_status gather_padded_interiors(pnpula_ctx *c, const std::vector<const float *> &src, float *host,
+                                      bool global) {
+  // pack interiors to contiguous, then gather
+  std::vector<float *> bufs;
+  for (int li = 0; li < c->n_local; ++li) {
+    const TileGeom &g = c->tiles[li].g;
+    float *d = nullptr;
+    CU(c, cudaMalloc(&d, (size_t)g.th * g.tw * sizeof(float)));
+    CU(c, cudaMemcpy2DAsync(d, (size_t)g.tw * sizeof(float), src[li] + (size_t)g.h * g.pitch + g.hx,
+                            (size_t)g.pitch * sizeof(float), (size_t)g.tw * sizeof(float), g.th,
+                            cudaMemcpyDeviceToDevice, c->stream));
+    bufs.push_back(d);
+  }
+  pnpula_rect dst = global ? pnpula_rect{0, 0, c->ny, c->nx} : c->bbox;
+  pnpula_status s = gather_fields(c, bufs, 1, {host}, dst, global);
+  for (float *d : bufs) cudaFree(d);
+  return s;
+}
+
+}  // namespace
+
+extern "C" {
+
+pnpula_status pnpula_get_moments(pnpula_ctx *c, float *mean, float *var, int64_t *n_samples, int32_t scope) {
+  pnpula_status s = check_ctx(c);
+  if (s) return s;
+  if (!c->have_reset) { set_error("no chain has been run"); return PNPULA_E_STATE; }
+  const bool global = scope == PNPULA_SCOPE_GLOBAL_ON_ROOT;
+  CU(c, cudaSetDevice(c->device));
+  const int64_t n = std::max<int64_t>(0, c->t - c->burn_in);
+  if (n_samples) *n_samples = n;
+  if ((mean && n < 1) || (var && n < 2)) { set_error("not enough post-burn-in samples (%lld)", (long long)n); return PNPULA_E_STATS_EMPTY; }
+  if (global && c->rank == 0 && c->world > 1 && ((mean && false) || false)) {}
+  std::vector<float *> bufs;
+  for (auto &td : c->tiles) {
+    const TileGeom &g = td.g;
+    float *d = nullptr;
+    CU(c, cudaMalloc(&d, (size_t)g.th * g.tw * 2 * sizeof(float)));
+    FinalizeParams p{};
+    p.mean = td.mean; p.m2 = td.m2; p.g = g;
+    p.out_mean = d; p.out_var = d + (size_t)g.th * g.tw;
+    p.inv_nm1 = n >= 2 ? (float)(1.0 / (double)(n - 1)) : 0.f;
+    CU(c, launch_finalize(p, c->stream));
+    bufs.push_back(d);
+  }
+  pnpula_rect dst = global ? pnpula_rect{0, 0, c->ny, c->nx} : c->bbox;
+  s = gather_fields(c, bufs, 2, {mean, var}, dst, global);
+  for (float *d : bufs) cudaFree(d);
+  return s;
+}
+
+pnpula_status pnpula_get_state(pnpula_ctx *c, float *x, float *z, int64_t *t, int32_t scope) {
+  pnpula_status s = check_ctx(c);
+  if (s) return s;
+  CU(c, cudaSetDevice(c->device));
+  const bool global = scope == PNPULA_SCOPE_GLOBAL_ON_ROOT;
+  if (t) *t = c->t;
+  std::vector<const float *> xs;
+  for (auto &td : c->tiles) xs.push_back(td.x[c->cur]);
+  s = gather_padded_interiors(c, xs, x, global);
+  if (s) return s;
+  if (c->rho > 0) {
+    std::vector<const float *> zs;
+    for (auto &td : c->tiles) zs.push_back(td.z);
+    s = gather_padded_interiors(c, zs, z, global);
+  } else if (z && (!global || c->rank == 0)) {
+    pnpula_rect d = global ? pnpula_rect{0, 0, c->ny, c->nx} : c->bbox;
+    memset(z, 0, (size_t)d.h * d.w * sizeof(float));
+  }
+  return s;
+}
+
+pnpula_status pnpula_get_padded_x(pnpula_ctx *c, int32_t li, float *out) {
+  pnpula_status s = check_ctx(c);
+  if (s) return s;
+  if (li < 0 || li >= c->n_local || !out) { set_error("bad tile index / null output"); return PNPULA_E_INVALID_ARG; }
+  CU(c, cudaSetDevice(c->device));
+  const TileGeom &g = c->tiles[li].g;
+  const int w = g.tw + 2 * g.h;
+  CU(c, cudaMemcpy2DAsync(out, (size_t)w * sizeof(float), c->tiles[li].x[c->cur] + (g.hx - g.h),
+                          (size_t)g.pitch * sizeof(float), (size_t)w * sizeof(float), g.ph,
+                          cudaMemcpyDeviceToHost, c->stream));
+  CU(c, cudaStreamSynchronize(c->stream));
+  return PNPULA_OK;
+}
+
+pnpula_status pnpula_get_denoiser_residual(pnpula_ctx *c, float *G) {
+  pnpula_status s = check_ctx(c);
+  if (s) return s;
+  if (c->n_layers == 0) { set_error("no denoiser configured"); return PNPULA_E_STATE; }
+  if (!c->have_reset) { set_error("pnpula_reset must precede this call"); return PNPULA_E_STATE; }
+  CU(c, cudaSetDevice(c->device));
+  s = run_cnn(c, c->cur);
+  if (s) return s;
+  s = pnpula_synchronize(c);
+  if (s) return s;
+  std::vector<const float *> gs;
+  for (auto &td : c->tiles) gs.push_back(td.G);
+  return gather_padded_interiors(c, gs, G, false);
+}
+
+pnpula_status pnpula_set_timing(pnpula_ctx *c, int32_t enable) {
+  pnpula_status s = check_ctx(c);
+  if (s) return s;
+  c->timing = enable != 0;
+  return PNPULA_OK;
+}
+
+pnpula_status pnpula_kernel_time(pnpula_ctx *c, const char *name, double *ms, int64_t *launches, int32_t reset) {
+  pnpula_status s = check_ctx(c);
+  if (s) return s;
+  Timer *t = nullptr;
+  if (!name) { set_error("null name"); return PNPULA_E_INVALID_ARG; }
+  if (!strcmp(name, "cnn")) t = &c->tm_cnn;
+  else if (!strcmp(name, "update")) t = &c->tm_update;
+  else if (!strcmp(name, "halo")) t = &c->tm_halo;
+  else { set_error("unknown timer '%s'", name); return PNPULA_E_INVALID_ARG; }
+  timer_collect(*t);
+  if (ms) *ms = t->ms;
+  if (launches) *launches = t->launches;
+  if (reset) { t->ms = 0; t->launches = 0; }
+  return PNPULA_OK;
+}
+
+pnpula_status pnpula_destroy(pnpula_ctx *c) {
+  if (!c) return PNPULA_OK;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  for (auto &td : c->tiles) {
+    cudaFree(td.x[0]); cudaFree(td.x[1]); cudaFree(td.x0); cudaFree(td.y); cudaFree(td.mask);
+    cudaFree(td.z); cudaFree(td.mean); cudaFree(td.m2); cudaFree(td.G);
+    cudaFree(td.act[0]); cudaFree(td.act[1]);
+  }
+  for (auto p : c->d_w) cudaFree(p);
+  for (auto p : c->d_b) cudaFree(p);
+  for (int b = 0; b < 2; ++b) {
+    cudaFree(c->d_local_jobs[b]); cudaFree(c->d_pack_jobs[b]); cudaFree(c->d_unpack_jobs[b]);
+  }
+  cudaFree(c->d_sendbuf); cudaFree(c->d_recvbuf); cudaFree(c->d_err);
+  for (Timer *t : {&c->tm_cnn, &c->tm_update, &c->tm_halo})
+    for (auto &e : t->ev) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
+  if (c->comm) ncclCommDestroy(c->comm);
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return PNPULA_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,393 @@
+// update_kernels.cu -- K7: the fused, memory-bound part of one PnP-ULA iteration
+// (Algorithm 1 lines 6-13) for one tile, plus halo copy / fill /
+// moment-finalisation helpers.  sm_100a.
+//
+// Per owned pixel (i, j) the kernel computes, in this fixed order (fp32):
+//   r   = (H1 x - y) on tile (+) r_H (zero outside the image)   P:612 (true conv, zero BC)
+//   g   = H1^T r                                                 P:612, P:619 (owner computes its
+//                                                                 whole adjoint: no overlap-add)
+//   x+  = x - a_g g - a_rho (x - z) - a_d G + a_lam (clamp(x) - x) + a_xi xi
+//   z+  = clamp(z - b_rho (z - x+) + b_zeta zeta, z_lo, z_hi)
+//   Welford(mean, M2; x+) if t+1 > burn_in
+// with a_g = gamma/sigma2, a_rho = gamma/rho, a_d = alpha gamma/eps^2, a_lam = gamma/lambda,
+// a_xi = sqrt(2 gamma), b_rho = kappa/rho, b_zeta = sqrt(2 kappa).
+// xi, zeta: Philox4x32-10 (key = seed, counter = (j>>2, i, t+1, stream)) + Box-Muller.
+//
+// The stencil is staged through shared memory: a block owns a 32 x 64 output
+// block, loads x on the block (+) 2 r_H once, and runs the separable (4 passes of
+// L taps) or general 2-D (2 passes of L^2 taps) forward/adjoint stencil there.
+// Every pixel's arithmetic is independent of the block / tile it lands in, so the
+// chain is bitwise identical for any tile grid.
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "internal.h"
+
+namespace pnpula {
+
+namespace {
+
+constexpr int TY = 32;            // output rows per block
+constexpr int TX = 64;            // output columns per block (16 quads)
+constexpr int NTHREADS = 256;
+
+// ---------------------------------------------------------------- Philox4x32-10
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t lo0 = 0xD2511F53u * c.x;
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c.x);
+    const uint32_t lo1 = 0xCD9E8D57u * c.z;
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z);
+    c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  return c;
+}
+
+// ln(u), u = (U + 0.5) 2^-32, accurate for u near 0 and near 1.
+__device__ __forceinline__ float log_unit(uint32_t U) {
+  if (U < 0x80000000u) {
+    return logf(fmaf((float)U, 0x1p-32f, 0x1p-33f));
+  }
+  const float v = fmaf((float)(~U), 0x1p-32f, 0x1p-33f);   // 1 - u
+  return log1pf(-v);
+}
+
+// Box-Muller pair from (Ua, Ub): (rho cos theta, rho sin theta), theta = 2 pi (Ub+0.5) 2^-32,
+// evaluated as pi * x with x = ((int)Ub + 0.5) 2^-31 in (-1, 1) (same angle mod 2 pi).
+__device__ __forceinline__ float2 box_muller(uint32_t Ua, uint32_t Ub) {
+  const float rho = sqrtf(-2.0f * log_unit(Ua));
+  const float xs = fmaf((float)(int32_t)Ub, 0x1p-31f, 0x1p-32f);
+  float s, c;
+  sincospif(xs, &s, &c);
+  return make_float2(rho * c, rho * s);
+}
+
+__device__ __forceinline__ void normals4(uint32_t seed_lo, uint32_t seed_hi, uint32_t quad,
+                                         uint32_t row, uint32_t t1, uint32_t stream, float out[4]) {
+  const uint4 w = philox4x32_10(make_uint4(quad, row, t1, stream), seed_lo, seed_hi);
+  const float2 a = box_muller(w.x, w.y);
+  const float2 b = box_muller(w.z, w.w);
+  out[0] = a.x; out[1] = a.y; out[2] = b.x; out[3] = b.y;
+}
+
+__device__ __forceinline__ int64_t pidx(const TileGeom &g, int gi, int gj) {
+  return (int64_t)(gi - (g.i0 - g.h)) * g.pitch + (gj - (g.j0 - g.hx));
+}
+
+// Elementwise tail of K7 for one quad of 4 horizontally adjacent pixels starting at
+// global column gj4 (multiple of 4) in row gi; gr[] = H1^T(H1 x - y) (unscaled).
+__device__ __forceinline__ void ula_quad(const UpdateParams &p, int gi, int gj4, const float gr[4]) {
+  const TileGeom &g = p.g;
+  const int64_t base = pidx(g, gi, gj4);
+  const bool full = gj4 >= g.j0 && gj4 + 4 <= g.j0 + g.tw;
+  float xv[4], Gv[4] = {0.f, 0.f, 0.f, 0.f}, zv[4] = {0.f, 0.f, 0.f, 0.f}, mv[4], sv[4];
+  if (full) {
+    const float4 a = *reinterpret_cast<const float4 *>(p.x + base);
+    xv[0] = a.x; xv[1] = a.y; xv[2] = a.z; xv[3] = a.w;
+    if (p.has_G) {
+      const float4 b = *reinterpret_cast<const float4 *>(p.G + base);
+      Gv[0] = b.x; Gv[1] = b.y; Gv[2] = b.z; Gv[3] = b.w;
+    }
+    if (p.has_z) {
+      const float4 b = *reinterpret_cast<const float4 *>(p.z + base);
+      zv[0] = b.x; zv[1] = b.y; zv[2] = b.z; zv[3] = b.w;
+    }
+  } else {
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+      xv[l] = p.x[base + l];
+      if (p.has_G) Gv[l] = p.G[base + l];
+      if (p.has_z) zv[l] = p.z[base + l];
+    }
+  }
+  float xi[4];
+  normals4(p.seed_lo, p.seed_hi, (uint32_t)gj4 >> 2, (uint32_t)gi, p.t1, 0u, xi);
+  float xn[4];
+#pragma unroll
+  for (int l = 0; l < 4; ++l) {
+    float v = xv[l] - p.a_g * gr[l];
+    if (p.has_z) v -= p.a_rho * (xv[l] - zv[l]);
+    if (p.has_G) v += p.a_d * (-Gv[l]);
+    if (p.has_box) v += p.a_lam * (fminf(fmaxf(xv[l], p.c_lo), p.c_hi) - xv[l]);
+    v += p.a_xi * xi[l];
+    xn[l] = v;
+  }
+  float zn[4];
+  if (p.has_z) {
+    float ze[4];
+    normals4(p.seed_lo, p.seed_hi, (uint32_t)gj4 >> 2, (uint32_t)gi, p.t1, 1u, ze);
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+      const float v = zv[l] - p.b_rho * (zv[l] - xn[l]) + p.b_zeta * ze[l];
+      zn[l] = fminf(fmaxf(v, p.z_lo), p.z_hi);
+    }
+  }
+  if (p.accumulate) {
+    if (full) {
+      const float4 a = *reinterpret_cast<const float4 *>(p.mean + base);
+      const float4 b = *reinterpret_cast<const float4 *>(p.m2 + base);
+      mv[0] = a.x; mv[1] = a.y; mv[2] = a.z; mv[3] = a.w;
+      sv[0] = b.x; sv[1] = b.y; sv[2] = b.z; sv[3] = b.w;
+    } else {
+#pragma unroll
+      for (int l = 0; l < 4; ++l) { mv[l] = p.mean[base + l]; sv[l] = p.m2[base + l]; }
+    }
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+      const float d = xn[l] - mv[l];
+      mv[l] = mv[l] + d * p.inv_n;
+      sv[l] = sv[l] + d * (xn[l] - mv[l]);
+    }
+  }
+  if (full) {
+    *reinterpret_cast<float4 *>(p.xn + base) = make_float4(xn[0], xn[1], xn[2], xn[3]);
+    if (p.has_z) *reinterpret_cast<float4 *>(p.z + base) = make_float4(zn[0], zn[1], zn[2], zn[3]);
+    if (p.accumulate) {
+      *reinterpret_cast<float4 *>(p.mean + base) = make_float4(mv[0], mv[1], mv[2], mv[3]);
+      *reinterpret_cast<float4 *>(p.m2 + base) = make_float4(sv[0], sv[1], sv[2], sv[3]);
+    }
+  } else {
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+      const int gj = gj4 + l;
+      if (gj < g.j0 || gj >= g.j0 + g.tw) continue;
+      p.xn[base + l] = xn[l];
+      if (p.has_z) p.z[base + l] = zn[l];
+      if (p.accumulate) { p.mean[base + l] = mv[l]; p.m2[base + l] = sv[l]; }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- conv K7
+// RY/RX >= 0: compile-time radii; -1: runtime (p.ry, p.rx).
+template <int RY_, int RX_, bool SEP>
+__global__ void __launch_bounds__(NTHREADS)
+update_conv_kernel(const __grid_constant__ UpdateParams p) {
+  extern __shared__ float smem[];
+  const int RY = RY_ >= 0 ? RY_ : p.ry;
+  const int RX = RX_ >= 0 ? RX_ : p.rx;
+  const TileGeom &g = p.g;
+  const int bi0 = g.i0 + blockIdx.y * TY;
+  const int bj0 = (g.j0 & ~3) + blockIdx.x * TX;
+  const int XR = TY + 4 * RY, XC = TX + 4 * RX;     // x region
+  const int RR = TY + 2 * RY, RC = TX + 2 * RX;     // residual region
+  float *X = smem;                                   // XR x XC
+  float *T1 = X + XR * XC;                           // XR x RC   (separable only)
+  float *Rr = SEP ? T1 + XR * RC : T1;               // RR x RC
+  float *T2 = X;                                     // RR x TX   (reuses X, separable only)
+  const int tid = threadIdx.x;
+
+  // phase 0: x on block (+) 2 r_H, zero outside the padded buffer
+  for (int e = tid; e < XR * XC; e += NTHREADS) {
+    const int a = e / XC, b = e - a * XC;
+    const int pr = bi0 - 2 * RY + a - (g.i0 - g.h);
+    const int pc = bj0 - 2 * RX + b - (g.j0 - g.hx);
+    float v = 0.f;
+    if (pr >= 0 && pr < g.ph && pc >= 0 && pc < g.pitch) v = p.x[(int64_t)pr * g.pitch + pc];
+    X[e] = v;
+  }
+  __syncthreads();
+
+  if (SEP) {
+    // phase 1: horizontal forward pass  T1[a][b] = sum_q kx[q] X[a][b + RX - q]
+    for (int e = tid; e < XR * RC; e += NTHREADS) {
+      const int a = e / RC, b = e - a * RC;
+      const float *xr = X + a * XC + b + RX;
+      float s = 0.f;
+#pragma unroll
+      for (int q = -RX; q <= RX; ++q) s = fmaf(p.kx[q + RX], xr[-q], s);
+      T1[e] = s;
+    }
+    __syncthreads();
+    // phase 2: vertical forward pass minus y -> residual (zero outside the image)
+    for (int e = tid; e < RR * RC; e += NTHREADS) {
+      const int a = e / RC, b = e - a * RC;
+      const int gi = bi0 - RY + a, gj = bj0 - RX + b;
+      float s = 0.f;
+#pragma unroll
+      for (int q = -RY; q <= RY; ++q) s = fmaf(p.ky[q + RY], T1[(a + RY - q) * RC + b], s);
+      float r = 0.f;
+      if (gi >= 0 && gi < p.ny && gj >= 0 && gj < p.nx) {
+        const int pr = gi - (g.i0 - g.h), pc = gj - (g.j0 - g.hx);
+        const float yv = (pr >= 0 && pr < g.ph && pc >= 0 && pc < g.pitch) ? p.y[(int64_t)pr * g.pitch + pc] : 0.f;
+        r = s - yv;
+      }
+      Rr[e] = r;
+    }
+    __syncthreads();
+    // phase 3: horizontal adjoint pass  T2[a][b] = sum_q kx[q] Rr[a][b + RX + q]
+    for (int e = tid; e < RR * TX; e += NTHREADS) {
+      const int a = e / TX, b = e - a * TX;
+      const float *rr = Rr + a * RC + b + RX;
+      float s = 0.f;
+#pragma unroll
+      for (int q = -RX; q <= RX; ++q) s = fmaf(p.kx[q + RX], rr[q], s);
+      T2[e] = s;
+    }
+    __syncthreads();
+  } else {
+    // phase 2': residual with the 2-D kernel
+    for (int e = tid; e < RR * RC; e += NTHREADS) {
+      const int a = e / RC, b = e - a * RC;
+      const int gi = bi0 - RY + a, gj = bj0 - RX + b;
+      float r = 0.f;
+      if (gi >= 0 && gi < p.ny && gj >= 0 && gj < p.nx) {
+        float s = 0.f;
+        for (int q1 = -RY; q1 <= RY; ++q1) {
+          const float *xr = X + (a + RY - q1) * XC + b + RX;
+          const float *kr = p.k2d + (q1 + RY) * (2 * RX + 1) + RX;
+#pragma unroll 5
+          for (int q2 = -RX; q2 <= RX; ++q2) s = fmaf(kr[q2], xr[-q2], s);
+        }
+        const int pr = gi - (g.i0 - g.h), pc = gj - (g.j0 - g.hx);
+        const float yv = (pr >= 0 && pr < g.ph && pc >= 0 && pc < g.pitch) ? p.y[(int64_t)pr * g.pitch + pc] : 0.f;
+        r = s - yv;
+      }
+      Rr[e] = r;
+    }
+    __syncthreads();
+  }
+
+  // phase 4: vertical adjoint pass (or 2-D adjoint) + elementwise update, one quad per thread-row
+  const int qx = tid & 15;
+  for (int rr = tid >> 4; rr < TY; rr += NTHREADS / 16) {
+    const int gi = bi0 + rr;
+    const int gj4 = bj0 + 4 * qx;
+    if (gi >= g.i0 + g.th || gj4 >= g.j0 + g.tw || gj4 + 4 <= g.j0) continue;
+    float gr[4];
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+      const int b = 4 * qx + l;
+      float s = 0.f;
+      if (SEP) {
+#pragma unroll
+        for (int q = -RY; q <= RY; ++q) s = fmaf(p.ky[q + RY], T2[(rr + RY + q) * TX + b], s);
+      } else {
+        for (int q1 = -RY; q1 <= RY; ++q1) {
+          const float *rw = Rr + (rr + RY + q1) * RC + b + RX;
+          const float *kr = p.k2d + (q1 + RY) * (2 * RX + 1) + RX;
+#pragma unroll 5
+          for (int q2 = -RX; q2 <= RX; ++q2) s = fmaf(kr[q2], rw[q2], s);
+        }
+      }
+      gr[l] = s;
+    }
+    ula_quad(p, gi, gj4, gr);
+  }
+}
+
+// ---------------------------------------------------------------- mask K7 (no stencil)
+__global__ void __launch_bounds__(NTHREADS) update_mask_kernel(const __grid_constant__ UpdateParams p) {
+  const TileGeom &g = p.g;
+  const int nq = ((g.j0 + g.tw + 3) >> 2) - (g.j0 >> 2);
+  const int64_t total = (int64_t)nq * g.th;
+  for (int64_t e = (int64_t)blockIdx.x * NTHREADS + threadIdx.x; e < total; e += (int64_t)gridDim.x * NTHREADS) {
+    const int rr = (int)(e / nq), q = (int)(e - (int64_t)rr * nq);
+    const int gi = g.i0 + rr, gj4 = (g.j0 & ~3) + 4 * q;
+    const int64_t base = pidx(g, gi, gj4);
+    float gr[4];
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+      const float m = p.mask[base + l] ? 1.f : 0.f;
+      gr[l] = m * (m * p.x[base + l] - p.y[base + l]);
+    }
+    ula_quad(p, gi, gj4, gr);
+  }
+}
+
+__global__ void copy_jobs_kernel(const CopyJob *__restrict__ jobs) {
+  const CopyJob j = jobs[blockIdx.y];
+  const int64_t n = (int64_t)j.rows * j.cols;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(e / j.cols), c = (int)(e - (int64_t)r * j.cols);
+    j.dst[(int64_t)r * j.dst_pitch + c] = j.src[(int64_t)r * j.src_pitch + c];
+  }
+}
+
+__global__ void fill_kernel(float *p, float v, size_t n) {
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x) p[e] = v;
+}
+
+__global__ void finalize_kernel(const FinalizeParams p) {
+  const TileGeom &g = p.g;
+  const int64_t n = (int64_t)g.th * g.tw;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(e / g.tw), c = (int)(e - (int64_t)r * g.tw);
+    const int64_t s = (int64_t)(r + g.h) * g.pitch + (c + g.hx);
+    if (p.out_mean) p.out_mean[e] = p.mean[s];
+    if (p.out_var) p.out_var[e] = p.m2[s] * p.inv_nm1;
+  }
+}
+
+template <int RY, int RX, bool SEP>
+cudaError_t launch_conv(const UpdateParams &p, cudaStream_t s) {
+  const int ry = RY >= 0 ? RY : p.ry, rx = RX >= 0 ? RX : p.rx;
+  const int XR = TY + 4 * ry, XC = TX + 4 * rx, RR = TY + 2 * ry, RC = TX + 2 * rx;
+  size_t smem = (size_t)XR * XC + (SEP ? (size_t)XR * RC : 0) + (size_t)RR * RC;
+  if (SEP && (size_t)RR * TX > (size_t)XR * XC) return cudaErrorInvalidValue;
+  smem *= sizeof(float);
+  auto kfn = update_conv_kernel<RY, RX, SEP>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  const int cols = p.g.j0 + p.g.tw - (p.g.j0 & ~3);
+  dim3 grid((cols + TX - 1) / TX, (p.g.th + TY - 1) / TY);
+  kfn<<<grid, NTHREADS, smem, s>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_update(const UpdateParams &p, cudaStream_t s) {
+  if (p.op == 1) {
+    const int nq = ((p.g.j0 + p.g.tw + 3) >> 2) - (p.g.j0 >> 2);
+    const int64_t total = (int64_t)nq * p.g.th;
+    int blocks = (int)((total + NTHREADS - 1) / NTHREADS);
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    if (blocks < 1) blocks = 1;
+    update_mask_kernel<<<blocks, NTHREADS, 0, s>>>(p);
+    return cudaGetLastError();
+  }
+  if (p.separable) {
+    if (p.ry == 4 && p.rx == 4) return launch_conv<4, 4, true>(p, s);
+    if (p.ry == 2 && p.rx == 2) return launch_conv<2, 2, true>(p, s);
+    return launch_conv<-1, -1, true>(p, s);
+  }
+  if (p.ry == 2 && p.rx == 2) return launch_conv<2, 2, false>(p, s);
+  if (p.ry == 4 && p.rx == 4) return launch_conv<4, 4, false>(p, s);
+  return launch_conv<-1, -1, false>(p, s);
+}
+
+cudaError_t launch_copy_jobs(const CopyJob *d_jobs, int njobs, int max_elems, cudaStream_t s) {
+  if (njobs == 0) return cudaSuccess;
+  int bx = (max_elems + 255) / 256;
+  if (bx > 64) bx = 64;
+  if (bx < 1) bx = 1;
+  copy_jobs_kernel<<<dim3(bx, njobs), 256, 0, s>>>(d_jobs);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fill(float *ptr, float v, size_t n, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  size_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  fill_kernel<<<(unsigned)blocks, 256, 0, s>>>(ptr, v, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_finalize(const FinalizeParams &p, cudaStream_t s) {
+  const int64_t n = (int64_t)p.g.th * p.g.tw;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  if (blocks < 1) blocks = 1;
+  finalize_kernel<<<(unsigned)blocks, 256, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace pnpula
