@@ -48,17 +48,28 @@ def ground_truth(ny: int, nx: int, rect=None, seed: int = GT_SEED) -> np.ndarray
     Pixels outside [0,ny)x[0,nx) are returned as 0 (zero boundary)."""
     i0, j0, h, w = rect if rect is not None else (0, 0, ny, nx)
     amps, freqs, phases, centers, radii, vals = _gt_params(seed)
-    ii = (np.arange(i0, i0 + h, dtype=np.float64) / ny)[:, None]
-    jj = (np.arange(j0, j0 + w, dtype=np.float64) / nx)[None, :]
+    ii = np.arange(i0, i0 + h, dtype=np.float64) / ny
+    jj = np.arange(j0, j0 + w, dtype=np.float64) / nx
     out = np.full((h, w), 0.5, dtype=np.float64)
     for a, f, ph in zip(amps, freqs, phases):
-        out += a * np.cos(2 * np.pi * (f[0] * ii + f[1] * jj) + ph)
+        # cos(A_i + B_j) = cos A_i cos B_j - sin A_i sin B_j  (outer products)
+        A = 2 * np.pi * f[0] * ii + ph
+        B = 2 * np.pi * f[1] * jj
+        out += a * (np.outer(np.cos(A), np.cos(B)) - np.outer(np.sin(A), np.sin(B)))
     for c, r, v in zip(centers, radii, vals):
-        out += v * (((ii - c[0]) ** 2 + (jj - c[1]) ** 2) < r * r)
+        a0 = max(int(np.floor((c[0] - r) * ny)) - i0 - 1, 0)
+        a1 = min(int(np.ceil((c[0] + r) * ny)) - i0 + 2, h)
+        b0 = max(int(np.floor((c[1] - r) * nx)) - j0 - 1, 0)
+        b1 = min(int(np.ceil((c[1] + r) * nx)) - j0 + 2, w)
+        if a0 >= a1 or b0 >= b1:
+            continue
+        d2 = (ii[a0:a1, None] - c[0]) ** 2 + (jj[None, b0:b1] - c[1]) ** 2
+        out[a0:a1, b0:b1] += v * (d2 < r * r)
     np.clip(out, 0.0, 1.0, out=out)
-    inside = ((np.arange(i0, i0 + h) >= 0) & (np.arange(i0, i0 + h) < ny))[:, None] & \
-             ((np.arange(j0, j0 + w) >= 0) & (np.arange(j0, j0 + w) < nx))[None, :]
-    out[~inside] = 0.0
+    ri = np.arange(i0, i0 + h)
+    rj = np.arange(j0, j0 + w)
+    out[(ri < 0) | (ri >= ny), :] = 0.0
+    out[:, (rj < 0) | (rj >= nx)] = 0.0
     return out.astype(np.float32)
 
 
