@@ -1,0 +1,396 @@
+#!/usr/bin/env python
+"""Benchmark of the distributed PnP-ULA hot path (arXiv 2511.00870) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c5|c2|c3|c4|c1] [--impl ours|reference]
+
+For N > 1 launch with torchrun (one rank per GPU); rank 0 prints ONE JSON line.
+
+A "step" is one full iteration of Algorithm 1 over the whole image: CNN
+prior (tcgen05 kernels), fused stencil/prox/ULA/Philox/Welford update, halo exchange.
+metric = Mpixel-iterations/s = ny*nx*K / (max over ranks of the device time of K steps).
+
+Default workload c5 (BASELINE.json configs[4], the metric's headline): weak scaling
+with a fixed 4096x8192 shard per GPU -- N=1: 4096x8192, 2: 8192^2, 4: 8192x16384,
+8: 16384^2 (the 16384^2 deblurring chain), 9x9 Gaussian blur, 25 dB, DnCNN-lite
+8x32 random-init denoiser, row-strip tiles.  Inputs are synthetic (synth/), resident
+in HBM before the timed region; the working set (>10 GB per GPU) exceeds the 126 MB L2.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CNN_MAC_PER_PX = {(8, 32): 55872, (4, 16): 4896}
+
+
+def cnn_macs(K, P):
+    return P * 9 + (K - 2) * P * P * 9 + P * 9
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=60)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="c5", choices=["c5", "c2", "c3", "c4", "c1"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--flags", type=int, default=0)
+    ap.add_argument("--seed", type=int, default=870)
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------- workloads
+def workload(name, n):
+    """Global problem description for N ranks (no arrays)."""
+    if name == "c5":
+        shapes = {1: (4096, 8192), 2: (8192, 8192), 4: (8192, 16384), 8: (16384, 16384)}
+        ny, nx = shapes.get(n, (4096 * n, 8192))
+        return dict(name="c5", desc="weak scaling, 4096x8192 px per GPU (16384^2 at 8 GPUs), 9x9 Gaussian "
+                    "deblur 25 dB, DnCNN-lite 8x32", ny=ny, nx=nx, tiles=(n, 1), op="conv", L=9, sb=2.0,
+                    cnn=(8, 32), z=False, scaling="weak")
+    if name == "c2":
+        return dict(name="c2", desc="1024x1024 deblur, 9x9 Gaussian blur, DnCNN-lite 8x32", ny=1024, nx=1024,
+                    tiles=(n, 1), op="conv", L=9, sb=2.0, cnn=(8, 32), z=False, scaling="strong")
+    if name == "c3":
+        return dict(name="c3", desc="4096x4096 random-mask inpainting (30%), box prox + AXDA z-block, "
+                    "DnCNN-lite 8x32", ny=4096, nx=4096, tiles=(n, 1), op="mask", cnn=(8, 32), z=True,
+                    scaling="strong")
+    if name == "c4":
+        return dict(name="c4", desc="2048x2048 linear-Gaussian posterior (9x9 blur, no denoiser)", ny=2048,
+                    nx=2048, tiles=(n, 1), op="conv", L=9, sb=2.0, cnn=None, z=False, scaling="strong")
+    return dict(name="c1", desc="64x64 deblur, 5x5 Gaussian blur, 2x2 tiles, 4-layer 16-ch CNN", ny=64, nx=64,
+                tiles=(2, 2), op="conv", L=5, sb=1.0, cnn=(4, 16), z=False, scaling="strong")
+
+
+def build_inputs(wl, rect, pinned=False):
+    """Sampler kwargs for the rectangle rect of the global image (y / mask cover rect)."""
+    import synth
+    from paper_2511_00870_b200 import params
+    ny, nx = wl["ny"], wl["nx"]
+    kw = {}
+    if wl["op"] == "conv":
+        ky, kx = synth.gaussian_factors(wl["L"], wl["sb"])
+        k2 = synth.outer(ky, kx)
+        s2 = synth.noise_sigma2_blur(ny, nx, k2, 25.0)
+        y = synth.observe_blur(ny, nx, k2, s2, rect)
+        kw.update(kernel_sep=(ky, kx))
+    else:
+        s2 = synth.noise_sigma2_mask(ny, nx, 15.0)
+        y, m = synth.observe_mask(ny, nx, s2, rect=rect)
+        kw.update(op="mask", mask=m)
+    if wl["name"] == "c4":
+        hp = dict(gamma=0.99 / 120, lam=0.05)
+        s2 = 1e-2
+        kw.update(lam=0.05, c_lo=0.5, c_hi=0.5)
+    else:
+        hp = params.gaussian_pnp(s2, 1.0, 1.0, rho=1e-3 if wl["z"] else 0.0)
+        kw.update(lam=hp["lam"], c_lo=0.0, c_hi=1.0)
+        if wl["z"]:
+            kw.update(rho=hp["rho"], kappa=hp["kappa"], z_lo=0.0, z_hi=1.0)
+    if wl["cnn"]:
+        K, P = wl["cnn"]
+        w, b = synth.dncnn_weights(K, P)
+        kw.update(weights=w, biases=b, n_layers=K, channels=P, alpha=1.0, eps=float(np.sqrt(s2)))
+    if pinned:
+        import torch
+        t = torch.empty(y.shape, dtype=torch.float32, pin_memory=True)
+        t.numpy()[...] = y
+        y = t.numpy()
+        kw["_pin"] = t
+    kw.update(ny=ny, nx=nx, y=y, sigma2=s2, gamma=hp["gamma"], in_rect=rect)
+    return kw
+
+
+def rank_rect(wl, rank, world):
+    from paper_2511_00870_b200 import pnpula_halo_width, pnpula_partition
+    ty, tx = wl["tiles"]
+    nt = ty * tx
+    per = nt // world
+    i0 = j0 = 1 << 30
+    i1 = j1 = -1
+    for t in range(rank * per, (rank + 1) * per):
+        a, b = pnpula_partition(wl["ny"], ty, t // tx)
+        c, d = pnpula_partition(wl["nx"], tx, t % tx)
+        i0, i1, j0, j1 = min(i0, a), max(i1, b), min(j0, c), max(j1, d)
+    r = wl.get("L", 0) // 2
+    a0, a1 = max(i0 - r, 0), min(i1 + r, wl["ny"])
+    b0, b1 = max(j0 - r, 0), min(j1 + r, wl["nx"])
+    return (a0, b0, a1 - a0, b1 - b0), (i1 - i0) * (j1 - j0)
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = "clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown," \
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown," \
+             "clocks_event_reasons.sw_power_cap"
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
+    def __init__(self, device):
+        self.device = device
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                       "-lms", "100", "-i", str(self.device)], stdout=subprocess.PIPE,
+                                      stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.p.terminate()
+        out, _ = self.p.communicate(timeout=10)
+        sm, mx, pw, reasons = [], [], [], set()
+        for ln in out.strip().splitlines():
+            f = [v.strip() for v in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0])); mx.append(float(f[1])); pw.append(float(f[2]))
+            except ValueError:
+                continue
+            for name, v in zip(self.NAMES, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "power_w_max": max(pw) if pw else None, "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get("hbm_gbs", 6650.0), d.get("bf16_tflops_sustained", 1590.0), d.get("bf16_tflops", 1590.0), \
+            "measured (MEASURED_PEAKS.json)"
+    return 6650.0, 1590.0, 1590.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic():
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    return json.load(open(p)) if os.path.exists(p) else {}
+
+
+# ---------------------------------------------------------------- oracle timings (CPU)
+def oracle_crop_problem(wl, size):
+    import oracle
+    ny, nx = wl["ny"], wl["nx"]
+    i0, j0 = (ny - size) // 2, (nx - size) // 2
+    kw = build_inputs(wl, (i0, j0, size, size))
+    okw = {k: v for k, v in kw.items() if k in ("sigma2", "gamma", "mask", "weights", "biases", "n_layers",
+                                                "channels", "alpha", "eps", "lam", "c_lo", "c_hi", "rho", "kappa",
+                                                "z_lo", "z_hi")}
+    if "kernel_sep" in kw:
+        okw.update(op="conv", ksep=kw["kernel_sep"])
+    else:
+        okw.update(op="mask")
+    return oracle.Problem(y=kw["y"], **okw), (i0, j0)
+
+
+def time_oracle(wl, size, n_iter, warm=0):
+    import oracle
+    pb, origin = oracle_crop_problem(wl, size)
+    if warm:
+        oracle.run(pb, warm, 0, 1, want_var=False, origin=origin)
+    t0 = time.perf_counter()
+    oracle.run(pb, n_iter, 0, 1, want_var=False, origin=origin)
+    return time.perf_counter() - t0
+
+
+def reference_arm(args, wl, world, rank):
+    if rank != 0:
+        return
+    size = 64 if wl["cnn"] else 256
+    dt = time_oracle(wl, size, args.steps, warm=args.warmup)
+    val = size * size * args.steps / dt / 1e6
+    line = {"impl": "reference", "metric": "Mpixel-iterations/s", "value": val, "unit": "Mpx-it/s",
+            "higher_is_better": True, "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": dt * 1e3 / args.steps, "scaling": wl["scaling"], "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{wl['name']}: {wl['desc']}", "image": [wl["ny"], wl["nx"]],
+                       "reference_sample": f"{size}x{size} central crop per step"},
+            "vs_baseline": None,
+            "cpu_baseline": {"value": val, "unit": "Mpx-it/s", "cores": 1, "kind": "oracle",
+                             "sample": f"{size}x{size} central crop of the {wl['name']} workload, "
+                                       f"{args.warmup} untimed + {args.steps} timed iterations, plain C fp64, 1 thread"},
+            "e2e": {"value": val, "unit": "Mpx-it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- our arm
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        if world == 1 and args.gpus > 1:
+            sys.exit("for --gpus > 1 launch with torchrun (one rank per GPU)")
+    wl = workload(args.workload, world)
+    if args.impl == "reference":
+        reference_arm(args, wl, world, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("cpu:gloo,cuda:nccl", rank=rank, world_size=world)
+    from paper_2511_00870_b200 import Sampler, build, pnpula_get_unique_id
+    build.build()
+
+    uid = None
+    if world > 1:
+        obj = [pnpula_get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+
+    rect, own_px = rank_rect(wl, rank, world)
+    t_gen = time.perf_counter()
+    kw = build_inputs(wl, rect)
+    t_gen = time.perf_counter() - t_gen
+    stream = torch.cuda.current_stream()
+    common = dict(tiles=wl["tiles"], rank=rank, world_size=world, device=local, nccl_uid=uid,
+                  stream=stream.cuda_stream, flags=args.flags)
+    kw.pop("_pin", None)
+    s = Sampler(**kw, **common)
+    K, W = args.steps, args.warmup
+    s.reset(W, args.seed)
+    s.advance(W)
+    s.synchronize()
+    s.set_timing(True)
+    for name in ("cnn", "update", "halo", "all"):
+        s.kernel_time(name, reset=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    s.advance(K)
+    e1.record(stream)
+    e1.synchronize()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    s.synchronize()
+    cnn_ms, cnn_n = s.kernel_time("cnn")
+    upd_ms, upd_n = s.kernel_time("update")
+    halo_ms, halo_n = s.kernel_time("halo")
+    _, launches = s.kernel_time("all")
+    s.set_timing(False)
+    _, _, n_samples = s.moments(want_var=False)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    px = wl["ny"] * wl["nx"]
+    value = px * K / (ms * 1e-3) / 1e6
+
+    # ---------------- e2e through the public API with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        kw2 = build_inputs(wl, rect, pinned=True)
+        pin = kw2.pop("_pin")
+        if world > 1:
+            obj = [pnpula_get_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            common["nccl_uid"] = obj[0]
+            dist.barrier()
+        s.close()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        s2 = Sampler(**kw2, **common)
+        s2.reset(0, args.seed)
+        s2.advance(K)
+        mean, var, _ = s2.moments()
+        t1 = time.perf_counter()
+        s2.close()
+        dt = t1 - t0
+        if world > 1:
+            t = torch.tensor([dt], dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        h2d = pin.numel() * 4 + kw2["weights"].nbytes + kw2["biases"].nbytes if wl["cnn"] else pin.numel() * 4
+        if wl["op"] == "mask":
+            h2d += kw2["mask"].nbytes
+        d2h = (mean.nbytes + var.nbytes)
+        e2e = {"value": px * K / dt / 1e6, "unit": "Mpx-it/s", "h2d_bytes_per_step": int(h2d * world // K),
+               "d2h_bytes_per_step": int(d2h * world // K),
+               "timed": "create (H2D of y/weights from pinned host memory) + reset + K iterations + "
+                        "get_moments (D2H of mean and variance); wall clock, max over ranks"}
+    else:
+        s.close()
+
+    # ---------------- roofline of the dominant kernel (the CNN, tensor-bound) + the update kernel
+    hbm, tf_sus, tf_burst, peak_src = measured_peaks()
+    traffic = ncu_traffic()
+    roof = None
+    if wl["cnn"] and cnn_n:
+        Kc, P = wl["cnn"]
+        flops = 2.0 * cnn_macs(Kc, P) * own_px * K
+        ach = flops / (cnn_ms * 1e-3) / 1e12
+        tpp = traffic.get("cnn_bytes_per_px")
+        roof = {"kernel": "cnn_chunk_kernel (tcgen05, %d launches/iteration)" % (cnn_n // K),
+                "bound": "tensor", "achieved": ach, "peak": tf_sus, "unit": "TFLOP/s", "frac": ach / tf_sus,
+                "traffic": (tpp * own_px) if tpp else None,
+                "share_of_step": cnn_ms / ms if ms else None,
+                "algorithmic": f"2*{cnn_macs(Kc, P)} FLOP/px (2 MAC) x {own_px} px per evaluation",
+                "peak_source": peak_src + " bf16_tflops_sustained"}
+    upd_bytes_px = 32 + (8 if wl["z"] else 0) - (4 if not wl["cnn"] else 0) + (1 if wl["op"] == "mask" else 0)
+    upd_ach = upd_bytes_px * own_px * K / (upd_ms * 1e-3) / 1e9 if upd_ms else None
+    roof_upd = {"kernel": "update (fused stencil/prox/ULA/Philox/Welford)", "bound": "hbm", "achieved": upd_ach,
+                "peak": hbm, "unit": "GB/s", "frac": (upd_ach / hbm) if upd_ach else None,
+                "traffic": (traffic.get("update_bytes_per_px") or 0) * own_px or None,
+                "share_of_step": upd_ms / ms if ms else None,
+                "algorithmic": f"{upd_bytes_px} B/px x {own_px} px per launch"}
+    if roof is None:
+        roof = roof_upd
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        size = 224 if wl["cnn"] else 512
+        its = 2
+        dt = time_oracle(wl, size, its)
+        cpu = {"value": size * size * its / dt / 1e6, "unit": "Mpx-it/s", "cores": 1, "kind": "oracle",
+               "sample": f"{size}x{size} central crop of the {wl['name']} workload, {its} iterations, plain C fp64, "
+                         f"1 thread ({dt:.1f} s)"}
+
+    if rank == 0:
+        line = {"metric": "Mpixel-iterations/s", "value": value, "unit": "Mpx-it/s", "n_gpus": world,
+                "steps": K, "warmup": W, "ms_per_step": ms / K, "higher_is_better": True,
+                "scaling": wl["scaling"] if world > 1 else "weak" if wl["name"] == "c5" else "strong",
+                "vs_baseline": None, "dtype": "bf16", "state_dtype": "f32", "data": "synthetic",
+                "config": {"workload": f"{wl['name']}: {wl['desc']}", "image": [wl["ny"], wl["nx"]],
+                           "tiles": list(wl["tiles"]), "global_batch": 1, "seq_len": None,
+                           "parallelism": f"spatial tiles {wl['tiles'][0]}x{wl['tiles'][1]} over {world} GPU(s)",
+                           "burn_in": W, "samples_accumulated": n_samples,
+                           "l2": "no flush: per-GPU working set > 10 GB >> 126 MB L2",
+                           "input_generation_s": round(t_gen, 1)},
+                "roofline": roof, "roofline_update": roof_upd,
+                "kernel_ms_per_step": {"cnn": cnn_ms / K, "update": upd_ms / K, "halo": halo_ms / K},
+                "gpu_launches": int(launches), "clocks": clk, "e2e": e2e, "cpu_baseline": cpu}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -190,7 +190,8 @@ pnpula_status pnpula_get_denoiser_residual(pnpula_ctx *ctx, float *G);
 
 /* Per-kernel-class device time accumulated since the last call with reset != 0,
  * measured with CUDA events on the launching stream while timing is enabled.
- * name: "cnn", "update", "halo".  ms = total milliseconds, launches = count. */
+ * name: "cnn", "update", "halo" (launches = timed launch groups), or "all": the number
+ * of kernels this library launched (counted even with timing off; ms = 0). */
 pnpula_status pnpula_set_timing(pnpula_ctx *ctx, int32_t enable);
 pnpula_status pnpula_kernel_time(pnpula_ctx *ctx, const char *name, double *ms, int64_t *launches,
                                  int32_t reset);

@@ -105,6 +105,7 @@ struct pnpula_ctx {
   // timing
   bool timing = false;
   Timer tm_cnn, tm_update, tm_halo;
+  int64_t n_launches = 0;   // kernels of this library launched (all classes)
 };
 
 namespace {
@@ -233,6 +234,7 @@ pnpula_status run_cnn(pnpula_ctx *c, int buf) {
       cudaEvent_t end;
       timer_begin(c, c->tm_cnn, &end);
       CU(c, launch_cnn_chunk(p, c->num_sms, c->stream));
+      c->n_launches++;
       timer_end(c, end);
     }
   }
@@ -242,14 +244,14 @@ pnpula_status run_cnn(pnpula_ctx *c, int buf) {
 pnpula_status exchange(pnpula_ctx *c, int buf) {
   cudaEvent_t end;
   timer_begin(c, c->tm_halo, &end);
-  if (c->n_local_jobs) CU(c, launch_copy_jobs(c->d_local_jobs[buf], c->n_local_jobs, c->max_local, c->stream));
+  if (c->n_local_jobs) { CU(c, launch_copy_jobs(c->d_local_jobs[buf], c->n_local_jobs, c->max_local, c->stream)); c->n_launches++; }
   if (!c->sends.empty() || !c->recvs.empty()) {
-    if (c->n_pack) CU(c, launch_copy_jobs(c->d_pack_jobs[buf], c->n_pack, c->max_pack, c->stream));
+    if (c->n_pack) { CU(c, launch_copy_jobs(c->d_pack_jobs[buf], c->n_pack, c->max_pack, c->stream)); c->n_launches++; }
     NC(c, ncclGroupStart());
     for (auto &m : c->sends) NC(c, ncclSend(c->d_sendbuf + m.off, m.count, ncclFloat32, m.peer, c->comm, c->stream));
     for (auto &m : c->recvs) NC(c, ncclRecv(c->d_recvbuf + m.off, m.count, ncclFloat32, m.peer, c->comm, c->stream));
     NC(c, ncclGroupEnd());
-    if (c->n_unpack) CU(c, launch_copy_jobs(c->d_unpack_jobs[buf], c->n_unpack, c->max_unpack, c->stream));
+    if (c->n_unpack) { CU(c, launch_copy_jobs(c->d_unpack_jobs[buf], c->n_unpack, c->max_unpack, c->stream)); c->n_launches++; }
   }
   timer_end(c, end);
   return PNPULA_OK;
@@ -309,6 +311,7 @@ pnpula_status step(pnpula_ctx *c) {
     cudaEvent_t end;
     timer_begin(c, c->tm_update, &end);
     CU(c, launch_update(p, c->stream));
+    c->n_launches++;
     timer_end(c, end);
   }
   pnpula_status s = exchange(c, buf ^ 1);
@@ -955,6 +958,12 @@ pnpula_status pnpula_kernel_time(pnpula_ctx *c, const char *name, double *ms, in
   if (s) return s;
   Timer *t = nullptr;
   if (!name) { set_error("null name"); return PNPULA_E_INVALID_ARG; }
+  if (!strcmp(name, "all")) {   // every kernel this library launched (timing not needed)
+    if (ms) *ms = 0.0;
+    if (launches) *launches = c->n_launches;
+    if (reset) c->n_launches = 0;
+    return PNPULA_OK;
+  }
   if (!strcmp(name, "cnn")) t = &c->tm_cnn;
   else if (!strcmp(name, "update")) t = &c->tm_update;
   else if (!strcmp(name, "halo")) t = &c->tm_halo;
