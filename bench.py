@@ -263,7 +263,8 @@ def main():
     t_gen = time.perf_counter()
     kw = build_inputs(wl, rect)
     t_gen = time.perf_counter() - t_gen
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream()          # a real stream (handle != 0) shared with the library
+    torch.cuda.set_stream(stream)
     common = dict(tiles=wl["tiles"], rank=rank, world_size=world, device=local, nccl_uid=uid,
                   stream=stream.cuda_stream, flags=args.flags)
     kw.pop("_pin", None)
