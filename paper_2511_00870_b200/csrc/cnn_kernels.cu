@@ -1,5 +1,5 @@
 // cnn_kernels.cu -- the DnCNN-style prior G_eps on 5th-generation tensor
-// cores (tcgen05 + TMEM), sm_100a.  One launch evaluates a chain of `nl` consecutive
+// cores (tcgen05 + TMEM), sm_100a.  One launch evaluates a chain of NL consecutive
 // 3x3 conv layers (eq:cnn:convolution P:358-363) of the net on a tile region.
 //
 // Design:
@@ -15,9 +15,11 @@
 //    j-1, so in one step all layers are independent and the tensor core always has
 //    work while the epilogue drains another layer;
 //  * warp roles: warp 0 loads input rows (x -> bf16 im2col rows for the first layer,
-//    or bf16 activation rows from HBM), warp 1 (one lane) issues tcgen05.mma and
-//    tcgen05.commit, warps 2-5 are the epilogue (tcgen05.ld -> +bias, ReLU, zero
-//    outside the image -> bf16 -> next layer's ring, or HBM for the last layer);
+//    or bf16 activation rows from HBM), warp 1 issues tcgen05.mma / tcgen05.commit
+//    (warp-uniform operands, one elected lane issues), warps 2-9 are the epilogue
+//    (tcgen05.ld -> +bias, ReLU, zero outside the image -> bf16 -> next layer's ring,
+//    or HBM for the chain's last layer); two warps per TMEM lane quarter, each
+//    handling half of the channels;
 //  * fp32 accumulation in TMEM, double-buffered per layer.
 // Every output pixel's arithmetic (K order, rounding points) is independent of the
 // strip/tile it falls in, so results are bitwise identical for every tile grid.
@@ -33,7 +35,8 @@ namespace pnpula {
 namespace {
 
 constexpr int kRowPos = 130;        // positions per ring row (128 MMA rows + 1 each side)
-constexpr int kThreads = 192;       // warp 0 producer, warp 1 MMA, warps 2..5 epilogue
+constexpr int kEpiWarps = 8;
+constexpr int kThreads = 64 + 32 * kEpiWarps;   // producer warp, MMA warp, epilogue warps
 constexpr int kRing = 4;
 
 struct SmemLayout {
@@ -100,9 +103,7 @@ __device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
 }
 // Bounded wait: gives up (sets the CTA abort flag and the device error flag) after
 // ~4e9 cycles so a pipeline bug cannot hang the GPU.
-__device__ __forceinline__ bool mbar_wait(uint32_t bar, uint32_t parity, volatile int *abort, int *err,
-                                          int code) {
-  if (mbar_test(bar, parity)) return true;
+__device__ __noinline__ bool mbar_wait_slow(uint32_t bar, uint32_t parity, volatile int *abort, int *err, int code) {
   const long long t0 = clock64();
   while (true) {
     if (mbar_test(bar, parity)) return true;
@@ -113,6 +114,20 @@ __device__ __forceinline__ bool mbar_wait(uint32_t bar, uint32_t parity, volatil
       return false;
     }
   }
+}
+__device__ __forceinline__ bool mbar_wait(uint32_t bar, uint32_t parity, volatile int *abort, int *err, int code) {
+  if (mbar_test(bar, parity)) return true;
+  return mbar_wait_slow(bar, parity, abort, err, code);
+}
+
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "elect.sync _|p, 0xffffffff;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
 }
 
 __device__ __forceinline__ void fence_proxy_async() {
@@ -127,6 +142,7 @@ __device__ __forceinline__ void tc_fence_after() {
 
 // UMMA shared-memory descriptor, K-major, no swizzle (canonical layout
 // ((8,m),(8,2)) : ((16B, SBO), (2B, LBO)) -- core matrix = 8 rows x 16 bytes).
+// Adding k to the descriptor moves its start address by 16k bytes.
 __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
@@ -138,7 +154,7 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint
 }
 
 // Instruction descriptor, kind::f16: D = F32, A = B = BF16, both K-major, M = 128.
-__device__ __forceinline__ uint32_t make_idesc(int N) {
+__host__ __device__ constexpr uint32_t make_idesc(int N) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
 }
 
@@ -167,6 +183,16 @@ __device__ __forceinline__ void tmem_load<1>(uint32_t taddr, float *v) {
   v[0] = __uint_as_float(r);
 }
 template <>
+__device__ __forceinline__ void tmem_load<8>(uint32_t taddr, float *v) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr)
+               : "memory");
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+template <>
 __device__ __forceinline__ void tmem_load<16>(uint32_t taddr, float *v) {
   uint32_t r[16];
   asm volatile(
@@ -183,11 +209,6 @@ __device__ __forceinline__ void tmem_load<32>(uint32_t taddr, float *v) {
   tmem_load<16>(taddr, v);
   tmem_load<16>(taddr + 16, v + 16);
 }
-template <>
-__device__ __forceinline__ void tmem_load<64>(uint32_t taddr, float *v) {
-  tmem_load<32>(taddr, v);
-  tmem_load<32>(taddr + 32, v + 32);
-}
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
@@ -196,64 +217,58 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 }
 
 // ---------------------------------------------------------------- the kernel
-template <int P>
+template <int P, int NL>
 __global__ void __launch_bounds__(kThreads, 1) cnn_chunk_kernel(const __grid_constant__ CnnChunkParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr int G = P / 8;              // channel groups of 8
   constexpr int KS = P / 16;            // K steps per tap
+  constexpr int PH = P / 2;             // channels per epilogue thread
   constexpr uint32_t GS = kRowPos * 16; // bytes between channel groups in a ring row
-  const int nl = p.nl;
   const bool first = p.first_is_input != 0;
   const bool last = p.last_is_output != 0;
-  const SmemLayout L = make_layout(P, nl, first, last);
+  const SmemLayout L = make_layout(P, NL, first, last);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t sbase = smem_u32(smem);
-
-  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + L.bar_off);
+  const uint32_t bar0 = sbase + L.bar_off;
   // barrier indices: full[l][4], empty[l][4], tfull[l][2], tempty[l][2]
-  auto bar_full = [&](int l, int s) { return smem_u32(bars + l * 12 + s); };
-  auto bar_empty = [&](int l, int s) { return smem_u32(bars + l * 12 + 4 + s); };
-  auto bar_tfull = [&](int l, int b) { return smem_u32(bars + l * 12 + 8 + b); };
-  auto bar_tempty = [&](int l, int b) { return smem_u32(bars + l * 12 + 10 + b); };
+  auto bar_full = [&](int l, uint32_t s) { return bar0 + (uint32_t)(l * 12 + s) * 8u; };
+  auto bar_empty = [&](int l, uint32_t s) { return bar0 + (uint32_t)(l * 12 + 4 + s) * 8u; };
+  auto bar_tfull = [&](int l, uint32_t b) { return bar0 + (uint32_t)(l * 12 + 8 + b) * 8u; };
+  auto bar_tempty = [&](int l, uint32_t b) { return bar0 + (uint32_t)(l * 12 + 10 + b) * 8u; };
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + L.misc_off);
   volatile int *abort_flag = reinterpret_cast<volatile int *>(smem + L.misc_off + 4);
+  const uint32_t bar_done = sbase + L.misc_off + 8;
   float *sbias = reinterpret_cast<float *>(smem + L.bias_off);
-
-  const uint32_t tmem_cols = [&] {
-    uint32_t need = (uint32_t)(2 * nl * P);
-    uint32_t c = 32;
-    while (c < need) c <<= 1;
-    return c;
-  }();
+  constexpr uint32_t tmem_cols = (2 * NL * P <= 32) ? 32 : (2 * NL * P <= 64) ? 64 : (2 * NL * P <= 128) ? 128
+                                 : (2 * NL * P <= 256) ? 256 : 512;
 
   // ---- one-time setup: weights, biases, zero rings, barriers, TMEM
-  for (int l = 0; l < nl; ++l) {
+#pragma unroll
+  for (int l = 0; l < NL; ++l) {
     const int cin = (l == 0 && first) ? 1 : P;
-    const int cout = (l == nl - 1 && last) ? 1 : P;
+    const int cout = (l == NL - 1 && last) ? 1 : P;
     const uint32_t n16 = packed_layer_elems(cout, cin) / 8;   // 16-byte chunks
     const uint4 *src = reinterpret_cast<const uint4 *>(p.w[l]);
     uint4 *dst = reinterpret_cast<uint4 *>(smem + L.w_off[l]);
     for (uint32_t e = threadIdx.x; e < n16; e += kThreads) dst[e] = src[e];
     for (int c = threadIdx.x; c < P; c += kThreads) sbias[l * P + c] = (c < cout) ? p.b[l][c] : 0.f;
-  }
-  for (int l = 0; l < nl; ++l) {
     uint4 *r = reinterpret_cast<uint4 *>(smem + L.ring_off[l]);
-    const uint32_t n16 = kRing * L.slot_bytes[l] / 16;
-    for (uint32_t e = threadIdx.x; e < n16; e += kThreads) r[e] = make_uint4(0, 0, 0, 0);
+    const uint32_t nr = kRing * L.slot_bytes[l] / 16;
+    for (uint32_t e = threadIdx.x; e < nr; e += kThreads) r[e] = make_uint4(0, 0, 0, 0);
   }
   if (threadIdx.x == 0) {
-    for (int l = 0; l < nl; ++l) {
+    for (int l = 0; l < NL; ++l) {
       for (int s = 0; s < 4; ++s) {
-        mbar_init(bar_full(l, s), (l == 0) ? 1 : 4);
+        mbar_init(bar_full(l, s), (l == 0) ? 1 : kEpiWarps);
         mbar_init(bar_empty(l, s), 1);
       }
       for (int b = 0; b < 2; ++b) {
         mbar_init(bar_tfull(l, b), 1);
-        mbar_init(bar_tempty(l, b), 4);
+        mbar_init(bar_tempty(l, b), kEpiWarps);
       }
     }
+    mbar_init(bar_done, 1);
     *abort_flag = 0;
-    mbar_init(smem_u32(smem + L.misc_off + 8), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -268,53 +283,52 @@ __global__ void __launch_bounds__(kThreads, 1) cnn_chunk_kernel(const __grid_con
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const int Wv = kRowPos - 2 * nl;                 // valid output columns per strip
-  const int strips = (p.ow + Wv - 1) / Wv;
+  const int Wv = kRowPos - 2 * NL;                 // valid output columns per strip
+  const int strips = p.strips;
   const int R = p.rows_per_unit;
-  const int rblocks = (p.oh + R - 1) / R;
-  const int units = strips * rblocks;
+  const int units = p.units;
 
   // running counters (identical in every role)
-  uint32_t Fcnt[kMaxChunk];   // ring fills before this unit
-  uint32_t Acnt[kMaxChunk];   // accumulator uses before this unit
-  for (int l = 0; l < kMaxChunk; ++l) { Fcnt[l] = 0; Acnt[l] = 0; }
+  uint32_t Fcnt[NL], Acnt[NL];
+#pragma unroll
+  for (int l = 0; l < NL; ++l) { Fcnt[l] = 0; Acnt[l] = 0; }
 
   for (int u = blockIdx.x; u < units; u += gridDim.x) {
     if (*abort_flag) break;
-    const int rb = u / strips, strip = u % strips;
+    const int rb = u / strips, strip = u - (u / strips) * strips;
     const int r_lo = p.oi0 + rb * R;
     const int r_hi = min(r_lo + R, p.oi0 + p.oh);
     const int Rn = r_hi - r_lo;
     const int c_strip0 = p.oj0 + strip * Wv;         // first valid output column of the strip
-    const int col0 = c_strip0 - nl + 1;              // column of MMA row 0
-    const int S = Rn + 3 * nl;
-    // fills of ring l in this unit
-    auto nfill = [&](int l) { return (l == 0) ? (first ? Rn + 2 * nl - 2 : Rn + 2 * nl) : Rn + 2 * (nl - l); };
-    auto nact = [&](int l) { return Rn + 2 * (nl - l - 1); };   // active steps of layer l
+    const int col0 = c_strip0 - NL + 1;              // column of MMA row 0
+    const int S = Rn + 3 * NL;
 
     if (warp == 0) {
       // ================= producer: ring 0
-      const int nf = nfill(0);
+      const int nf = first ? Rn + 2 * NL - 2 : Rn + 2 * NL;
       for (int f = 0; f < nf; ++f) {
         const uint32_t Fg = Fcnt[0] + f;
         if (Fg >= 4 && !mbar_wait(bar_empty(0, Fg & 3), ((Fg >> 2) - 1) & 1, abort_flag, p.err, 1)) break;
         uint8_t *slot = smem + L.ring_off[0] + (Fg & 3) * L.slot_bytes[0];
         if (first) {
           // im2col row for layer-1 output row o: 9 taps of x (bf16), K padded to 16
-          const int o = r_lo - nl + f + 1;
+          const int o = r_lo - NL + f + 1;
           const TileGeom &g = p.xg;
           for (int m = lane; m < 128; m += 32) {
             const int cm = col0 + m;
             float t[9];
 #pragma unroll
-            for (int u2 = -1; u2 <= 1; ++u2)
+            for (int u2 = -1; u2 <= 1; ++u2) {
+              const int pr = o + u2 - (g.i0 - g.h);
+              const bool rok = pr >= 0 && pr < g.ph;
 #pragma unroll
               for (int v2 = -1; v2 <= 1; ++v2) {
-                const int pr = o + u2 - (g.i0 - g.h), pc = cm + v2 - (g.j0 - g.hx);
+                const int pc = cm + v2 - (g.j0 - g.hx);
                 float v = 0.f;
-                if (pr >= 0 && pr < g.ph && pc >= 0 && pc < g.pitch) v = __ldg(p.x + (int64_t)pr * g.pitch + pc);
+                if (rok && pc >= 0 && pc < g.pitch) v = __ldg(p.x + (int64_t)pr * g.pitch + pc);
                 t[(u2 + 1) * 3 + (v2 + 1)] = v;
               }
+            }
             uint4 a0 = make_uint4(pack_bf16(t[0], t[1]), pack_bf16(t[2], t[3]), pack_bf16(t[4], t[5]),
                                   pack_bf16(t[6], t[7]));
             uint4 a1 = make_uint4(pack_bf16(t[8], 0.f), 0u, 0u, 0u);
@@ -322,17 +336,17 @@ __global__ void __launch_bounds__(kThreads, 1) cnn_chunk_kernel(const __grid_con
             *reinterpret_cast<uint4 *>(slot + 2048 + m * 16) = a1;
           }
         } else {
-          const int row = r_lo - nl + f;
+          const int row = r_lo - NL + f;
           const int c0 = col0 - 1;
           const bool row_ok = row >= p.a_i0 && row < p.a_i0 + p.a_rows;
+          const uint4 *src = reinterpret_cast<const uint4 *>(p.ain) + ((int64_t)(row - p.a_i0) * p.a_cols - p.a_j0);
+#pragma unroll 4
           for (int e = lane; e < G * kRowPos; e += 32) {
             const int gq = e / kRowPos, q = e - gq * kRowPos;
             const int col = c0 + q;
             uint4 v = make_uint4(0, 0, 0, 0);
-            if (row_ok && col >= p.a_j0 && col < p.a_j0 + p.a_cols) {
-              const int64_t idx = (((int64_t)gq * p.a_rows + (row - p.a_i0)) * p.a_cols + (col - p.a_j0)) * 8;
-              v = __ldg(reinterpret_cast<const uint4 *>(p.ain + idx));
-            }
+            if (row_ok && col >= p.a_j0 && col < p.a_j0 + p.a_cols)
+              v = __ldg(src + (int64_t)gq * p.a_rows * p.a_cols + col);
             *reinterpret_cast<uint4 *>(slot + gq * GS + q * 16) = v;
           }
         }
@@ -341,146 +355,166 @@ __global__ void __launch_bounds__(kThreads, 1) cnn_chunk_kernel(const __grid_con
         if (lane == 0) mbar_arrive(bar_full(0, Fg & 3));
       }
     } else if (warp == 1) {
-      // ================= MMA issuer (one lane)
-      if (lane == 0) {
-        bool ok = true;
-        for (int s = 0; s < S && ok; ++s) {
-          for (int l = 0; l < nl && ok; ++l) {
-            const int a = s - 3 * (l + 1);
-            if (a < 0 || a >= nact(l)) continue;
-            const bool im2col = (l == 0 && first);
-            const int ndep = im2col ? 1 : 3;
-            for (int d = 0; d < ndep && ok; ++d) {
-              const uint32_t Fg = Fcnt[l] + a + d;
-              ok = mbar_wait(bar_full(l, Fg & 3), (Fg >> 2) & 1, abort_flag, p.err, 2);
-            }
-            const uint32_t U = Acnt[l] + a;
-            const int b = U & 1;
-            if (ok && U >= 2) ok = mbar_wait(bar_tempty(l, b), ((U >> 1) - 1) & 1, abort_flag, p.err, 3);
-            if (!ok) break;
-            tc_fence_after();
-            const int N = (l == nl - 1 && last) ? 16 : P;
-            const uint32_t idesc = make_idesc(N);
-            const uint32_t dcol = tmem_base + (uint32_t)((2 * l + b) * P);
-            const uint32_t wbase = sbase + L.w_off[l];
-            if (im2col) {
-              const uint32_t slot = sbase + L.ring_off[0] + ((Fcnt[0] + a) & 3) * L.slot_bytes[0];
-              mma_bf16(dcol, make_desc(slot, 2048, 128), make_desc(wbase, (uint32_t)N * 16, 128), idesc, 0);
-            } else {
-              uint32_t acc = 0;
-#pragma unroll 1
-              for (int dy = -1; dy <= 1; ++dy) {
-                const uint32_t Fg = Fcnt[l] + a + 1 + dy;
-                const uint32_t slot = sbase + L.ring_off[l] + (Fg & 3) * L.slot_bytes[l];
+      // ================= MMA issuer (whole warp walks the schedule; one elected lane issues)
+      bool ok = true;
+      for (int s = 0; s < S && ok; ++s) {
 #pragma unroll
-                for (int dx = -1; dx <= 1; ++dx) {
-                  const int tap = (dy + 1) * 3 + (dx + 1);
+        for (int l = 0; l < NL; ++l) {
+          const int a = s - 3 * (l + 1);
+          const int nact = Rn + 2 * (NL - l - 1);
+          if (!ok || a < 0 || a >= nact) continue;
+          const bool im2col = (l == 0) && first;
+          const uint32_t F0 = Fcnt[l] + (uint32_t)a;
+          if (im2col) {
+            ok = mbar_wait(bar_full(l, F0 & 3), (F0 >> 2) & 1, abort_flag, p.err, 2);
+          } else {
+#pragma unroll
+            for (int d = 0; d < 3; ++d)
+              if (ok) ok = mbar_wait(bar_full(l, (F0 + d) & 3), ((F0 + d) >> 2) & 1, abort_flag, p.err, 2);
+          }
+          const uint32_t U = Acnt[l] + (uint32_t)a;
+          const uint32_t b = U & 1;
+          if (ok && U >= 2) ok = mbar_wait(bar_tempty(l, b), ((U >> 1) - 1) & 1, abort_flag, p.err, 3);
+          ok = __shfl_sync(0xffffffffu, ok ? 1 : 0, 0) != 0;
+          if (!ok) continue;
+          tc_fence_after();
+          const bool netlast = (l == NL - 1) && last;
+          const uint32_t idesc = netlast ? make_idesc(16) : make_idesc(P);
+          const uint32_t dcol = tmem_base + (uint32_t)((2 * l + (int)b) * P);
+          const uint32_t wbase = sbase + L.w_off[l];
+          if (im2col) {
+            const uint32_t slot = sbase + L.ring_off[0] + (F0 & 3) * L.slot_bytes[0];
+            const uint64_t ad = make_desc(slot, 2048, 128);
+            const uint64_t bd = make_desc(wbase, (uint32_t)P * 16, 128);
+            if (elect_one()) mma_bf16(dcol, ad, bd, idesc, 0);
+          } else {
+            const uint32_t N = netlast ? 16u : (uint32_t)P;
+            const uint64_t bd0 = make_desc(wbase, N * 16, 128);
+            const uint32_t bstep = N * 2;     // (16 * N * 2 bytes) >> 4 per (tap, ks) block
+            uint64_t ad0[3];
+#pragma unroll
+            for (int dy = 0; dy < 3; ++dy)
+              ad0[dy] = make_desc(sbase + L.ring_off[l] + ((F0 + dy) & 3) * L.slot_bytes[l], GS, 128);
+            if (elect_one()) {
+#pragma unroll
+              for (int dy = 0; dy < 3; ++dy) {
+#pragma unroll
+                for (int dx = 0; dx < 3; ++dx) {
 #pragma unroll
                   for (int ks = 0; ks < KS; ++ks) {
-                    const uint32_t aaddr = slot + (uint32_t)(2 * ks) * GS + (uint32_t)(1 + dx) * 16;
-                    const uint32_t baddr = wbase + (uint32_t)((tap * KS + ks) * 16 * N * 2);
-                    mma_bf16(dcol, make_desc(aaddr, GS, 128), make_desc(baddr, (uint32_t)N * 16, 128), idesc, acc);
-                    acc = 1;
+                    const int tap = dy * 3 + dx;
+                    const uint64_t ad = ad0[dy] + (uint64_t)((2 * ks * GS + dx * 16) >> 4);
+                    const uint64_t bd = bd0 + (uint64_t)((tap * KS + ks) * bstep);
+                    mma_bf16(dcol, ad, bd, idesc, (tap | ks) != 0);
                   }
                 }
               }
             }
+            __syncwarp();
+          }
+          if (elect_one()) {
             mma_commit(bar_tfull(l, b));
-            mma_commit(bar_empty(l, (Fcnt[l] + a) & 3));
-            if (!im2col && a == nact(l) - 1) {
-              mma_commit(bar_empty(l, (Fcnt[l] + a + 1) & 3));
-              mma_commit(bar_empty(l, (Fcnt[l] + a + 2) & 3));
+            mma_commit(bar_empty(l, F0 & 3));
+            if (!im2col && a == nact - 1) {
+              mma_commit(bar_empty(l, (F0 + 1) & 3));
+              mma_commit(bar_empty(l, (F0 + 2) & 3));
             }
           }
+          __syncwarp();
         }
       }
-      __syncwarp();
     } else {
-      // ================= epilogue (warps 2..5, one thread per MMA row / pixel)
+      // ================= epilogue (warps 2..9: lane quarter = warp % 4, channel half = (warp-2)/4)
       const int quarter = warp & 3;
+      const int half = (warp - 2) >> 2;
       const int m = quarter * 32 + lane;
       const int cm = col0 + m;
       const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
+      const bool col_valid = cm >= c_strip0 && cm < c_strip0 + Wv && cm < p.oj0 + p.ow;
+      const bool col_in = cm >= 0 && cm < p.nx;
       bool ok = true;
       for (int s = 0; s < S && ok; ++s) {
-        for (int l = 0; l < nl && ok; ++l) {
+#pragma unroll
+        for (int l = 0; l < NL; ++l) {
           const int a = s - 3 * (l + 1);
-          if (a < 0 || a >= nact(l)) continue;
-          const uint32_t U = Acnt[l] + a;
-          const int b = U & 1;
-          if (!mbar_wait(bar_tfull(l, b), (U >> 1) & 1, abort_flag, p.err, 4)) { ok = false; break; }
+          const int nact = Rn + 2 * (NL - l - 1);
+          if (!ok || a < 0 || a >= nact) continue;
+          const uint32_t U = Acnt[l] + (uint32_t)a;
+          const uint32_t b = U & 1;
+          if (!mbar_wait(bar_tfull(l, b), (U >> 1) & 1, abort_flag, p.err, 4)) { ok = false; continue; }
           tc_fence_after();
-          const uint32_t taddr = tmem_base + lane_base + (uint32_t)((2 * l + b) * P);
-          const int o = r_lo - nl + s - 2 * (l + 1);       // output row of layer l at step s
-          const bool inside = o >= 0 && o < p.ny && cm >= 0 && cm < p.nx;
-          const float *bl = sbias + l * P;
-          if (l == nl - 1 && last) {
-            float v[1];
-            tmem_load<1>(taddr, v);
-            tmem_wait_ld();
+          const uint32_t taddr = tmem_base + lane_base + (uint32_t)((2 * l + (int)b) * P);
+          const int o = r_lo - NL + s - 2 * (l + 1);       // output row of layer l at step s
+          const bool inside = col_in && o >= 0 && o < p.ny;
+          if ((l == NL - 1) && last) {
+            float v[1] = {0.f};
+            if (half == 0) {
+              tmem_load<1>(taddr, v);
+              tmem_wait_ld();
+            }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(bar_tempty(l, b));
             // network output G (no ReLU), valid columns of the strip only
-            if (cm >= c_strip0 && cm < c_strip0 + Wv && cm < p.oj0 + p.ow) {
+            if (half == 0 && col_valid) {
               const TileGeom &g = p.gg;
-              p.G[(int64_t)(o - (g.i0 - g.h)) * g.pitch + (cm - (g.j0 - g.hx))] = v[0] + bl[0];
+              p.G[(int64_t)(o - (g.i0 - g.h)) * g.pitch + (cm - (g.j0 - g.hx))] = v[0] + sbias[l * P];
             }
             continue;
           }
-          float v[P];
-          tmem_load<P>(taddr, v);
+          float v[PH];
+          tmem_load<PH>(taddr + half * PH, v);
           tmem_wait_ld();
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(bar_tempty(l, b));
-          uint32_t w[P / 2];
+          const float *bl = sbias + l * P + half * PH;
+          uint32_t w[PH / 2];
 #pragma unroll
-          for (int c = 0; c < P; c += 2) {
+          for (int c = 0; c < PH; c += 2) {
             const float v0 = inside ? fmaxf(v[c] + bl[c], 0.f) : 0.f;
             const float v1 = inside ? fmaxf(v[c + 1] + bl[c + 1], 0.f) : 0.f;
             w[c / 2] = pack_bf16(v0, v1);
           }
-          if (l < nl - 1) {
-            const uint32_t Fg = Fcnt[l + 1] + a;
+          if (l < NL - 1) {
+            const uint32_t Fg = Fcnt[l + 1] + (uint32_t)a;
             if (Fg >= 4 && !mbar_wait(bar_empty(l + 1, Fg & 3), ((Fg >> 2) - 1) & 1, abort_flag, p.err, 5)) {
               ok = false;
-              break;
+              continue;
             }
-            uint8_t *slot = smem + L.ring_off[l + 1] + (Fg & 3) * L.slot_bytes[l + 1];
+            uint8_t *slot = smem + L.ring_off[l + 1] + (Fg & 3) * L.slot_bytes[l + 1] + (m + 1) * 16;
 #pragma unroll
-            for (int gq = 0; gq < G; ++gq)
-              *reinterpret_cast<uint4 *>(slot + gq * GS + (m + 1) * 16) =
+            for (int gq = 0; gq < G / 2; ++gq)
+              *reinterpret_cast<uint4 *>(slot + (half * (G / 2) + gq) * GS) =
                   make_uint4(w[4 * gq], w[4 * gq + 1], w[4 * gq + 2], w[4 * gq + 3]);
             fence_proxy_async();
             __syncwarp();
             if (lane == 0) mbar_arrive(bar_full(l + 1, Fg & 3));
-          } else {
+          } else if (col_valid) {
             // chunk output (activations for the next launch), valid columns only
-            if (cm >= c_strip0 && cm < c_strip0 + Wv && cm < p.oj0 + p.ow) {
 #pragma unroll
-              for (int gq = 0; gq < G; ++gq) {
-                const int64_t idx = (((int64_t)gq * p.o_rows + (o - p.o_i0)) * p.o_cols + (cm - p.o_j0)) * 8;
-                *reinterpret_cast<uint4 *>(p.aout + idx) =
-                    make_uint4(w[4 * gq], w[4 * gq + 1], w[4 * gq + 2], w[4 * gq + 3]);
-              }
+            for (int gq = 0; gq < G / 2; ++gq) {
+              const int64_t idx =
+                  (((int64_t)(half * (G / 2) + gq) * p.o_rows + (o - p.o_i0)) * p.o_cols + (cm - p.o_j0)) * 8;
+              *reinterpret_cast<uint4 *>(p.aout + idx) = make_uint4(w[4 * gq], w[4 * gq + 1], w[4 * gq + 2], w[4 * gq + 3]);
             }
           }
         }
       }
     }
     // advance running counters (all roles identically)
-    for (int l = 0; l < nl; ++l) {
-      Fcnt[l] += nfill(l);
-      Acnt[l] += nact(l);
+#pragma unroll
+    for (int l = 0; l < NL; ++l) {
+      Fcnt[l] += (l == 0) ? (first ? Rn + 2 * NL - 2 : Rn + 2 * NL) : Rn + 2 * (NL - l);
+      Acnt[l] += Rn + 2 * (NL - l - 1);
     }
   }
 
   // ---- teardown: make sure every tcgen05 op (and its mbarrier arrivals) has retired
-  if (warp == 1 && lane == 0) {
-    const uint32_t done = smem_u32(smem + L.misc_off + 8);
-    mma_commit(done);
-    mbar_wait(done, 0, abort_flag, p.err, 6);
+  if (warp == 1) {
+    if (elect_one()) mma_commit(bar_done);
+    __syncwarp();
+    mbar_wait(bar_done, 0, abort_flag, p.err, 6);
   }
   tc_fence_before();
   __syncthreads();
@@ -491,11 +525,11 @@ __global__ void __launch_bounds__(kThreads, 1) cnn_chunk_kernel(const __grid_con
   }
 }
 
-template <int P>
-cudaError_t launch_p(const CnnChunkParams &p0, int num_sms, cudaStream_t s) {
+template <int P, int NL>
+cudaError_t launch_pn(const CnnChunkParams &p0, int num_sms, cudaStream_t s) {
   CnnChunkParams p = p0;
-  const SmemLayout L = make_layout(P, p.nl, p.first_is_input, p.last_is_output);
-  const int Wv = kRowPos - 2 * p.nl;
+  const SmemLayout L = make_layout(P, NL, p.first_is_input, p.last_is_output);
+  const int Wv = kRowPos - 2 * NL;
   const int strips = (p.ow + Wv - 1) / Wv;
   // rows per unit: minimise (waves) x (rows per unit + pipeline fill) over row-block counts
   int R = p.oh;
@@ -505,24 +539,40 @@ cudaError_t launch_p(const CnnChunkParams &p0, int num_sms, cudaStream_t s) {
       const int r = (p.oh + rb - 1) / rb;
       const int nrb = (p.oh + r - 1) / r;
       const int waves = (strips * nrb + num_sms - 1) / num_sms;
-      const double cost = (double)waves * (r + 2.0 * p.nl);
+      const double cost = (double)waves * (r + 2.0 * NL);
       if (cost < best) { best = cost; R = r; }
     }
   }
   p.strips = strips;
   p.rows_per_unit = R;
   p.units = strips * ((p.oh + R - 1) / R);
-  cudaError_t e = cudaFuncSetAttribute(cnn_chunk_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
+  auto kfn = cnn_chunk_kernel<P, NL>;
+  cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
   if (e != cudaSuccess) return e;
   const int grid = p.units < num_sms ? p.units : num_sms;
-  cnn_chunk_kernel<P><<<grid, kThreads, L.total, s>>>(p);
+  kfn<<<grid, kThreads, L.total, s>>>(p);
   return cudaGetLastError();
+}
+
+// compile-time chain lengths: limited by 227 KB of shared memory per CTA
+constexpr int max_nl(int P) { return P == 16 ? 8 : P == 32 ? 5 : 1; }
+
+template <int P, int NL>
+cudaError_t dispatch_nl(const CnnChunkParams &p, int num_sms, cudaStream_t s) {
+  if constexpr (NL > max_nl(P)) {
+    return cudaErrorInvalidValue;
+  } else {
+    if (p.nl == NL) return launch_pn<P, NL>(p, num_sms, s);
+    if constexpr (NL < kMaxChunk) return dispatch_nl<P, NL + 1>(p, num_sms, s);
+    return cudaErrorInvalidValue;
+  }
 }
 
 }  // namespace
 
 size_t cnn_chunk_smem_bytes(int P, int nl, int first, int last) {
   if (nl < 1 || nl > kMaxChunk) return SIZE_MAX;
+  if (nl > max_nl(P)) return SIZE_MAX;
   if (2 * nl * P > 512) return SIZE_MAX;    // TMEM columns
   return make_layout(P, nl, first, last).total;
 }
@@ -568,9 +618,9 @@ void cnn_pack_layer(const float *w, int cout, int cin, uint16_t *out) {
 
 cudaError_t launch_cnn_chunk(const CnnChunkParams &p, int num_sms, cudaStream_t s) {
   switch (p.P) {
-    case 16: return launch_p<16>(p, num_sms, s);
-    case 32: return launch_p<32>(p, num_sms, s);
-    case 64: return launch_p<64>(p, num_sms, s);
+    case 16: return dispatch_nl<16, 1>(p, num_sms, s);
+    case 32: return dispatch_nl<32, 1>(p, num_sms, s);
+    case 64: return dispatch_nl<64, 1>(p, num_sms, s);
     default: return cudaErrorInvalidValue;
   }
 }
