@@ -211,6 +211,16 @@ __device__ __forceinline__ void tmem_load<32>(uint32_t taddr, float *v) {
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
+// Pipeline trace (diagnostics only; p.trace == nullptr in production): one 64-bit record
+// per event = clock64 << 20 | code << 16 | step << 4 | layer.
+__device__ __forceinline__ void trace_ev(unsigned long long *tr, bool on, int code, int s, int l) {
+  if (!on) return;
+  const unsigned long long t = (unsigned long long)clock64();
+  const unsigned long long idx = atomicAdd(tr, 1ull);
+  if (idx < (1ull << 20))
+    tr[1 + idx] = (t << 20) | ((unsigned long long)code << 16) | ((unsigned long long)(s & 0xfff) << 4) | (unsigned)l;
+}
+
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t *>(&v);
@@ -302,6 +312,7 @@ __global__ void __launch_bounds__(kThreads, 1) cnn_chunk_kernel(const __grid_con
     const int c_strip0 = p.oj0 + strip * Wv;         // first valid output column of the strip
     const int col0 = c_strip0 - NL + 1;              // column of MMA row 0
     const int S = Rn + 3 * NL;
+    const bool tr_on = p.trace != nullptr && blockIdx.x == 0 && u == (int)blockIdx.x;
 
     if (warp == 0) {
       // ================= producer: ring 0
@@ -309,6 +320,7 @@ __global__ void __launch_bounds__(kThreads, 1) cnn_chunk_kernel(const __grid_con
       for (int f = 0; f < nf; ++f) {
         const uint32_t Fg = Fcnt[0] + f;
         if (Fg >= 4 && !mbar_wait(bar_empty(0, Fg & 3), ((Fg >> 2) - 1) & 1, abort_flag, p.err, 1)) break;
+        trace_ev(p.trace, tr_on && lane == 0, 1, f, 0);
         uint8_t *slot = smem + L.ring_off[0] + (Fg & 3) * L.slot_bytes[0];
         if (first) {
           // im2col row for layer-1 output row o: 9 taps of x (bf16), K padded to 16
@@ -353,6 +365,7 @@ __global__ void __launch_bounds__(kThreads, 1) cnn_chunk_kernel(const __grid_con
         fence_proxy_async();
         __syncwarp();
         if (lane == 0) mbar_arrive(bar_full(0, Fg & 3));
+        trace_ev(p.trace, tr_on && lane == 0, 2, f, 0);
       }
     } else if (warp == 1) {
       // ================= MMA issuer (whole warp walks the schedule; one elected lane issues)
@@ -365,6 +378,7 @@ __global__ void __launch_bounds__(kThreads, 1) cnn_chunk_kernel(const __grid_con
           if (!ok || a < 0 || a >= nact) continue;
           const bool im2col = (l == 0) && first;
           const uint32_t F0 = Fcnt[l] + (uint32_t)a;
+          trace_ev(p.trace, tr_on && lane == 0, 3, s, l);
           if (im2col) {
             ok = mbar_wait(bar_full(l, F0 & 3), (F0 >> 2) & 1, abort_flag, p.err, 2);
           } else {
@@ -376,6 +390,7 @@ __global__ void __launch_bounds__(kThreads, 1) cnn_chunk_kernel(const __grid_con
           const uint32_t b = U & 1;
           if (ok && U >= 2) ok = mbar_wait(bar_tempty(l, b), ((U >> 1) - 1) & 1, abort_flag, p.err, 3);
           ok = __shfl_sync(0xffffffffu, ok ? 1 : 0, 0) != 0;
+          trace_ev(p.trace, tr_on && lane == 0, 4, s, l);
           if (!ok) continue;
           tc_fence_after();
           const bool netlast = (l == NL - 1) && last;
@@ -421,6 +436,7 @@ __global__ void __launch_bounds__(kThreads, 1) cnn_chunk_kernel(const __grid_con
             }
           }
           __syncwarp();
+          trace_ev(p.trace, tr_on && lane == 0, 5, s, l);
         }
       }
     } else {
@@ -442,6 +458,7 @@ __global__ void __launch_bounds__(kThreads, 1) cnn_chunk_kernel(const __grid_con
           const uint32_t U = Acnt[l] + (uint32_t)a;
           const uint32_t b = U & 1;
           if (!mbar_wait(bar_tfull(l, b), (U >> 1) & 1, abort_flag, p.err, 4)) { ok = false; continue; }
+          trace_ev(p.trace, tr_on && warp == 2 && lane == 0, 6, s, l);
           tc_fence_after();
           const uint32_t taddr = tmem_base + lane_base + (uint32_t)((2 * l + (int)b) * P);
           const int o = r_lo - NL + s - 2 * (l + 1);       // output row of layer l at step s
@@ -490,6 +507,7 @@ __global__ void __launch_bounds__(kThreads, 1) cnn_chunk_kernel(const __grid_con
             fence_proxy_async();
             __syncwarp();
             if (lane == 0) mbar_arrive(bar_full(l + 1, Fg & 3));
+            trace_ev(p.trace, tr_on && warp == 2 && lane == 0, 8, s, l);
           } else if (col_valid) {
             // chunk output (activations for the next launch), valid columns only
 #pragma unroll

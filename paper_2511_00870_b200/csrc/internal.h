@@ -81,6 +81,7 @@ struct CnnChunkParams {
   int rows_per_unit;     // output rows per work unit
   int units;             // strips * row blocks
   int *err;              // device error flag (watchdog)
+  unsigned long long *trace;   // optional pipeline trace (CTA 0, first unit): [0] = count, then records
 };
 
 // Launchers (return cudaGetLastError()).

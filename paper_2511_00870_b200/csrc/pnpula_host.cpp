@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -106,6 +107,7 @@ struct pnpula_ctx {
   bool timing = false;
   Timer tm_cnn, tm_update, tm_halo;
   int64_t n_launches = 0;   // kernels of this library launched (all classes)
+  bool traced = false;      // PNPULA_CNN_TRACE written
 };
 
 namespace {
@@ -231,11 +233,34 @@ pnpula_status run_cnn(pnpula_ctx *c, int buf) {
       }
       p.ny = c->ny; p.nx = c->nx;
       p.err = c->d_err;
+      // optional pipeline trace of the first evaluation (diagnostics; env PNPULA_CNN_TRACE=<path prefix>)
+      const char *trace_path = getenv("PNPULA_CNN_TRACE");
+      unsigned long long *d_trace = nullptr;
+      if (trace_path && !c->traced) {
+        CU(c, cudaMalloc(&d_trace, sizeof(unsigned long long) << 21));
+        CU(c, cudaMemsetAsync(d_trace, 0, sizeof(unsigned long long), c->stream));
+        p.trace = d_trace;
+      }
       cudaEvent_t end;
       timer_begin(c, c->tm_cnn, &end);
       CU(c, launch_cnn_chunk(p, c->num_sms, c->stream));
       c->n_launches++;
       timer_end(c, end);
+      if (d_trace) {
+        std::vector<unsigned long long> h((size_t)1 << 21);
+        CU(c, cudaMemcpyAsync(h.data(), d_trace, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                              c->stream));
+        CU(c, cudaStreamSynchronize(c->stream));
+        cudaFree(d_trace);
+        char fn[1024];
+        snprintf(fn, sizeof(fn), "%s.chunk%zu.bin", trace_path, ci);
+        if (FILE *fp = fopen(fn, "wb")) {
+          const size_t n = std::min<size_t>(h[0], ((size_t)1 << 20)) + 1;
+          fwrite(h.data(), sizeof(unsigned long long), n, fp);
+          fclose(fp);
+        }
+        if (ci + 1 == c->chunks.size()) c->traced = true;
+      }
     }
   }
   return PNPULA_OK;
