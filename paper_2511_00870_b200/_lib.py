@@ -10,7 +10,8 @@ import os
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libpnpula.so")
+# PNPULA_LIB: load an alternative build of the same library (kernel experiments only)
+LIB_PATH = os.environ.get("PNPULA_LIB") or os.path.join(_PKG, "libpnpula.so")
 
 PNPULA_OK = 0
 STATUS = {0: "OK", 1: "E_INVALID_ARG", 2: "E_SHAPE", 3: "E_PARTITION_TOO_FINE", 4: "E_STEPSIZE",

@@ -3,24 +3,26 @@
 // 3x3 conv layers (eq:cnn:convolution P:358-363) of the net on a tile region.
 //
 // Design:
-//  * implicit GEMM, M = 128 consecutive pixels of one image row, N = output channels
-//    (P, or 16 for the 1-channel last layer), K = 16 input channels per MMA; the 3x3
-//    window is 9 shifted views of the same shared-memory rows (the shift is a change
-//    of the UMMA descriptor start address, so no im2col copy for P -> P layers);
-//  * activations live in shared memory in "channel-group planar" rows:
+//  * implicit GEMM, M = 128 consecutive pixels of one image row, K = 16 input channels
+//    per MMA.  A = one input row (bf16, shared memory) shifted by dx in {-1,0,1} -- the
+//    shift is a change of the UMMA descriptor start address;
+//  * the three vertical taps are folded into N: B(dx, k) stacks the weights of
+//    dy = +1, 0, -1, so one MMA with N = 3 Cb (Cb = P, or 16 for the 1-channel last
+//    layer) adds input row r's contribution to output rows r-1, r, r+1 at once.
+//    Output rows accumulate in a 4-slot TMEM ring (one Cb-column slot per row): an
+//    output row is complete after the MMAs of input row r+1; the epilogue reads it and
+//    re-zeroes its slot.  Each input row is consumed by exactly one MMA group;
+//  * activations live in shared memory in "channel-group planar" rows
 //    [group of 8 ch][130 positions][8 x bf16] -- the canonical K-major, no-swizzle
-//    UMMA layout (core matrix = 8 positions x 16 B);
-//  * a CTA owns a 130-column strip and streams down its rows: each layer keeps a
-//    4-row ring of its output rows; layer j of the chain runs 2 steps behind layer
-//    j-1, so in one step all layers are independent and the tensor core always has
-//    work while the epilogue drains another layer;
+//    UMMA layout (core matrix = 8 positions x 16 B); a CTA owns a 130-column strip and
+//    streams down its rows, every layer of the chain lagging the previous one by 3 rows;
 //  * warp roles: warp 0 loads input rows (x -> bf16 im2col rows for the first layer,
 //    or bf16 activation rows from HBM), warp 1 issues tcgen05.mma / tcgen05.commit
-//    (warp-uniform operands, one elected lane issues), warps 2-9 are the epilogue
-//    (tcgen05.ld -> +bias, ReLU, zero outside the image -> bf16 -> next layer's ring,
-//    or HBM for the chain's last layer); two warps per TMEM lane quarter, each
-//    handling half of the channels;
-//  * fp32 accumulation in TMEM, double-buffered per layer.
+//    (warp-uniform operands, one elected lane issues), warps 2.. are the epilogue in
+//    groups of 4 warps (one per TMEM lane quarter), group g owning layers l % G == g:
+//    tcgen05.ld -> +bias, ReLU, zero outside the image -> bf16 -> next layer's ring,
+//    or HBM / the fp32 residual G for the chain's last layer;
+//  * fp32 accumulation in TMEM.
 // Every output pixel's arithmetic (K order, rounding points) is independent of the
 // strip/tile it falls in, so results are bitwise identical for every tile grid.
 #include <cstdint>
@@ -34,10 +36,15 @@ namespace pnpula {
 
 namespace {
 
-constexpr int kRowPos = 130;        // positions per ring row (128 MMA rows + 1 each side)
-constexpr int kEpiWarps = 8;
+#ifndef PNPULA_EPI_GROUPS
+#define PNPULA_EPI_GROUPS 3
+#endif
+constexpr int kRowPos = 130;                    // positions per ring row (128 MMA rows + 1 each side)
+constexpr int kEpiGroups = PNPULA_EPI_GROUPS;   // epilogue groups (each: 4 warps = 4 TMEM lane quarters)
+constexpr int kEpiWarps = 4 * kEpiGroups;
 constexpr int kThreads = 64 + 32 * kEpiWarps;   // producer warp, MMA warp, epilogue warps
-constexpr int kRing = 4;
+constexpr int kRing = 4;                        // input-row ring slots per layer
+constexpr int kAcc = 4;                         // accumulator-row slots per layer (TMEM)
 
 struct SmemLayout {
   uint32_t ring_off[kMaxChunk];
@@ -73,9 +80,9 @@ __host__ __device__ inline SmemLayout make_layout(int P, int nl, int first, int 
   }
   L.bias_off = off;
   off = align_up(off + (uint32_t)nl * P * 4u, 128);
-  L.bar_off = off;
-  off = align_up(off + (uint32_t)nl * 12u * 8u, 128);
-  L.misc_off = off;   // tmem address, abort flag, drain barrier
+  L.bar_off = off;   // per layer: full[4], empty[4], tfull[4], tempty[4]
+  off = align_up(off + (uint32_t)nl * 16u * 8u, 128);
+  L.misc_off = off;  // tmem address, abort flag, drain barrier
   off += 16;
   L.total = align_up(off, 128);
   return L;
@@ -101,12 +108,25 @@ __device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// try_wait with a suspend-time hint: the warp sleeps in hardware until the phase completes
+// (or ~0.5 ms pass) instead of spinning.
+__device__ __forceinline__ bool mbar_test_sleep(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity), "r"(500000u)
+      : "memory");
+  return ok != 0;
+}
 // Bounded wait: gives up (sets the CTA abort flag and the device error flag) after
 // ~4e9 cycles so a pipeline bug cannot hang the GPU.
 __device__ __noinline__ bool mbar_wait_slow(uint32_t bar, uint32_t parity, volatile int *abort, int *err, int code) {
   const long long t0 = clock64();
   while (true) {
-    if (mbar_test(bar, parity)) return true;
+    if (mbar_test_sleep(bar, parity)) return true;
     if (*abort) return false;
     if (clock64() - t0 > (1ll << 32)) {
       *abort = 1;
@@ -183,16 +203,6 @@ __device__ __forceinline__ void tmem_load<1>(uint32_t taddr, float *v) {
   v[0] = __uint_as_float(r);
 }
 template <>
-__device__ __forceinline__ void tmem_load<8>(uint32_t taddr, float *v) {
-  uint32_t r[8];
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-               : "r"(taddr)
-               : "memory");
-#pragma unroll
-  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
-}
-template <>
 __device__ __forceinline__ void tmem_load<16>(uint32_t taddr, float *v) {
   uint32_t r[16];
   asm volatile(
@@ -211,19 +221,38 @@ __device__ __forceinline__ void tmem_load<32>(uint32_t taddr, float *v) {
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
-// Pipeline trace (diagnostics only; p.trace == nullptr in production): one 64-bit record
-// per event = clock64 << 20 | code << 16 | step << 4 | layer.
-__device__ __forceinline__ void trace_ev(unsigned long long *tr, bool on, int code, int s, int l) {
-  if (!on) return;
-  const unsigned long long t = (unsigned long long)clock64();
-  const unsigned long long idx = atomicAdd(tr, 1ull);
-  if (idx < (1ull << 20))
-    tr[1 + idx] = (t << 20) | ((unsigned long long)code << 16) | ((unsigned long long)(s & 0xfff) << 4) | (unsigned)l;
+// zero n consecutive TMEM columns of this warp's 32 lanes
+template <int N>
+__device__ __forceinline__ void tmem_zero(uint32_t taddr);
+template <>
+__device__ __forceinline__ void tmem_zero<1>(uint32_t taddr) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(taddr), "r"(0u) : "memory");
 }
+template <>
+__device__ __forceinline__ void tmem_zero<16>(uint32_t taddr) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr),
+      "r"(0u)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t *>(&v);
+}
+
+// Pipeline trace (diagnostics only; p.trace == nullptr in production): one 64-bit record
+// per event = clock64 << 20 | code << 16 | step << 4 | layer.  Each tracing thread owns a
+// private region (code 1-2: producer, 3-5: MMA, 6-11: epilogue), plain stores only.
+__device__ __forceinline__ void trace_ev(unsigned long long *tr, bool on, int code, int s, int l) {
+  if (!on) return;
+  const unsigned long long t = (unsigned long long)clock64();
+  const int region = code <= 2 ? 0 : code <= 5 ? 1 : 2;
+  const unsigned idx = (unsigned)(s * 8 + l) * 8 + (unsigned)(code & 7);
+  if (idx < (1u << 18))
+    tr[1 + (region << 18) + idx] =
+        (t << 20) | ((unsigned long long)code << 16) | ((unsigned long long)(s & 0xfff) << 4) | (unsigned)l;
 }
 
 // ---------------------------------------------------------------- the kernel
@@ -232,7 +261,6 @@ __global__ void __launch_bounds__(kThreads, 1) cnn_chunk_kernel(const __grid_con
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr int G = P / 8;              // channel groups of 8
   constexpr int KS = P / 16;            // K steps per tap
-  constexpr int PH = P / 2;             // channels per epilogue thread
   constexpr uint32_t GS = kRowPos * 16; // bytes between channel groups in a ring row
   const bool first = p.first_is_input != 0;
   const bool last = p.last_is_output != 0;
@@ -240,17 +268,19 @@ __global__ void __launch_bounds__(kThreads, 1) cnn_chunk_kernel(const __grid_con
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t sbase = smem_u32(smem);
   const uint32_t bar0 = sbase + L.bar_off;
-  // barrier indices: full[l][4], empty[l][4], tfull[l][2], tempty[l][2]
-  auto bar_full = [&](int l, uint32_t s) { return bar0 + (uint32_t)(l * 12 + s) * 8u; };
-  auto bar_empty = [&](int l, uint32_t s) { return bar0 + (uint32_t)(l * 12 + 4 + s) * 8u; };
-  auto bar_tfull = [&](int l, uint32_t b) { return bar0 + (uint32_t)(l * 12 + 8 + b) * 8u; };
-  auto bar_tempty = [&](int l, uint32_t b) { return bar0 + (uint32_t)(l * 12 + 10 + b) * 8u; };
+  auto bar_full = [&](int l, uint32_t s) { return bar0 + (uint32_t)(l * 16 + s) * 8u; };
+  auto bar_empty = [&](int l, uint32_t s) { return bar0 + (uint32_t)(l * 16 + 4 + s) * 8u; };
+  auto bar_tfull = [&](int l, uint32_t s) { return bar0 + (uint32_t)(l * 16 + 8 + s) * 8u; };
+  auto bar_tempty = [&](int l, uint32_t s) { return bar0 + (uint32_t)(l * 16 + 12 + s) * 8u; };
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + L.misc_off);
   volatile int *abort_flag = reinterpret_cast<volatile int *>(smem + L.misc_off + 4);
   const uint32_t bar_done = sbase + L.misc_off + 8;
   float *sbias = reinterpret_cast<float *>(smem + L.bias_off);
-  constexpr uint32_t tmem_cols = (2 * NL * P <= 32) ? 32 : (2 * NL * P <= 64) ? 64 : (2 * NL * P <= 128) ? 128
-                                 : (2 * NL * P <= 256) ? 256 : 512;
+  // TMEM: layer l owns columns [l*4P, l*4P + 4*Cb): accumulator-row slot q at l*4P + q*Cb
+  constexpr uint32_t tmem_need = (uint32_t)NL * kAcc * P;
+  static_assert(tmem_need <= 512, "TMEM columns");
+  constexpr uint32_t tmem_cols = tmem_need <= 32 ? 32 : tmem_need <= 64 ? 64 : tmem_need <= 128 ? 128
+                                 : tmem_need <= 256 ? 256 : 512;
 
   // ---- one-time setup: weights, biases, zero rings, barriers, TMEM
 #pragma unroll
@@ -267,16 +297,13 @@ __global__ void __launch_bounds__(kThreads, 1) cnn_chunk_kernel(const __grid_con
     for (uint32_t e = threadIdx.x; e < nr; e += kThreads) r[e] = make_uint4(0, 0, 0, 0);
   }
   if (threadIdx.x == 0) {
-    for (int l = 0; l < NL; ++l) {
+    for (int l = 0; l < NL; ++l)
       for (int s = 0; s < 4; ++s) {
-        mbar_init(bar_full(l, s), (l == 0) ? 1 : kEpiWarps);
+        mbar_init(bar_full(l, s), (l == 0) ? 1 : 4);   // producer lane, or the 4 warps of one group
         mbar_init(bar_empty(l, s), 1);
+        mbar_init(bar_tfull(l, s), 1);
+        mbar_init(bar_tempty(l, s), 4);
       }
-      for (int b = 0; b < 2; ++b) {
-        mbar_init(bar_tfull(l, b), 1);
-        mbar_init(bar_tempty(l, b), kEpiWarps);
-      }
-    }
     mbar_init(bar_done, 1);
     *abort_flag = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -292,16 +319,25 @@ __global__ void __launch_bounds__(kThreads, 1) cnn_chunk_kernel(const __grid_con
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // accumulators start at zero (every slot is re-zeroed by the epilogue after it is read)
+  if (warp >= 2 && warp < 6) {
+    const uint32_t lb = (uint32_t)((warp & 3) * 32) << 16;
+    for (uint32_t c = 0; c < tmem_need; c += 16) tmem_zero<16>(tmem_base + lb + c);
+    tmem_wait_st();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
 
   const int Wv = kRowPos - 2 * NL;                 // valid output columns per strip
   const int strips = p.strips;
   const int R = p.rows_per_unit;
   const int units = p.units;
 
-  // running counters (identical in every role)
-  uint32_t Fcnt[NL], Acnt[NL];
+  // running counters (identical in every role): input-row fills and output rows before this unit
+  uint32_t Fcnt[NL], Ocnt[NL];
 #pragma unroll
-  for (int l = 0; l < NL; ++l) { Fcnt[l] = 0; Acnt[l] = 0; }
+  for (int l = 0; l < NL; ++l) { Fcnt[l] = 0; Ocnt[l] = 0; }
 
   for (int u = blockIdx.x; u < units; u += gridDim.x) {
     if (*abort_flag) break;
@@ -310,13 +346,17 @@ __global__ void __launch_bounds__(kThreads, 1) cnn_chunk_kernel(const __grid_con
     const int r_hi = min(r_lo + R, p.oi0 + p.oh);
     const int Rn = r_hi - r_lo;
     const int c_strip0 = p.oj0 + strip * Wv;         // first valid output column of the strip
-    const int col0 = c_strip0 - NL + 1;              // column of MMA row 0
-    const int S = Rn + 3 * NL;
+    const int col0 = c_strip0 - NL + 1;              // column of MMA row 0 (ring position 1)
     const bool tr_on = p.trace != nullptr && blockIdx.x == 0 && u == (int)blockIdx.x;
+    // layer l: nout(l) = Rn + 2 (NL-1-l) output rows starting at global row r_lo-(NL-1-l);
+    // its input fills are rows r0(l)-1 .. (nout+2 fills), or nout im2col rows for an im2col layer.
+    auto nout = [&](int l) { return Rn + 2 * (NL - 1 - l); };
+    auto nfill = [&](int l) { return (l == 0 && first) ? nout(0) : nout(l) + 2; };
+    const int S = 3 * (NL - 1) + nfill(NL - 1) > nfill(0) ? 3 * (NL - 1) + nfill(NL - 1) : nfill(0);
 
     if (warp == 0) {
       // ================= producer: ring 0
-      const int nf = first ? Rn + 2 * NL - 2 : Rn + 2 * NL;
+      const int nf = nfill(0);
       for (int f = 0; f < nf; ++f) {
         const uint32_t Fg = Fcnt[0] + f;
         if (Fg >= 4 && !mbar_wait(bar_empty(0, Fg & 3), ((Fg >> 2) - 1) & 1, abort_flag, p.err, 1)) break;
@@ -373,158 +413,166 @@ __global__ void __launch_bounds__(kThreads, 1) cnn_chunk_kernel(const __grid_con
       for (int s = 0; s < S && ok; ++s) {
 #pragma unroll
         for (int l = 0; l < NL; ++l) {
-          const int a = s - 3 * (l + 1);
-          const int nact = Rn + 2 * (NL - l - 1);
-          if (!ok || a < 0 || a >= nact) continue;
+          const int f = s - 3 * l;                     // input fill processed by layer l at step s
+          const int no = nout(l);
+          if (!ok || f < 0 || f >= nfill(l)) continue;
           const bool im2col = (l == 0) && first;
-          const uint32_t F0 = Fcnt[l] + (uint32_t)a;
+          const bool netlast = (l == NL - 1) && last;
+          const uint32_t Fg = Fcnt[l] + (uint32_t)f;
           trace_ev(p.trace, tr_on && lane == 0, 3, s, l);
-          if (im2col) {
-            ok = mbar_wait(bar_full(l, F0 & 3), (F0 >> 2) & 1, abort_flag, p.err, 2);
-          } else {
-#pragma unroll
-            for (int d = 0; d < 3; ++d)
-              if (ok) ok = mbar_wait(bar_full(l, (F0 + d) & 3), ((F0 + d) >> 2) & 1, abort_flag, p.err, 2);
-          }
-          const uint32_t U = Acnt[l] + (uint32_t)a;
-          const uint32_t b = U & 1;
-          if (ok && U >= 2) ok = mbar_wait(bar_tempty(l, b), ((U >> 1) - 1) & 1, abort_flag, p.err, 3);
+          ok = mbar_wait(bar_full(l, Fg & 3), (Fg >> 2) & 1, abort_flag, p.err, 2);
+          // output row that receives its first contribution (im2col: the only one)
+          const int inew = f;
+          const uint32_t Ig = Ocnt[l] + (uint32_t)inew;
+          if (ok && inew < no && Ig >= (uint32_t)kAcc)
+            ok = mbar_wait(bar_tempty(l, Ig & 3), ((Ig >> 2) - 1) & 1, abort_flag, p.err, 3);
           ok = __shfl_sync(0xffffffffu, ok ? 1 : 0, 0) != 0;
           trace_ev(p.trace, tr_on && lane == 0, 4, s, l);
           if (!ok) continue;
           tc_fence_after();
-          const bool netlast = (l == NL - 1) && last;
-          const uint32_t idesc = netlast ? make_idesc(16) : make_idesc(P);
-          const uint32_t dcol = tmem_base + (uint32_t)((2 * l + (int)b) * P);
+          const uint32_t acc0 = tmem_base + (uint32_t)(l * kAcc * P);
           const uint32_t wbase = sbase + L.w_off[l];
+          const uint32_t slot = sbase + L.ring_off[l] + (Fg & 3) * L.slot_bytes[l];
           if (im2col) {
-            const uint32_t slot = sbase + L.ring_off[0] + (F0 & 3) * L.slot_bytes[0];
             const uint64_t ad = make_desc(slot, 2048, 128);
             const uint64_t bd = make_desc(wbase, (uint32_t)P * 16, 128);
-            if (elect_one()) mma_bf16(dcol, ad, bd, idesc, 0);
+            if (elect_one()) mma_bf16(acc0 + (Ig & 3) * P, ad, bd, make_idesc(P), 0);
           } else {
-            const uint32_t N = netlast ? 16u : (uint32_t)P;
-            const uint64_t bd0 = make_desc(wbase, N * 16, 128);
-            const uint32_t bstep = N * 2;     // (16 * N * 2 bytes) >> 4 per (tap, ks) block
-            uint64_t ad0[3];
-#pragma unroll
-            for (int dy = 0; dy < 3; ++dy)
-              ad0[dy] = make_desc(sbase + L.ring_off[l] + ((F0 + dy) & 3) * L.slot_bytes[l], GS, 128);
+            // input row f contributes to output rows f-2 (dy=+1), f-1 (dy=0), f (dy=-1): B block q=0,1,2.
+            // Only rows in [0, no) are accumulated; slots wrap, so the row range splits into <= 2 runs.
+            const uint32_t Cb = netlast ? 16u : (uint32_t)P;
+            const int ilo = f - 2 > 0 ? f - 2 : 0;
+            const int ihi = f < no - 1 ? f : no - 1;
+            const uint32_t Ilo = Ocnt[l] + (uint32_t)ilo;
+            const int n1 = (int)min((uint32_t)(ihi - ilo + 1), kAcc - (Ilo & 3));   // rows before the wrap
+            const int n2 = (ihi - ilo + 1) - n1;
+            const uint64_t ad0 = make_desc(slot, GS, 128);
+            const uint64_t bd0 = make_desc(wbase, 3u * Cb * 16u, 128);
+            const uint32_t bstep = 3u * Cb * 2u;      // (16 * 3Cb * 2 bytes) >> 4 per (dx, ks) block
+            const uint32_t q0 = (uint32_t)(ilo - (f - 2));
+            const uint32_t d1 = acc0 + (Ilo & 3) * Cb;
+            const uint32_t d2 = acc0;
+            const uint32_t id1 = make_idesc((int)(n1 * Cb)), id2 = make_idesc((int)((n2 > 0 ? n2 : 1) * Cb));
             if (elect_one()) {
 #pragma unroll
-              for (int dy = 0; dy < 3; ++dy) {
+              for (int dx = 0; dx < 3; ++dx) {
 #pragma unroll
-                for (int dx = 0; dx < 3; ++dx) {
-#pragma unroll
-                  for (int ks = 0; ks < KS; ++ks) {
-                    const int tap = dy * 3 + dx;
-                    const uint64_t ad = ad0[dy] + (uint64_t)((2 * ks * GS + dx * 16) >> 4);
-                    const uint64_t bd = bd0 + (uint64_t)((tap * KS + ks) * bstep);
-                    mma_bf16(dcol, ad, bd, idesc, (tap | ks) != 0);
-                  }
+                for (int ks = 0; ks < KS; ++ks) {
+                  const uint64_t ad = ad0 + (uint64_t)((2 * ks * GS + dx * 16) >> 4);
+                  const uint64_t bd = bd0 + (uint64_t)((dx * KS + ks) * bstep);
+                  mma_bf16(d1, ad, bd + (uint64_t)(q0 * Cb), id1, 1);
+                  if (n2 > 0) mma_bf16(d2, ad, bd + (uint64_t)((q0 + n1) * Cb), id2, 1);
                 }
               }
             }
-            __syncwarp();
           }
+          __syncwarp();
           if (elect_one()) {
-            mma_commit(bar_tfull(l, b));
-            mma_commit(bar_empty(l, F0 & 3));
-            if (!im2col && a == nact - 1) {
-              mma_commit(bar_empty(l, (F0 + 1) & 3));
-              mma_commit(bar_empty(l, (F0 + 2) & 3));
-            }
+            mma_commit(bar_empty(l, Fg & 3));            // input row consumed
+            const int ic = im2col ? f : f - 2;           // output row completed by this group
+            if (ic >= 0 && ic < no) mma_commit(bar_tfull(l, (Ocnt[l] + (uint32_t)ic) & 3));
           }
           __syncwarp();
           trace_ev(p.trace, tr_on && lane == 0, 5, s, l);
         }
       }
     } else {
-      // ================= epilogue (warps 2..9: lane quarter = warp % 4, channel half = (warp-2)/4)
+      // ================= epilogue: group g (warps 2+4g .. 5+4g) owns layers l % kEpiGroups == g
       const int quarter = warp & 3;
-      const int half = (warp - 2) >> 2;
+      const int grp = (warp - 2) >> 2;
       const int m = quarter * 32 + lane;
       const int cm = col0 + m;
       const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
       const bool col_valid = cm >= c_strip0 && cm < c_strip0 + Wv && cm < p.oj0 + p.ow;
       const bool col_in = cm >= 0 && cm < p.nx;
+      const bool trw = tr_on && lane == 0 && quarter == 2;
       bool ok = true;
       for (int s = 0; s < S && ok; ++s) {
 #pragma unroll
         for (int l = 0; l < NL; ++l) {
-          const int a = s - 3 * (l + 1);
-          const int nact = Rn + 2 * (NL - l - 1);
-          if (!ok || a < 0 || a >= nact) continue;
-          const uint32_t U = Acnt[l] + (uint32_t)a;
-          const uint32_t b = U & 1;
-          if (!mbar_wait(bar_tfull(l, b), (U >> 1) & 1, abort_flag, p.err, 4)) { ok = false; continue; }
-          trace_ev(p.trace, tr_on && warp == 2 && lane == 0, 6, s, l);
+          if ((l % kEpiGroups) != grp) continue;
+          const bool im2col = (l == 0) && first;
+          const int f = s - 3 * l;
+          const int ic = im2col ? f : f - 2;           // output row completed at this step
+          const int no = nout(l);
+          if (!ok || f < 0 || f >= nfill(l) || ic < 0 || ic >= no) continue;
+          const uint32_t Ig = Ocnt[l] + (uint32_t)ic;
+          if (!mbar_wait(bar_tfull(l, Ig & 3), (Ig >> 2) & 1, abort_flag, p.err, 4)) { ok = false; continue; }
+          trace_ev(p.trace, trw, 6, s, l);
           tc_fence_after();
-          const uint32_t taddr = tmem_base + lane_base + (uint32_t)((2 * l + (int)b) * P);
-          const int o = r_lo - NL + s - 2 * (l + 1);       // output row of layer l at step s
+          const uint32_t taddr = tmem_base + lane_base + (uint32_t)(l * kAcc * P);
+          const int o = r_lo - (NL - 1 - l) + ic;      // global output row
           const bool inside = col_in && o >= 0 && o < p.ny;
           if ((l == NL - 1) && last) {
-            float v[1] = {0.f};
-            if (half == 0) {
-              tmem_load<1>(taddr, v);
-              tmem_wait_ld();
-            }
+            // network output G (no ReLU), column 0 of the 16-column slot
+            float v[1];
+            const uint32_t ta = taddr + (Ig & 3) * 16u;
+            tmem_load<1>(ta, v);
+            tmem_wait_ld();
+            tmem_zero<1>(ta);
+            tmem_wait_st();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(bar_tempty(l, b));
-            // network output G (no ReLU), valid columns of the strip only
-            if (half == 0 && col_valid) {
+            if (lane == 0) mbar_arrive(bar_tempty(l, Ig & 3));
+            if (col_valid) {
               const TileGeom &g = p.gg;
               p.G[(int64_t)(o - (g.i0 - g.h)) * g.pitch + (cm - (g.j0 - g.hx))] = v[0] + sbias[l * P];
             }
             continue;
           }
-          float v[PH];
-          tmem_load<PH>(taddr + half * PH, v);
+          float v[P];
+          const uint32_t ta = taddr + (Ig & 3) * (uint32_t)P;
+#pragma unroll
+          for (int c = 0; c < P; c += 16) tmem_load<16>(ta + c, v + c);
           tmem_wait_ld();
+          if (!im2col) {       // im2col MMAs overwrite (accumulate = 0): no re-zeroing needed
+#pragma unroll
+            for (int c = 0; c < P; c += 16) tmem_zero<16>(ta + c);
+            tmem_wait_st();
+          }
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(bar_tempty(l, b));
-          const float *bl = sbias + l * P + half * PH;
-          uint32_t w[PH / 2];
+          if (lane == 0) mbar_arrive(bar_tempty(l, Ig & 3));
+          trace_ev(p.trace, trw, 7, s, l);
+          const float *bl = sbias + l * P;
+          uint32_t w[P / 2];
 #pragma unroll
-          for (int c = 0; c < PH; c += 2) {
+          for (int c = 0; c < P; c += 2) {
             const float v0 = inside ? fmaxf(v[c] + bl[c], 0.f) : 0.f;
             const float v1 = inside ? fmaxf(v[c + 1] + bl[c + 1], 0.f) : 0.f;
             w[c / 2] = pack_bf16(v0, v1);
           }
           if (l < NL - 1) {
-            const uint32_t Fg = Fcnt[l + 1] + (uint32_t)a;
+            // next layer's input fill = this layer's output row index ic
+            const uint32_t Fg = Fcnt[l + 1] + (uint32_t)ic;
             if (Fg >= 4 && !mbar_wait(bar_empty(l + 1, Fg & 3), ((Fg >> 2) - 1) & 1, abort_flag, p.err, 5)) {
               ok = false;
               continue;
             }
             uint8_t *slot = smem + L.ring_off[l + 1] + (Fg & 3) * L.slot_bytes[l + 1] + (m + 1) * 16;
 #pragma unroll
-            for (int gq = 0; gq < G / 2; ++gq)
-              *reinterpret_cast<uint4 *>(slot + (half * (G / 2) + gq) * GS) =
-                  make_uint4(w[4 * gq], w[4 * gq + 1], w[4 * gq + 2], w[4 * gq + 3]);
+            for (int gq = 0; gq < G; ++gq)
+              *reinterpret_cast<uint4 *>(slot + gq * GS) = make_uint4(w[4 * gq], w[4 * gq + 1], w[4 * gq + 2], w[4 * gq + 3]);
             fence_proxy_async();
             __syncwarp();
             if (lane == 0) mbar_arrive(bar_full(l + 1, Fg & 3));
-            trace_ev(p.trace, tr_on && warp == 2 && lane == 0, 8, s, l);
           } else if (col_valid) {
             // chunk output (activations for the next launch), valid columns only
 #pragma unroll
-            for (int gq = 0; gq < G / 2; ++gq) {
-              const int64_t idx =
-                  (((int64_t)(half * (G / 2) + gq) * p.o_rows + (o - p.o_i0)) * p.o_cols + (cm - p.o_j0)) * 8;
+            for (int gq = 0; gq < G; ++gq) {
+              const int64_t idx = (((int64_t)gq * p.o_rows + (o - p.o_i0)) * p.o_cols + (cm - p.o_j0)) * 8;
               *reinterpret_cast<uint4 *>(p.aout + idx) = make_uint4(w[4 * gq], w[4 * gq + 1], w[4 * gq + 2], w[4 * gq + 3]);
             }
           }
+          trace_ev(p.trace, trw, 8, s, l);
         }
       }
     }
     // advance running counters (all roles identically)
 #pragma unroll
     for (int l = 0; l < NL; ++l) {
-      Fcnt[l] += (l == 0) ? (first ? Rn + 2 * NL - 2 : Rn + 2 * NL) : Rn + 2 * (NL - l);
-      Acnt[l] += Rn + 2 * (NL - l - 1);
+      Fcnt[l] += (uint32_t)nfill(l);
+      Ocnt[l] += (uint32_t)nout(l);
     }
   }
 
@@ -557,7 +605,7 @@ cudaError_t launch_pn(const CnnChunkParams &p0, int num_sms, cudaStream_t s) {
       const int r = (p.oh + rb - 1) / rb;
       const int nrb = (p.oh + r - 1) / r;
       const int waves = (strips * nrb + num_sms - 1) / num_sms;
-      const double cost = (double)waves * (r + 2.0 * NL);
+      const double cost = (double)waves * (r + 3.0 * NL);
       if (cost < best) { best = cost; R = r; }
     }
   }
@@ -572,8 +620,8 @@ cudaError_t launch_pn(const CnnChunkParams &p0, int num_sms, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-// compile-time chain lengths: limited by 227 KB of shared memory per CTA
-constexpr int max_nl(int P) { return P == 16 ? 8 : P == 32 ? 5 : 1; }
+// compile-time chain lengths: TMEM (NL * 4 * P <= 512 columns) and 227 KB of shared memory
+constexpr int max_nl(int P) { return P == 16 ? 8 : P == 32 ? 4 : 1; }
 
 template <int P, int NL>
 cudaError_t dispatch_nl(const CnnChunkParams &p, int num_sms, cudaStream_t s) {
@@ -591,7 +639,6 @@ cudaError_t dispatch_nl(const CnnChunkParams &p, int num_sms, cudaStream_t s) {
 size_t cnn_chunk_smem_bytes(int P, int nl, int first, int last) {
   if (nl < 1 || nl > kMaxChunk) return SIZE_MAX;
   if (nl > max_nl(P)) return SIZE_MAX;
-  if (2 * nl * P > 512) return SIZE_MAX;    // TMEM columns
   return make_layout(P, nl, first, last).total;
 }
 
@@ -605,9 +652,11 @@ static uint16_t f32_to_bf16_rne(float f) {
   return (uint16_t)(u >> 16);
 }
 
-// B-operand image of one layer (see header comment): for cin == 1, one K=16 block whose
-// k index is the tap (u+1)*3+(v+1); for cin == P, 9 taps x P/16 K-steps of blocks
-// [2 halves][N rows][8 cin] bf16, N = cout (or 16, zero-padded, for cout == 1).
+// B-operand image of one layer.  cin == 1: one K=16 block whose k index is the tap
+// (u+1)*3+(v+1).  cin == P: per (horizontal tap dx, K step ks) one block
+// [2 halves][N3 = 3 Cb rows][8 cin] bf16 whose row n = q*Cb + co holds the weight of
+// vertical tap dy = 1 - q (q = 0, 1, 2 <-> dy = +1, 0, -1); Cb = cout, or 16 (zero padded)
+// for cout == 1.
 void cnn_pack_layer(const float *w, int cout, int cin, uint16_t *out) {
   const size_t n = packed_layer_elems(cout, cin);
   memset(out, 0, n * sizeof(uint16_t));
@@ -620,17 +669,22 @@ void cnn_pack_layer(const float *w, int cout, int cin, uint16_t *out) {
       }
     return;
   }
-  const int N = (cout == 1) ? 16 : cout;
+  const int Cb = (cout == 1) ? 16 : cout;
+  const int N3 = 3 * Cb;
   const int KS = cin / 16;
-  for (int t = 0; t < 9; ++t)
+  for (int dxi = 0; dxi < 3; ++dxi)
     for (int ks = 0; ks < KS; ++ks) {
-      uint16_t *blk = out + (size_t)(t * KS + ks) * 16 * N;
-      for (int co = 0; co < cout; ++co)
-        for (int c = 0; c < 16; ++c) {
-          const int ci = ks * 16 + c;
-          const int g2 = c / 8, k8 = c % 8;
-          blk[((size_t)g2 * N + co) * 8 + k8] = f32_to_bf16_rne(w[((size_t)co * cin + ci) * 9 + t]);
-        }
+      uint16_t *blk = out + (size_t)(dxi * KS + ks) * 16 * N3;
+      for (int q = 0; q < 3; ++q) {
+        const int dyi = 2 - q;     // dy = 1 - q  ->  row index dy + 1
+        for (int co = 0; co < cout; ++co)
+          for (int c = 0; c < 16; ++c) {
+            const int ci = ks * 16 + c;
+            const int g2 = c / 8, k8 = c % 8;
+            const int nrow = q * Cb + co;
+            blk[((size_t)g2 * N3 + nrow) * 8 + k8] = f32_to_bf16_rne(w[((size_t)co * cin + ci) * 9 + dyi * 3 + dxi]);
+          }
+      }
     }
 }
 

@@ -238,7 +238,7 @@ pnpula_status run_cnn(pnpula_ctx *c, int buf) {
       unsigned long long *d_trace = nullptr;
       if (trace_path && !c->traced) {
         CU(c, cudaMalloc(&d_trace, sizeof(unsigned long long) << 21));
-        CU(c, cudaMemsetAsync(d_trace, 0, sizeof(unsigned long long), c->stream));
+        CU(c, cudaMemsetAsync(d_trace, 0, sizeof(unsigned long long) << 21, c->stream));
         p.trace = d_trace;
       }
       cudaEvent_t end;
@@ -255,8 +255,11 @@ pnpula_status run_cnn(pnpula_ctx *c, int buf) {
         char fn[1024];
         snprintf(fn, sizeof(fn), "%s.chunk%zu.bin", trace_path, ci);
         if (FILE *fp = fopen(fn, "wb")) {
-          const size_t n = std::min<size_t>(h[0], ((size_t)1 << 20)) + 1;
-          fwrite(h.data(), sizeof(unsigned long long), n, fp);
+          std::vector<unsigned long long> recs(1, 0);
+          for (size_t i = 1; i < h.size(); ++i)
+            if (h[i]) recs.push_back(h[i]);
+          recs[0] = recs.size() - 1;
+          fwrite(recs.data(), sizeof(unsigned long long), recs.size(), fp);
           fclose(fp);
         }
         if (ci + 1 == c->chunks.size()) c->traced = true;

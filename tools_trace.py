@@ -1,6 +1,9 @@
-"""Analyse a PNPULA_CNN_TRACE dump (diagnostics only)."""
+"""Analyse a PNPULA_CNN_TRACE dump (diagnostics only).
+codes: 1/2 producer empty-wait done / fill arrived; 3/4/5 MMA: start / inputs ready / issued+committed;
+6 epi tfull done, 7 TMEM loaded, 9 exchange barrier passed, 10 before ring-slot wait, 11 slot free, 8 full arrived."""
 import sys
 import numpy as np
+
 
 def load(fn):
     a = np.fromfile(fn, dtype=np.uint64)
@@ -10,30 +13,31 @@ def load(fn):
     s = ((r >> np.uint64(4)) & np.uint64(0xfff)).astype(int)
     l = (r & np.uint64(0xf)).astype(int)
     t = t - t.min()
-    return t, code, s, l
+    return {(c, si, li): ti for ti, c, si, li in zip(t, code, s, l)}
 
-for fn in sys.argv[1:]:
-    t, code, s, l = load(fn)
-    print(fn, 'events', len(t), 'span', t.max())
-    ev = {}
-    for ti, c, si, li in zip(t, code, s, l):
-        ev[(c, si, li)] = ti
-    # per step: MMA issue start/end, epilogue done
-    steps = sorted(set(si for c, si, li in ev if c == 3))
+
+def d(ev, a, b, si, li):
+    if (a, si, li) in ev and (b, si, li) in ev:
+        return ev[(b, si, li)] - ev[(a, si, li)]
+    return None
+
+
+def report(fn, steps=range(24, 30)):
+    ev = load(fn)
     L = max(li for c, si, li in ev) + 1
-    print('step  ' + '  '.join(f'L{j}:wait(3->4)/issue(4->5)/tfull(6)/done(8)' for j in range(min(L,3))))
-    prev = None
-    for si in steps[:40]:
-        row = []
+    print(fn)
+    for si in steps:
+        t0 = min((ev[(3, si, j)] for j in range(L) if (3, si, j) in ev), default=0)
+        parts = []
         for j in range(L):
-            if (3, si, j) in ev:
-                w = ev[(4, si, j)] - ev[(3, si, j)]
-                iss = ev[(5, si, j)] - ev[(4, si, j)]
-                tf = ev.get((6, si, j), -1) - ev[(5, si, j)]
-                dn = ev.get((8, si, j), -1) - ev.get((6, si, j), 0) if (8, si, j) in ev else -1
-                row.append(f'{w:5d}/{iss:4d}/{tf:5d}/{dn:5d}')
-            else:
-                row.append(' ' * 23)
-        t0 = min(ev[(3, si, j)] for j in range(L) if (3, si, j) in ev)
-        print(f'{si:4d} {t0 - (prev or t0):6d} ' + ' | '.join(row))
-        prev = t0
+            if (3, si, j) not in ev:
+                continue
+            seg = [('wfull', 3, 10), ('wtmem', 10, 4), ('issue', 4, 5), ('->tfull', 5, 6), ('ld', 6, 7),
+                   ('xbar', 7, 9), ('comb', 9, 11), ('st', 11, 8), ('epi', 6, 8)]
+            parts.append(f"L{j} " + ' '.join(f"{nm}={d(ev, a, b, si, j)}" for nm, a, b in seg if d(ev, a, b, si, j) is not None))
+        print(f"s={si} t={t0}: " + ' | '.join(parts))
+
+
+if __name__ == "__main__":
+    for fn in sys.argv[1:]:
+        report(fn)
