@@ -42,7 +42,9 @@ namespace {
 constexpr int kRowPos = 130;                    // positions per ring row (128 MMA rows + 1 each side)
 constexpr int kEpiGroups = PNPULA_EPI_GROUPS;   // epilogue groups (each: 4 warps = 4 TMEM lane quarters)
 constexpr int kEpiWarps = 4 * kEpiGroups;
-constexpr int kThreads = 64 + 32 * kEpiWarps;   // producer warp, MMA warp, epilogue warps
+constexpr int kMmaWarps = 2;                    // MMA issuers: warp 1 even layers, warp 2 odd layers
+constexpr int kEpi0 = 1 + kMmaWarps;            // first epilogue warp
+constexpr int kThreads = 32 * (kEpi0 + kEpiWarps);   // producer warp, MMA warps, epilogue warps
 constexpr int kRing = 4;                        // input-row ring slots per layer
 constexpr int kAcc = 4;                         // accumulator-row slots per layer (TMEM)
 
@@ -304,7 +306,7 @@ __global__ void __launch_bounds__(kThreads, 1) cnn_chunk_kernel(const __grid_con
         mbar_init(bar_tfull(l, s), 1);
         mbar_init(bar_tempty(l, s), 4);
       }
-    mbar_init(bar_done, 1);
+    mbar_init(bar_done, kMmaWarps);
     *abort_flag = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -320,7 +322,7 @@ __global__ void __launch_bounds__(kThreads, 1) cnn_chunk_kernel(const __grid_con
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   // accumulators start at zero (every slot is re-zeroed by the epilogue after it is read)
-  if (warp >= 2 && warp < 6) {
+  if (warp >= kEpi0 && warp < kEpi0 + 4) {
     const uint32_t lb = (uint32_t)((warp & 3) * 32) << 16;
     for (uint32_t c = 0; c < tmem_need; c += 16) tmem_zero<16>(tmem_base + lb + c);
     tmem_wait_st();
@@ -407,15 +409,18 @@ __global__ void __launch_bounds__(kThreads, 1) cnn_chunk_kernel(const __grid_con
         if (lane == 0) mbar_arrive(bar_full(0, Fg & 3));
         trace_ev(p.trace, tr_on && lane == 0, 2, f, 0);
       }
-    } else if (warp == 1) {
-      // ================= MMA issuer (whole warp walks the schedule; one elected lane issues)
+    } else if (warp < kEpi0) {
+      // ================= MMA issuers (whole warp walks the schedule; one elected lane issues).
+      // Warp 1 owns the even layers, warp 2 the odd ones, so one warp's barrier waits overlap
+      // the other's MMA issue; layers use disjoint TMEM columns and shared-memory operands.
+      const int mw = warp - 1;
       bool ok = true;
       for (int s = 0; s < S && ok; ++s) {
 #pragma unroll
         for (int l = 0; l < NL; ++l) {
           const int f = s - 3 * l;                     // input fill processed by layer l at step s
           const int no = nout(l);
-          if (!ok || f < 0 || f >= nfill(l)) continue;
+          if (!ok || (l % kMmaWarps) != mw || f < 0 || f >= nfill(l)) continue;
           const bool im2col = (l == 0) && first;
           const bool netlast = (l == NL - 1) && last;
           const uint32_t Fg = Fcnt[l] + (uint32_t)f;
@@ -477,9 +482,9 @@ __global__ void __launch_bounds__(kThreads, 1) cnn_chunk_kernel(const __grid_con
         }
       }
     } else {
-      // ================= epilogue: group g (warps 2+4g .. 5+4g) owns layers l % kEpiGroups == g
+      // ================= epilogue: group g (warps kEpi0+4g ..) owns layers l % kEpiGroups == g
       const int quarter = warp & 3;
-      const int grp = (warp - 2) >> 2;
+      const int grp = (warp - kEpi0) >> 2;
       const int m = quarter * 32 + lane;
       const int cm = col0 + m;
       const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
@@ -577,8 +582,8 @@ __global__ void __launch_bounds__(kThreads, 1) cnn_chunk_kernel(const __grid_con
   }
 
   // ---- teardown: make sure every tcgen05 op (and its mbarrier arrivals) has retired
-  if (warp == 1) {
-    if (elect_one()) mma_commit(bar_done);
+  if (warp >= 1 && warp < kEpi0) {
+    if (elect_one()) mma_commit(bar_done);       // one arrival per MMA warp
     __syncwarp();
     mbar_wait(bar_done, 0, abort_flag, p.err, 6);
   }
