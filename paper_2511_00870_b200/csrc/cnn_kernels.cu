@@ -42,7 +42,10 @@ namespace {
 constexpr int kRowPos = 130;                    // positions per ring row (128 MMA rows + 1 each side)
 constexpr int kEpiGroups = PNPULA_EPI_GROUPS;   // epilogue groups (each: 4 warps = 4 TMEM lane quarters)
 constexpr int kEpiWarps = 4 * kEpiGroups;
-constexpr int kMmaWarps = 2;                    // MMA issuers: warp 1 even layers, warp 2 odd layers
+#ifndef PNPULA_MMA_WARPS
+#define PNPULA_MMA_WARPS 4
+#endif
+constexpr int kMmaWarps = PNPULA_MMA_WARPS;     // MMA issuers: warp 1+w owns layers l % kMmaWarps == w
 constexpr int kEpi0 = 1 + kMmaWarps;            // first epilogue warp
 constexpr int kThreads = 32 * (kEpi0 + kEpiWarps);   // producer warp, MMA warps, epilogue warps
 constexpr int kRing = 4;                        // input-row ring slots per layer
@@ -390,19 +393,38 @@ __global__ void __launch_bounds__(kThreads, 1) cnn_chunk_kernel(const __grid_con
             *reinterpret_cast<uint4 *>(slot + 2048 + m * 16) = a1;
           }
         } else {
+          // activation row from HBM: one TMA bulk copy per 8-channel group (16 B per position,
+          // contiguous in the [group][row][col][8] layout); positions outside the stored region
+          // are zero-filled with plain stores (only at region edges).
           const int row = r_lo - NL + f;
           const int c0 = col0 - 1;
           const bool row_ok = row >= p.a_i0 && row < p.a_i0 + p.a_rows;
-          const uint4 *src = reinterpret_cast<const uint4 *>(p.ain) + ((int64_t)(row - p.a_i0) * p.a_cols - p.a_j0);
-#pragma unroll 4
+          const int qlo = row_ok ? max(0, p.a_j0 - c0) : kRowPos;
+          const int qhi = row_ok ? min(kRowPos, p.a_j0 + p.a_cols - c0) : kRowPos;
+          const uint32_t nbytes = qhi > qlo ? (uint32_t)(qhi - qlo) * 16u : 0u;
           for (int e = lane; e < G * kRowPos; e += 32) {
             const int gq = e / kRowPos, q = e - gq * kRowPos;
-            const int col = c0 + q;
-            uint4 v = make_uint4(0, 0, 0, 0);
-            if (row_ok && col >= p.a_j0 && col < p.a_j0 + p.a_cols)
-              v = __ldg(src + (int64_t)gq * p.a_rows * p.a_cols + col);
-            *reinterpret_cast<uint4 *>(slot + gq * GS + q * 16) = v;
+            if (q < qlo || q >= qhi) *reinterpret_cast<uint4 *>(slot + gq * GS + q * 16) = make_uint4(0, 0, 0, 0);
           }
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) {
+            const uint32_t fb = bar_full(0, Fg & 3);
+            asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(fb),
+                         "r"(nbytes * G)
+                         : "memory");
+            if (nbytes) {
+              const uint16_t *src = p.ain + ((int64_t)(row - p.a_i0) * p.a_cols + (c0 + qlo - p.a_j0)) * 8;
+              for (int gq = 0; gq < G; ++gq)
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                        smem_u32(slot + gq * GS + qlo * 16)),
+                    "l"(src + (int64_t)gq * p.a_rows * p.a_cols * 8), "r"(nbytes), "r"(fb)
+                    : "memory");
+            }
+          }
+          trace_ev(p.trace, tr_on && lane == 0, 2, f, 0);
+          continue;
         }
         fence_proxy_async();
         __syncwarp();
