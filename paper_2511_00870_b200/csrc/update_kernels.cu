@@ -46,22 +46,25 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1
   return c;
 }
 
-// ln(u), u = (U + 0.5) 2^-32, accurate for u near 0 and near 1.
+// ln(u), u = (U + 0.5) 2^-32, accurate for u near 0 and near 1: for u <= 1/2 the hardware
+// log2 (abs. error ~2^-22 on |log2 u| >= 1, i.e. relative 2^-22); for u > 1/2, log1p(-v)
+// with v = 1 - u formed exactly from the integer.
 __device__ __forceinline__ float log_unit(uint32_t U) {
   if (U < 0x80000000u) {
-    return logf(fmaf((float)U, 0x1p-32f, 0x1p-33f));
+    return __log2f(fmaf((float)U, 0x1p-32f, 0x1p-33f)) * 0.69314718055994531f;
   }
   const float v = fmaf((float)(~U), 0x1p-32f, 0x1p-33f);   // 1 - u
   return log1pf(-v);
 }
 
 // Box-Muller pair from (Ua, Ub): (rho cos theta, rho sin theta), theta = 2 pi (Ub+0.5) 2^-32,
-// evaluated as pi * x with x = ((int)Ub + 0.5) 2^-31 in (-1, 1) (same angle mod 2 pi).
+// evaluated as pi * x with x = ((int)Ub + 0.5) 2^-31 in (-1, 1) (same angle mod 2 pi) with
+// the hardware sin/cos (abs. error ~2^-21 on [-pi, pi]).
 __device__ __forceinline__ float2 box_muller(uint32_t Ua, uint32_t Ub) {
   const float rho = sqrtf(-2.0f * log_unit(Ua));
   const float xs = fmaf((float)(int32_t)Ub, 0x1p-31f, 0x1p-32f);
   float s, c;
-  sincospif(xs, &s, &c);
+  __sincosf(3.14159265358979323846f * xs, &s, &c);
   return make_float2(rho * c, rho * s);
 }
 
@@ -79,30 +82,52 @@ __device__ __forceinline__ int64_t pidx(const TileGeom &g, int gi, int gj) {
 
 // Elementwise tail of K7 for one quad of 4 horizontally adjacent pixels starting at
 // global column gj4 (multiple of 4) in row gi; gr[] = H1^T(H1 x - y) (unscaled).
-__device__ __forceinline__ void ula_quad(const UpdateParams &p, int gi, int gj4, const float gr[4]) {
+// Per-quad inputs of the elementwise tail (loaded early so their latency overlaps the
+// stencil arithmetic and the Philox / Box-Muller work).
+struct QuadIn {
+  float x[4], G[4], z[4], m[4], s[4];
+};
+
+__device__ __forceinline__ void ula_load(const UpdateParams &p, int gi, int gj4, QuadIn &q) {
   const TileGeom &g = p.g;
   const int64_t base = pidx(g, gi, gj4);
   const bool full = gj4 >= g.j0 && gj4 + 4 <= g.j0 + g.tw;
-  float xv[4], Gv[4] = {0.f, 0.f, 0.f, 0.f}, zv[4] = {0.f, 0.f, 0.f, 0.f}, mv[4], sv[4];
+#pragma unroll
+  for (int l = 0; l < 4; ++l) { q.G[l] = 0.f; q.z[l] = 0.f; q.m[l] = 0.f; q.s[l] = 0.f; }
   if (full) {
-    const float4 a = *reinterpret_cast<const float4 *>(p.x + base);
-    xv[0] = a.x; xv[1] = a.y; xv[2] = a.z; xv[3] = a.w;
+    const float4 a = __ldg(reinterpret_cast<const float4 *>(p.x + base));
+    q.x[0] = a.x; q.x[1] = a.y; q.x[2] = a.z; q.x[3] = a.w;
     if (p.has_G) {
-      const float4 b = *reinterpret_cast<const float4 *>(p.G + base);
-      Gv[0] = b.x; Gv[1] = b.y; Gv[2] = b.z; Gv[3] = b.w;
+      const float4 b = __ldg(reinterpret_cast<const float4 *>(p.G + base));
+      q.G[0] = b.x; q.G[1] = b.y; q.G[2] = b.z; q.G[3] = b.w;
     }
     if (p.has_z) {
       const float4 b = *reinterpret_cast<const float4 *>(p.z + base);
-      zv[0] = b.x; zv[1] = b.y; zv[2] = b.z; zv[3] = b.w;
+      q.z[0] = b.x; q.z[1] = b.y; q.z[2] = b.z; q.z[3] = b.w;
+    }
+    if (p.accumulate) {
+      const float4 a2 = *reinterpret_cast<const float4 *>(p.mean + base);
+      const float4 b2 = *reinterpret_cast<const float4 *>(p.m2 + base);
+      q.m[0] = a2.x; q.m[1] = a2.y; q.m[2] = a2.z; q.m[3] = a2.w;
+      q.s[0] = b2.x; q.s[1] = b2.y; q.s[2] = b2.z; q.s[3] = b2.w;
     }
   } else {
 #pragma unroll
     for (int l = 0; l < 4; ++l) {
-      xv[l] = p.x[base + l];
-      if (p.has_G) Gv[l] = p.G[base + l];
-      if (p.has_z) zv[l] = p.z[base + l];
+      q.x[l] = p.x[base + l];
+      if (p.has_G) q.G[l] = p.G[base + l];
+      if (p.has_z) q.z[l] = p.z[base + l];
+      if (p.accumulate) { q.m[l] = p.mean[base + l]; q.s[l] = p.m2[base + l]; }
     }
   }
+}
+
+__device__ __forceinline__ void ula_finish(const UpdateParams &p, int gi, int gj4, const float gr[4], QuadIn &q) {
+  const TileGeom &g = p.g;
+  const int64_t base = pidx(g, gi, gj4);
+  const bool full = gj4 >= g.j0 && gj4 + 4 <= g.j0 + g.tw;
+  const float *xv = q.x, *Gv = q.G, *zv = q.z;
+  float *mv = q.m, *sv = q.s;
   float xi[4];
   normals4(p.seed_lo, p.seed_hi, (uint32_t)gj4 >> 2, (uint32_t)gi, p.t1, 0u, xi);
   float xn[4];
@@ -126,15 +151,6 @@ __device__ __forceinline__ void ula_quad(const UpdateParams &p, int gi, int gj4,
     }
   }
   if (p.accumulate) {
-    if (full) {
-      const float4 a = *reinterpret_cast<const float4 *>(p.mean + base);
-      const float4 b = *reinterpret_cast<const float4 *>(p.m2 + base);
-      mv[0] = a.x; mv[1] = a.y; mv[2] = a.z; mv[3] = a.w;
-      sv[0] = b.x; sv[1] = b.y; sv[2] = b.z; sv[3] = b.w;
-    } else {
-#pragma unroll
-      for (int l = 0; l < 4; ++l) { mv[l] = p.mean[base + l]; sv[l] = p.m2[base + l]; }
-    }
 #pragma unroll
     for (int l = 0; l < 4; ++l) {
       const float d = xn[l] - mv[l];
@@ -159,6 +175,12 @@ __device__ __forceinline__ void ula_quad(const UpdateParams &p, int gi, int gj4,
       if (p.accumulate) { p.mean[base + l] = mv[l]; p.m2[base + l] = sv[l]; }
     }
   }
+}
+
+__device__ __forceinline__ void ula_quad(const UpdateParams &p, int gi, int gj4, const float gr[4]) {
+  QuadIn q;
+  ula_load(p, gi, gj4, q);
+  ula_finish(p, gi, gj4, gr, q);
 }
 
 // ---------------------------------------------------------------- conv K7
@@ -279,6 +301,153 @@ update_conv_kernel(const __grid_constant__ UpdateParams p) {
   }
 }
 
+// ---------------------------------------------------------------- separable conv K7 (v2)
+// Same arithmetic contract as update_conv_kernel<R, R, true>, restructured for throughput:
+// float4 staging of x, every stencil pass register-blocked on 4-wide (horizontal) or
+// 4x4 / 2x4 (vertical) output blocks read with 128-bit shared-memory loads.
+template <int R>
+__global__ void __launch_bounds__(NTHREADS) update_sep_kernel(const __grid_constant__ UpdateParams p) {
+  constexpr int XR = TY + 4 * R, XC = TX + 4 * R;   // x region
+  constexpr int RR = TY + 2 * R, RC = TX + 2 * R;   // residual region
+  constexpr int NW = 2 * R + 4;                     // inputs of a 4-wide output block
+  static_assert(RC % 4 == 0 && XC % 4 == 0 && NW % 4 == 0, "R must be even");
+  __shared__ __align__(16) float X[XR * XC];        // x; reused for T2 (RR x TX)
+  __shared__ __align__(16) float T1[XR * RC];       // horizontal forward pass
+  __shared__ __align__(16) float Rs[RR * RC];       // residual H x - y
+  float *T2 = X;
+  const TileGeom &g = p.g;
+  const int bi0 = g.i0 + blockIdx.y * TY;
+  const int bj0 = (g.j0 & ~3) + blockIdx.x * TX;
+  const int tid = threadIdx.x;
+  float ky[2 * R + 1], kx[2 * R + 1];
+#pragma unroll
+  for (int i = 0; i <= 2 * R; ++i) { ky[i] = p.ky[i]; kx[i] = p.kx[i]; }
+
+  // phase 0: x on block (+) 2R, float4 (columns are quad-aligned in the padded buffer)
+  for (int e = tid; e < XR * (XC / 4); e += NTHREADS) {
+    const int a = e / (XC / 4), c4 = e - a * (XC / 4);
+    const int pr = bi0 - 2 * R + a - (g.i0 - g.h);
+    const int pc = bj0 - 2 * R + 4 * c4 - (g.j0 - g.hx);
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (pr >= 0 && pr < g.ph && pc >= 0 && pc + 3 < g.pitch)
+      v = __ldg(reinterpret_cast<const float4 *>(p.x + (int64_t)pr * g.pitch + pc));
+    *reinterpret_cast<float4 *>(X + a * XC + 4 * c4) = v;
+  }
+  __syncthreads();
+  // phase 1: T1[a][b] = sum_q kx[q+R] X[a][b+R-q]   (4 outputs per item)
+  for (int e = tid; e < XR * (RC / 4); e += NTHREADS) {
+    const int a = e / (RC / 4), k4 = e - a * (RC / 4);
+    float xs[NW];
+#pragma unroll
+    for (int i = 0; i < NW; i += 4) {
+      const float4 t = *reinterpret_cast<const float4 *>(X + a * XC + 4 * k4 + i);
+      xs[i] = t.x; xs[i + 1] = t.y; xs[i + 2] = t.z; xs[i + 3] = t.w;
+    }
+    float o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float s = 0.f;
+#pragma unroll
+      for (int q = -R; q <= R; ++q) s = fmaf(kx[q + R], xs[j + R - q], s);
+      o[j] = s;
+    }
+    *reinterpret_cast<float4 *>(T1 + a * RC + 4 * k4) = make_float4(o[0], o[1], o[2], o[3]);
+  }
+  __syncthreads();
+  // phase 2: Rs[a][b] = sum_p ky[p+R] T1[a+R-p][b] - y, zero outside the image (4x4 per item)
+  for (int e = tid; e < (RR / 4) * (RC / 4); e += NTHREADS) {
+    const int a4 = e / (RC / 4), k4 = e - a4 * (RC / 4);
+    float col[NW][4];
+#pragma unroll
+    for (int i = 0; i < NW; ++i) {
+      const float4 t = *reinterpret_cast<const float4 *>(T1 + (4 * a4 + i) * RC + 4 * k4);
+      col[i][0] = t.x; col[i][1] = t.y; col[i][2] = t.z; col[i][3] = t.w;
+    }
+    const int gj = bj0 - R + 4 * k4;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int a = 4 * a4 + r;
+      const int gi = bi0 - R + a;
+      float o[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float s = 0.f;
+#pragma unroll
+        for (int q = -R; q <= R; ++q) s = fmaf(ky[q + R], col[r + R - q][j], s);
+        o[j] = s;
+      }
+      const int pr = gi - (g.i0 - g.h), pc = gj - (g.j0 - g.hx);
+      float yv[4] = {0.f, 0.f, 0.f, 0.f};
+      if (pr >= 0 && pr < g.ph && pc >= 0 && pc + 3 < g.pitch) {
+        if (R % 4 == 0) {   // quad-aligned in the padded buffer
+          const float4 t = __ldg(reinterpret_cast<const float4 *>(p.y + (int64_t)pr * g.pitch + pc));
+          yv[0] = t.x; yv[1] = t.y; yv[2] = t.z; yv[3] = t.w;
+        } else {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) yv[j] = __ldg(p.y + (int64_t)pr * g.pitch + pc + j);
+        }
+      }
+      const bool rin = gi >= 0 && gi < p.ny;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) o[j] = (rin && gj + j >= 0 && gj + j < p.nx) ? o[j] - yv[j] : 0.f;
+      *reinterpret_cast<float4 *>(Rs + a * RC + 4 * k4) = make_float4(o[0], o[1], o[2], o[3]);
+    }
+  }
+  __syncthreads();
+  // phase 3: T2[a][b] = sum_q kx[q+R] Rs[a][b+R+q]   (4 outputs per item)
+  for (int e = tid; e < RR * (TX / 4); e += NTHREADS) {
+    const int a = e / (TX / 4), k4 = e - a * (TX / 4);
+    float rs[NW];
+#pragma unroll
+    for (int i = 0; i < NW; i += 4) {
+      const float4 t = *reinterpret_cast<const float4 *>(Rs + a * RC + 4 * k4 + i);
+      rs[i] = t.x; rs[i + 1] = t.y; rs[i + 2] = t.z; rs[i + 3] = t.w;
+    }
+    float o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float s = 0.f;
+#pragma unroll
+      for (int q = -R; q <= R; ++q) s = fmaf(kx[q + R], rs[j + R + q], s);
+      o[j] = s;
+    }
+    *reinterpret_cast<float4 *>(T2 + a * TX + 4 * k4) = make_float4(o[0], o[1], o[2], o[3]);
+  }
+  __syncthreads();
+  // phase 4: g = sum_p ky[p+R] T2[a+R+p][b] for 2 rows x 1 quad per thread, then the update
+  {
+    const int q = tid & 15, a2 = tid >> 4;   // 16 quads x 16 row pairs
+    const int gj4 = bj0 + 4 * q;
+    bool act[2];
+    QuadIn qin[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {            // issue the update's global loads first
+      const int gi = bi0 + 2 * a2 + r;
+      act[r] = !(gi >= g.i0 + g.th || gj4 >= g.j0 + g.tw || gj4 + 4 <= g.j0);
+      if (act[r]) ula_load(p, gi, gj4, qin[r]);
+    }
+    float col[2 * R + 2][4];
+#pragma unroll
+    for (int i = 0; i < 2 * R + 2; ++i) {
+      const float4 t = *reinterpret_cast<const float4 *>(T2 + (2 * a2 + i) * TX + 4 * q);
+      col[i][0] = t.x; col[i][1] = t.y; col[i][2] = t.z; col[i][3] = t.w;
+    }
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      if (!act[r]) continue;
+      float gr[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float s = 0.f;
+#pragma unroll
+        for (int pp = -R; pp <= R; ++pp) s = fmaf(ky[pp + R], col[r + R + pp][j], s);
+        gr[j] = s;
+      }
+      ula_finish(p, bi0 + 2 * a2 + r, gj4, gr, qin[r]);
+    }
+  }
+}
+
 // ---------------------------------------------------------------- mask K7 (no stencil)
 __global__ void __launch_bounds__(NTHREADS) update_mask_kernel(const __grid_constant__ UpdateParams p) {
   const TileGeom &g = p.g;
@@ -355,8 +524,19 @@ cudaError_t launch_update(const UpdateParams &p, cudaStream_t s) {
     return cudaGetLastError();
   }
   if (p.separable) {
-    if (p.ry == 4 && p.rx == 4) return launch_conv<4, 4, true>(p, s);
-    if (p.ry == 2 && p.rx == 2) return launch_conv<2, 2, true>(p, s);
+    if (p.ry == p.rx && (p.ry == 4 || p.ry == 2)) {
+      const int cols = p.g.j0 + p.g.tw - (p.g.j0 & ~3);
+      dim3 grid((cols + TX - 1) / TX, (p.g.th + TY - 1) / TY);
+      static bool carve = false;   // all of the unified L1/shared array as shared memory (4+ blocks/SM)
+      if (!carve) {
+        cudaFuncSetAttribute(update_sep_kernel<4>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        cudaFuncSetAttribute(update_sep_kernel<2>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        carve = true;
+      }
+      if (p.ry == 4) update_sep_kernel<4><<<grid, NTHREADS, 0, s>>>(p);
+      else update_sep_kernel<2><<<grid, NTHREADS, 0, s>>>(p);
+      return cudaGetLastError();
+    }
     return launch_conv<-1, -1, true>(p, s);
   }
   if (p.ry == 2 && p.rx == 2) return launch_conv<2, 2, false>(p, s);
