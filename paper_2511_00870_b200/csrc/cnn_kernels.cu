@@ -16,9 +16,10 @@
 //    [group of 8 ch][130 positions][8 x bf16] -- the canonical K-major, no-swizzle
 //    UMMA layout (core matrix = 8 positions x 16 B); a CTA owns a 130-column strip and
 //    streams down its rows, every layer of the chain lagging the previous one by 3 rows;
-//  * warp roles: warp 0 loads input rows (x -> bf16 im2col rows for the first layer,
-//    or bf16 activation rows from HBM), warp 1 issues tcgen05.mma / tcgen05.commit
-//    (warp-uniform operands, one elected lane issues), warps 2.. are the epilogue in
+//  * warp roles: 4 producer warps load input rows (x -> bf16 im2col rows for the first
+//    layer, or one TMA bulk copy per 8-channel group for activation rows from HBM),
+//    4 MMA warps (one per layer) issue tcgen05.mma / tcgen05.commit (warp-uniform
+//    operands, one elected lane issues), the remaining warps are the epilogue in
 //    groups of 4 warps (one per TMEM lane quarter), group g owning layers l % G == g:
 //    tcgen05.ld -> +bias, ReLU, zero outside the image -> bf16 -> next layer's ring,
 //    or HBM / the fp32 residual G for the chain's last layer;
@@ -39,6 +40,9 @@ namespace {
 #ifndef PNPULA_EPI_GROUPS
 #define PNPULA_EPI_GROUPS 3
 #endif
+#ifndef PNPULA_EXP
+#define PNPULA_EXP 0   // timing experiments (exp/); 0 in every real build
+#endif
 constexpr int kRowPos = 130;                    // positions per ring row (128 MMA rows + 1 each side)
 constexpr int kEpiGroups = PNPULA_EPI_GROUPS;   // epilogue groups (each: 4 warps = 4 TMEM lane quarters)
 constexpr int kEpiWarps = 4 * kEpiGroups;
@@ -46,7 +50,12 @@ constexpr int kEpiWarps = 4 * kEpiGroups;
 #define PNPULA_MMA_WARPS 4
 #endif
 constexpr int kMmaWarps = PNPULA_MMA_WARPS;     // MMA issuers: warp 1+w owns layers l % kMmaWarps == w
-constexpr int kEpi0 = 1 + kMmaWarps;            // first epilogue warp
+#ifndef PNPULA_PROD_WARPS
+#define PNPULA_PROD_WARPS 4
+#endif
+constexpr int kProdWarps = PNPULA_PROD_WARPS;   // producers: warp w fills ring-0 rows f % kProdWarps == w
+constexpr int kMma0 = kProdWarps;               // first MMA warp (also allocates TMEM)
+constexpr int kEpi0 = kMma0 + kMmaWarps;        // first epilogue warp
 constexpr int kThreads = 32 * (kEpi0 + kEpiWarps);   // producer warp, MMA warps, epilogue warps
 constexpr int kRing = 4;                        // input-row ring slots per layer
 constexpr int kAcc = 4;                         // accumulator-row slots per layer (TMEM)
@@ -313,7 +322,7 @@ __global__ void __launch_bounds__(kThreads, 1) cnn_chunk_kernel(const __grid_con
     *abort_flag = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 1) {
+  if (warp == kMma0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                  "r"(tmem_cols)
                  : "memory");
@@ -359,10 +368,14 @@ __global__ void __launch_bounds__(kThreads, 1) cnn_chunk_kernel(const __grid_con
     auto nfill = [&](int l) { return (l == 0 && first) ? nout(0) : nout(l) + 2; };
     const int S = 3 * (NL - 1) + nfill(NL - 1) > nfill(0) ? 3 * (NL - 1) + nfill(NL - 1) : nfill(0);
 
-    if (warp == 0) {
-      // ================= producer: ring 0
+    if (warp < kProdWarps) {
+      // ================= producers: ring 0.  Warp w owns ring slot w for the whole kernel (fills
+      // with (Fcnt + f) & 3 == w): a slot's fills are then issued in order by one warp, which can
+      // never run two mbarrier phases ahead of the slot (a parity wait would pass spuriously).
+      static_assert(kProdWarps == kRing || kProdWarps == 1, "one producer per ring slot");
       const int nf = nfill(0);
-      for (int f = 0; f < nf; ++f) {
+      const int f0 = (kProdWarps == 1) ? 0 : (int)(((uint32_t)warp - Fcnt[0]) & 3u);
+      for (int f = f0; f < nf; f += kProdWarps) {
         const uint32_t Fg = Fcnt[0] + f;
         if (Fg >= 4 && !mbar_wait(bar_empty(0, Fg & 3), ((Fg >> 2) - 1) & 1, abort_flag, p.err, 1)) break;
         trace_ev(p.trace, tr_on && lane == 0, 1, f, 0);
@@ -433,9 +446,9 @@ __global__ void __launch_bounds__(kThreads, 1) cnn_chunk_kernel(const __grid_con
       }
     } else if (warp < kEpi0) {
       // ================= MMA issuers (whole warp walks the schedule; one elected lane issues).
-      // Warp 1 owns the even layers, warp 2 the odd ones, so one warp's barrier waits overlap
-      // the other's MMA issue; layers use disjoint TMEM columns and shared-memory operands.
-      const int mw = warp - 1;
+      // MMA warp w owns the layers l % kMmaWarps == w, so one warp's barrier waits overlap the
+      // others' MMA issue; layers use disjoint TMEM columns and shared-memory operands.
+      const int mw = warp - kMma0;
       bool ok = true;
       for (int s = 0; s < S && ok; ++s) {
 #pragma unroll
@@ -477,9 +490,17 @@ __global__ void __launch_bounds__(kThreads, 1) cnn_chunk_kernel(const __grid_con
             const uint64_t bd0 = make_desc(wbase, 3u * Cb * 16u, 128);
             const uint32_t bstep = 3u * Cb * 2u;      // (16 * 3Cb * 2 bytes) >> 4 per (dx, ks) block
             const uint32_t q0 = (uint32_t)(ilo - (f - 2));
+#if PNPULA_EXP == 4
+            // timing experiment only (wrong results): never split at the ring wrap
+            const uint32_t d1 = acc0;
+            const uint32_t id1 = make_idesc((int)((ihi - ilo + 1) * Cb)), id2 = id1;
+            const int n2x = 0;
+#define n2 n2x
+#else
             const uint32_t d1 = acc0 + (Ilo & 3) * Cb;
-            const uint32_t d2 = acc0;
             const uint32_t id1 = make_idesc((int)(n1 * Cb)), id2 = make_idesc((int)((n2 > 0 ? n2 : 1) * Cb));
+#endif
+            const uint32_t d2 = acc0;
             if (elect_one()) {
 #pragma unroll
               for (int dx = 0; dx < 3; ++dx) {
@@ -492,6 +513,9 @@ __global__ void __launch_bounds__(kThreads, 1) cnn_chunk_kernel(const __grid_con
                 }
               }
             }
+#if PNPULA_EXP == 4
+#undef n2
+#endif
           }
           __syncwarp();
           if (elect_one()) {
@@ -549,10 +573,17 @@ __global__ void __launch_bounds__(kThreads, 1) cnn_chunk_kernel(const __grid_con
           }
           float v[P];
           const uint32_t ta = taddr + (Ig & 3) * (uint32_t)P;
+#if PNPULA_EXP == 5
+          // timing experiment only (wrong results): no TMEM traffic in the epilogue
+#pragma unroll
+          for (int c = 0; c < P; ++c) v[c] = 0.f;
+          if (false) {
+#else
 #pragma unroll
           for (int c = 0; c < P; c += 16) tmem_load<16>(ta + c, v + c);
           tmem_wait_ld();
-          if (!im2col) {       // im2col MMAs overwrite (accumulate = 0): no re-zeroing needed
+          if (!im2col && PNPULA_EXP != 3) {       // im2col MMAs overwrite (accumulate = 0): no re-zeroing needed
+#endif
 #pragma unroll
             for (int c = 0; c < P; c += 16) tmem_zero<16>(ta + c);
             tmem_wait_st();
@@ -604,7 +635,7 @@ __global__ void __launch_bounds__(kThreads, 1) cnn_chunk_kernel(const __grid_con
   }
 
   // ---- teardown: make sure every tcgen05 op (and its mbarrier arrivals) has retired
-  if (warp >= 1 && warp < kEpi0) {
+  if (warp >= kMma0 && warp < kEpi0) {
     if (elect_one()) mma_commit(bar_done);       // one arrival per MMA warp
     __syncwarp();
     mbar_wait(bar_done, 0, abort_flag, p.err, 6);
@@ -612,7 +643,7 @@ __global__ void __launch_bounds__(kThreads, 1) cnn_chunk_kernel(const __grid_con
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 1) {
+  if (warp == kMma0) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tmem_cols)
                  : "memory");
   }
