@@ -1,5 +1,6 @@
 #!/bin/bash
-# kernel timing experiments: same bench, alternative library builds
+# kernel timing experiments: same bench, alternative library builds (WL=workload)
+WL=${WL:-c2}
 for v in "$@"; do
-  PNPULA_LIB=exp/lib_$v.so python bench.py --workload c2 --steps 30 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/var_$v.log 2>&1
+  PNPULA_LIB=exp/lib_$v.so python bench.py --workload $WL --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/var_$v.log 2>&1
 done

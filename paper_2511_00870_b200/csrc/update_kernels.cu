@@ -319,9 +319,20 @@ __global__ void __launch_bounds__(NTHREADS) update_sep_kernel(const __grid_const
   const int bi0 = g.i0 + blockIdx.y * TY;
   const int bj0 = (g.j0 & ~3) + blockIdx.x * TX;
   const int tid = threadIdx.x;
-  float ky[2 * R + 1], kx[2 * R + 1];
+  const float *ky = p.ky, *kx = p.kx;   // parameter space: FFMA constant-bank operands
+
+  // the update's own operands (x, G, z, mean, M2 of this thread's 2 rows x 1 quad) are
+  // requested first, so their latency overlaps the staging loads and the stencil passes
+  const int q4 = tid & 15, a2 = tid >> 4;   // 16 quads x 16 row pairs
+  const int gj4 = bj0 + 4 * q4;
+  bool act[2];
+  QuadIn qin[2];
 #pragma unroll
-  for (int i = 0; i <= 2 * R; ++i) { ky[i] = p.ky[i]; kx[i] = p.kx[i]; }
+  for (int r = 0; r < 2; ++r) {
+    const int gi = bi0 + 2 * a2 + r;
+    act[r] = !(gi >= g.i0 + g.th || gj4 >= g.j0 + g.tw || gj4 + 4 <= g.j0);
+    if (act[r]) ula_load(p, gi, gj4, qin[r]);
+  }
 
   // phase 0: x on block (+) 2R, float4 (columns are quad-aligned in the padded buffer)
   for (int e = tid; e < XR * (XC / 4); e += NTHREADS) {
@@ -416,16 +427,7 @@ __global__ void __launch_bounds__(NTHREADS) update_sep_kernel(const __grid_const
   __syncthreads();
   // phase 4: g = sum_p ky[p+R] T2[a+R+p][b] for 2 rows x 1 quad per thread, then the update
   {
-    const int q = tid & 15, a2 = tid >> 4;   // 16 quads x 16 row pairs
-    const int gj4 = bj0 + 4 * q;
-    bool act[2];
-    QuadIn qin[2];
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {            // issue the update's global loads first
-      const int gi = bi0 + 2 * a2 + r;
-      act[r] = !(gi >= g.i0 + g.th || gj4 >= g.j0 + g.tw || gj4 + 4 <= g.j0);
-      if (act[r]) ula_load(p, gi, gj4, qin[r]);
-    }
+    const int q = q4;
     float col[2 * R + 2][4];
 #pragma unroll
     for (int i = 0; i < 2 * R + 2; ++i) {
