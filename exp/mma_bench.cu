@@ -18,7 +18,7 @@ __host__ __device__ constexpr uint32_t make_idesc(int N) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
 }
 
-template <int N, bool TS>
+template <int N, bool TS, int NACC = 1, int ISS = 1>
 __global__ void __launch_bounds__(128, 1) bench(int iters, long long *out) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint32_t tslot;
@@ -26,7 +26,7 @@ __global__ void __launch_bounds__(128, 1) bench(int iters, long long *out) {
   const int warp = threadIdx.x >> 5;
   for (int i = threadIdx.x; i < 64 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t *>(smem)[i] = 0x3c003c00u;
   if (threadIdx.x == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&bar)), "r"(ISS));
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   if (warp == 0) {
@@ -39,7 +39,7 @@ __global__ void __launch_bounds__(128, 1) bench(int iters, long long *out) {
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tbase = tslot;
   long long t0 = 0, t1 = 0;
-  if (threadIdx.x == 0) {
+  if ((threadIdx.x & 31) == 0 && warp < ISS) {
     const uint32_t s0 = smem_u32(smem);
     const uint64_t ad = make_desc(s0, 2080, 128);             // A: 128 rows, activation-ring geometry
     const uint64_t bd = make_desc(s0 + 32768, N * 16, 128);   // B: N rows
@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(128, 1) bench(int iters, long long *out) {
       } else {
         asm volatile(
             "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %3, 0;\n\t"
-            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %4, p;\n\t}" ::"r"(tbase),
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %4, p;\n\t}" ::"r"(tbase + (uint32_t)(((i % NACC) + warp * NACC) * N)),
             "l"(ad + (uint64_t)((i & 3) * 1)), "l"(bd), "r"(1), "r"(id));
       }
     }
@@ -65,18 +65,18 @@ __global__ void __launch_bounds__(128, 1) bench(int iters, long long *out) {
                    : "=r"(ok) : "r"(smem_u32(&bar)));
     }
     t1 = clock64();
-    out[blockIdx.x] = t1 - t0;
+    if (warp == 0) out[blockIdx.x] = t1 - t0;
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tbase));
 }
 
-template <int N, bool TS>
+template <int N, bool TS, int NACC = 1, int ISS = 1>
 void run(int sms) {
   long long *d;
   cudaMalloc(&d, sms * sizeof(long long));
-  auto k = bench<N, TS>;
+  auto k = bench<N, TS, NACC, ISS>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
   const int iters = 4096;
   k<<<sms, 128, 64 * 1024>>>(64, d);
@@ -95,8 +95,8 @@ void run(int sms) {
   double avg = 0;
   for (int i = 0; i < sms; ++i) avg += h[i];
   avg /= sms;
-  const double flops = 2.0 * 128 * N * 16 * (double)iters * sms;
-  printf("N=%3d %s: %7.1f cyc/MMA (ideal %5.1f)  %7.1f TFLOP/s  err=%s\n", N, TS ? "TS" : "SS", avg / iters,
+  const double flops = 2.0 * 128 * N * 16 * (double)iters * sms * ISS;
+  printf("N=%3d %s acc=%d issuers=%d: %7.1f cyc/MMA (ideal %5.1f)  %7.1f TFLOP/s  err=%s\n", N, TS ? "TS" : "SS", NACC, ISS, avg / iters / ISS,
          128.0 * N / 256.0, flops / (ms * 1e-3) / 1e12, cudaGetErrorString(cudaGetLastError()));
   cudaFree(d);
 }
@@ -112,5 +112,15 @@ int main() {
   run<32, true>(sms);
   run<96, true>(sms);
   run<256, true>(sms);
+  run<32, false, 4>(sms);
+  run<64, false, 4>(sms);
+  run<96, false, 4>(sms);
+  run<32, false, 1, 2>(sms);
+  run<64, false, 1, 2>(sms);
+  run<96, false, 1, 2>(sms);
+  run<32, false, 2, 2>(sms);
+  run<96, false, 2, 2>(sms);
+  run<32, true, 4>(sms);
+  run<64, true, 4>(sms);
   return 0;
 }

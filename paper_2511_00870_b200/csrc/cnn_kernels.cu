@@ -18,11 +18,14 @@
 //    streams down its rows, every layer of the chain lagging the previous one by 3 rows;
 //  * warp roles: 4 producer warps load input rows (x -> bf16 im2col rows for the first
 //    layer, or one TMA bulk copy per 8-channel group for activation rows from HBM),
-//    4 MMA warps (one per layer) issue tcgen05.mma / tcgen05.commit (warp-uniform
-//    operands, one elected lane issues), the remaining warps are the epilogue in
+//    up to 4 MMA warps (one per layer) issue tcgen05.mma / tcgen05.commit (warp-uniform
+//    operands, one elected lane issues), the remaining warps are the epilogue in up to 4
 //    groups of 4 warps (one per TMEM lane quarter), group g owning layers l % G == g:
 //    tcgen05.ld -> +bias, ReLU, zero outside the image -> bf16 -> next layer's ring,
 //    or HBM / the fp32 residual G for the chain's last layer;
+//  * every role loops over schedule steps and its own layers with a run-time layer index
+//    (one compact code path per role: the layer-unrolled form lost ~20% of its warp time
+//    to instruction-fetch stalls, profiles/r01_cnn_icache.md);
 //  * fp32 accumulation in TMEM.
 // Every output pixel's arithmetic (K order, rounding points) is independent of the
 // strip/tile it falls in, so results are bitwise identical for every tile grid.
@@ -38,27 +41,35 @@ namespace pnpula {
 namespace {
 
 #ifndef PNPULA_EPI_GROUPS
-#define PNPULA_EPI_GROUPS 3
+#define PNPULA_EPI_GROUPS 4
 #endif
 #ifndef PNPULA_EXP
 #define PNPULA_EXP 0   // timing experiments (exp/); 0 in every real build
 #endif
 constexpr int kRowPos = 130;                    // positions per ring row (128 MMA rows + 1 each side)
-constexpr int kEpiGroups = PNPULA_EPI_GROUPS;   // epilogue groups (each: 4 warps = 4 TMEM lane quarters)
-constexpr int kEpiWarps = 4 * kEpiGroups;
+constexpr int kEpiGroups = PNPULA_EPI_GROUPS;   // max epilogue groups (each: 4 warps = 4 TMEM lane quarters)
 #ifndef PNPULA_MMA_WARPS
 #define PNPULA_MMA_WARPS 4
 #endif
-constexpr int kMmaWarps = PNPULA_MMA_WARPS;     // MMA issuers: warp 1+w owns layers l % kMmaWarps == w
+constexpr int kMmaWarps = PNPULA_MMA_WARPS;     // max MMA issuers: MMA warp w owns layers l % MW == w
 #ifndef PNPULA_PROD_WARPS
 #define PNPULA_PROD_WARPS 4
 #endif
 constexpr int kProdWarps = PNPULA_PROD_WARPS;   // producers: warp w fills ring-0 rows f % kProdWarps == w
 constexpr int kMma0 = kProdWarps;               // first MMA warp (also allocates TMEM)
-constexpr int kEpi0 = kMma0 + kMmaWarps;        // first epilogue warp
-constexpr int kThreads = 32 * (kEpi0 + kEpiWarps);   // producer warp, MMA warps, epilogue warps
+// Per chain length NL: MMA warps MW and epilogue groups EG (at most one per layer), first
+// epilogue warp, block size -- producer warps, MMA warps, epilogue warps.
+__host__ __device__ constexpr int mma_warps(int nl) { return nl < kMmaWarps ? nl : kMmaWarps; }
+__host__ __device__ constexpr int epi_groups(int nl) { return nl < kEpiGroups ? nl : kEpiGroups; }
+__host__ __device__ constexpr int epi0(int nl) { return kMma0 + mma_warps(nl); }
+__host__ __device__ constexpr int block_threads(int nl) { return 32 * (epi0(nl) + 4 * epi_groups(nl)); }
 constexpr int kRing = 4;                        // input-row ring slots per layer
 constexpr int kAcc = 4;                         // accumulator-row slots per layer (TMEM)
+#ifndef PNPULA_LAG
+#define PNPULA_LAG 3
+#endif
+constexpr int kLag = PNPULA_LAG;                // schedule steps between consecutive layers
+static_assert(kLag >= 3 && kLag <= 5, "layer l+1 needs rows completed 2 fills later; ring holds 4");
 
 struct SmemLayout {
   uint32_t ring_off[kMaxChunk];
@@ -96,8 +107,8 @@ __host__ __device__ inline SmemLayout make_layout(int P, int nl, int first, int 
   off = align_up(off + (uint32_t)nl * P * 4u, 128);
   L.bar_off = off;   // per layer: full[4], empty[4], tfull[4], tempty[4]
   off = align_up(off + (uint32_t)nl * 16u * 8u, 128);
-  L.misc_off = off;  // tmem address, abort flag, drain barrier
-  off += 16;
+  L.misc_off = off;  // tmem address, abort flag, drain barrier, per-layer table {ring, slot, w, 0}
+  off += 16 + 16u * (uint32_t)nl;
   L.total = align_up(off, 128);
   return L;
 }
@@ -258,11 +269,11 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 
 // Pipeline trace (diagnostics only; p.trace == nullptr in production): one 64-bit record
 // per event = clock64 << 20 | code << 16 | step << 4 | layer.  Each tracing thread owns a
-// private region (code 1-2: producer, 3-5: MMA, 6-11: epilogue), plain stores only.
+// private region (code 1-2: producer, 3-5 and 14: MMA, 6-11: epilogue), plain stores only.
 __device__ __forceinline__ void trace_ev(unsigned long long *tr, bool on, int code, int s, int l) {
   if (!on) return;
   const unsigned long long t = (unsigned long long)clock64();
-  const int region = code <= 2 ? 0 : code <= 5 ? 1 : 2;
+  const int region = code <= 2 ? 0 : (code <= 5 || code == 14) ? 1 : 2;
   const unsigned idx = (unsigned)(s * 8 + l) * 8 + (unsigned)(code & 7);
   if (idx < (1u << 18))
     tr[1 + (region << 18) + idx] =
@@ -271,7 +282,9 @@ __device__ __forceinline__ void trace_ev(unsigned long long *tr, bool on, int co
 
 // ---------------------------------------------------------------- the kernel
 template <int P, int NL>
-__global__ void __launch_bounds__(kThreads, 1) cnn_chunk_kernel(const __grid_constant__ CnnChunkParams p) {
+__global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const __grid_constant__ CnnChunkParams p) {
+  constexpr int kMmaWarps = mma_warps(NL), kEpiGroups = epi_groups(NL), kEpi0 = epi0(NL);
+  constexpr int kThreads = block_threads(NL);
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr int G = P / 8;              // channel groups of 8
   constexpr int KS = P / 16;            // K steps per tap
@@ -320,6 +333,8 @@ __global__ void __launch_bounds__(kThreads, 1) cnn_chunk_kernel(const __grid_con
       }
     mbar_init(bar_done, kMmaWarps);
     *abort_flag = 0;
+    uint4 *tab = reinterpret_cast<uint4 *>(smem + L.misc_off + 16);
+    for (int l = 0; l < NL; ++l) tab[l] = make_uint4(L.ring_off[l], L.slot_bytes[l], L.w_off[l], 0u);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == kMma0) {
@@ -347,11 +362,17 @@ __global__ void __launch_bounds__(kThreads, 1) cnn_chunk_kernel(const __grid_con
   const int strips = p.strips;
   const int R = p.rows_per_unit;
   const int units = p.units;
-
-  // running counters (identical in every role): input-row fills and output rows before this unit
-  uint32_t Fcnt[NL], Ocnt[NL];
-#pragma unroll
-  for (int l = 0; l < NL; ++l) { Fcnt[l] = 0; Ocnt[l] = 0; }
+  // The role loops below index layers at run time (no unrolling over layers): every warp
+  // executes one compact code path, which keeps the hot code inside the instruction cache
+  // (the layer-unrolled form spent ~20% of its warp time in instruction-fetch stalls).
+  // Per-layer shared-memory offsets come from the table written at setup.
+  const uint4 *ltab = reinterpret_cast<const uint4 *>(smem + L.misc_off + 16);   // {ring, slot, w, -}
+  auto is_im2col = [&](int l) { return l == 0 && first; };
+  // running counters before the current unit (k = units this CTA finished, sumRn = their rows):
+  // fills of layer l: sumRn + k (2 (NL-1-l) + 2 [l not im2col]); output rows: sumRn + k 2 (NL-1-l)
+  uint32_t sumRn = 0, kdone = 0;
+  auto Fcnt = [&](int l) { return sumRn + kdone * (uint32_t)(2 * (NL - 1 - l) + (is_im2col(l) ? 0 : 2)); };
+  auto Ocnt = [&](int l) { return sumRn + kdone * (uint32_t)(2 * (NL - 1 - l)); };
 
   for (int u = blockIdx.x; u < units; u += gridDim.x) {
     if (*abort_flag) break;
@@ -365,8 +386,8 @@ __global__ void __launch_bounds__(kThreads, 1) cnn_chunk_kernel(const __grid_con
     // layer l: nout(l) = Rn + 2 (NL-1-l) output rows starting at global row r_lo-(NL-1-l);
     // its input fills are rows r0(l)-1 .. (nout+2 fills), or nout im2col rows for an im2col layer.
     auto nout = [&](int l) { return Rn + 2 * (NL - 1 - l); };
-    auto nfill = [&](int l) { return (l == 0 && first) ? nout(0) : nout(l) + 2; };
-    const int S = 3 * (NL - 1) + nfill(NL - 1) > nfill(0) ? 3 * (NL - 1) + nfill(NL - 1) : nfill(0);
+    auto nfill = [&](int l) { return is_im2col(l) ? nout(0) : nout(l) + 2; };
+    const int S = kLag * (NL - 1) + nfill(NL - 1) > nfill(0) ? kLag * (NL - 1) + nfill(NL - 1) : nfill(0);
 
     if (warp < kProdWarps) {
       // ================= producers: ring 0.  Warp w owns ring slot w for the whole kernel (fills
@@ -374,12 +395,14 @@ __global__ void __launch_bounds__(kThreads, 1) cnn_chunk_kernel(const __grid_con
       // never run two mbarrier phases ahead of the slot (a parity wait would pass spuriously).
       static_assert(kProdWarps == kRing || kProdWarps == 1, "one producer per ring slot");
       const int nf = nfill(0);
-      const int f0 = (kProdWarps == 1) ? 0 : (int)(((uint32_t)warp - Fcnt[0]) & 3u);
+      const uint32_t F0 = Fcnt(0);
+      const uint32_t ring0 = ltab[0].x, slot0 = ltab[0].y;
+      const int f0 = (kProdWarps == 1) ? 0 : (int)(((uint32_t)warp - F0) & 3u);
       for (int f = f0; f < nf; f += kProdWarps) {
-        const uint32_t Fg = Fcnt[0] + f;
+        const uint32_t Fg = F0 + f;
         if (Fg >= 4 && !mbar_wait(bar_empty(0, Fg & 3), ((Fg >> 2) - 1) & 1, abort_flag, p.err, 1)) break;
         trace_ev(p.trace, tr_on && lane == 0, 1, f, 0);
-        uint8_t *slot = smem + L.ring_off[0] + (Fg & 3) * L.slot_bytes[0];
+        uint8_t *slot = smem + ring0 + (Fg & 3) * slot0;
         if (first) {
           // im2col row for layer-1 output row o: 9 taps of x (bf16), K padded to 16
           const int o = r_lo - NL + f + 1;
@@ -405,6 +428,9 @@ __global__ void __launch_bounds__(kThreads, 1) cnn_chunk_kernel(const __grid_con
             *reinterpret_cast<uint4 *>(slot + m * 16) = a0;
             *reinterpret_cast<uint4 *>(slot + 2048 + m * 16) = a1;
           }
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(bar_full(0, Fg & 3));
         } else {
           // activation row from HBM: one TMA bulk copy per 8-channel group (16 B per position,
           // contiguous in the [group][row][col][8] layout); positions outside the stored region
@@ -415,11 +441,13 @@ __global__ void __launch_bounds__(kThreads, 1) cnn_chunk_kernel(const __grid_con
           const int qlo = row_ok ? max(0, p.a_j0 - c0) : kRowPos;
           const int qhi = row_ok ? min(kRowPos, p.a_j0 + p.a_cols - c0) : kRowPos;
           const uint32_t nbytes = qhi > qlo ? (uint32_t)(qhi - qlo) * 16u : 0u;
-          for (int e = lane; e < G * kRowPos; e += 32) {
-            const int gq = e / kRowPos, q = e - gq * kRowPos;
-            if (q < qlo || q >= qhi) *reinterpret_cast<uint4 *>(slot + gq * GS + q * 16) = make_uint4(0, 0, 0, 0);
+          if (qlo > 0 || qhi < kRowPos) {
+            for (int e = lane; e < G * kRowPos; e += 32) {
+              const int gq = e / kRowPos, q = e - gq * kRowPos;
+              if (q < qlo || q >= qhi) *reinterpret_cast<uint4 *>(slot + gq * GS + q * 16) = make_uint4(0, 0, 0, 0);
+            }
+            fence_proxy_async();
           }
-          fence_proxy_async();
           __syncwarp();
           if (lane == 0) {
             const uint32_t fb = bar_full(0, Fg & 3);
@@ -436,12 +464,7 @@ __global__ void __launch_bounds__(kThreads, 1) cnn_chunk_kernel(const __grid_con
                     : "memory");
             }
           }
-          trace_ev(p.trace, tr_on && lane == 0, 2, f, 0);
-          continue;
         }
-        fence_proxy_async();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(bar_full(0, Fg & 3));
         trace_ev(p.trace, tr_on && lane == 0, 2, f, 0);
       }
     } else if (warp < kEpi0) {
@@ -451,28 +474,30 @@ __global__ void __launch_bounds__(kThreads, 1) cnn_chunk_kernel(const __grid_con
       const int mw = warp - kMma0;
       bool ok = true;
       for (int s = 0; s < S && ok; ++s) {
-#pragma unroll
-        for (int l = 0; l < NL; ++l) {
-          const int f = s - 3 * l;                     // input fill processed by layer l at step s
+#pragma unroll 1
+        for (int l = mw; l < NL; l += kMmaWarps) {
+          const int f = s - kLag * l;                  // input fill processed by layer l at step s
           const int no = nout(l);
-          if (!ok || (l % kMmaWarps) != mw || f < 0 || f >= nfill(l)) continue;
-          const bool im2col = (l == 0) && first;
+          if (f < 0 || f >= nfill(l)) continue;
+          const bool im2col = is_im2col(l);
           const bool netlast = (l == NL - 1) && last;
-          const uint32_t Fg = Fcnt[l] + (uint32_t)f;
+          const uint32_t Fg = Fcnt(l) + (uint32_t)f;
           trace_ev(p.trace, tr_on && lane == 0, 3, s, l);
           ok = mbar_wait(bar_full(l, Fg & 3), (Fg >> 2) & 1, abort_flag, p.err, 2);
+          trace_ev(p.trace, tr_on && lane == 0, 14, s, l);
           // output row that receives its first contribution (im2col: the only one)
-          const int inew = f;
-          const uint32_t Ig = Ocnt[l] + (uint32_t)inew;
-          if (ok && inew < no && Ig >= (uint32_t)kAcc)
+          const uint32_t O0 = Ocnt(l);
+          const uint32_t Ig = O0 + (uint32_t)f;
+          if (ok && f < no && Ig >= (uint32_t)kAcc && PNPULA_EXP != 7)
             ok = mbar_wait(bar_tempty(l, Ig & 3), ((Ig >> 2) - 1) & 1, abort_flag, p.err, 3);
           ok = __shfl_sync(0xffffffffu, ok ? 1 : 0, 0) != 0;
           trace_ev(p.trace, tr_on && lane == 0, 4, s, l);
-          if (!ok) continue;
+          if (!ok) break;
           tc_fence_after();
+          const uint4 lt = ltab[l];
           const uint32_t acc0 = tmem_base + (uint32_t)(l * kAcc * P);
-          const uint32_t wbase = sbase + L.w_off[l];
-          const uint32_t slot = sbase + L.ring_off[l] + (Fg & 3) * L.slot_bytes[l];
+          const uint32_t wbase = sbase + lt.z;
+          const uint32_t slot = sbase + lt.x + (Fg & 3) * lt.y;
           if (im2col) {
             const uint64_t ad = make_desc(slot, 2048, 128);
             const uint64_t bd = make_desc(wbase, (uint32_t)P * 16, 128);
@@ -483,23 +508,15 @@ __global__ void __launch_bounds__(kThreads, 1) cnn_chunk_kernel(const __grid_con
             const uint32_t Cb = netlast ? 16u : (uint32_t)P;
             const int ilo = f - 2 > 0 ? f - 2 : 0;
             const int ihi = f < no - 1 ? f : no - 1;
-            const uint32_t Ilo = Ocnt[l] + (uint32_t)ilo;
+            const uint32_t Ilo = O0 + (uint32_t)ilo;
             const int n1 = (int)min((uint32_t)(ihi - ilo + 1), kAcc - (Ilo & 3));   // rows before the wrap
             const int n2 = (ihi - ilo + 1) - n1;
             const uint64_t ad0 = make_desc(slot, GS, 128);
             const uint64_t bd0 = make_desc(wbase, 3u * Cb * 16u, 128);
             const uint32_t bstep = 3u * Cb * 2u;      // (16 * 3Cb * 2 bytes) >> 4 per (dx, ks) block
             const uint32_t q0 = (uint32_t)(ilo - (f - 2));
-#if PNPULA_EXP == 4
-            // timing experiment only (wrong results): never split at the ring wrap
-            const uint32_t d1 = acc0;
-            const uint32_t id1 = make_idesc((int)((ihi - ilo + 1) * Cb)), id2 = id1;
-            const int n2x = 0;
-#define n2 n2x
-#else
             const uint32_t d1 = acc0 + (Ilo & 3) * Cb;
             const uint32_t id1 = make_idesc((int)(n1 * Cb)), id2 = make_idesc((int)((n2 > 0 ? n2 : 1) * Cb));
-#endif
             const uint32_t d2 = acc0;
             if (elect_one()) {
 #pragma unroll
@@ -513,15 +530,12 @@ __global__ void __launch_bounds__(kThreads, 1) cnn_chunk_kernel(const __grid_con
                 }
               }
             }
-#if PNPULA_EXP == 4
-#undef n2
-#endif
           }
           __syncwarp();
           if (elect_one()) {
             mma_commit(bar_empty(l, Fg & 3));            // input row consumed
             const int ic = im2col ? f : f - 2;           // output row completed by this group
-            if (ic >= 0 && ic < no) mma_commit(bar_tfull(l, (Ocnt[l] + (uint32_t)ic) & 3));
+            if (ic >= 0 && ic < no) mma_commit(bar_tfull(l, (O0 + (uint32_t)ic) & 3));
           }
           __syncwarp();
           trace_ev(p.trace, tr_on && lane == 0, 5, s, l);
@@ -539,21 +553,37 @@ __global__ void __launch_bounds__(kThreads, 1) cnn_chunk_kernel(const __grid_con
       const bool trw = tr_on && lane == 0 && quarter == 2;
       bool ok = true;
       for (int s = 0; s < S && ok; ++s) {
-#pragma unroll
-        for (int l = 0; l < NL; ++l) {
-          if ((l % kEpiGroups) != grp) continue;
-          const bool im2col = (l == 0) && first;
-          const int f = s - 3 * l;
+#pragma unroll 1
+        for (int l = grp; l < NL; l += kEpiGroups) {
+          const bool im2col = is_im2col(l);
+          const int f = s - kLag * l;
           const int ic = im2col ? f : f - 2;           // output row completed at this step
           const int no = nout(l);
-          if (!ok || f < 0 || f >= nfill(l) || ic < 0 || ic >= no) continue;
-          const uint32_t Ig = Ocnt[l] + (uint32_t)ic;
-          if (!mbar_wait(bar_tfull(l, Ig & 3), (Ig >> 2) & 1, abort_flag, p.err, 4)) { ok = false; continue; }
+          if (f < 0 || f >= nfill(l) || ic < 0 || ic >= no) continue;
+          const uint32_t Ig = Ocnt(l) + (uint32_t)ic;
+          if (!mbar_wait(bar_tfull(l, Ig & 3), (Ig >> 2) & 1, abort_flag, p.err, 4)) { ok = false; break; }
           trace_ev(p.trace, trw, 6, s, l);
           tc_fence_after();
           const uint32_t taddr = tmem_base + lane_base + (uint32_t)(l * kAcc * P);
           const int o = r_lo - (NL - 1 - l) + ic;      // global output row
           const bool inside = col_in && o >= 0 && o < p.ny;
+#if PNPULA_EXP == 8
+          // timing experiment only (wrong results): the epilogue only passes the barriers on
+          {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bar_tempty(l, Ig & 3));
+            if (l < NL - 1) {
+              const uint32_t Fg = Fcnt(l + 1) + (uint32_t)ic;
+              if (Fg >= 4 && !mbar_wait(bar_empty(l + 1, Fg & 3), ((Fg >> 2) - 1) & 1, abort_flag, p.err, 5)) {
+                ok = false;
+                break;
+              }
+              __syncwarp();
+              if (lane == 0) mbar_arrive(bar_full(l + 1, Fg & 3));
+            }
+            continue;
+          }
+#endif
           if ((l == NL - 1) && last) {
             // network output G (no ReLU), column 0 of the 16-column slot
             float v[1];
@@ -573,17 +603,10 @@ __global__ void __launch_bounds__(kThreads, 1) cnn_chunk_kernel(const __grid_con
           }
           float v[P];
           const uint32_t ta = taddr + (Ig & 3) * (uint32_t)P;
-#if PNPULA_EXP == 5
-          // timing experiment only (wrong results): no TMEM traffic in the epilogue
-#pragma unroll
-          for (int c = 0; c < P; ++c) v[c] = 0.f;
-          if (false) {
-#else
 #pragma unroll
           for (int c = 0; c < P; c += 16) tmem_load<16>(ta + c, v + c);
           tmem_wait_ld();
-          if (!im2col && PNPULA_EXP != 3) {       // im2col MMAs overwrite (accumulate = 0): no re-zeroing needed
-#endif
+          if (!im2col) {       // im2col MMAs overwrite (accumulate = 0): no re-zeroing needed
 #pragma unroll
             for (int c = 0; c < P; c += 16) tmem_zero<16>(ta + c);
             tmem_wait_st();
@@ -592,22 +615,24 @@ __global__ void __launch_bounds__(kThreads, 1) cnn_chunk_kernel(const __grid_con
           __syncwarp();
           if (lane == 0) mbar_arrive(bar_tempty(l, Ig & 3));
           trace_ev(p.trace, trw, 7, s, l);
-          const float *bl = sbias + l * P;
+          const float4 *bl = reinterpret_cast<const float4 *>(sbias + l * P);
           uint32_t w[P / 2];
 #pragma unroll
-          for (int c = 0; c < P; c += 2) {
-            const float v0 = inside ? fmaxf(v[c] + bl[c], 0.f) : 0.f;
-            const float v1 = inside ? fmaxf(v[c + 1] + bl[c + 1], 0.f) : 0.f;
-            w[c / 2] = pack_bf16(v0, v1);
+          for (int c = 0; c < P; c += 4) {
+            const float4 b4 = bl[c / 4];
+            w[c / 2] = pack_bf16(inside ? fmaxf(v[c] + b4.x, 0.f) : 0.f, inside ? fmaxf(v[c + 1] + b4.y, 0.f) : 0.f);
+            w[c / 2 + 1] = pack_bf16(inside ? fmaxf(v[c + 2] + b4.z, 0.f) : 0.f, inside ? fmaxf(v[c + 3] + b4.w, 0.f) : 0.f);
           }
           if (l < NL - 1) {
             // next layer's input fill = this layer's output row index ic
-            const uint32_t Fg = Fcnt[l + 1] + (uint32_t)ic;
+            const uint32_t Fg = Fcnt(l + 1) + (uint32_t)ic;
             if (Fg >= 4 && !mbar_wait(bar_empty(l + 1, Fg & 3), ((Fg >> 2) - 1) & 1, abort_flag, p.err, 5)) {
               ok = false;
-              continue;
+              break;
             }
-            uint8_t *slot = smem + L.ring_off[l + 1] + (Fg & 3) * L.slot_bytes[l + 1] + (m + 1) * 16;
+            trace_ev(p.trace, trw, 9, s, l);
+            const uint4 lt = ltab[l + 1];
+            uint8_t *slot = smem + lt.x + (Fg & 3) * lt.y + (m + 1) * 16;
 #pragma unroll
             for (int gq = 0; gq < G; ++gq)
               *reinterpret_cast<uint4 *>(slot + gq * GS) = make_uint4(w[4 * gq], w[4 * gq + 1], w[4 * gq + 2], w[4 * gq + 3]);
@@ -626,12 +651,8 @@ __global__ void __launch_bounds__(kThreads, 1) cnn_chunk_kernel(const __grid_con
         }
       }
     }
-    // advance running counters (all roles identically)
-#pragma unroll
-    for (int l = 0; l < NL; ++l) {
-      Fcnt[l] += (uint32_t)nfill(l);
-      Ocnt[l] += (uint32_t)nout(l);
-    }
+    sumRn += (uint32_t)Rn;
+    ++kdone;
   }
 
   // ---- teardown: make sure every tcgen05 op (and its mbarrier arrivals) has retired
@@ -674,7 +695,7 @@ cudaError_t launch_pn(const CnnChunkParams &p0, int num_sms, cudaStream_t s) {
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
   if (e != cudaSuccess) return e;
   const int grid = p.units < num_sms ? p.units : num_sms;
-  kfn<<<grid, kThreads, L.total, s>>>(p);
+  kfn<<<grid, block_threads(NL), L.total, s>>>(p);
   return cudaGetLastError();
 }
 

@@ -33,11 +33,31 @@ def report(fn, steps=range(24, 30)):
             if (3, si, j) not in ev:
                 continue
             seg = [('wfull', 3, 10), ('wtmem', 10, 4), ('issue', 4, 5), ('->tfull', 5, 6), ('ld', 6, 7),
-                   ('xbar', 7, 9), ('comb', 9, 11), ('st', 11, 8), ('epi', 6, 8)]
+                   ('wempty', 7, 9), ('st', 9, 8), ('epi', 6, 8)]
             parts.append(f"L{j} " + ' '.join(f"{nm}={d(ev, a, b, si, j)}" for nm, a, b in seg if d(ev, a, b, si, j) is not None))
         print(f"s={si} t={t0}: " + ' | '.join(parts))
 
 
+
+
+def summary(fn, lo=20, hi=None):
+    """Mean per-step segment durations (cycles) over steps [lo, hi) for every layer."""
+    ev = load(fn)
+    L = max(li for c, si, li in ev) + 1
+    S = max(si for c, si, li in ev) + 1
+    hi = hi or S - 20
+    segs = [('wfull', 3, 14), ('wtmem', 14, 4), ('issue', 4, 5), ('ld', 6, 7), ('wempty', 7, 9), ('st', 9, 8)]
+    print(fn, f"steps {lo}..{hi}, step time {np.mean([ev[(3, s + 1, 1)] - ev[(3, s, 1)] for s in range(lo, hi) if (3, s, 1) in ev and (3, s + 1, 1) in ev]):.0f}")
+    for l in range(L):
+        out = []
+        for nm, a, b in segs:
+            v = [d(ev, a, b, s, l) for s in range(lo, hi)]
+            v = [x for x in v if x is not None]
+            if v:
+                out.append(f"{nm}={np.mean(v):.0f}")
+        print(f"  L{l}: " + ' '.join(out))
+
+
 if __name__ == "__main__":
     for fn in sys.argv[1:]:
-        report(fn)
+        summary(fn)
