@@ -23,9 +23,10 @@
 //    groups of 4 warps (one per TMEM lane quarter), group g owning layers l % G == g:
 //    tcgen05.ld -> +bias, ReLU, zero outside the image -> bf16 -> next layer's ring,
 //    or HBM / the fp32 residual G for the chain's last layer;
-//  * every role loops over schedule steps and its own layers with a run-time layer index
-//    (one compact code path per role: the layer-unrolled form lost ~20% of its warp time
-//    to instruction-fetch stalls, profiles/r01_cnn_icache.md);
+//  * each role runs one compact code path with a run-time layer index (a warp that owns a
+//    single layer walks its fills / output rows directly; the layer-unrolled form lost
+//    ~20% of its warp time to instruction-fetch stalls, profiles/r01_cnn_icache.md);
+//    the pipeline trace is compiled only with -DPNPULA_TRACE=1;
 //  * fp32 accumulation in TMEM.
 // Every output pixel's arithmetic (K order, rounding points) is independent of the
 // strip/tile it falls in, so results are bitwise identical for every tile grid.
@@ -270,8 +271,11 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 // Pipeline trace (diagnostics only; p.trace == nullptr in production): one 64-bit record
 // per event = clock64 << 20 | code << 16 | step << 4 | layer.  Each tracing thread owns a
 // private region (code 1-2: producer, 3-5 and 14: MMA, 6-11: epilogue), plain stores only.
+#ifndef PNPULA_TRACE
+#define PNPULA_TRACE 0   // 1: compile the pipeline trace (diagnostics builds only)
+#endif
 __device__ __forceinline__ void trace_ev(unsigned long long *tr, bool on, int code, int s, int l) {
-  if (!on) return;
+  if (!PNPULA_TRACE || !on) return;
   const unsigned long long t = (unsigned long long)clock64();
   const int region = code <= 2 ? 0 : (code <= 5 || code == 14) ? 1 : 2;
   const unsigned idx = (unsigned)(s * 8 + l) * 8 + (unsigned)(code & 7);
@@ -472,13 +476,11 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
       // MMA warp w owns the layers l % kMmaWarps == w, so one warp's barrier waits overlap the
       // others' MMA issue; layers use disjoint TMEM columns and shared-memory operands.
       const int mw = warp - kMma0;
-      bool ok = true;
-      for (int s = 0; s < S && ok; ++s) {
-#pragma unroll 1
-        for (int l = mw; l < NL; l += kMmaWarps) {
-          const int f = s - kLag * l;                  // input fill processed by layer l at step s
+      // one schedule step of layer l: input fill f (step s = f + kLag l); false on abort
+      auto mma_step = [&](const int l, const int f) -> bool {
+          const int s = f + kLag * l;
           const int no = nout(l);
-          if (f < 0 || f >= nfill(l)) continue;
+          bool ok;
           const bool im2col = is_im2col(l);
           const bool netlast = (l == NL - 1) && last;
           const uint32_t Fg = Fcnt(l) + (uint32_t)f;
@@ -492,7 +494,7 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
             ok = mbar_wait(bar_tempty(l, Ig & 3), ((Ig >> 2) - 1) & 1, abort_flag, p.err, 3);
           ok = __shfl_sync(0xffffffffu, ok ? 1 : 0, 0) != 0;
           trace_ev(p.trace, tr_on && lane == 0, 4, s, l);
-          if (!ok) break;
+          if (!ok) return false;
           tc_fence_after();
           const uint4 lt = ltab[l];
           const uint32_t acc0 = tmem_base + (uint32_t)(l * kAcc * P);
@@ -539,6 +541,21 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
           }
           __syncwarp();
           trace_ev(p.trace, tr_on && lane == 0, 5, s, l);
+          return true;
+      };
+      if constexpr (NL <= kMmaWarps) {
+        // one layer per MMA warp: walk its fills directly
+        const int nf = nfill(mw);
+        for (int f = 0; f < nf; ++f)
+          if (!mma_step(mw, f)) break;
+      } else {
+        bool ok = true;
+        for (int s = 0; s < S && ok; ++s) {
+#pragma unroll 1
+          for (int l = mw; l < NL && ok; l += kMmaWarps) {
+            const int f = s - kLag * l;                  // input fill processed by layer l at step s
+            if (f >= 0 && f < nfill(l)) ok = mma_step(l, f);
+          }
         }
       }
     } else {
@@ -551,17 +568,13 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
       const bool col_valid = cm >= c_strip0 && cm < c_strip0 + Wv && cm < p.oj0 + p.ow;
       const bool col_in = cm >= 0 && cm < p.nx;
       const bool trw = tr_on && lane == 0 && quarter == 2;
-      bool ok = true;
-      for (int s = 0; s < S && ok; ++s) {
-#pragma unroll 1
-        for (int l = grp; l < NL; l += kEpiGroups) {
+      // output row ic of layer l (completed at step s = f + kLag l, f = ic, or ic + 2 with the
+      // dy fold); false on abort
+      auto epi_step = [&](const int l, const int ic) -> bool {
           const bool im2col = is_im2col(l);
-          const int f = s - kLag * l;
-          const int ic = im2col ? f : f - 2;           // output row completed at this step
-          const int no = nout(l);
-          if (f < 0 || f >= nfill(l) || ic < 0 || ic >= no) continue;
+          const int s = (im2col ? ic : ic + 2) + kLag * l;
           const uint32_t Ig = Ocnt(l) + (uint32_t)ic;
-          if (!mbar_wait(bar_tfull(l, Ig & 3), (Ig >> 2) & 1, abort_flag, p.err, 4)) { ok = false; break; }
+          if (!mbar_wait(bar_tfull(l, Ig & 3), (Ig >> 2) & 1, abort_flag, p.err, 4)) return false;
           trace_ev(p.trace, trw, 6, s, l);
           tc_fence_after();
           const uint32_t taddr = tmem_base + lane_base + (uint32_t)(l * kAcc * P);
@@ -574,14 +587,12 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
             if (lane == 0) mbar_arrive(bar_tempty(l, Ig & 3));
             if (l < NL - 1) {
               const uint32_t Fg = Fcnt(l + 1) + (uint32_t)ic;
-              if (Fg >= 4 && !mbar_wait(bar_empty(l + 1, Fg & 3), ((Fg >> 2) - 1) & 1, abort_flag, p.err, 5)) {
-                ok = false;
-                break;
-              }
+              if (Fg >= 4 && !mbar_wait(bar_empty(l + 1, Fg & 3), ((Fg >> 2) - 1) & 1, abort_flag, p.err, 5))
+                return false;
               __syncwarp();
               if (lane == 0) mbar_arrive(bar_full(l + 1, Fg & 3));
             }
-            continue;
+            return true;
           }
 #endif
           if ((l == NL - 1) && last) {
@@ -599,7 +610,7 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
               const TileGeom &g = p.gg;
               p.G[(int64_t)(o - (g.i0 - g.h)) * g.pitch + (cm - (g.j0 - g.hx))] = v[0] + sbias[l * P];
             }
-            continue;
+            return true;
           }
           float v[P];
           const uint32_t ta = taddr + (Ig & 3) * (uint32_t)P;
@@ -626,10 +637,8 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
           if (l < NL - 1) {
             // next layer's input fill = this layer's output row index ic
             const uint32_t Fg = Fcnt(l + 1) + (uint32_t)ic;
-            if (Fg >= 4 && !mbar_wait(bar_empty(l + 1, Fg & 3), ((Fg >> 2) - 1) & 1, abort_flag, p.err, 5)) {
-              ok = false;
-              break;
-            }
+            if (Fg >= 4 && !mbar_wait(bar_empty(l + 1, Fg & 3), ((Fg >> 2) - 1) & 1, abort_flag, p.err, 5))
+              return false;
             trace_ev(p.trace, trw, 9, s, l);
             const uint4 lt = ltab[l + 1];
             uint8_t *slot = smem + lt.x + (Fg & 3) * lt.y + (m + 1) * 16;
@@ -648,6 +657,22 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
             }
           }
           trace_ev(p.trace, trw, 8, s, l);
+          return true;
+      };
+      if constexpr (NL <= kEpiGroups) {
+        // one layer per group: walk its output rows directly
+        const int no = nout(grp);
+        for (int ic = 0; ic < no; ++ic)
+          if (!epi_step(grp, ic)) break;
+      } else {
+        bool ok = true;
+        for (int s = 0; s < S && ok; ++s) {
+#pragma unroll 1
+          for (int l = grp; l < NL && ok; l += kEpiGroups) {
+            const int f = s - kLag * l;
+            const int ic = is_im2col(l) ? f : f - 2;     // output row completed at this step
+            if (f >= 0 && f < nfill(l) && ic >= 0 && ic < nout(l)) ok = epi_step(l, ic);
+          }
         }
       }
     }
