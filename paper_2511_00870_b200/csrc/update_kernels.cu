@@ -301,152 +301,196 @@ update_conv_kernel(const __grid_constant__ UpdateParams p) {
   }
 }
 
-// ---------------------------------------------------------------- separable conv K7 (v2)
+// ---------------------------------------------------------------- separable conv K7 (v3)
 // Same arithmetic contract as update_conv_kernel<R, R, true>, restructured for throughput:
-// float4 staging of x, every stencil pass register-blocked on 4-wide (horizontal) or
-// 4x4 / 2x4 (vertical) output blocks read with 128-bit shared-memory loads.
+//  * persistent CTAs (2 per SM) walk the 32 x 64 output blocks of the tile; the x region
+//    (block (+) 2R) and the y region (block (+) R rows) of the NEXT block are staged into a
+//    second shared-memory buffer with cp.async (zero-filled outside the padded buffer) while
+//    the current block computes, so the HBM stream never waits for a stencil pass;
+//  * every stencil pass is register-blocked on 4-wide (horizontal) or 4x4 / 2x4 (vertical)
+//    output blocks read with 128-bit shared-memory loads.
+__device__ __forceinline__ void cp_async16(void *dst, const void *src, uint32_t bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
 template <int R>
-__global__ void __launch_bounds__(NTHREADS) update_sep_kernel(const __grid_constant__ UpdateParams p) {
-  constexpr int XR = TY + 4 * R, XC = TX + 4 * R;   // x region
-  constexpr int RR = TY + 2 * R, RC = TX + 2 * R;   // residual region
-  constexpr int NW = 2 * R + 4;                     // inputs of a 4-wide output block
+struct SepGeom {
+  static constexpr int XR = TY + 4 * R, XC = TX + 4 * R;   // x region
+  static constexpr int RR = TY + 2 * R, RC = TX + 2 * R;   // residual region (y staged RR x XC)
+  static constexpr int NW = 2 * R + 4;                     // inputs of a 4-wide output block
+  static constexpr size_t floats = 2 * (size_t)XR * XC + 2 * (size_t)RR * XC + (size_t)XR * RC + (size_t)RR * RC;
+  static constexpr size_t bytes = floats * sizeof(float);
+};
+
+template <int R>
+__global__ void __launch_bounds__(NTHREADS, 2) update_sep_kernel(const __grid_constant__ UpdateParams p, int nbx, int nblk) {
+  using Gm = SepGeom<R>;
+  constexpr int XR = Gm::XR, XC = Gm::XC, RR = Gm::RR, RC = Gm::RC, NW = Gm::NW;
   static_assert(RC % 4 == 0 && XC % 4 == 0 && NW % 4 == 0, "R must be even");
-  __shared__ __align__(16) float X[XR * XC];        // x; reused for T2 (RR x TX)
-  __shared__ __align__(16) float T1[XR * RC];       // horizontal forward pass
-  __shared__ __align__(16) float Rs[RR * RC];       // residual H x - y
-  float *T2 = X;
+  static_assert(RR * TX <= XR * XC, "T2 reuses the x buffer");
+  extern __shared__ __align__(16) float sm[];
+  float *const T1 = sm + 2 * XR * XC + 2 * RR * XC;   // horizontal forward pass, XR x RC
+  float *const Rs = T1 + XR * RC;                     // residual H x - y, RR x RC
   const TileGeom &g = p.g;
-  const int bi0 = g.i0 + blockIdx.y * TY;
-  const int bj0 = (g.j0 & ~3) + blockIdx.x * TX;
   const int tid = threadIdx.x;
   const float *ky = p.ky, *kx = p.kx;   // parameter space: FFMA constant-bank operands
+  const int q4 = tid & 15, a2 = tid >> 4;   // phase 4: 16 quads x 16 row pairs
 
-  // the update's own operands (x, G, z, mean, M2 of this thread's 2 rows x 1 quad) are
-  // requested first, so their latency overlaps the staging loads and the stencil passes
-  const int q4 = tid & 15, a2 = tid >> 4;   // 16 quads x 16 row pairs
-  const int gj4 = bj0 + 4 * q4;
-  bool act[2];
-  QuadIn qin[2];
-#pragma unroll
-  for (int r = 0; r < 2; ++r) {
-    const int gi = bi0 + 2 * a2 + r;
-    act[r] = !(gi >= g.i0 + g.th || gj4 >= g.j0 + g.tw || gj4 + 4 <= g.j0);
-    if (act[r]) ula_load(p, gi, gj4, qin[r]);
-  }
+  // stage block blk's x and y regions into buffer buf (one cp.async group)
+  auto stage = [&](int blk, int buf) {
+    const int bi0 = g.i0 + (blk / nbx) * TY;
+    const int bj0 = (g.j0 & ~3) + (blk - (blk / nbx) * nbx) * TX;
+    float *X = sm + buf * XR * XC;
+    float *Y = sm + 2 * XR * XC + buf * RR * XC;
+    for (int e = tid; e < XR * (XC / 4); e += NTHREADS) {
+      const int a = e / (XC / 4), c4 = e - a * (XC / 4);
+      const int pr = bi0 - 2 * R + a - (g.i0 - g.h);
+      const int pc = bj0 - 2 * R + 4 * c4 - (g.j0 - g.hx);
+      const bool in = pr >= 0 && pr < g.ph && pc >= 0 && pc + 3 < g.pitch;
+      cp_async16(X + a * XC + 4 * c4, in ? p.x + (int64_t)pr * g.pitch + pc : p.x, in ? 16u : 0u);
+    }
+    for (int e = tid; e < RR * (XC / 4); e += NTHREADS) {
+      const int a = e / (XC / 4), c4 = e - a * (XC / 4);
+      const int pr = bi0 - R + a - (g.i0 - g.h);
+      const int pc = bj0 - 2 * R + 4 * c4 - (g.j0 - g.hx);
+      const bool in = pr >= 0 && pr < g.ph && pc >= 0 && pc + 3 < g.pitch;
+      cp_async16(Y + a * XC + 4 * c4, in ? p.y + (int64_t)pr * g.pitch + pc : p.y, in ? 16u : 0u);
+    }
+    cp_async_commit();
+  };
 
-  // phase 0: x on block (+) 2R, float4 (columns are quad-aligned in the padded buffer)
-  for (int e = tid; e < XR * (XC / 4); e += NTHREADS) {
-    const int a = e / (XC / 4), c4 = e - a * (XC / 4);
-    const int pr = bi0 - 2 * R + a - (g.i0 - g.h);
-    const int pc = bj0 - 2 * R + 4 * c4 - (g.j0 - g.hx);
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (pr >= 0 && pr < g.ph && pc >= 0 && pc + 3 < g.pitch)
-      v = __ldg(reinterpret_cast<const float4 *>(p.x + (int64_t)pr * g.pitch + pc));
-    *reinterpret_cast<float4 *>(X + a * XC + 4 * c4) = v;
-  }
-  __syncthreads();
-  // phase 1: T1[a][b] = sum_q kx[q+R] X[a][b+R-q]   (4 outputs per item)
-  for (int e = tid; e < XR * (RC / 4); e += NTHREADS) {
-    const int a = e / (RC / 4), k4 = e - a * (RC / 4);
-    float xs[NW];
+  int blk = blockIdx.x;
+  if (blk < nblk) stage(blk, 0);
+  for (int k = 0; blk < nblk; blk += gridDim.x, ++k) {
+    const int buf = k & 1;
+    const int nxt = blk + gridDim.x;
+    if (nxt < nblk) stage(nxt, buf ^ 1);
+    else cp_async_commit();   // empty group keeps wait_group 1 meaning "all but the newest"
+    const int bi0 = g.i0 + (blk / nbx) * TY;
+    const int bj0 = (g.j0 & ~3) + (blk - (blk / nbx) * nbx) * TX;
+    float *const X = sm + buf * XR * XC;
+    const float *const Y = sm + 2 * XR * XC + buf * RR * XC;
+    float *const T2 = X;
+
+    // the update's own operands (x, G, z, mean, M2 of this thread's 2 rows x 1 quad) are
+    // requested before the stencil so their latency overlaps it
+    const int gj4 = bj0 + 4 * q4;
+    bool act[2];
+    QuadIn qin[2];
 #pragma unroll
-    for (int i = 0; i < NW; i += 4) {
-      const float4 t = *reinterpret_cast<const float4 *>(X + a * XC + 4 * k4 + i);
-      xs[i] = t.x; xs[i + 1] = t.y; xs[i + 2] = t.z; xs[i + 3] = t.w;
+    for (int r = 0; r < 2; ++r) {
+      const int gi = bi0 + 2 * a2 + r;
+      act[r] = !(gi >= g.i0 + g.th || gj4 >= g.j0 + g.tw || gj4 + 4 <= g.j0);
+      if (act[r]) ula_load(p, gi, gj4, qin[r]);
     }
-    float o[4];
+    cp_async_wait1();
+    __syncthreads();
+
+    // phase 1: T1[a][b] = sum_q kx[q+R] X[a][b+R-q]   (4 outputs per item)
+    for (int e = tid; e < XR * (RC / 4); e += NTHREADS) {
+      const int a = e / (RC / 4), k4 = e - a * (RC / 4);
+      float xs[NW];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      float s = 0.f;
-#pragma unroll
-      for (int q = -R; q <= R; ++q) s = fmaf(kx[q + R], xs[j + R - q], s);
-      o[j] = s;
-    }
-    *reinterpret_cast<float4 *>(T1 + a * RC + 4 * k4) = make_float4(o[0], o[1], o[2], o[3]);
-  }
-  __syncthreads();
-  // phase 2: Rs[a][b] = sum_p ky[p+R] T1[a+R-p][b] - y, zero outside the image (4x4 per item)
-  for (int e = tid; e < (RR / 4) * (RC / 4); e += NTHREADS) {
-    const int a4 = e / (RC / 4), k4 = e - a4 * (RC / 4);
-    float col[NW][4];
-#pragma unroll
-    for (int i = 0; i < NW; ++i) {
-      const float4 t = *reinterpret_cast<const float4 *>(T1 + (4 * a4 + i) * RC + 4 * k4);
-      col[i][0] = t.x; col[i][1] = t.y; col[i][2] = t.z; col[i][3] = t.w;
-    }
-    const int gj = bj0 - R + 4 * k4;
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const int a = 4 * a4 + r;
-      const int gi = bi0 - R + a;
+      for (int i = 0; i < NW; i += 4) {
+        const float4 t = *reinterpret_cast<const float4 *>(X + a * XC + 4 * k4 + i);
+        xs[i] = t.x; xs[i + 1] = t.y; xs[i + 2] = t.z; xs[i + 3] = t.w;
+      }
       float o[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         float s = 0.f;
 #pragma unroll
-        for (int q = -R; q <= R; ++q) s = fmaf(ky[q + R], col[r + R - q][j], s);
+        for (int q = -R; q <= R; ++q) s = fmaf(kx[q + R], xs[j + R - q], s);
         o[j] = s;
       }
-      const int pr = gi - (g.i0 - g.h), pc = gj - (g.j0 - g.hx);
-      float yv[4] = {0.f, 0.f, 0.f, 0.f};
-      if (pr >= 0 && pr < g.ph && pc >= 0 && pc + 3 < g.pitch) {
-        if (R % 4 == 0) {   // quad-aligned in the padded buffer
-          const float4 t = __ldg(reinterpret_cast<const float4 *>(p.y + (int64_t)pr * g.pitch + pc));
+      *reinterpret_cast<float4 *>(T1 + a * RC + 4 * k4) = make_float4(o[0], o[1], o[2], o[3]);
+    }
+    __syncthreads();
+    // phase 2: Rs[a][b] = sum_p ky[p+R] T1[a+R-p][b] - y, zero outside the image (4x4 per item)
+    for (int e = tid; e < (RR / 4) * (RC / 4); e += NTHREADS) {
+      const int a4 = e / (RC / 4), k4 = e - a4 * (RC / 4);
+      float col[NW][4];
+#pragma unroll
+      for (int i = 0; i < NW; ++i) {
+        const float4 t = *reinterpret_cast<const float4 *>(T1 + (4 * a4 + i) * RC + 4 * k4);
+        col[i][0] = t.x; col[i][1] = t.y; col[i][2] = t.z; col[i][3] = t.w;
+      }
+      const int gj = bj0 - R + 4 * k4;
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int a = 4 * a4 + r;
+        const int gi = bi0 - R + a;
+        float o[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          float s = 0.f;
+#pragma unroll
+          for (int q = -R; q <= R; ++q) s = fmaf(ky[q + R], col[r + R - q][j], s);
+          o[j] = s;
+        }
+        float yv[4];
+        const float *yr = Y + a * XC + R + 4 * k4;   // y column gj + j  <->  staged column R + 4 k4 + j
+        if (R % 4 == 0) {
+          const float4 t = *reinterpret_cast<const float4 *>(yr);
           yv[0] = t.x; yv[1] = t.y; yv[2] = t.z; yv[3] = t.w;
         } else {
-#pragma unroll
-          for (int j = 0; j < 4; ++j) yv[j] = __ldg(p.y + (int64_t)pr * g.pitch + pc + j);
+          const float2 t0 = *reinterpret_cast<const float2 *>(yr), t1 = *reinterpret_cast<const float2 *>(yr + 2);
+          yv[0] = t0.x; yv[1] = t0.y; yv[2] = t1.x; yv[3] = t1.y;
         }
+        const bool rin = gi >= 0 && gi < p.ny;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) o[j] = (rin && gj + j >= 0 && gj + j < p.nx) ? o[j] - yv[j] : 0.f;
+        *reinterpret_cast<float4 *>(Rs + a * RC + 4 * k4) = make_float4(o[0], o[1], o[2], o[3]);
       }
-      const bool rin = gi >= 0 && gi < p.ny;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) o[j] = (rin && gj + j >= 0 && gj + j < p.nx) ? o[j] - yv[j] : 0.f;
-      *reinterpret_cast<float4 *>(Rs + a * RC + 4 * k4) = make_float4(o[0], o[1], o[2], o[3]);
     }
-  }
-  __syncthreads();
-  // phase 3: T2[a][b] = sum_q kx[q+R] Rs[a][b+R+q]   (4 outputs per item)
-  for (int e = tid; e < RR * (TX / 4); e += NTHREADS) {
-    const int a = e / (TX / 4), k4 = e - a * (TX / 4);
-    float rs[NW];
+    __syncthreads();
+    // phase 3: T2[a][b] = sum_q kx[q+R] Rs[a][b+R+q]   (4 outputs per item)
+    for (int e = tid; e < RR * (TX / 4); e += NTHREADS) {
+      const int a = e / (TX / 4), k4 = e - a * (TX / 4);
+      float rs[NW];
 #pragma unroll
-    for (int i = 0; i < NW; i += 4) {
-      const float4 t = *reinterpret_cast<const float4 *>(Rs + a * RC + 4 * k4 + i);
-      rs[i] = t.x; rs[i + 1] = t.y; rs[i + 2] = t.z; rs[i + 3] = t.w;
-    }
-    float o[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      float s = 0.f;
-#pragma unroll
-      for (int q = -R; q <= R; ++q) s = fmaf(kx[q + R], rs[j + R + q], s);
-      o[j] = s;
-    }
-    *reinterpret_cast<float4 *>(T2 + a * TX + 4 * k4) = make_float4(o[0], o[1], o[2], o[3]);
-  }
-  __syncthreads();
-  // phase 4: g = sum_p ky[p+R] T2[a+R+p][b] for 2 rows x 1 quad per thread, then the update
-  {
-    const int q = q4;
-    float col[2 * R + 2][4];
-#pragma unroll
-    for (int i = 0; i < 2 * R + 2; ++i) {
-      const float4 t = *reinterpret_cast<const float4 *>(T2 + (2 * a2 + i) * TX + 4 * q);
-      col[i][0] = t.x; col[i][1] = t.y; col[i][2] = t.z; col[i][3] = t.w;
-    }
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      if (!act[r]) continue;
-      float gr[4];
+      for (int i = 0; i < NW; i += 4) {
+        const float4 t = *reinterpret_cast<const float4 *>(Rs + a * RC + 4 * k4 + i);
+        rs[i] = t.x; rs[i + 1] = t.y; rs[i + 2] = t.z; rs[i + 3] = t.w;
+      }
+      float o[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         float s = 0.f;
 #pragma unroll
-        for (int pp = -R; pp <= R; ++pp) s = fmaf(ky[pp + R], col[r + R + pp][j], s);
-        gr[j] = s;
+        for (int q = -R; q <= R; ++q) s = fmaf(kx[q + R], rs[j + R + q], s);
+        o[j] = s;
       }
-      ula_finish(p, bi0 + 2 * a2 + r, gj4, gr, qin[r]);
+      *reinterpret_cast<float4 *>(T2 + a * TX + 4 * k4) = make_float4(o[0], o[1], o[2], o[3]);
     }
+    __syncthreads();
+    // phase 4: g = sum_p ky[p+R] T2[a+R+p][b] for 2 rows x 1 quad per thread, then the update
+    {
+      float col[2 * R + 2][4];
+#pragma unroll
+      for (int i = 0; i < 2 * R + 2; ++i) {
+        const float4 t = *reinterpret_cast<const float4 *>(T2 + (2 * a2 + i) * TX + 4 * q4);
+        col[i][0] = t.x; col[i][1] = t.y; col[i][2] = t.z; col[i][3] = t.w;
+      }
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        if (!act[r]) continue;
+        float gr[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          float s = 0.f;
+#pragma unroll
+          for (int pp = -R; pp <= R; ++pp) s = fmaf(ky[pp + R], col[r + R + pp][j], s);
+          gr[j] = s;
+        }
+        ula_finish(p, bi0 + 2 * a2 + r, gj4, gr, qin[r]);
+      }
+    }
+    __syncthreads();   // buffer buf is restaged by the next iteration's prefetch
   }
 }
 
@@ -528,15 +572,19 @@ cudaError_t launch_update(const UpdateParams &p, cudaStream_t s) {
   if (p.separable) {
     if (p.ry == p.rx && (p.ry == 4 || p.ry == 2)) {
       const int cols = p.g.j0 + p.g.tw - (p.g.j0 & ~3);
-      dim3 grid((cols + TX - 1) / TX, (p.g.th + TY - 1) / TY);
-      static bool carve = false;   // all of the unified L1/shared array as shared memory (4+ blocks/SM)
-      if (!carve) {
-        cudaFuncSetAttribute(update_sep_kernel<4>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        cudaFuncSetAttribute(update_sep_kernel<2>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        carve = true;
-      }
-      if (p.ry == 4) update_sep_kernel<4><<<grid, NTHREADS, 0, s>>>(p);
-      else update_sep_kernel<2><<<grid, NTHREADS, 0, s>>>(p);
+      const int nbx = (cols + TX - 1) / TX, nby = (p.g.th + TY - 1) / TY;
+      const int nblk = nbx * nby;
+      // opt in to > 48 KB of shared memory (a per-device attribute: set on every launch)
+      int dev = 0, num_sms = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaError_t e = p.ry == 4
+          ? cudaFuncSetAttribute(update_sep_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SepGeom<4>::bytes)
+          : cudaFuncSetAttribute(update_sep_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SepGeom<2>::bytes);
+      if (e != cudaSuccess) return e;
+      const int grid = nblk < 2 * num_sms ? nblk : 2 * num_sms;
+      if (p.ry == 4) update_sep_kernel<4><<<grid, NTHREADS, SepGeom<4>::bytes, s>>>(p, nbx, nblk);
+      else update_sep_kernel<2><<<grid, NTHREADS, SepGeom<2>::bytes, s>>>(p, nbx, nblk);
       return cudaGetLastError();
     }
     return launch_conv<-1, -1, true>(p, s);
