@@ -76,7 +76,6 @@ struct SmemLayout {
   uint32_t ring_off[kMaxChunk];
   uint32_t slot_bytes[kMaxChunk];
   uint32_t w_off[kMaxChunk];
-  uint32_t bias_off;
   uint32_t bar_off;
   uint32_t misc_off;
   uint32_t total;
@@ -104,8 +103,6 @@ __host__ __device__ inline SmemLayout make_layout(int P, int nl, int first, int 
     L.w_off[l] = off;
     off = align_up(off + packed_layer_elems(cout, cin) * 2u, 128);
   }
-  L.bias_off = off;
-  off = align_up(off + (uint32_t)nl * P * 4u, 128);
   L.bar_off = off;   // per layer: full[4], empty[4], tfull[4], tempty[4]
   off = align_up(off + (uint32_t)nl * 16u * 8u, 128);
   L.misc_off = off;  // tmem address, abort flag, drain barrier, per-layer table {ring, slot, w, 0}
@@ -306,7 +303,6 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + L.misc_off);
   volatile int *abort_flag = reinterpret_cast<volatile int *>(smem + L.misc_off + 4);
   const uint32_t bar_done = sbase + L.misc_off + 8;
-  float *sbias = reinterpret_cast<float *>(smem + L.bias_off);
   // TMEM: layer l owns columns [l*4P, l*4P + 4*Cb): accumulator-row slot q at l*4P + q*Cb
   constexpr uint32_t tmem_need = (uint32_t)NL * kAcc * P;
   static_assert(tmem_need <= 512, "TMEM columns");
@@ -322,7 +318,6 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
     const uint4 *src = reinterpret_cast<const uint4 *>(p.w[l]);
     uint4 *dst = reinterpret_cast<uint4 *>(smem + L.w_off[l]);
     for (uint32_t e = threadIdx.x; e < n16; e += kThreads) dst[e] = src[e];
-    for (int c = threadIdx.x; c < P; c += kThreads) sbias[l * P + c] = (c < cout) ? p.b[l][c] : 0.f;
     uint4 *r = reinterpret_cast<uint4 *>(smem + L.ring_off[l]);
     const uint32_t nr = kRing * L.slot_bytes[l] / 16;
     for (uint32_t e = threadIdx.x; e < nr; e += kThreads) r[e] = make_uint4(0, 0, 0, 0);
@@ -608,15 +603,26 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
             if (lane == 0) mbar_arrive(bar_tempty(l, Ig & 3));
             if (col_valid) {
               const TileGeom &g = p.gg;
-              p.G[(int64_t)(o - (g.i0 - g.h)) * g.pitch + (cm - (g.j0 - g.hx))] = v[0] + sbias[l * P];
+              p.G[(int64_t)(o - (g.i0 - g.h)) * g.pitch + (cm - (g.j0 - g.hx))] = v[0] + p.bias[l][0];
             }
             return true;
           }
-          float v[P];
           const uint32_t ta = taddr + (Ig & 3) * (uint32_t)P;
+          uint32_t w[P / 2];
+          // 16 channels at a time (tcgen05.ld -> +bias, ReLU -> bf16 pairs): keeps at most 16
+          // accumulator values live next to the bias registers
 #pragma unroll
-          for (int c = 0; c < P; c += 16) tmem_load<16>(ta + c, v + c);
-          tmem_wait_ld();
+          for (int h = 0; h < P; h += 16) {
+            float v[16];
+            tmem_load<16>(ta + h, v);
+            tmem_wait_ld();
+#pragma unroll
+            for (int c = 0; c < 16; c += 4) {
+              const float4 b4 = *reinterpret_cast<const float4 *>(&p.bias[l][h + c]);   // constant cache
+              w[(h + c) / 2] = pack_bf16(inside ? fmaxf(v[c] + b4.x, 0.f) : 0.f, inside ? fmaxf(v[c + 1] + b4.y, 0.f) : 0.f);
+              w[(h + c) / 2 + 1] = pack_bf16(inside ? fmaxf(v[c + 2] + b4.z, 0.f) : 0.f, inside ? fmaxf(v[c + 3] + b4.w, 0.f) : 0.f);
+            }
+          }
           if (!im2col) {       // im2col MMAs overwrite (accumulate = 0): no re-zeroing needed
 #pragma unroll
             for (int c = 0; c < P; c += 16) tmem_zero<16>(ta + c);
@@ -626,14 +632,6 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
           __syncwarp();
           if (lane == 0) mbar_arrive(bar_tempty(l, Ig & 3));
           trace_ev(p.trace, trw, 7, s, l);
-          const float4 *bl = reinterpret_cast<const float4 *>(sbias + l * P);
-          uint32_t w[P / 2];
-#pragma unroll
-          for (int c = 0; c < P; c += 4) {
-            const float4 b4 = bl[c / 4];
-            w[c / 2] = pack_bf16(inside ? fmaxf(v[c] + b4.x, 0.f) : 0.f, inside ? fmaxf(v[c + 1] + b4.y, 0.f) : 0.f);
-            w[c / 2 + 1] = pack_bf16(inside ? fmaxf(v[c + 2] + b4.z, 0.f) : 0.f, inside ? fmaxf(v[c + 3] + b4.w, 0.f) : 0.f);
-          }
           if (l < NL - 1) {
             // next layer's input fill = this layer's output row index ic
             const uint32_t Fg = Fcnt(l + 1) + (uint32_t)ic;

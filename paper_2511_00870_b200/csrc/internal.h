@@ -68,7 +68,8 @@ struct CnnChunkParams {
   int first_is_input;    // layer l0 == 1: input is x (fp32, 1 channel)
   int last_is_output;    // layer l0+nl-1 == K: output is G (fp32, 1 channel, no ReLU)
   const uint16_t *w[kMaxChunk];   // packed bf16 B-operand images, one per layer
-  const float *b[kMaxChunk];      // fp32 biases per layer
+  float bias[kMaxChunk][64];      // fp32 biases per layer (zero padded): kernel parameter space,
+                                  // read through the constant cache (no shared-memory traffic)
   // input: x (padded fp32) or activation buffer
   const float *x; TileGeom xg;
   const uint16_t *ain; int a_i0, a_j0, a_rows, a_cols;   // activation region (global origin, extent)

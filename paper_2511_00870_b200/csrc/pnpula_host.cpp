@@ -85,6 +85,7 @@ struct pnpula_ctx {
   std::vector<CnnChunk> chunks;
   std::vector<uint16_t *> d_w;      // per layer packed weights
   std::vector<float *> d_b;         // per layer biases
+  std::vector<std::vector<float>> h_b;   // host copies (passed to the CNN kernel as parameters)
 
   // halo plan
   std::vector<pnpula_halo_msg> msgs;
@@ -211,7 +212,8 @@ pnpula_status run_cnn(pnpula_ctx *c, int buf) {
       p.last_is_output = ch.l0 + ch.nl - 1 == c->n_layers;
       for (int l = 0; l < ch.nl; ++l) {
         p.w[l] = c->d_w[ch.l0 - 1 + l];
-        p.b[l] = c->d_b[ch.l0 - 1 + l];
+        const std::vector<float> &hb = c->h_b[ch.l0 - 1 + l];
+        for (size_t k = 0; k < hb.size() && k < 64; ++k) p.bias[l][k] = hb[k];
       }
       const TileGeom &g = td.g;
       p.x = td.x[buf];
@@ -710,6 +712,7 @@ pnpula_status pnpula_create(const pnpula_config *cfg, pnpula_ctx **out) {
       CUB(cudaMemcpy(db, b, cout * sizeof(float), cudaMemcpyHostToDevice));
       c->d_w.push_back(dw);
       c->d_b.push_back(db);
+      c->h_b.emplace_back(b, b + cout);
       w += (size_t)cout * cin * 9;
       b += cout;
       cin = cout;
