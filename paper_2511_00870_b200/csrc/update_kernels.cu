@@ -19,6 +19,7 @@
 // Every pixel's arithmetic is independent of the block / tile it lands in, so the
 // chain is bitwise identical for any tile grid.
 #include <cstdint>
+#include <cuda.h>   // CUtensorMap (encoded through the runtime's driver entry point: no -lcuda)
 #include <cuda_runtime.h>
 
 #include "internal.h"
@@ -305,17 +306,33 @@ update_conv_kernel(const __grid_constant__ UpdateParams p) {
 // Same arithmetic contract as update_conv_kernel<R, R, true>, restructured for throughput:
 //  * persistent CTAs (2 per SM) walk the 32 x 64 output blocks of the tile; the x region
 //    (block (+) 2R) and the y region (block (+) R rows) of the NEXT block are staged into a
-//    second shared-memory buffer with cp.async (zero-filled outside the padded buffer) while
-//    the current block computes, so the HBM stream never waits for a stencil pass;
+//    second shared-memory buffer by two 2-D TMA tile loads (zero fill outside the padded
+//    buffer = the kernel's boundary rule) while the current block computes, so the HBM stream
+//    never waits for a stencil pass and no thread spends instructions on staging;
 //  * every stencil pass is register-blocked on 4-wide (horizontal) or 4x4 / 2x4 (vertical)
 //    output blocks read with 128-bit shared-memory loads.
-__device__ __forceinline__ void cp_async16(void *dst, const void *src, uint32_t bytes) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
-               "l"(src), "r"(bytes)
-               : "memory");
+__device__ __forceinline__ void mbar_init1(uint32_t bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+__device__ __forceinline__ void mbar_wait_parity(uint32_t bar, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+}
+// 2-D TMA tile load (zero fill outside the tensor), completion counted on an mbarrier
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map, int c0, int r0, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(r0), "r"(bar)
+      : "memory");
+}
 
 template <int R>
 struct SepGeom {
@@ -323,16 +340,22 @@ struct SepGeom {
   static constexpr int RR = TY + 2 * R, RC = TX + 2 * R;   // residual region (y staged RR x XC)
   static constexpr int NW = 2 * R + 4;                     // inputs of a 4-wide output block
   static constexpr size_t floats = 2 * (size_t)XR * XC + 2 * (size_t)RR * XC + (size_t)XR * RC + (size_t)RR * RC;
-  static constexpr size_t bytes = floats * sizeof(float);
+  static_assert((XR * XC * 4) % 128 == 0 && (RR * XC * 4) % 128 == 0, "TMA destinations 128-B aligned");
+  static constexpr size_t bytes = floats * sizeof(float) + 16;   // + 2 mbarriers
 };
 
 template <int R>
-__global__ void __launch_bounds__(NTHREADS, 2) update_sep_kernel(const __grid_constant__ UpdateParams p, int nbx, int nblk) {
+__global__ void __launch_bounds__(NTHREADS, 2)
+update_sep_kernel(const __grid_constant__ UpdateParams p, const __grid_constant__ CUtensorMap tmx,
+                  const __grid_constant__ CUtensorMap tmy, int nbx, int nblk) {
   using Gm = SepGeom<R>;
   constexpr int XR = Gm::XR, XC = Gm::XC, RR = Gm::RR, RC = Gm::RC, NW = Gm::NW;
   static_assert(RC % 4 == 0 && XC % 4 == 0 && NW % 4 == 0, "R must be even");
   static_assert(RR * TX <= XR * XC, "T2 reuses the x buffer");
-  extern __shared__ __align__(16) float sm[];
+  extern __shared__ __align__(128) float sm[];
+  // TMA completion barrier per staging buffer, after the float regions (no static shared
+  // memory: the dynamic region then starts 1024-B aligned, as the TMA destinations need)
+  uint64_t *const full_bar = reinterpret_cast<uint64_t *>(sm + Gm::floats);
   float *const T1 = sm + 2 * XR * XC + 2 * RR * XC;   // horizontal forward pass, XR x RC
   float *const Rs = T1 + XR * RC;                     // residual H x - y, RR x RC
   const TileGeom &g = p.g;
@@ -340,36 +363,32 @@ __global__ void __launch_bounds__(NTHREADS, 2) update_sep_kernel(const __grid_co
   const float *ky = p.ky, *kx = p.kx;   // parameter space: FFMA constant-bank operands
   const int q4 = tid & 15, a2 = tid >> 4;   // phase 4: 16 quads x 16 row pairs
 
-  // stage block blk's x and y regions into buffer buf (one cp.async group)
+  // stage block blk's x and y regions into buffer buf: one thread, two TMA tile loads
   auto stage = [&](int blk, int buf) {
     const int bi0 = g.i0 + (blk / nbx) * TY;
     const int bj0 = (g.j0 & ~3) + (blk - (blk / nbx) * nbx) * TX;
-    float *X = sm + buf * XR * XC;
-    float *Y = sm + 2 * XR * XC + buf * RR * XC;
-    for (int e = tid; e < XR * (XC / 4); e += NTHREADS) {
-      const int a = e / (XC / 4), c4 = e - a * (XC / 4);
-      const int pr = bi0 - 2 * R + a - (g.i0 - g.h);
-      const int pc = bj0 - 2 * R + 4 * c4 - (g.j0 - g.hx);
-      const bool in = pr >= 0 && pr < g.ph && pc >= 0 && pc + 3 < g.pitch;
-      cp_async16(X + a * XC + 4 * c4, in ? p.x + (int64_t)pr * g.pitch + pc : p.x, in ? 16u : 0u);
-    }
-    for (int e = tid; e < RR * (XC / 4); e += NTHREADS) {
-      const int a = e / (XC / 4), c4 = e - a * (XC / 4);
-      const int pr = bi0 - R + a - (g.i0 - g.h);
-      const int pc = bj0 - 2 * R + 4 * c4 - (g.j0 - g.hx);
-      const bool in = pr >= 0 && pr < g.ph && pc >= 0 && pc + 3 < g.pitch;
-      cp_async16(Y + a * XC + 4 * c4, in ? p.y + (int64_t)pr * g.pitch + pc : p.y, in ? 16u : 0u);
-    }
-    cp_async_commit();
+    const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&full_bar[buf]);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // buffer was read by generic loads
+    asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                 "r"((uint32_t)((XR + RR) * XC * 4))
+                 : "memory");
+    const int c0 = bj0 - 2 * R - (g.j0 - g.hx);
+    tma_load_2d((uint32_t)__cvta_generic_to_shared(sm + buf * XR * XC), &tmx, c0, bi0 - 2 * R - (g.i0 - g.h), bar);
+    tma_load_2d((uint32_t)__cvta_generic_to_shared(sm + 2 * XR * XC + buf * RR * XC), &tmy, c0, bi0 - R - (g.i0 - g.h), bar);
   };
 
+  if (tid == 0) {
+    mbar_init1((uint32_t)__cvta_generic_to_shared(&full_bar[0]));
+    mbar_init1((uint32_t)__cvta_generic_to_shared(&full_bar[1]));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
   int blk = blockIdx.x;
-  if (blk < nblk) stage(blk, 0);
+  if (tid == 0 && blk < nblk) stage(blk, 0);
   for (int k = 0; blk < nblk; blk += gridDim.x, ++k) {
     const int buf = k & 1;
     const int nxt = blk + gridDim.x;
-    if (nxt < nblk) stage(nxt, buf ^ 1);
-    else cp_async_commit();   // empty group keeps wait_group 1 meaning "all but the newest"
+    if (tid == 0 && nxt < nblk) stage(nxt, buf ^ 1);
     const int bi0 = g.i0 + (blk / nbx) * TY;
     const int bj0 = (g.j0 & ~3) + (blk - (blk / nbx) * nbx) * TX;
     float *const X = sm + buf * XR * XC;
@@ -387,8 +406,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) update_sep_kernel(const __grid_co
       act[r] = !(gi >= g.i0 + g.th || gj4 >= g.j0 + g.tw || gj4 + 4 <= g.j0);
       if (act[r]) ula_load(p, gi, gj4, qin[r]);
     }
-    cp_async_wait1();
-    __syncthreads();
+    mbar_wait_parity((uint32_t)__cvta_generic_to_shared(&full_bar[buf]), (uint32_t)(k >> 1) & 1u);
 
     // phase 1: T1[a][b] = sum_q kx[q+R] X[a][b+R-q]   (4 outputs per item)
     for (int e = tid; e < XR * (RC / 4); e += NTHREADS) {
@@ -557,6 +575,37 @@ cudaError_t launch_conv(const UpdateParams &p, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (the library links cudart only)
+using EncodeTiledFn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                   const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_tiled_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void *f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(f);
+  }
+  return fn;
+}
+
+// 2-D fp32 map over a padded tile buffer (ph rows x pitch floats), box = box_c x box_r,
+// out-of-bounds elements read as zero
+bool encode_padded_2d(CUtensorMap *m, const float *base, const TileGeom &g, int box_c, int box_r) {
+  EncodeTiledFn fn = encode_tiled_fn();
+  if (!fn) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)g.pitch, (cuuint64_t)g.ph};
+  const cuuint64_t strides[1] = {(cuuint64_t)g.pitch * sizeof(float)};
+  const cuuint32_t box[2] = {(cuuint32_t)box_c, (cuuint32_t)box_r};
+  const cuuint32_t estr[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 }  // namespace
 
 cudaError_t launch_update(const UpdateParams &p, cudaStream_t s) {
@@ -578,13 +627,20 @@ cudaError_t launch_update(const UpdateParams &p, cudaStream_t s) {
       int dev = 0, num_sms = 148;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-      cudaError_t e = p.ry == 4
-          ? cudaFuncSetAttribute(update_sep_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SepGeom<4>::bytes)
-          : cudaFuncSetAttribute(update_sep_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SepGeom<2>::bytes);
+      const int R = p.ry;
+      const size_t smem = R == 4 ? SepGeom<4>::bytes : SepGeom<2>::bytes;
+      cudaError_t e = R == 4
+          ? cudaFuncSetAttribute(update_sep_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+          : cudaFuncSetAttribute(update_sep_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
+      // TMA maps of the padded x and y buffers (ph x pitch fp32), boxes = the staged regions
+      CUtensorMap tmx, tmy;
+      const int XC = TX + 4 * R;
+      if (!encode_padded_2d(&tmx, p.x, p.g, XC, TY + 4 * R) || !encode_padded_2d(&tmy, p.y, p.g, XC, TY + 2 * R))
+        return cudaErrorInvalidValue;
       const int grid = nblk < 2 * num_sms ? nblk : 2 * num_sms;
-      if (p.ry == 4) update_sep_kernel<4><<<grid, NTHREADS, SepGeom<4>::bytes, s>>>(p, nbx, nblk);
-      else update_sep_kernel<2><<<grid, NTHREADS, SepGeom<2>::bytes, s>>>(p, nbx, nblk);
+      if (R == 4) update_sep_kernel<4><<<grid, NTHREADS, smem, s>>>(p, tmx, tmy, nbx, nblk);
+      else update_sep_kernel<2><<<grid, NTHREADS, smem, s>>>(p, tmx, tmy, nbx, nblk);
       return cudaGetLastError();
     }
     return launch_conv<-1, -1, true>(p, s);
