@@ -85,7 +85,8 @@ __host__ __device__ inline uint32_t align_up(uint32_t v, uint32_t a) { return (v
 
 __host__ __device__ inline uint32_t packed_layer_elems(int cout, int cin) {
   if (cin == 1) return 16u * (uint32_t)cout;
-  return 9u * (uint32_t)cin * (uint32_t)(cout == 1 ? 16 : cout);
+  if (cout == 1) return 16u * (uint32_t)cin;   // folded P -> 1 layer: [K step][2][16 taps][8]
+  return 9u * (uint32_t)cin * (uint32_t)cout;
 }
 
 __host__ __device__ inline SmemLayout make_layout(int P, int nl, int first, int last) {
@@ -105,8 +106,9 @@ __host__ __device__ inline SmemLayout make_layout(int P, int nl, int first, int 
   }
   L.bar_off = off;   // per layer: full[4], empty[4], tfull[4], tempty[4]
   off = align_up(off + (uint32_t)nl * 16u * 8u, 128);
-  L.misc_off = off;  // tmem address, abort flag, drain barrier, per-layer table {ring, slot, w, 0}
-  off += 16 + 16u * (uint32_t)nl;
+  L.misc_off = off;  // tmem address, abort flag, drain barrier, per-layer table {ring, slot, w, 0},
+                     // folded last layer's warp-edge exchange [2][4 warps][6] floats
+  off += 16 + 16u * (uint32_t)nl + 192u;
   L.total = align_up(off, 128);
   return L;
 }
@@ -357,7 +359,11 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
   __syncthreads();
   tc_fence_after();
 
-  const int Wv = kRowPos - 2 * NL;                 // valid output columns per strip
+  // valid output columns per strip: each fused layer costs one column per side; the folded
+  // P -> 1 layer needs its MMA rows m +- 1, so a 1-layer chunk ending the net counts as 2
+  constexpr int NLg0 = NL < 2 ? 2 : NL;
+  const int NLg = last ? NLg0 : NL;
+  const int Wv = kRowPos - 2 * NLg;
   const int strips = p.strips;
   const int R = p.rows_per_unit;
   const int units = p.units;
@@ -380,7 +386,7 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
     const int r_hi = min(r_lo + R, p.oi0 + p.oh);
     const int Rn = r_hi - r_lo;
     const int c_strip0 = p.oj0 + strip * Wv;         // first valid output column of the strip
-    const int col0 = c_strip0 - NL + 1;              // column of MMA row 0 (ring position 1)
+    const int col0 = c_strip0 - NLg + 1;             // column of MMA row 0 (ring position 1)
     const bool tr_on = p.trace != nullptr && blockIdx.x == 0 && u == (int)blockIdx.x;
     // layer l: nout(l) = Rn + 2 (NL-1-l) output rows starting at global row r_lo-(NL-1-l);
     // its input fills are rows r0(l)-1 .. (nout+2 fills), or nout im2col rows for an im2col layer.
@@ -477,7 +483,7 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
           const int no = nout(l);
           bool ok;
           const bool im2col = is_im2col(l);
-          const bool netlast = (l == NL - 1) && last;
+          const bool netlast = (l == NL - 1) && last && !im2col;
           const uint32_t Fg = Fcnt(l) + (uint32_t)f;
           trace_ev(p.trace, tr_on && lane == 0, 3, s, l);
           ok = mbar_wait(bar_full(l, Fg & 3), (Fg >> 2) & 1, abort_flag, p.err, 2);
@@ -485,7 +491,9 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
           // output row that receives its first contribution (im2col: the only one)
           const uint32_t O0 = Ocnt(l);
           const uint32_t Ig = O0 + (uint32_t)f;
-          if (ok && f < no && Ig >= (uint32_t)kAcc && PNPULA_EXP != 7)
+          if (netlast) {   // 2-slot ring of per-fill accumulators: fill Fg-2 must have been read
+            if (ok && Fg >= 2u) ok = mbar_wait(bar_tempty(l, Fg & 1), ((Fg >> 1) - 1) & 1, abort_flag, p.err, 3);
+          } else if (ok && f < no && Ig >= (uint32_t)kAcc && PNPULA_EXP != 7)
             ok = mbar_wait(bar_tempty(l, Ig & 3), ((Ig >> 2) - 1) & 1, abort_flag, p.err, 3);
           ok = __shfl_sync(0xffffffffu, ok ? 1 : 0, 0) != 0;
           trace_ev(p.trace, tr_on && lane == 0, 4, s, l);
@@ -499,10 +507,23 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
             const uint64_t ad = make_desc(slot, 2048, 128);
             const uint64_t bd = make_desc(wbase, (uint32_t)P * 16, 128);
             if (elect_one()) mma_bf16(acc0 + (Ig & 3) * P, ad, bd, make_idesc(P), 0);
+          } else if (netlast) {
+            // P -> 1 layer: all nine taps folded into N = 16 (column n = q*3 + dxi, q = 1 - dy),
+            // A unshifted (MMA row m = pixel col0 + m); the epilogue adds the dx-shifted columns
+            // of neighbouring lanes and the dy rows of consecutive fills.  Fresh 16-column slot
+            // per fill (accumulate = 0 on the first K step): no zeroing, no ring wrap.
+            const uint64_t ad0 = make_desc(slot + 16, GS, 128);
+            const uint64_t bd0 = make_desc(wbase, 16u * 16u, 128);
+            if (elect_one()) {
+#pragma unroll
+              for (int ks = 0; ks < KS; ++ks)
+                mma_bf16(acc0 + (Fg & 1) * 16u, ad0 + (uint64_t)((2 * ks * GS) >> 4), bd0 + (uint64_t)(ks * 32),
+                         make_idesc(16), ks > 0 ? 1u : 0u);
+            }
           } else {
             // input row f contributes to output rows f-2 (dy=+1), f-1 (dy=0), f (dy=-1): B block q=0,1,2.
             // Only rows in [0, no) are accumulated; slots wrap, so the row range splits into <= 2 runs.
-            const uint32_t Cb = netlast ? 16u : (uint32_t)P;
+            const uint32_t Cb = (uint32_t)P;
             const int ilo = f - 2 > 0 ? f - 2 : 0;
             const int ihi = f < no - 1 ? f : no - 1;
             const uint32_t Ilo = O0 + (uint32_t)ilo;
@@ -531,8 +552,12 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
           __syncwarp();
           if (elect_one()) {
             mma_commit(bar_empty(l, Fg & 3));            // input row consumed
-            const int ic = im2col ? f : f - 2;           // output row completed by this group
-            if (ic >= 0 && ic < no) mma_commit(bar_tfull(l, (O0 + (uint32_t)ic) & 3));
+            if (netlast) {
+              mma_commit(bar_tfull(l, Fg & 1));          // this fill's tap sums
+            } else {
+              const int ic = im2col ? f : f - 2;         // output row completed by this group
+              if (ic >= 0 && ic < no) mma_commit(bar_tfull(l, (O0 + (uint32_t)ic) & 3));
+            }
           }
           __syncwarp();
           trace_ev(p.trace, tr_on && lane == 0, 5, s, l);
@@ -563,6 +588,65 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
       const bool col_valid = cm >= c_strip0 && cm < c_strip0 + Wv && cm < p.oj0 + p.ow;
       const bool col_in = cm >= 0 && cm < p.nx;
       const bool trw = tr_on && lane == 0 && quarter == 2;
+      // Folded P -> 1 output layer, one input fill f at a time: tap sums d[q*3 + dxi] of this
+      // lane's pixel; pixel m's contribution to output row (f - 2 + q) is
+      // d_{m-1}[q*3] + d_m[q*3+1] + d_{m+1}[q*3+2] (lanes m +- 1: shuffles, warp edges through
+      // shared memory); a row is complete after its third fill.  Lanes 0 / 127 of the strip
+      // are never valid output columns.
+      float nacc0 = 0.f, nacc1 = 0.f;   // running sums of output rows f-2 and f-1
+      float *const xch = reinterpret_cast<float *>(smem + L.misc_off + 16 + 16 * NL);
+      auto netlast_fill = [&](const int l, const int f) -> bool {
+          const int s = f + kLag * l;
+          const uint32_t Fg = Fcnt(l) + (uint32_t)f;
+          if (!mbar_wait(bar_tfull(l, Fg & 1), (Fg >> 1) & 1, abort_flag, p.err, 4)) return false;
+          trace_ev(p.trace, trw, 6, s, l);
+          tc_fence_after();
+          float d[16];
+          tmem_load<16>(tmem_base + lane_base + (uint32_t)(l * kAcc * P) + (Fg & 1) * 16u, d);
+          tmem_wait_ld();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(bar_tempty(l, Fg & 1));
+          float lft[3], rgt[3];
+#pragma unroll
+          for (int q = 0; q < 3; ++q) {
+            lft[q] = __shfl_up_sync(0xffffffffu, d[q * 3], 1);
+            rgt[q] = __shfl_down_sync(0xffffffffu, d[q * 3 + 2], 1);
+          }
+          float *xb = xch + (f & 1) * 24;   // [quarter][0-2: lane 31's left taps, 3-5: lane 0's right taps]
+          if (lane == 31) {
+#pragma unroll
+            for (int q = 0; q < 3; ++q) xb[quarter * 6 + q] = d[q * 3];
+          }
+          if (lane == 0) {
+#pragma unroll
+            for (int q = 0; q < 3; ++q) xb[quarter * 6 + 3 + q] = d[q * 3 + 2];
+          }
+          asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory");   // the group's 4 warps
+          if (lane == 0 && quarter > 0) {
+#pragma unroll
+            for (int q = 0; q < 3; ++q) lft[q] = xb[(quarter - 1) * 6 + q];
+          }
+          if (lane == 31 && quarter < 3) {
+#pragma unroll
+            for (int q = 0; q < 3; ++q) rgt[q] = xb[(quarter + 1) * 6 + 3 + q];
+          }
+          float c[3];
+#pragma unroll
+          for (int q = 0; q < 3; ++q) c[q] = (lft[q] + d[q * 3 + 1]) + rgt[q];
+          const float row_done = nacc0 + c[0];   // output row f-2 (dy = +1 is its last fill)
+          nacc0 = nacc1 + c[1];
+          nacc1 = c[2];
+          const int ic = f - 2;
+          if (ic >= 0 && ic < nout(l) && col_valid) {
+            const int o = r_lo - (NL - 1 - l) + ic;
+            const TileGeom &g = p.gg;
+            p.G[(int64_t)(o - (g.i0 - g.h)) * g.pitch + (cm - (g.j0 - g.hx))] = row_done + p.bias[l][0];
+          }
+          trace_ev(p.trace, trw, 8, s, l);
+          return true;
+      };
+      auto is_netlast = [&](int l) { return l == NL - 1 && last && !is_im2col(l); };
       // output row ic of layer l (completed at step s = f + kLag l, f = ic, or ic + 2 with the
       // dy fold); false on abort
       auto epi_step = [&](const int l, const int ic) -> bool {
@@ -658,18 +742,29 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
           return true;
       };
       if constexpr (NL <= kEpiGroups) {
-        // one layer per group: walk its output rows directly
-        const int no = nout(grp);
-        for (int ic = 0; ic < no; ++ic)
-          if (!epi_step(grp, ic)) break;
+        // one layer per group: walk its output rows (or, folded last layer, its fills) directly
+        if (is_netlast(grp)) {
+          const int nf = nfill(grp);
+          for (int f = 0; f < nf; ++f)
+            if (!netlast_fill(grp, f)) break;
+        } else {
+          const int no = nout(grp);
+          for (int ic = 0; ic < no; ++ic)
+            if (!epi_step(grp, ic)) break;
+        }
       } else {
         bool ok = true;
         for (int s = 0; s < S && ok; ++s) {
 #pragma unroll 1
           for (int l = grp; l < NL && ok; l += kEpiGroups) {
             const int f = s - kLag * l;
-            const int ic = is_im2col(l) ? f : f - 2;     // output row completed at this step
-            if (f >= 0 && f < nfill(l) && ic >= 0 && ic < nout(l)) ok = epi_step(l, ic);
+            if (f < 0 || f >= nfill(l)) continue;
+            if (is_netlast(l)) {
+              ok = netlast_fill(l, f);
+            } else {
+              const int ic = is_im2col(l) ? f : f - 2;   // output row completed at this step
+              if (ic >= 0 && ic < nout(l)) ok = epi_step(l, ic);
+            }
           }
         }
       }
@@ -697,7 +792,7 @@ template <int P, int NL>
 cudaError_t launch_pn(const CnnChunkParams &p0, int num_sms, cudaStream_t s) {
   CnnChunkParams p = p0;
   const SmemLayout L = make_layout(P, NL, p.first_is_input, p.last_is_output);
-  const int Wv = kRowPos - 2 * NL;
+  const int Wv = kRowPos - 2 * ((p.last_is_output && NL < 2) ? 2 : NL);   // as in the kernel
   const int strips = (p.ow + Wv - 1) / Wv;
   // rows per unit: minimise (waves) x (rows per unit + pipeline fill) over row-block counts
   int R = p.oh;
@@ -771,9 +866,22 @@ void cnn_pack_layer(const float *w, int cout, int cin, uint16_t *out) {
       }
     return;
   }
-  const int Cb = (cout == 1) ? 16 : cout;
-  const int N3 = 3 * Cb;
   const int KS = cin / 16;
+  if (cout == 1) {
+    // folded P -> 1 layer: per K step one block [2 halves][16 taps][8 cin]; tap row
+    // n = q*3 + dxi holds W(dy = 1 - q, dx = dxi - 1); rows 9..15 zero
+    for (int ks = 0; ks < KS; ++ks)
+      for (int q = 0; q < 3; ++q)
+        for (int dxi = 0; dxi < 3; ++dxi)
+          for (int c = 0; c < 16; ++c) {
+            const int ci = ks * 16 + c, dyi = 2 - q;
+            out[(size_t)ks * 256 + ((size_t)(c / 8) * 16 + (size_t)(q * 3 + dxi)) * 8 + (c % 8)] =
+                f32_to_bf16_rne(w[(size_t)ci * 9 + dyi * 3 + dxi]);
+          }
+    return;
+  }
+  const int Cb = cout;
+  const int N3 = 3 * Cb;
   for (int dxi = 0; dxi < 3; ++dxi)
     for (int ks = 0; ks < KS; ++ks) {
       uint16_t *blk = out + (size_t)(dxi * KS + ks) * 16 * N3;
