@@ -11,7 +11,7 @@ file with gcc and marshals numpy arrays through ctypes.
 
 Parity status per function:
   partition, philox, normal, conv fwd/adj, mask, dncnn residual, step-size
-  check, run (untiled + tiled): pinned (tests/test_oracle_*.py).
+  check, run (untiled + tiled), KL prox, Poisson run: pinned (tests/test_oracle_*.py).
 """
 from __future__ import annotations
 
@@ -54,6 +54,7 @@ class _Config(C.Structure):
         ("n_iter", C.c_int64), ("burn_in", C.c_int64), ("seed", C.c_uint64),
         ("tiles_y", C.c_int32), ("tiles_x", C.c_int32),
         ("i_off", C.c_int64), ("j_off", C.c_int64),
+        ("eta", C.c_double), ("rho1", C.c_double), ("kappa1", C.c_double),
     ]
 
 
@@ -77,6 +78,10 @@ def _load():
         _lib.or_check_stepsizes.restype = C.c_int
         _lib.or_run.argtypes = [C.POINTER(_Config), vp, vp, vp, vp, C.POINTER(i64)]
         _lib.or_run.restype = C.c_int
+        _lib.or_run_ex.argtypes = [C.POINTER(_Config), vp, vp, vp, vp, vp, C.POINTER(i64)]
+        _lib.or_run_ex.restype = C.c_int
+        _lib.or_prox_kl.argtypes = [d, d, d]
+        _lib.or_prox_kl.restype = d
     return _lib
 
 
@@ -152,6 +157,11 @@ def check_stepsizes(L, h2_over_rho, alpha, eps, L_D, lam, gamma) -> int:
     return int(_load().or_check_stepsizes(L, h2_over_rho, alpha, eps, L_D, lam, gamma))
 
 
+def prox_kl(v: float, y: float, kappa: float) -> float:
+    """prox of kappa KL(y || .) (Poisson likelihood, closed form; reading R31)."""
+    return float(_load().or_prox_kl(v, y, kappa))
+
+
 # ---------------------------------------------------------------- chain
 @dataclass
 class Problem:
@@ -159,7 +169,7 @@ class Problem:
     y: np.ndarray
     sigma2: float
     gamma: float
-    op: str = "conv"                      # "conv" | "mask"
+    op: str = "conv"                      # "conv" | "mask" | "poisson"
     kernel: Optional[np.ndarray] = None   # 2-D true-convolution kernel
     ksep: Optional[tuple] = None          # (ky, kx) separable factors
     mask: Optional[np.ndarray] = None
@@ -177,6 +187,9 @@ class Problem:
     z_lo: float = -np.inf
     z_hi: float = np.inf
     x0: Optional[np.ndarray] = None
+    eta: float = 0.0                      # op "poisson": y ~ Poisson(eta H x), z1 ~ eta H x
+    rho1: float = 0.0
+    kappa1: float = 0.0
     extra: dict = field(default_factory=dict)
 
 
@@ -190,8 +203,8 @@ def run(pb: Problem, n_iter: int, burn_in: int, seed: int, tiles=(1, 1), bf16_em
     keep = [y]
     cfg = _Config()
     cfg.ny, cfg.nx = ny, nx
-    cfg.op = 0 if pb.op == "conv" else 1
-    if pb.op == "conv":
+    cfg.op = {"conv": 0, "mask": 1, "poisson": 2}[pb.op]
+    if pb.op in ("conv", "poisson"):
         if pb.ksep is not None:
             ky, kx = _f32(pb.ksep[0]), _f32(pb.ksep[1])
             keep += [ky, kx]
@@ -224,14 +237,15 @@ def run(pb: Problem, n_iter: int, burn_in: int, seed: int, tiles=(1, 1), bf16_em
     cfg.n_iter, cfg.burn_in, cfg.seed = n_iter, burn_in, seed
     cfg.tiles_y, cfg.tiles_x = tiles
     cfg.i_off, cfg.j_off = origin
-    x = np.zeros((ny, nx)); z = np.zeros((ny, nx))
+    cfg.eta, cfg.rho1, cfg.kappa1 = pb.eta, pb.rho1, pb.kappa1
+    x = np.zeros((ny, nx)); z = np.zeros((ny, nx)); z1 = np.zeros((ny, nx))
     mean = np.zeros((ny, nx)); var = np.zeros((ny, nx))
     n = C.c_int64()
     have_mean = n_iter > burn_in
     have_var = want_var and n_iter - burn_in >= 2
-    e = lib.or_run(C.byref(cfg), x.ctypes.data, z.ctypes.data, mean.ctypes.data if have_mean else None,
-                   var.ctypes.data if have_var else None, C.byref(n))
+    e = lib.or_run_ex(C.byref(cfg), x.ctypes.data, z.ctypes.data, z1.ctypes.data,
+                      mean.ctypes.data if have_mean else None, var.ctypes.data if have_var else None, C.byref(n))
     if e:
         raise ValueError(f"or_run failed with status {e}")
-    return {"x": x, "z": z, "mean": mean if have_mean else None, "var": var if have_var else None,
+    return {"x": x, "z": z, "z1": z1, "mean": mean if have_mean else None, "var": var if have_var else None,
             "n": n.value}

@@ -26,6 +26,12 @@
  *   or_run (tiles>1)    same chain, every tile computed from its own padded copy S_b x
  *                       (Def. prop:localselection P:135-152, ghost regions P:494-498)
  *   or_check_stepsizes  eq:stepsize_cond P:581-587 (reading R11: ||H2||^2 -> ||H2||^2/rho)
+ *   or_prox_kl          prox of kappa KL(y || .) for the Poisson likelihood (eq:poisson:f2 P:737-741;
+ *                       closed form = the positive root of u^2 - (v - kappa) u - kappa y = 0, reading R31)
+ *   or_run (op = 2)     Poisson deconvolution (sec:poisson_deconvolution P:727-744):
+ *                       f1 = 0, z = (z1, z2), z1 ~ eta H x with f2,1 = KL(y || .) (rho1, kappa1),
+ *                       z2 ~ x with f2,2 = indicator of [z_lo, z_hi] (rho, kappa); Algorithm 1 lines
+ *                       6-13 with H2 = [eta H; I] (readings R32-R34)
  *
  * Parity pins for each function live in tests/test_oracle_*.py (see DESIGN.md
  * section "Oracle pins").
@@ -225,9 +231,21 @@ int or_check_stepsizes(double L, double h2_over_rho, double alpha, double eps, d
 }
 
 /* ------------------------------------------------------------------ */
+/* prox_{kappa KL(y || .)}(v) = argmin_{u > 0} kappa (u - y log u) + (u - v)^2 / 2 (the Poisson
+ * negative log-likelihood of eq:likelihood:poisson_deconvolution up to constants).
+ * Stationarity: kappa (1 - y/u) + u - v = 0  <=>  u^2 - (v - kappa) u - kappa y = 0; the prox
+ * is the non-negative root  u = ((v - kappa) + sqrt((v - kappa)^2 + 4 kappa y)) / 2
+ * (y = 0: max(v - kappa, 0)).  Reading R31.                                                   */
+double or_prox_kl(double v, double y, double kappa) {
+  double a = v - kappa;
+  return 0.5 * (a + sqrt(a * a + 4.0 * kappa * y));
+}
+
+/* ------------------------------------------------------------------ */
 typedef struct {
   int32_t ny, nx;
-  int32_t op;                    /* 0 = convolution H1, 1 = mask H1 = diag(m) */
+  int32_t op;                    /* 0 = convolution H1, 1 = mask H1 = diag(m),
+                                    2 = Poisson deconvolution (f1 = 0; z1 ~ eta H x, KL prox) */
   const float *kernel;           /* kh x kw true-convolution kernel, or NULL when separable given */
   const float *ksep_y;           /* optional separable factors: k[p][q] = ksep_y[p] * ksep_x[q] */
   const float *ksep_x;
@@ -249,6 +267,7 @@ typedef struct {
   int64_t i_off, j_off;          /* global coordinates of pixel (0,0) of this (cropped) image:
                                     the noise is indexed by global pixel (reading R9), so a crop
                                     of a larger image draws the same xi/zeta at the same pixel */
+  double eta, rho1, kappa1;      /* op = 2: Poisson scale and the z1 block's coupling / step */
 } or_config;
 
 static void or_kernel2d(const or_config *c, double *k) {
@@ -260,8 +279,8 @@ static void or_kernel2d(const or_config *c, double *k) {
 
 /* One untiled iteration of Algorithm 1 (lines 5-13) on global arrays. */
 static int or_step_global(const or_config *c, const double *k, const double *yd, uint64_t t,
-                          const double *x, const double *z, double *xn, double *zn,
-                          double *r, double *g, double *G) {
+                          const double *x, const double *z, const double *z1, double *xn, double *zn,
+                          double *z1n, double *r, double *g, double *G) {
   int ny = c->ny, nx = c->nx;
   int64_t npx = (int64_t)ny * nx;
   /* line 6: u1 = H1^T grad f1(H1 x),  f1(v) = ||y - v||^2/(2 sigma^2) (eq:potential_gaussian_likelihood) */
@@ -269,13 +288,20 @@ static int or_step_global(const or_config *c, const double *k, const double *yd,
     or_conv_fwd(x, ny, nx, k, c->kh, c->kw, r);
     for (int64_t n = 0; n < npx; n++) r[n] -= yd[n];
     or_conv_adj(r, ny, nx, k, c->kh, c->kw, g);
-  } else {
+    for (int64_t n = 0; n < npx; n++) g[n] /= c->sigma2;
+  } else if (c->op == 1) {
     for (int64_t n = 0; n < npx; n++) {
       double m = c->mask[n] ? 1.0 : 0.0;
       g[n] = m * (m * x[n] - yd[n]);
     }
+    for (int64_t n = 0; n < npx; n++) g[n] /= c->sigma2;
+  } else {
+    /* op 2: f1 = 0; line 7 for the z1 block: (1/rho1) (eta H)^T (eta H x - z1) */
+    or_conv_fwd(x, ny, nx, k, c->kh, c->kw, r);
+    for (int64_t n = 0; n < npx; n++) r[n] = c->eta * r[n] - z1[n];
+    or_conv_adj(r, ny, nx, k, c->kh, c->kw, g);
+    for (int64_t n = 0; n < npx; n++) g[n] = c->eta * g[n] / c->rho1;
   }
-  for (int64_t n = 0; n < npx; n++) g[n] /= c->sigma2;
   /* line 8: D_eps(x) - x = -G_eps(x) */
   int use_cnn = c->n_layers > 0 && c->alpha != 0.0;
   if (use_cnn) {
@@ -309,6 +335,18 @@ static int or_step_global(const or_config *c, const double *k, const double *yd,
         zn[n] = v < c->z_lo ? c->z_lo : (v > c->z_hi ? c->z_hi : v);
       }
   }
+  if (c->op == 2) {
+    /* lines 11-13 for the z1 block: H2,1 = eta H, prox of kappa1 KL(y || .), stream 2 */
+    or_conv_fwd(xn, ny, nx, k, c->kh, c->kw, r);
+    double sq2k1 = sqrt(2.0 * c->kappa1);
+    for (int64_t i = 0; i < ny; i++)
+      for (int64_t j = 0; j < nx; j++) {
+        int64_t n = i * nx + j;
+        double v = z1[n] - (c->kappa1 / c->rho1) * (z1[n] - c->eta * r[n]) +
+                   sq2k1 * or_normal(c->seed, (uint32_t)(t + 1), i + c->i_off, j + c->j_off, 2);
+        z1n[n] = or_prox_kl(v, yd[n], c->kappa1);
+      }
+  }
   return OR_OK;
 }
 
@@ -316,11 +354,12 @@ static int or_step_global(const or_config *c, const double *k, const double *yd,
  * from S_b x only (the tile plus a ghost frame of width h, zero outside the
  * image), exactly as worker b of Algorithm 1 would after line 5. */
 static int or_step_tiled(const or_config *c, const double *k, const double *yd, uint64_t t,
-                         const double *x, const double *z, double *xn, double *zn) {
+                         const double *x, const double *z, const double *z1, double *xn, double *zn,
+                         double *z1n) {
   int ny = c->ny, nx = c->nx;
   int ry = c->kh / 2, rx = c->kw / 2;
   int use_cnn = c->n_layers > 0 && c->alpha != 0.0;
-  int hr = (c->op == 0) ? 2 * (ry > rx ? ry : rx) : 0;
+  int hr = (c->op != 1) ? 2 * (ry > rx ? ry : rx) : 0;
   int h = use_cnn && c->n_layers > hr ? c->n_layers : hr;
   for (int ty = 0; ty < c->tiles_y; ty++)
     for (int tx = 0; tx < c->tiles_x; tx++) {
@@ -341,8 +380,10 @@ static int or_step_tiled(const or_config *c, const double *k, const double *yd, 
           int64_t gi = i0 - h + a, gj = j0 - h + b;
           if (gi >= 0 && gi < ny && gj >= 0 && gj < nx) xp[(int64_t)a * pw + b] = x[gi * nx + gj];
         }
-      if (c->op == 0) {
-        /* residual on tile (+) r, zero outside the image (reading R7) */
+      if (c->op != 1) {
+        /* residual on tile (+) r, zero outside the image (reading R7); op 2: eta H x - z1, where
+         * z1 on the ring is worker b's own copy (identical values: it is computed redundantly on
+         * tile (+) r_H, reading R33) */
         for (int a = h - ry; a < h + th + ry; a++)
           for (int b = h - rx; b < h + tw + rx; b++) {
             int64_t gi = i0 - h + a, gj = j0 - h + b;
@@ -354,7 +395,7 @@ static int or_step_tiled(const or_config *c, const double *k, const double *yd, 
                 if (ii < 0 || ii >= ny || jj < 0 || jj >= nx) continue;
                 s += k[(p + ry) * c->kw + (q + rx)] * xp[(a - p) * (int64_t)pw + (b - q)];
               }
-            rp[(int64_t)a * pw + b] = s - yd[gi * nx + gj];
+            rp[(int64_t)a * pw + b] = c->op == 2 ? c->eta * s - z1[gi * nx + gj] : s - yd[gi * nx + gj];
           }
         for (int a = 0; a < th; a++)
           for (int b = 0; b < tw; b++) {
@@ -376,7 +417,8 @@ static int or_step_tiled(const or_config *c, const double *k, const double *yd, 
             gl[(int64_t)a * tw + b] = m * (m * xp[(int64_t)(a + h) * pw + (b + h)] - yd[n]);
           }
       }
-      for (int64_t n = 0; n < (int64_t)th * tw; n++) gl[n] /= c->sigma2;
+      for (int64_t n = 0; n < (int64_t)th * tw; n++)
+        gl[n] = c->op == 2 ? c->eta * gl[n] / c->rho1 : gl[n] / c->sigma2;
       if (use_cnn) {
         /* receptive-field strategy: layer k is evaluated on tile (+) (K-k),
          * activations outside the image are zero at every layer input (reading R8). */
@@ -450,17 +492,52 @@ static int or_step_tiled(const or_config *c, const double *k, const double *yd, 
       free(gl);
       free(Gl);
     }
+  if (c->op == 2) {
+    /* line 11: every worker retrieves S_{2,b} x^{t+1} (its tile plus a ghost frame of width
+     * r_H) once all blocks of x^{t+1} exist; lines 12-13 for its block of z1 */
+    double sq2k1 = sqrt(2.0 * c->kappa1);
+    for (int ty = 0; ty < c->tiles_y; ty++)
+      for (int tx = 0; tx < c->tiles_x; tx++) {
+        int64_t i0, i1, j0, j1;
+        or_partition(ny, c->tiles_y, ty, &i0, &i1);
+        or_partition(nx, c->tiles_x, tx, &j0, &j1);
+        int th = (int)(i1 - i0), tw = (int)(j1 - j0);
+        int ph = th + 2 * ry, pw = tw + 2 * rx;
+        double *xp = (double *)calloc((size_t)ph * pw, sizeof(double));
+        if (!xp) return OR_E_INVALID;
+        for (int a = 0; a < ph; a++)
+          for (int b = 0; b < pw; b++) {
+            int64_t gi = i0 - ry + a, gj = j0 - rx + b;
+            if (gi >= 0 && gi < ny && gj >= 0 && gj < nx) xp[(int64_t)a * pw + b] = xn[gi * nx + gj];
+          }
+        for (int a = 0; a < th; a++)
+          for (int b = 0; b < tw; b++) {
+            int64_t gi = i0 + a, gj = j0 + b, n = gi * nx + gj;
+            double s = 0.0;
+            for (int p = -ry; p <= ry; p++)
+              for (int q = -rx; q <= rx; q++)
+                s += k[(p + ry) * c->kw + (q + rx)] * xp[(int64_t)(a + ry - p) * pw + (b + rx - q)];
+            double v = z1[n] - (c->kappa1 / c->rho1) * (z1[n] - c->eta * s) +
+                       sq2k1 * or_normal(c->seed, (uint32_t)(t + 1), gi + c->i_off, gj + c->j_off, 2);
+            z1n[n] = or_prox_kl(v, yd[n], c->kappa1);
+          }
+        free(xp);
+      }
+  }
   return OR_OK;
 }
 
-/* Full chain.  Outputs (each ny*nx, any may be NULL): final x, final z,
- * MMSE mean and variance (M2/(n-1), reading R15) of x^{(t)}, t = burn_in+1..n_iter
- * (reading R14), accumulated with Welford's update (P:839 footnote). */
-int or_run(const or_config *c, double *x_out, double *z_out, double *mean_out, double *var_out,
-           int64_t *n_samples) {
-  if (c->ny <= 0 || c->nx <= 0 || c->gamma <= 0.0 || c->sigma2 <= 0.0) return OR_E_INVALID;
-  if (c->op == 0 && (c->kh % 2 == 0 || c->kw % 2 == 0)) return OR_E_INVALID;
+/* Full chain.  Outputs (each ny*nx, any may be NULL): final x, final z (z2 block for
+ * op = 2), final z1 (op = 2), MMSE mean and variance (M2/(n-1), reading R15) of x^{(t)},
+ * t = burn_in+1..n_iter (reading R14), accumulated with Welford's update (P:839 footnote). */
+int or_run_ex(const or_config *c, double *x_out, double *z_out, double *z1_out, double *mean_out,
+              double *var_out, int64_t *n_samples) {
+  if (c->ny <= 0 || c->nx <= 0 || c->gamma <= 0.0) return OR_E_INVALID;
+  if (c->op != 2 && c->sigma2 <= 0.0) return OR_E_INVALID;
+  if (c->op != 1 && (c->kh % 2 == 0 || c->kw % 2 == 0)) return OR_E_INVALID;
   if (c->rho > 0.0 && !(c->kappa > 0.0 && c->kappa < c->rho)) return OR_E_INVALID;
+  if (c->op == 2 && !(c->eta > 0.0 && c->rho1 > 0.0 && c->kappa1 > 0.0 && c->kappa1 < c->rho1))
+    return OR_E_INVALID;
   int64_t npx = (int64_t)c->ny * c->nx;
   double *k = (double *)calloc((size_t)(c->kh > 0 ? c->kh * c->kw : 1), sizeof(double));
   double *yd = (double *)malloc(sizeof(double) * (size_t)npx);
@@ -468,14 +545,19 @@ int or_run(const or_config *c, double *x_out, double *z_out, double *mean_out, d
   double *xn = (double *)calloc((size_t)npx, sizeof(double));
   double *z = (double *)calloc((size_t)npx, sizeof(double));
   double *zn = (double *)calloc((size_t)npx, sizeof(double));
+  double *z1 = (double *)calloc((size_t)npx, sizeof(double));
+  double *z1n = (double *)calloc((size_t)npx, sizeof(double));
   double *r = (double *)calloc((size_t)npx, sizeof(double));
   double *g = (double *)calloc((size_t)npx, sizeof(double));
   double *G = (double *)calloc((size_t)npx, sizeof(double));
   double *mu = (double *)calloc((size_t)npx, sizeof(double));
   double *m2 = (double *)calloc((size_t)npx, sizeof(double));
   int err = OR_OK;
-  if (!k || !yd || !x || !xn || !z || !zn || !r || !g || !G || !mu || !m2) { err = OR_E_INVALID; goto done; }
-  if (c->op == 0) or_kernel2d(c, k);
+  if (!k || !yd || !x || !xn || !z || !zn || !z1 || !z1n || !r || !g || !G || !mu || !m2) {
+    err = OR_E_INVALID;
+    goto done;
+  }
+  if (c->op != 1) or_kernel2d(c, k);
   for (int64_t n = 0; n < npx; n++) {
     yd[n] = (double)c->y[n];
     x[n] = c->x0 ? (double)c->x0[n] : 0.0;   /* x^0 */
@@ -483,9 +565,9 @@ int or_run(const or_config *c, double *x_out, double *z_out, double *mean_out, d
   int64_t cnt = 0;
   for (int64_t t = 0; t < c->n_iter; t++) {
     if (c->tiles_y > 1 || c->tiles_x > 1)
-      err = or_step_tiled(c, k, yd, (uint64_t)t, x, z, xn, zn);
+      err = or_step_tiled(c, k, yd, (uint64_t)t, x, z, z1, xn, zn, z1n);
     else
-      err = or_step_global(c, k, yd, (uint64_t)t, x, z, xn, zn, r, g, G);
+      err = or_step_global(c, k, yd, (uint64_t)t, x, z, z1, xn, zn, z1n, r, g, G);
     if (err) goto done;
     if (t + 1 > c->burn_in) {
       cnt++;
@@ -497,9 +579,11 @@ int or_run(const or_config *c, double *x_out, double *z_out, double *mean_out, d
     }
     double *tt = x; x = xn; xn = tt;
     if (c->rho > 0.0) { tt = z; z = zn; zn = tt; }
+    if (c->op == 2) { tt = z1; z1 = z1n; z1n = tt; }
   }
   if (x_out) memcpy(x_out, x, sizeof(double) * (size_t)npx);
   if (z_out) memcpy(z_out, z, sizeof(double) * (size_t)npx);
+  if (z1_out) memcpy(z1_out, z1, sizeof(double) * (size_t)npx);
   if (n_samples) *n_samples = cnt;
   if (mean_out) {
     if (cnt < 1) { err = OR_E_STATS_EMPTY; goto done; }
@@ -510,6 +594,12 @@ int or_run(const or_config *c, double *x_out, double *z_out, double *mean_out, d
     for (int64_t n = 0; n < npx; n++) var_out[n] = m2[n] / (double)(cnt - 1);
   }
 done:
-  free(k); free(yd); free(x); free(xn); free(z); free(zn); free(r); free(g); free(G); free(mu); free(m2);
+  free(k); free(yd); free(x); free(xn); free(z); free(zn); free(z1); free(z1n);
+  free(r); free(g); free(G); free(mu); free(m2);
   return err;
+}
+
+int or_run(const or_config *c, double *x_out, double *z_out, double *mean_out, double *var_out,
+           int64_t *n_samples) {
+  return or_run_ex(c, x_out, z_out, NULL, mean_out, var_out, n_samples);
 }
