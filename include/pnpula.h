@@ -69,7 +69,7 @@ typedef enum {
   PNPULA_E_UNSUPPORTED = 10        /* e.g. channels not in {16, 32, 64} */
 } pnpula_status;
 
-enum { PNPULA_OP_CONV = 0, PNPULA_OP_MASK = 1 };
+enum { PNPULA_OP_CONV = 0, PNPULA_OP_MASK = 1, PNPULA_OP_POISSON = 2 };
 enum { PNPULA_SCOPE_LOCAL = 0, PNPULA_SCOPE_GLOBAL_ON_ROOT = 1 };
 
 /* flags */
@@ -99,19 +99,22 @@ typedef struct {
   const uint8_t *nccl_uid;       /* 128 bytes from pnpula_get_unique_id on rank 0; required if world_size > 1 */
   uint64_t stream;               /* cudaStream_t to launch on, or 0 for a context-owned stream */
 
-  /* likelihood f1(H1 x) = ||y - H1 x||^2 / (2 sigma2)  (eq:potential_gaussian_likelihood P:708-711) */
-  int32_t op;                    /* PNPULA_OP_CONV or PNPULA_OP_MASK */
+  /* likelihood f1(H1 x) = ||y - H1 x||^2 / (2 sigma2)  (eq:potential_gaussian_likelihood P:708-711),
+   * or (PNPULA_OP_POISSON) y ~ Poisson(eta H x) handled through AXDA (eq:poisson:f2 P:737-741):
+   * f1 = 0, block z1 ~ eta H x with f2,1 = KL(y || .) (eta, rho1, kappa1 below), block z2 ~ x
+   * with f2,2 = indicator of [z_lo, z_hi] (rho, kappa; the paper's R+ is z_lo = 0, z_hi = inf) */
+  int32_t op;                    /* PNPULA_OP_CONV, PNPULA_OP_MASK or PNPULA_OP_POISSON */
   const float *kernel;           /* host kh x kw row-major true-convolution kernel; may be NULL if separable factors given */
   const float *kernel_y;         /* optional separable factors: kernel[p][q] = kernel_y[p] * kernel_x[q] exactly */
   const float *kernel_x;
   int32_t kh, kw;                /* odd sizes, <= 15 */
   const uint8_t *mask;           /* host, covers in_rect, OP_MASK only (nonzero = observed) */
-  const float *y;                /* host observations covering in_rect */
+  const float *y;                /* host observations covering in_rect (OP_POISSON: counts >= 0) */
   const float *x0;               /* host initial state covering in_rect, or NULL for zeros */
   pnpula_rect in_rect;           /* the rectangle y / mask / x0 cover (row-major h x w); must contain
                                     every owned tile (+) r_H clipped to the image.  Use the whole image
                                     {0, 0, ny, nx} when passing global arrays. */
-  double sigma2;                 /* noise variance > 0 */
+  double sigma2;                 /* noise variance > 0 (ignored by OP_POISSON) */
 
   /* prior */
   const pnpula_denoiser *den;    /* NULL or alpha == 0: no CNN term */
@@ -127,6 +130,13 @@ typedef struct {
   double lipschitz_L, lipschitz_LD;
 
   int32_t flags;                 /* PNPULA_FLAG_* */
+
+  /* OP_POISSON only (sec:poisson_deconvolution P:727-744; R31-R34):
+   * eta > 0 Poisson scale, rho1 > 0 coupling of z1 ~ eta H x, kappa1 in (0, rho1) its PSGLA step.
+   * Per iteration: x+ = x - (gamma/rho1)(eta H)^T(eta H x - z1) - (gamma/rho)(x - z2) + prior and
+   * box terms + sqrt(2 gamma) xi;  z2+ as for OP_CONV;  z1+ = prox_{kappa1 KL(y||.)}(z1 -
+   * (kappa1/rho1)(z1 - eta H x+) + sqrt(2 kappa1) zeta1), zeta1 = Philox stream 2. */
+  double eta, rho1, kappa1;
 } pnpula_config;
 
 typedef struct pnpula_ctx pnpula_ctx;
@@ -175,6 +185,10 @@ pnpula_status pnpula_get_moments(pnpula_ctx *ctx, float *mean, float *var, int64
 
 /* [collective for GLOBAL scope] Current state x^t, z^t (either may be NULL) and t. */
 pnpula_status pnpula_get_state(pnpula_ctx *ctx, float *x, float *z, int64_t *t, int32_t scope);
+
+/* [collective for GLOBAL scope] OP_POISSON: current z1 block (the AXDA variable ~ eta H x) on the
+ * LOCAL bbox or, on root, the whole image. */
+pnpula_status pnpula_get_z1(pnpula_ctx *ctx, float *z1, int32_t scope);
 
 /* Number of tiles owned by this rank; halo width h; the i-th owned tile's rectangle. */
 pnpula_status pnpula_tile_info(pnpula_ctx *ctx, int32_t local_index, pnpula_rect *rect,

@@ -16,7 +16,7 @@ LIB_PATH = os.environ.get("PNPULA_LIB") or os.path.join(_PKG, "libpnpula.so")
 PNPULA_OK = 0
 STATUS = {0: "OK", 1: "E_INVALID_ARG", 2: "E_SHAPE", 3: "E_PARTITION_TOO_FINE", 4: "E_STEPSIZE",
           5: "E_STATS_EMPTY", 6: "E_STATE", 7: "E_CUDA", 8: "E_NCCL", 9: "E_OOM", 10: "E_UNSUPPORTED"}
-OP_CONV, OP_MASK = 0, 1
+OP_CONV, OP_MASK, OP_POISSON = 0, 1, 2
 SCOPE_LOCAL, SCOPE_GLOBAL_ON_ROOT = 0, 1
 FLAG_HALO_VIA_NCCL, FLAG_CNN_LAYERWISE, FLAG_NO_GRAPH = 0x1, 0x2, 0x4
 
@@ -54,6 +54,7 @@ class Config(C.Structure):
         ("gamma", C.c_double),
         ("lipschitz_L", C.c_double), ("lipschitz_LD", C.c_double),
         ("flags", C.c_int32),
+        ("eta", C.c_double), ("rho1", C.c_double), ("kappa1", C.c_double),
     ]
 
 
@@ -85,6 +86,7 @@ def load():
         "pnpula_local_bbox": ([vp, C.POINTER(Rect)], C.c_int),
         "pnpula_get_moments": ([vp, vp, vp, C.POINTER(i64), i32], C.c_int),
         "pnpula_get_state": ([vp, vp, vp, C.POINTER(i64), i32], C.c_int),
+        "pnpula_get_z1": ([vp, vp, i32], C.c_int),
         "pnpula_tile_info": ([vp, i32, C.POINTER(Rect), C.POINTER(i32), C.POINTER(i32)], C.c_int),
         "pnpula_get_padded_x": ([vp, i32, vp], C.c_int),
         "pnpula_get_denoiser_residual": ([vp, vp], C.c_int),
@@ -107,7 +109,7 @@ def load():
 # names exported by include/pnpula.h (tests check the .so exports every one)
 EXPORTED = ["pnpula_version", "pnpula_last_error", "pnpula_get_unique_id", "pnpula_create", "pnpula_reset",
             "pnpula_advance", "pnpula_run", "pnpula_synchronize", "pnpula_local_bbox", "pnpula_get_moments",
-            "pnpula_get_state", "pnpula_tile_info", "pnpula_get_padded_x", "pnpula_get_denoiser_residual",
+            "pnpula_get_state", "pnpula_get_z1", "pnpula_tile_info", "pnpula_get_padded_x", "pnpula_get_denoiser_residual",
             "pnpula_set_timing", "pnpula_kernel_time", "pnpula_destroy", "pnpula_partition",
             "pnpula_halo_width", "pnpula_plan_halo", "pnpula_check_stepsizes"]
 

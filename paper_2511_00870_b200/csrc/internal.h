@@ -43,6 +43,23 @@ struct UpdateParams {
   uint32_t seed_lo, seed_hi, t1;   // Philox key and iteration index t+1
   int accumulate;                  // t+1 > burn_in
   float inv_n;                     // 1 / (t+1 - burn_in)
+  float eta;                       // residual r = eta (H x) - y: 1 for the Gaussian likelihood;
+                                   // Poisson (reading R32): eta, with y -> z1 (AXDA block eta H x)
+};
+
+// z1 block of the Poisson posterior (readings R32-R34): on tile (+) r_H (inside the image)
+//   z1 <- prox_{kappa1 KL(y || .)}( z1 - (kappa1/rho1)(z1 - eta H x+) + sqrt(2 kappa1) zeta1 )
+// with zeta1 = Philox stream 2 at the global pixel; x+ padded (halo >= 2 r_H valid).
+struct Z1Params {
+  const float *x;       // padded x^{t+1}
+  const float *y;       // padded counts (valid on tile (+) r_H)
+  float *z1;            // padded z1, in place on tile (+) r_H
+  TileGeom g;
+  int ny, nx;
+  int ry, rx;
+  float k2d[kMaxTaps * kMaxTaps];   // 2-D taps (separable factors multiplied out on the host)
+  float eta, b1, s1, kappa1;        // eta, kappa1/rho1, sqrt(2 kappa1), kappa1
+  uint32_t seed_lo, seed_hi, t1;
 };
 
 // One rectangular copy between pitched fp32 buffers (halo exchange, pack/unpack).
@@ -87,6 +104,7 @@ struct CnnChunkParams {
 
 // Launchers (return cudaGetLastError()).
 cudaError_t launch_update(const UpdateParams &p, cudaStream_t s);
+cudaError_t launch_z1_update(const Z1Params &p, cudaStream_t s);
 cudaError_t launch_copy_jobs(const CopyJob *d_jobs, int njobs, int max_rows, cudaStream_t s);
 cudaError_t launch_fill(float *p, float v, size_t n, cudaStream_t s);
 cudaError_t launch_finalize(const FinalizeParams &p, cudaStream_t s);

@@ -43,6 +43,7 @@ struct TileDev {
   float *y = nullptr;
   uint8_t *mask = nullptr;
   float *z = nullptr, *mean = nullptr, *m2 = nullptr, *G = nullptr;
+  float *z1 = nullptr;     // OP_POISSON: z1 block, valid on tile (+) r_H (reading R33)
   uint16_t *act[2] = {nullptr, nullptr};   // inter-chunk activations
 };
 
@@ -67,6 +68,7 @@ struct pnpula_ctx {
   std::vector<float> k2d, ky, kx;
   double sigma2 = 1, alpha = 0, eps = 1, lambda = 0, c_lo = 0, c_hi = 1, rho = 0, kappa = 0,
          z_lo = 0, z_hi = 0, gamma = 0;
+  double eta = 1, rho1 = 0, kappa1 = 0;   // OP_POISSON
   int flags = 0;
   int n_layers = 0, channels = 0;   // 0 layers = no CNN
   int h = 0;
@@ -299,15 +301,18 @@ UpdateParams make_update_params(pnpula_ctx *c, TileDev &td, int buf) {
   p.m2 = td.m2;
   p.g = td.g;
   p.ny = c->ny; p.nx = c->nx;
-  p.op = c->op;
+  const bool poisson = c->op == PNPULA_OP_POISSON;
+  p.op = poisson ? PNPULA_OP_CONV : c->op;   // the x-update runs the conv path with y -> z1 (R32)
   p.ry = c->ry; p.rx = c->rx;
   p.separable = c->separable;
-  if (c->op == PNPULA_OP_CONV) {
+  p.eta = 1.0f;
+  if (poisson) { p.y = td.z1; p.eta = (float)c->eta; }
+  if (c->op != PNPULA_OP_MASK) {
     for (size_t i = 0; i < c->k2d.size(); ++i) p.k2d[i] = c->k2d[i];
     for (size_t i = 0; i < c->ky.size(); ++i) p.ky[i] = c->ky[i];
     for (size_t i = 0; i < c->kx.size(); ++i) p.kx[i] = c->kx[i];
   }
-  p.a_g = (float)(c->gamma / c->sigma2);
+  p.a_g = poisson ? (float)(c->gamma * c->eta / c->rho1) : (float)(c->gamma / c->sigma2);
   p.has_z = c->rho > 0;
   p.a_rho = p.has_z ? (float)(c->gamma / c->rho) : 0.f;
   p.has_G = c->n_layers > 0;
@@ -346,6 +351,34 @@ pnpula_status step(pnpula_ctx *c) {
   }
   pnpula_status s = exchange(c, buf ^ 1);
   if (s) return s;
+  if (c->op == PNPULA_OP_POISSON) {
+    // line 11-13 for the z1 block: x^{t+1} (halo now valid) -> z1 on tile (+) r_H (R33, R34)
+    for (auto &td : c->tiles) {
+      Z1Params q{};
+      q.x = td.x[buf ^ 1];
+      q.y = td.y;
+      q.z1 = td.z1;
+      q.g = td.g;
+      q.ny = c->ny; q.nx = c->nx;
+      q.ry = c->ry; q.rx = c->rx;
+      const int kh = 2 * c->ry + 1, kw = 2 * c->rx + 1;
+      for (int a = 0; a < kh; ++a)
+        for (int b = 0; b < kw; ++b)
+          q.k2d[a * kw + b] = c->separable ? c->ky[a] * c->kx[b] : c->k2d[a * kw + b];
+      q.eta = (float)c->eta;
+      q.b1 = (float)(c->kappa1 / c->rho1);
+      q.s1 = (float)std::sqrt(2.0 * c->kappa1);
+      q.kappa1 = (float)c->kappa1;
+      q.seed_lo = (uint32_t)c->seed;
+      q.seed_hi = (uint32_t)(c->seed >> 32);
+      q.t1 = (uint32_t)t1;
+      cudaEvent_t end;
+      timer_begin(c, c->tm_update, &end);
+      CU(c, launch_z1_update(q, c->stream));
+      c->n_launches++;
+      timer_end(c, end);
+    }
+  }
   c->cur ^= 1;
   c->t += 1;
   return PNPULA_OK;
@@ -454,7 +487,7 @@ void pnpula_partition(int64_t n, int64_t parts, int64_t p, int64_t *lo, int64_t 
 }
 
 int32_t pnpula_halo_width(int32_t op, int32_t kh, int32_t kw, int32_t n_layers) {
-  int r = (op == PNPULA_OP_CONV) ? std::max(kh, kw) / 2 : 0;
+  int r = (op == PNPULA_OP_CONV || op == PNPULA_OP_POISSON) ? std::max(kh, kw) / 2 : 0;
   return std::max(2 * r, std::max(n_layers, 0));
 }
 
@@ -519,10 +552,16 @@ pnpula_status pnpula_create(const pnpula_config *cfg, pnpula_ctx **out) {
   if (f.world_size <= 0 || ntiles % f.world_size != 0 || f.rank < 0 || f.rank >= f.world_size) {
     set_error("world_size must divide the tile count and rank be in range"); return PNPULA_E_INVALID_ARG;
   }
-  if (!(f.gamma > 0) || !(f.sigma2 > 0)) { set_error("gamma and sigma2 must be > 0"); return PNPULA_E_INVALID_ARG; }
+  if (f.op != PNPULA_OP_CONV && f.op != PNPULA_OP_MASK && f.op != PNPULA_OP_POISSON) {
+    set_error("unknown op"); return PNPULA_E_INVALID_ARG;
+  }
+  const bool poisson = f.op == PNPULA_OP_POISSON;
+  if (!(f.gamma > 0) || (!poisson && !(f.sigma2 > 0))) { set_error("gamma and sigma2 must be > 0"); return PNPULA_E_INVALID_ARG; }
   if (!f.y) { set_error("y is required"); return PNPULA_E_INVALID_ARG; }
-  if (f.op != PNPULA_OP_CONV && f.op != PNPULA_OP_MASK) { set_error("unknown op"); return PNPULA_E_INVALID_ARG; }
-  if (f.op == PNPULA_OP_CONV) {
+  if (poisson && !(f.eta > 0 && f.rho1 > 0 && f.kappa1 > 0 && f.kappa1 < f.rho1)) {
+    set_error("OP_POISSON needs eta > 0, rho1 > 0 and kappa1 in (0, rho1)"); return PNPULA_E_INVALID_ARG;
+  }
+  if (f.op != PNPULA_OP_MASK) {
     if (f.kh <= 0 || f.kw <= 0 || f.kh % 2 == 0 || f.kw % 2 == 0 || f.kh > kMaxTaps || f.kw > kMaxTaps) {
       set_error("kernel sizes must be odd and <= %d", kMaxTaps); return PNPULA_E_INVALID_ARG;
     }
@@ -548,7 +587,8 @@ pnpula_status pnpula_create(const pnpula_config *cfg, pnpula_ctx **out) {
   c->sigma2 = f.sigma2; c->alpha = f.alpha; c->eps = f.eps; c->lambda = f.lambda;
   c->c_lo = f.c_lo; c->c_hi = f.c_hi; c->rho = f.rho; c->kappa = f.kappa;
   c->z_lo = f.z_lo; c->z_hi = f.z_hi; c->gamma = f.gamma;
-  if (f.op == PNPULA_OP_CONV) {
+  if (poisson) { c->eta = f.eta; c->rho1 = f.rho1; c->kappa1 = f.kappa1; }
+  if (f.op != PNPULA_OP_MASK) {
     c->kh = f.kh; c->kw = f.kw; c->ry = f.kh / 2; c->rx = f.kw / 2;
     c->separable = (f.kernel_y && f.kernel_x) ? 1 : 0;
     if (c->separable) {
@@ -567,9 +607,10 @@ pnpula_status pnpula_create(const pnpula_config *cfg, pnpula_ctx **out) {
   // step-size check (warning only)
   {
     double L = f.lipschitz_L;
+    double L_h2 = 0;
     if (L <= 0) {
       double s = 0;
-      if (f.op == PNPULA_OP_CONV) {
+      if (f.op != PNPULA_OP_MASK) {
         if (c->separable) {
           double a = 0, b = 0;
           for (float v : c->ky) a += std::fabs(v);
@@ -582,9 +623,13 @@ pnpula_status pnpula_create(const pnpula_config *cfg, pnpula_ctx **out) {
         s = 1;
       }
       L = s * s / f.sigma2;   // ||H||^2 <= ||k||_1^2 (Young)
+      // OP_POISSON: f1 = 0 and the z1 block contributes ||eta H||^2 / rho1 to ||H2||^2/rho
+      if (poisson) L = 0;
+      if (poisson) s = s * f.eta;
+      if (poisson) L_h2 = s * s / f.rho1;
     }
     const double lam = f.lambda > 0 ? f.lambda : 1e300;
-    int32_t bad = pnpula_check_stepsizes(L, f.rho > 0 ? 1.0 / f.rho : 0.0, use_cnn ? f.alpha : 0.0,
+    int32_t bad = pnpula_check_stepsizes(L, (f.rho > 0 ? 1.0 / f.rho : 0.0) + L_h2, use_cnn ? f.alpha : 0.0,
                                          use_cnn ? f.eps : 1.0, f.lipschitz_LD, lam, f.gamma);
     if (bad) set_error("warning: eq:stepsize_cond violated (mask %d) -- continuing", bad);
   }
@@ -672,6 +717,10 @@ pnpula_status pnpula_create(const pnpula_config *cfg, pnpula_ctx **out) {
     CUB(cudaMalloc(&td.mean, n * sizeof(float)));
     CUB(cudaMalloc(&td.m2, n * sizeof(float)));
     if (c->rho > 0) CUB(cudaMalloc(&td.z, n * sizeof(float)));
+    if (poisson) {
+      CUB(cudaMalloc(&td.z1, n * sizeof(float)));
+      CUB(cudaMemsetAsync(td.z1, 0, n * sizeof(float), c->stream));
+    }
     if (c->op == PNPULA_OP_MASK) {
       CUB(cudaMalloc(&td.mask, n));
       CUB(cudaMemsetAsync(td.mask, 0, n, c->stream));
@@ -752,6 +801,7 @@ pnpula_status pnpula_reset(pnpula_ctx *c, int64_t burn_in, uint64_t seed) {
     CU(c, cudaMemcpyAsync(td.x[0], td.x0, n, cudaMemcpyDeviceToDevice, c->stream));
     CU(c, cudaMemcpyAsync(td.x[1], td.x0, n, cudaMemcpyDeviceToDevice, c->stream));
     if (td.z) CU(c, cudaMemsetAsync(td.z, 0, n, c->stream));
+    if (td.z1) CU(c, cudaMemsetAsync(td.z1, 0, n, c->stream));
     CU(c, cudaMemsetAsync(td.mean, 0, n, c->stream));
     CU(c, cudaMemsetAsync(td.m2, 0, n, c->stream));
   }
@@ -948,6 +998,16 @@ pnpula_status pnpula_get_state(pnpula_ctx *c, float *x, float *z, int64_t *t, in
   return s;
 }
 
+pnpula_status pnpula_get_z1(pnpula_ctx *c, float *z1, int32_t scope) {
+  pnpula_status s = check_ctx(c);
+  if (s) return s;
+  if (c->op != PNPULA_OP_POISSON) { set_error("z1 exists only for OP_POISSON"); return PNPULA_E_STATE; }
+  CU(c, cudaSetDevice(c->device));
+  std::vector<const float *> zs;
+  for (auto &td : c->tiles) zs.push_back(td.z1);
+  return gather_padded_interiors(c, zs, z1, scope == PNPULA_SCOPE_GLOBAL_ON_ROOT);
+}
+
 pnpula_status pnpula_get_padded_x(pnpula_ctx *c, int32_t li, float *out) {
   pnpula_status s = check_ctx(c);
   if (s) return s;
@@ -1012,7 +1072,7 @@ pnpula_status pnpula_destroy(pnpula_ctx *c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (auto &td : c->tiles) {
     cudaFree(td.x[0]); cudaFree(td.x[1]); cudaFree(td.x0); cudaFree(td.y); cudaFree(td.mask);
-    cudaFree(td.z); cudaFree(td.mean); cudaFree(td.m2); cudaFree(td.G);
+    cudaFree(td.z); cudaFree(td.z1); cudaFree(td.mean); cudaFree(td.m2); cudaFree(td.G);
     cudaFree(td.act[0]); cudaFree(td.act[1]);
   }
   for (auto p : c->d_w) cudaFree(p);

@@ -236,7 +236,7 @@ update_conv_kernel(const __grid_constant__ UpdateParams p) {
       if (gi >= 0 && gi < p.ny && gj >= 0 && gj < p.nx) {
         const int pr = gi - (g.i0 - g.h), pc = gj - (g.j0 - g.hx);
         const float yv = (pr >= 0 && pr < g.ph && pc >= 0 && pc < g.pitch) ? p.y[(int64_t)pr * g.pitch + pc] : 0.f;
-        r = s - yv;
+        r = p.eta * s - yv;
       }
       Rr[e] = r;
     }
@@ -267,7 +267,7 @@ update_conv_kernel(const __grid_constant__ UpdateParams p) {
         }
         const int pr = gi - (g.i0 - g.h), pc = gj - (g.j0 - g.hx);
         const float yv = (pr >= 0 && pr < g.ph && pc >= 0 && pc < g.pitch) ? p.y[(int64_t)pr * g.pitch + pc] : 0.f;
-        r = s - yv;
+        r = p.eta * s - yv;
       }
       Rr[e] = r;
     }
@@ -461,7 +461,7 @@ update_sep_kernel(const __grid_constant__ UpdateParams p, const __grid_constant_
         }
         const bool rin = gi >= 0 && gi < p.ny;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) o[j] = (rin && gj + j >= 0 && gj + j < p.nx) ? o[j] - yv[j] : 0.f;
+        for (int j = 0; j < 4; ++j) o[j] = (rin && gj + j >= 0 && gj + j < p.nx) ? p.eta * o[j] - yv[j] : 0.f;
         *reinterpret_cast<float4 *>(Rs + a * RC + 4 * k4) = make_float4(o[0], o[1], o[2], o[3]);
       }
     }
@@ -509,6 +509,42 @@ update_sep_kernel(const __grid_constant__ UpdateParams p, const __grid_constant_
       }
     }
     __syncthreads();   // buffer buf is restaged by the next iteration's prefetch
+  }
+}
+
+// ---------------------------------------------------------------- Poisson z1 block
+// One thread per column quad of tile (+) r_H (quads aligned to global column multiples of 4,
+// so the Philox call is shared exactly as in the x-update), 2-D stencil of x+ read through L1.
+// Pixels outside tile (+) r_H or the image are skipped (z1 stays 0 outside the image).
+__global__ void __launch_bounds__(NTHREADS) z1_update_kernel(const __grid_constant__ Z1Params p) {
+  const TileGeom &g = p.g;
+  const int ry = p.ry, rx = p.rx, kw = 2 * rx + 1;
+  const int r0 = max(g.i0 - ry, 0), r1 = min(g.i0 + g.th + ry, p.ny);
+  const int c0 = max(g.j0 - rx, 0), c1 = min(g.j0 + g.tw + rx, p.nx);
+  const int q0 = c0 >> 2, nq = ((c1 + 3) >> 2) - q0;
+  const int64_t total = (int64_t)nq * (r1 - r0);
+  for (int64_t e = (int64_t)blockIdx.x * NTHREADS + threadIdx.x; e < total; e += (int64_t)gridDim.x * NTHREADS) {
+    const int gi = r0 + (int)(e / nq);
+    const int gj4 = 4 * (q0 + (int)(e % nq));
+    float ze[4];
+    normals4(p.seed_lo, p.seed_hi, (uint32_t)gj4 >> 2, (uint32_t)gi, p.t1, 2u, ze);
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+      const int gj = gj4 + l;
+      if (gj < c0 || gj >= c1) continue;
+      float s = 0.f;   // (H x+)[gi][gj] = sum_{a,b} k[a][b] x+[gi - (a - ry)][gj - (b - rx)]
+      for (int a = 0; a < 2 * ry + 1; ++a) {
+        const float *xr = p.x + pidx(g, gi - (a - ry), gj + rx);
+        const float *kr = p.k2d + a * kw;
+        for (int b = 0; b < kw; ++b) s = fmaf(kr[b], __ldg(xr - b), s);
+      }
+      const int64_t n = pidx(g, gi, gj);
+      const float z = p.z1[n];
+      const float v = z - p.b1 * (z - p.eta * s) + p.s1 * ze[l];
+      // prox of kappa1 KL(y || .): the non-negative root of u^2 - (v - kappa1) u - kappa1 y = 0 (R31)
+      const float a = v - p.kappa1;
+      p.z1[n] = 0.5f * (a + sqrtf(fmaf(a, a, 4.0f * p.kappa1 * __ldg(p.y + n))));
+    }
   }
 }
 
@@ -648,6 +684,19 @@ cudaError_t launch_update(const UpdateParams &p, cudaStream_t s) {
   if (p.ry == 2 && p.rx == 2) return launch_conv<2, 2, false>(p, s);
   if (p.ry == 4 && p.rx == 4) return launch_conv<4, 4, false>(p, s);
   return launch_conv<-1, -1, false>(p, s);
+}
+
+cudaError_t launch_z1_update(const Z1Params &p, cudaStream_t s) {
+  const int r0 = p.g.i0 - p.ry < 0 ? 0 : p.g.i0 - p.ry;
+  const int r1 = p.g.i0 + p.g.th + p.ry > p.ny ? p.ny : p.g.i0 + p.g.th + p.ry;
+  const int c0 = p.g.j0 - p.rx < 0 ? 0 : p.g.j0 - p.rx;
+  const int c1 = p.g.j0 + p.g.tw + p.rx > p.nx ? p.nx : p.g.j0 + p.g.tw + p.rx;
+  const int64_t total = (int64_t)(((c1 + 3) >> 2) - (c0 >> 2)) * (r1 - r0);
+  int64_t blocks = (total + NTHREADS - 1) / NTHREADS;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks < 1) blocks = 1;
+  z1_update_kernel<<<(unsigned)blocks, NTHREADS, 0, s>>>(p);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_copy_jobs(const CopyJob *d_jobs, int njobs, int max_elems, cudaStream_t s) {

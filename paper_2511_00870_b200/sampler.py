@@ -26,7 +26,8 @@ class Sampler:
                  rho: float = 0.0, kappa: float = 0.0, z_lo: float = -np.inf, z_hi: float = np.inf,
                  x0: Optional[np.ndarray] = None, in_rect=None, tiles=(1, 1),
                  rank: int = 0, world_size: int = 1, device: int = 0, nccl_uid: Optional[bytes] = None,
-                 stream: int = 0, flags: int = 0, lipschitz_L: float = 0.0, lipschitz_LD: float = 0.0):
+                 stream: int = 0, flags: int = 0, lipschitz_L: float = 0.0, lipschitz_LD: float = 0.0,
+                 eta: float = 0.0, rho1: float = 0.0, kappa1: float = 0.0):
         lib = L.load()
         keep = []
         cfg = L.Config()
@@ -38,8 +39,8 @@ class Sampler:
             keep.append(ub)
             cfg.nccl_uid = C.addressof(ub)
         cfg.stream = stream
-        cfg.op = L.OP_CONV if op == "conv" else L.OP_MASK
-        if op == "conv":
+        cfg.op = {"conv": L.OP_CONV, "mask": L.OP_MASK, "poisson": L.OP_POISSON}[op]
+        if op in ("conv", "poisson"):
             if kernel_sep is not None:
                 ky, kx = _f32(kernel_sep[0]), _f32(kernel_sep[1])
                 keep += [ky, kx]
@@ -78,6 +79,7 @@ class Sampler:
         cfg.gamma = gamma
         cfg.lipschitz_L, cfg.lipschitz_LD = lipschitz_L, lipschitz_LD
         cfg.flags = flags
+        cfg.eta, cfg.rho1, cfg.kappa1 = eta, rho1, kappa1
         h = C.c_void_p()
         L.check(lib.pnpula_create(C.byref(cfg), C.byref(h)))
         self.warning = L.last_error()
@@ -85,6 +87,7 @@ class Sampler:
         self._lib = lib
         self.ny, self.nx = ny, nx
         self.has_z = rho > 0
+        self.op = op
         bb = L.Rect()
         L.check(lib.pnpula_local_bbox(h, C.byref(bb)))
         self.bbox = bb.tup()
@@ -126,6 +129,13 @@ class Sampler:
         t = C.c_int64()
         L.check(self._lib.pnpula_get_state(self._h, L._ptr(x), L._ptr(z), C.byref(t), scope))
         return x, z, t.value
+
+    def z1(self, scope: int = L.SCOPE_LOCAL):
+        """OP_POISSON: the AXDA block z1 (~ eta H x)."""
+        shp = self._out_shape(scope)
+        out = np.zeros(shp, np.float32) if shp else None
+        L.check(self._lib.pnpula_get_z1(self._h, L._ptr(out), scope))
+        return out
 
     def tile_info(self, i: int):
         r = L.Rect()

@@ -8,8 +8,9 @@ the library).  It only draws inputs shaped like the paper's workloads
   ("cropped ... normalized into C = [0,1]^N", P:692-693);
 * blur kernels: normalised Gaussian (separable factors) and random asymmetric
   normalised kernels (parity cases; asymmetry exposes flip bugs);
-* observations: y = conv(xbar, K) + sigma w or y = m (xbar + sigma w)
-  with m ~ Bernoulli(0.3).  The data-generation convolution uses
+* observations: y = conv(xbar, K) + sigma w, y = m (xbar + sigma w)
+  with m ~ Bernoulli(0.3), or counts y ~ Poisson(eta conv(xbar, K))
+  (P:731-735).  The data-generation convolution uses
   scipy.signal.fftconvolve (a library routine independent of both the oracle
   and the CUDA path);
 * random-init DnCNN-style weights, each layer rescaled to
@@ -167,6 +168,23 @@ def observe_blur(ny, nx, k2d, sigma2, rect=None) -> np.ndarray:
     if j0 + w > nx:
         y[:, nx - j0:] = 0
     return y.astype(np.float32)
+
+
+def observe_poisson(ny, nx, k2d, eta=250.0, rect=None) -> np.ndarray:
+    """Counts y ~ Poisson(eta conv(xbar, K)) (eq:likelihood:poisson_deconvolution, P:731-735;
+    eta = 250 in the paper), drawn per aligned 256x256 block from (seed, block) so any rectangle
+    reproduces the global image's values; zero outside the image."""
+    rect = rect if rect is not None else (0, 0, ny, nx)
+    lam = eta * np.clip(blurred_truth(ny, nx, k2d, rect), 0.0, None)
+    u = _block_field(ny, nx, rect, NOISE_SEED, 3, lambda rng, shp: rng.random(shp))
+    # inverse-CDF Poisson draw from the block uniforms (scipy's ppf: deterministic given u)
+    from scipy.stats import poisson
+    y = poisson.ppf(u, lam)
+    i0, j0, h, w = rect
+    ii = np.arange(i0, i0 + h)[:, None]
+    jj = np.arange(j0, j0 + w)[None, :]
+    inside = (ii >= 0) & (ii < ny) & (jj >= 0) & (jj < nx)
+    return np.where(inside, y, 0.0).astype(np.float32)
 
 
 def observe_mask(ny, nx, sigma2, p=0.3, rect=None):

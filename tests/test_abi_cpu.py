@@ -18,7 +18,7 @@ build.build()
 def _header_functions():
     src = open(os.path.join(ROOT, "include", "pnpula.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(pnpula_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(pnpula_[a-z0-9_]+)\s*\(", src)))
 
 
 def test_exports_every_declared_symbol():
