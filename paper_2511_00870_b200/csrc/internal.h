@@ -58,6 +58,8 @@ struct Z1Params {
   int ny, nx;
   int ry, rx;
   float k2d[kMaxTaps * kMaxTaps];   // 2-D taps (separable factors multiplied out on the host)
+  int separable;                    // ky / kx valid: separable fast path (R = 2, 4)
+  float ky[kMaxTaps], kx[kMaxTaps];
   float eta, b1, s1, kappa1;        // eta, kappa1/rho1, sqrt(2 kappa1), kappa1
   uint32_t seed_lo, seed_hi, t1;
 };

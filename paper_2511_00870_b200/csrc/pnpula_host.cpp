@@ -365,6 +365,11 @@ pnpula_status step(pnpula_ctx *c) {
       for (int a = 0; a < kh; ++a)
         for (int b = 0; b < kw; ++b)
           q.k2d[a * kw + b] = c->separable ? c->ky[a] * c->kx[b] : c->k2d[a * kw + b];
+      q.separable = c->separable;
+      if (c->separable) {
+        for (int a = 0; a < kh; ++a) q.ky[a] = c->ky[a];
+        for (int b = 0; b < kw; ++b) q.kx[b] = c->kx[b];
+      }
       q.eta = (float)c->eta;
       q.b1 = (float)(c->kappa1 / c->rho1);
       q.s1 = (float)std::sqrt(2.0 * c->kappa1);

@@ -548,6 +548,75 @@ __global__ void __launch_bounds__(NTHREADS) z1_update_kernel(const __grid_consta
   }
 }
 
+// Separable fast path of the z1 block: a CTA owns a 32 x 64 block of tile (+) r_H (columns
+// quad-aligned), stages x+ on block (+) R with one 2-D TMA tile load (zero fill outside the
+// padded buffer), runs the horizontal then the vertical pass of H = ky (x) kx in shared memory,
+// and updates 2 rows x 1 quad per thread (one Philox call per quad, stream 2).
+template <int R>
+__global__ void __launch_bounds__(NTHREADS) z1_sep_kernel(const __grid_constant__ Z1Params p,
+                                                        const __grid_constant__ CUtensorMap tmx, int r0, int q0,
+                                                        int nbx) {
+  constexpr int XR = TY + 2 * R, XC = TX + 2 * R;
+  static_assert((XC * 4) % 16 == 0, "TMA row bytes");
+  __shared__ __align__(128) float X[XR * XC];
+  __shared__ __align__(16) float T[XR * TX];
+  __shared__ __align__(8) uint64_t bar;
+  const float *kys = p.ky, *kxs = p.kx;   // parameter space
+  const TileGeom &g = p.g;
+  const int tid = threadIdx.x;
+  const int bi0 = r0 + (int)(blockIdx.x / nbx) * TY;
+  const int bj0 = 4 * q0 + (int)(blockIdx.x % nbx) * TX;
+  const uint32_t b = (uint32_t)__cvta_generic_to_shared(&bar);
+  if (tid == 0) {
+    mbar_init1(b);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(b),
+                 "r"((uint32_t)(XR * XC * 4))
+                 : "memory");
+    tma_load_2d((uint32_t)__cvta_generic_to_shared(X), &tmx, bj0 - R - (g.j0 - g.hx), bi0 - R - (g.i0 - g.h), b);
+  }
+  __syncthreads();
+  mbar_wait_parity(b, 0);
+  // horizontal: T[a][c] = sum_q kx[q+R] X[a][c + R - q]   (x+ column bj0 + c - q)
+  for (int e = tid; e < XR * (TX / 4); e += NTHREADS) {
+    const int a = e / (TX / 4), c4 = 4 * (e - a * (TX / 4));
+    float o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float s = 0.f;
+#pragma unroll
+      for (int q = -R; q <= R; ++q) s = fmaf(kxs[q + R], X[a * XC + c4 + j + R - q], s);
+      o[j] = s;
+    }
+    *reinterpret_cast<float4 *>(T + a * TX + 4 * (e - a * (TX / 4))) = make_float4(o[0], o[1], o[2], o[3]);
+  }
+  __syncthreads();
+  const int q = tid & 15, a2 = tid >> 4;
+  const int gj4 = bj0 + 4 * q;
+  const int rlo = g.i0 - p.ry < 0 ? 0 : g.i0 - p.ry, rhi = g.i0 + g.th + p.ry > p.ny ? p.ny : g.i0 + g.th + p.ry;
+  const int clo = g.j0 - p.rx < 0 ? 0 : g.j0 - p.rx, chi = g.j0 + g.tw + p.rx > p.nx ? p.nx : g.j0 + g.tw + p.rx;
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const int a = 2 * a2 + r, gi = bi0 + a;
+    if (gi < rlo || gi >= rhi || gj4 >= chi || gj4 + 4 <= clo) continue;
+    float ze[4];
+    normals4(p.seed_lo, p.seed_hi, (uint32_t)gj4 >> 2, (uint32_t)gi, p.t1, 2u, ze);
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+      const int gj = gj4 + l;
+      if (gj < clo || gj >= chi) continue;
+      float s = 0.f;   // vertical: sum_p ky[p+R] T[a + R - p][c]
+#pragma unroll
+      for (int pp = -R; pp <= R; ++pp) s = fmaf(kys[pp + R], T[(a + R - pp) * TX + 4 * q + l], s);
+      const int64_t n = pidx(g, gi, gj);
+      const float z = p.z1[n];
+      const float v = z - p.b1 * (z - p.eta * s) + p.s1 * ze[l];
+      const float av = v - p.kappa1;
+      p.z1[n] = 0.5f * (av + sqrtf(fmaf(av, av, 4.0f * p.kappa1 * __ldg(p.y + n))));
+    }
+  }
+}
+
 // ---------------------------------------------------------------- mask K7 (no stencil)
 __global__ void __launch_bounds__(NTHREADS) update_mask_kernel(const __grid_constant__ UpdateParams p) {
   const TileGeom &g = p.g;
@@ -691,6 +760,15 @@ cudaError_t launch_z1_update(const Z1Params &p, cudaStream_t s) {
   const int r1 = p.g.i0 + p.g.th + p.ry > p.ny ? p.ny : p.g.i0 + p.g.th + p.ry;
   const int c0 = p.g.j0 - p.rx < 0 ? 0 : p.g.j0 - p.rx;
   const int c1 = p.g.j0 + p.g.tw + p.rx > p.nx ? p.nx : p.g.j0 + p.g.tw + p.rx;
+  if (p.separable && p.ry == p.rx && (p.ry == 4 || p.ry == 2)) {
+    const int R = p.ry, q0 = c0 >> 2;
+    const int nbx = (((c1 + 3) >> 2) - q0 + 15) / 16, nby = (r1 - r0 + TY - 1) / TY;
+    CUtensorMap tmx;
+    if (!encode_padded_2d(&tmx, p.x, p.g, TX + 2 * R, TY + 2 * R)) return cudaErrorInvalidValue;
+    if (R == 4) z1_sep_kernel<4><<<nbx * nby, NTHREADS, 0, s>>>(p, tmx, r0, q0, nbx);
+    else z1_sep_kernel<2><<<nbx * nby, NTHREADS, 0, s>>>(p, tmx, r0, q0, nbx);
+    return cudaGetLastError();
+  }
   const int64_t total = (int64_t)(((c1 + 3) >> 2) - (c0 >> 2)) * (r1 - r0);
   int64_t blocks = (total + NTHREADS - 1) / NTHREADS;
   if (blocks > 148 * 16) blocks = 148 * 16;

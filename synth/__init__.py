@@ -172,19 +172,25 @@ def observe_blur(ny, nx, k2d, sigma2, rect=None) -> np.ndarray:
 
 def observe_poisson(ny, nx, k2d, eta=250.0, rect=None) -> np.ndarray:
     """Counts y ~ Poisson(eta conv(xbar, K)) (eq:likelihood:poisson_deconvolution, P:731-735;
-    eta = 250 in the paper), drawn per aligned 256x256 block from (seed, block) so any rectangle
-    reproduces the global image's values; zero outside the image."""
-    rect = rect if rect is not None else (0, 0, ny, nx)
-    lam = eta * np.clip(blurred_truth(ny, nx, k2d, rect), 0.0, None)
-    u = _block_field(ny, nx, rect, NOISE_SEED, 3, lambda rng, shp: rng.random(shp))
-    # inverse-CDF Poisson draw from the block uniforms (scipy's ppf: deterministic given u)
-    from scipy.stats import poisson
-    y = poisson.ppf(u, lam)
-    i0, j0, h, w = rect
-    ii = np.arange(i0, i0 + h)[:, None]
-    jj = np.arange(j0, j0 + w)[None, :]
-    inside = (ii >= 0) & (ii < ny) & (jj >= 0) & (jj < nx)
-    return np.where(inside, y, 0.0).astype(np.float32)
+    eta = 250 in the paper).  Drawn per aligned 256x256 block with a generator seeded by
+    (seed, block) from that whole block's intensities (computed on the block alone), so any
+    rectangle reproduces the global image's values exactly; zero outside the image."""
+    i0, j0, h, w = rect if rect is not None else (0, 0, ny, nx)
+    out = np.zeros((h, w), dtype=np.float64)
+    bi0, bi1 = max(i0, 0) // BLOCK, (min(i0 + h, ny) - 1) // BLOCK
+    bj0, bj1 = max(j0, 0) // BLOCK, (min(j0 + w, nx) - 1) // BLOCK
+    for bi in range(bi0, bi1 + 1):
+        for bj in range(bj0, bj1 + 1):
+            gi0, gj0 = bi * BLOCK, bj * BLOCK
+            bh, bw = min(BLOCK, ny - gi0), min(BLOCK, nx - gj0)
+            lam = eta * np.clip(blurred_truth(ny, nx, k2d, (gi0, gj0, bh, bw)), 0.0, None)
+            rng = np.random.default_rng(np.random.SeedSequence([NOISE_SEED, 3, bi, bj]))
+            blk = rng.poisson(lam).astype(np.float64)
+            a0, a1 = max(gi0, i0), min(gi0 + bh, i0 + h)
+            b0, b1 = max(gj0, j0), min(gj0 + bw, j0 + w)
+            if a0 < a1 and b0 < b1:
+                out[a0 - i0:a1 - i0, b0 - j0:b1 - j0] = blk[a0 - gi0:a1 - gi0, b0 - gj0:b1 - gj0]
+    return out.astype(np.float32)
 
 
 def observe_mask(ny, nx, sigma2, p=0.3, rect=None):
