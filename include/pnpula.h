@@ -75,7 +75,7 @@ enum { PNPULA_SCOPE_LOCAL = 0, PNPULA_SCOPE_GLOBAL_ON_ROOT = 1 };
 /* flags */
 #define PNPULA_FLAG_HALO_VIA_NCCL 0x1  /* route same-rank halos through NCCL self send/recv (tests) */
 #define PNPULA_FLAG_CNN_LAYERWISE 0x2  /* one CNN layer per launch instead of fused layer chains */
-#define PNPULA_FLAG_NO_GRAPH      0x4  /* launch kernels directly instead of replaying a CUDA graph */
+#define PNPULA_FLAG_NO_GRAPH      0x4  /* reserved (kernels are always launched directly) */
 
 typedef struct {
   int32_t i0, j0, h, w; /* rectangle of global pixel coordinates: rows [i0, i0+h), cols [j0, j0+w) */

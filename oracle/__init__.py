@@ -55,6 +55,7 @@ class _Config(C.Structure):
         ("tiles_y", C.c_int32), ("tiles_x", C.c_int32),
         ("i_off", C.c_int64), ("j_off", C.c_int64),
         ("eta", C.c_double), ("rho1", C.c_double), ("kappa1", C.c_double),
+        ("tv_beta", C.c_double),
     ]
 
 
@@ -82,6 +83,9 @@ def _load():
         _lib.or_run_ex.restype = C.c_int
         _lib.or_prox_kl.argtypes = [d, d, d]
         _lib.or_prox_kl.restype = d
+        _lib.or_grad2d.argtypes = [vp, i32, i32, vp, vp]
+        _lib.or_grad2d_adj.argtypes = [vp, vp, i32, i32, vp]
+        _lib.or_prox_l21.argtypes = [d, d, d, C.POINTER(d), C.POINTER(d)]
     return _lib
 
 
@@ -157,6 +161,27 @@ def check_stepsizes(L, h2_over_rho, alpha, eps, L_D, lam, gamma) -> int:
     return int(_load().or_check_stepsizes(L, h2_over_rho, alpha, eps, L_D, lam, gamma))
 
 
+def grad2d(x):
+    """D x = (vertical, horizontal) forward differences, zero at the last row / column (R35)."""
+    x = _f64(x)
+    gv, gh = np.zeros_like(x), np.zeros_like(x)
+    _load().or_grad2d(x.ctypes.data, x.shape[0], x.shape[1], gv.ctypes.data, gh.ctypes.data)
+    return gv, gh
+
+
+def grad2d_adj(gv, gh):
+    gv, gh = _f64(gv), _f64(gh)
+    out = np.zeros_like(gv)
+    _load().or_grad2d_adj(gv.ctypes.data, gh.ctypes.data, gv.shape[0], gv.shape[1], out.ctypes.data)
+    return out
+
+
+def prox_l21(gv: float, gh: float, tau: float):
+    a, b = C.c_double(), C.c_double()
+    _load().or_prox_l21(gv, gh, tau, C.byref(a), C.byref(b))
+    return a.value, b.value
+
+
 def prox_kl(v: float, y: float, kappa: float) -> float:
     """prox of kappa KL(y || .) (Poisson likelihood, closed form; reading R31)."""
     return float(_load().or_prox_kl(v, y, kappa))
@@ -190,6 +215,7 @@ class Problem:
     eta: float = 0.0                      # op "poisson": y ~ Poisson(eta H x), z1 ~ eta H x
     rho1: float = 0.0
     kappa1: float = 0.0
+    tv_beta: float = 0.0                  # > 0: TV prior, z ~ D x (z = vertical, z1 = horizontal)
     extra: dict = field(default_factory=dict)
 
 
@@ -238,6 +264,7 @@ def run(pb: Problem, n_iter: int, burn_in: int, seed: int, tiles=(1, 1), bf16_em
     cfg.tiles_y, cfg.tiles_x = tiles
     cfg.i_off, cfg.j_off = origin
     cfg.eta, cfg.rho1, cfg.kappa1 = pb.eta, pb.rho1, pb.kappa1
+    cfg.tv_beta = pb.tv_beta
     x = np.zeros((ny, nx)); z = np.zeros((ny, nx)); z1 = np.zeros((ny, nx))
     mean = np.zeros((ny, nx)); var = np.zeros((ny, nx))
     n = C.c_int64()

@@ -28,6 +28,11 @@
  *   or_check_stepsizes  eq:stepsize_cond P:581-587 (reading R11: ||H2||^2 -> ||H2||^2/rho)
  *   or_prox_kl          prox of kappa KL(y || .) for the Poisson likelihood (eq:poisson:f2 P:737-741;
  *                       closed form = the positive root of u^2 - (v - kappa) u - kappa y = 0, reading R31)
+ *   or_grad2d / adj     D = 2-D discrete gradient (item:prior_choice:tv P:786-806): forward
+ *                       differences, zero at the last row / column; D^T its exact transpose (R35)
+ *   or_prox_l21         prox of tau ||.||_{2,1}: per-pixel block soft threshold (R36)
+ *   or_run (tv_beta>0)  TV prior with Gaussian noise: x by PSGLA with p = 1_{R+},
+ *                       z ~ D x with f2 = beta ||.||_{2,1} (rho, kappa) (readings R35-R38)
  *   or_run (op = 2)     Poisson deconvolution (sec:poisson_deconvolution P:727-744):
  *                       f1 = 0, z = (z1, z2), z1 ~ eta H x with f2,1 = KL(y || .) (rho1, kappa1),
  *                       z2 ~ x with f2,2 = indicator of [z_lo, z_hi] (rho, kappa); Algorithm 1 lines
@@ -242,6 +247,42 @@ double or_prox_kl(double v, double y, double kappa) {
 }
 
 /* ------------------------------------------------------------------ */
+/* 2-D discrete gradient D, reading R35:
+ *   (Dx)_v[i,j] = x[i+1,j] - x[i,j] for i < ny-1, 0 on the last row;
+ *   (Dx)_h[i,j] = x[i,j+1] - x[i,j] for j < nx-1, 0 on the last column.                       */
+void or_grad2d(const double *x, int32_t ny, int32_t nx, double *gv, double *gh) {
+  for (int64_t i = 0; i < ny; i++)
+    for (int64_t j = 0; j < nx; j++) {
+      int64_t n = i * nx + j;
+      gv[n] = (i < ny - 1) ? x[n + nx] - x[n] : 0.0;
+      gh[n] = (j < nx - 1) ? x[n + 1] - x[n] : 0.0;
+    }
+}
+
+/* D^T: (D^T g)[i,j] = g_v[i-1,j] [i >= 1] - g_v[i,j] [i < ny-1] + g_h[i,j-1] [j >= 1] - g_h[i,j] [j < nx-1]. */
+void or_grad2d_adj(const double *gv, const double *gh, int32_t ny, int32_t nx, double *out) {
+  for (int64_t i = 0; i < ny; i++)
+    for (int64_t j = 0; j < nx; j++) {
+      int64_t n = i * nx + j;
+      double s = 0.0;
+      if (i >= 1) s += gv[n - nx];
+      if (i < ny - 1) s -= gv[n];
+      if (j >= 1) s += gh[n - 1];
+      if (j < nx - 1) s -= gh[n];
+      out[n] = s;
+    }
+}
+
+/* prox of tau ||.||_{2,1} on one pixel's 2-vector, reading R36:
+ * g -> g max(0, 1 - tau / ||g||_2), 0 -> 0. */
+void or_prox_l21(double gv, double gh, double tau, double *ov, double *oh) {
+  double nrm = sqrt(gv * gv + gh * gh);
+  double sc = (nrm > tau) ? 1.0 - tau / nrm : 0.0;
+  *ov = gv * sc;
+  *oh = gh * sc;
+}
+
+/* ------------------------------------------------------------------ */
 typedef struct {
   int32_t ny, nx;
   int32_t op;                    /* 0 = convolution H1, 1 = mask H1 = diag(m),
@@ -268,6 +309,9 @@ typedef struct {
                                     the noise is indexed by global pixel (reading R9), so a crop
                                     of a larger image draws the same xi/zeta at the same pixel */
   double eta, rho1, kappa1;      /* op = 2: Poisson scale and the z1 block's coupling / step */
+  double tv_beta;                /* > 0: TV prior: the z block is z ~ D x (two
+                                    components) with f2 = tv_beta ||.||_{2,1} and x moves by PSGLA
+                                    with p = 1_{R+}; requires rho > 0, no CNN, no box term */
 } or_config;
 
 static void or_kernel2d(const or_config *c, double *k) {
@@ -310,6 +354,39 @@ static int or_step_global(const or_config *c, const double *k, const double *yd,
     if (e) return e;
   }
   double sq2g = sqrt(2.0 * c->gamma);
+  if (c->tv_beta > 0.0) {
+    /* TV prior: x^{t+1} = proj_{R+}( x - gamma grad f1(H1 x) - (gamma/rho) D^T (D x - z)
+     * + sqrt(2 gamma) xi )  (PSGLA with p = 1_{R+});  z = (z_v, z_h) = (z, z1) arrays here.      */
+    double *dv = (double *)malloc(sizeof(double) * (size_t)npx);
+    double *dh = (double *)malloc(sizeof(double) * (size_t)npx);
+    double *dt = (double *)malloc(sizeof(double) * (size_t)npx);
+    if (!dv || !dh || !dt) { free(dv); free(dh); free(dt); return OR_E_INVALID; }
+    or_grad2d(x, ny, nx, dv, dh);
+    for (int64_t n = 0; n < npx; n++) { dv[n] -= z[n]; dh[n] -= z1[n]; }
+    or_grad2d_adj(dv, dh, ny, nx, dt);
+    for (int64_t i = 0; i < ny; i++)
+      for (int64_t j = 0; j < nx; j++) {
+        int64_t n = i * nx + j;
+        double v = x[n] - c->gamma * g[n] - (c->gamma / c->rho) * dt[n] +
+                   sq2g * or_normal(c->seed, (uint32_t)(t + 1), i + c->i_off, j + c->j_off, 0);
+        xn[n] = v < 0.0 ? 0.0 : v;
+      }
+    /* lines 11-13: z^{t+1} = prox_{kappa beta ||.||_{2,1}}( z - (kappa/rho)(z - D x^{t+1}) + sqrt(2 kappa) zeta ),
+     * zeta_v = stream 1, zeta_h = stream 3 (reading R37) */
+    or_grad2d(xn, ny, nx, dv, dh);
+    double sq2k = sqrt(2.0 * c->kappa);
+    for (int64_t i = 0; i < ny; i++)
+      for (int64_t j = 0; j < nx; j++) {
+        int64_t n = i * nx + j;
+        double vv = z[n] - (c->kappa / c->rho) * (z[n] - dv[n]) +
+                    sq2k * or_normal(c->seed, (uint32_t)(t + 1), i + c->i_off, j + c->j_off, 1);
+        double vh = z1[n] - (c->kappa / c->rho) * (z1[n] - dh[n]) +
+                    sq2k * or_normal(c->seed, (uint32_t)(t + 1), i + c->i_off, j + c->j_off, 3);
+        or_prox_l21(vv, vh, c->kappa * c->tv_beta, &zn[n], &z1n[n]);
+      }
+    free(dv); free(dh); free(dt);
+    return OR_OK;
+  }
   for (int64_t i = 0; i < ny; i++)
     for (int64_t j = 0; j < nx; j++) {
       int64_t n = i * nx + j;
@@ -361,6 +438,7 @@ static int or_step_tiled(const or_config *c, const double *k, const double *yd, 
   int use_cnn = c->n_layers > 0 && c->alpha != 0.0;
   int hr = (c->op != 1) ? 2 * (ry > rx ? ry : rx) : 0;
   int h = use_cnn && c->n_layers > hr ? c->n_layers : hr;
+  if (c->tv_beta > 0.0 && h < 2) h = 2;   /* D^T D x needs x at distance 1; z on tile (+) 1 needs 2 */
   for (int ty = 0; ty < c->tiles_y; ty++)
     for (int tx = 0; tx < c->tiles_x; tx++) {
       int64_t i0, i1, j0, j1;
@@ -468,6 +546,24 @@ static int or_step_tiled(const or_config *c, const double *k, const double *yd, 
         free(B);
       }
       double sq2g = sqrt(2.0 * c->gamma);
+      if (c->tv_beta > 0.0) {
+        /* TV: worker b evaluates D^T (D x - z) on its tile from S_b x and the ring of z (R38) */
+        for (int a = 0; a < th; a++)
+          for (int b = 0; b < tw; b++) {
+            int64_t gi = i0 + a, gj = j0 + b, n = gi * nx + gj;
+            const double *xc = xp + (int64_t)(a + h) * pw + (b + h);
+            double s = 0.0;
+            if (gi >= 1) s += (xc[0] - xc[-pw]) - z[n - nx];          /* g_v[i-1,j] */
+            if (gi < ny - 1) s -= (xc[pw] - xc[0]) - z[n];            /* g_v[i,j]   */
+            if (gj >= 1) s += (xc[0] - xc[-1]) - z1[n - 1];           /* g_h[i,j-1] */
+            if (gj < nx - 1) s -= (xc[1] - xc[0]) - z1[n];            /* g_h[i,j]   */
+            double v = xc[0] - c->gamma * gl[(int64_t)a * tw + b] - (c->gamma / c->rho) * s +
+                       sq2g * or_normal(c->seed, (uint32_t)(t + 1), gi + c->i_off, gj + c->j_off, 0);
+            xn[n] = v < 0.0 ? 0.0 : v;
+          }
+        free(xp); free(rp); free(gl); free(Gl);
+        continue;
+      }
       for (int a = 0; a < th; a++)
         for (int b = 0; b < tw; b++) {
           int64_t gi = i0 + a, gj = j0 + b, n = gi * nx + gj;
@@ -492,6 +588,27 @@ static int or_step_tiled(const or_config *c, const double *k, const double *yd, 
       free(gl);
       free(Gl);
     }
+  if (c->tv_beta > 0.0) {
+    /* line 11: S_{2,b} x^{t+1} (ghost width 1); lines 12-13 for the worker's block of z = D x */
+    double sq2k = sqrt(2.0 * c->kappa);
+    for (int ty = 0; ty < c->tiles_y; ty++)
+      for (int tx = 0; tx < c->tiles_x; tx++) {
+        int64_t i0, i1, j0, j1;
+        or_partition(ny, c->tiles_y, ty, &i0, &i1);
+        or_partition(nx, c->tiles_x, tx, &j0, &j1);
+        for (int64_t gi = i0; gi < i1; gi++)
+          for (int64_t gj = j0; gj < j1; gj++) {
+            int64_t n = gi * nx + gj;
+            double dv = (gi < ny - 1) ? xn[n + nx] - xn[n] : 0.0;
+            double dh = (gj < nx - 1) ? xn[n + 1] - xn[n] : 0.0;
+            double vv = z[n] - (c->kappa / c->rho) * (z[n] - dv) +
+                        sq2k * or_normal(c->seed, (uint32_t)(t + 1), gi + c->i_off, gj + c->j_off, 1);
+            double vh = z1[n] - (c->kappa / c->rho) * (z1[n] - dh) +
+                        sq2k * or_normal(c->seed, (uint32_t)(t + 1), gi + c->i_off, gj + c->j_off, 3);
+            or_prox_l21(vv, vh, c->kappa * c->tv_beta, &zn[n], &z1n[n]);
+          }
+      }
+  }
   if (c->op == 2) {
     /* line 11: every worker retrieves S_{2,b} x^{t+1} (its tile plus a ghost frame of width
      * r_H) once all blocks of x^{t+1} exist; lines 12-13 for its block of z1 */
@@ -528,7 +645,7 @@ static int or_step_tiled(const or_config *c, const double *k, const double *yd, 
 }
 
 /* Full chain.  Outputs (each ny*nx, any may be NULL): final x, final z (z2 block for
- * op = 2), final z1 (op = 2), MMSE mean and variance (M2/(n-1), reading R15) of x^{(t)},
+ * op = 2; vertical component of z ~ D x for TV), final z1 (op = 2; horizontal TV component), MMSE mean and variance (M2/(n-1), reading R15) of x^{(t)},
  * t = burn_in+1..n_iter (reading R14), accumulated with Welford's update (P:839 footnote). */
 int or_run_ex(const or_config *c, double *x_out, double *z_out, double *z1_out, double *mean_out,
               double *var_out, int64_t *n_samples) {
@@ -538,6 +655,8 @@ int or_run_ex(const or_config *c, double *x_out, double *z_out, double *z1_out, 
   if (c->rho > 0.0 && !(c->kappa > 0.0 && c->kappa < c->rho)) return OR_E_INVALID;
   if (c->op == 2 && !(c->eta > 0.0 && c->rho1 > 0.0 && c->kappa1 > 0.0 && c->kappa1 < c->rho1))
     return OR_E_INVALID;
+  if (c->tv_beta > 0.0 && (c->op == 2 || !(c->rho > 0.0) || (c->n_layers > 0 && c->alpha != 0.0) || c->lambda > 0.0))
+    return OR_E_INVALID;   /* TV: Gaussian likelihood, z block on, no CNN, no box term */
   int64_t npx = (int64_t)c->ny * c->nx;
   double *k = (double *)calloc((size_t)(c->kh > 0 ? c->kh * c->kw : 1), sizeof(double));
   double *yd = (double *)malloc(sizeof(double) * (size_t)npx);
@@ -579,7 +698,7 @@ int or_run_ex(const or_config *c, double *x_out, double *z_out, double *z1_out, 
     }
     double *tt = x; x = xn; xn = tt;
     if (c->rho > 0.0) { tt = z; z = zn; zn = tt; }
-    if (c->op == 2) { tt = z1; z1 = z1n; z1n = tt; }
+    if (c->op == 2 || c->tv_beta > 0.0) { tt = z1; z1 = z1n; z1n = tt; }
   }
   if (x_out) memcpy(x_out, x, sizeof(double) * (size_t)npx);
   if (z_out) memcpy(z_out, z, sizeof(double) * (size_t)npx);
