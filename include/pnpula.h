@@ -137,6 +137,14 @@ typedef struct {
    * box terms + sqrt(2 gamma) xi;  z2+ as for OP_CONV;  z1+ = prox_{kappa1 KL(y||.)}(z1 -
    * (kappa1/rho1)(z1 - eta H x+) + sqrt(2 kappa1) zeta1), zeta1 = Philox stream 2. */
   double eta, rho1, kappa1;
+
+  /* TV prior instead of the denoiser (item:prior_choice:tv P:786-809; R35-R38):
+   * tv_beta > 0 turns the z block into z = (z_v, z_h) ~ D x (2-D forward differences) with
+   * f2 = tv_beta ||.||_{2,1} (coupling rho, step kappa), and x moves by PSGLA with p = 1_{R+}:
+   * x+ = max(x - gamma grad f1 - (gamma/rho) D^T (D x - z) + sqrt(2 gamma) xi, 0).
+   * Requires OP_CONV or OP_MASK, rho > 0, no denoiser, lambda <= 0.  pnpula_get_state returns
+   * z_v, pnpula_get_z1 z_h. */
+  double tv_beta;
 } pnpula_config;
 
 typedef struct pnpula_ctx pnpula_ctx;
@@ -186,8 +194,8 @@ pnpula_status pnpula_get_moments(pnpula_ctx *ctx, float *mean, float *var, int64
 /* [collective for GLOBAL scope] Current state x^t, z^t (either may be NULL) and t. */
 pnpula_status pnpula_get_state(pnpula_ctx *ctx, float *x, float *z, int64_t *t, int32_t scope);
 
-/* [collective for GLOBAL scope] OP_POISSON: current z1 block (the AXDA variable ~ eta H x) on the
- * LOCAL bbox or, on root, the whole image. */
+/* [collective for GLOBAL scope] OP_POISSON: current z1 block (the AXDA variable ~ eta H x);
+ * TV prior: the horizontal component z_h of z ~ D x.  LOCAL bbox or, on root, the whole image. */
 pnpula_status pnpula_get_z1(pnpula_ctx *ctx, float *z1, int32_t scope);
 
 /* Number of tiles owned by this rank; halo width h; the i-th owned tile's rectangle. */

@@ -55,6 +55,7 @@ class Config(C.Structure):
         ("lipschitz_L", C.c_double), ("lipschitz_LD", C.c_double),
         ("flags", C.c_int32),
         ("eta", C.c_double), ("rho1", C.c_double), ("kappa1", C.c_double),
+        ("tv_beta", C.c_double),
     ]
 
 

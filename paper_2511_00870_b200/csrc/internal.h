@@ -45,6 +45,21 @@ struct UpdateParams {
   float inv_n;                     // 1 / (t+1 - burn_in)
   float eta;                       // residual r = eta (H x) - y: 1 for the Gaussian likelihood;
                                    // Poisson (reading R32): eta, with y -> z1 (AXDA block eta H x)
+  int has_tv;                      // TV prior (R37): - a_tv D^T (D x - z) and x+ = max(., 0)
+  float a_tv;                      // gamma / rho
+  const float *zv, *zh;            // padded z = (z_v, z_h) ~ D x, valid on tile (+) 1
+};
+
+// TV z block (R37, R38): on tile (+) 1 inside the image
+//   z <- prox_{kappa beta ||.||_{2,1}}( z - (kappa/rho)(z - D x+) + sqrt(2 kappa) zeta ),
+// zeta_v = Philox stream 1, zeta_h = stream 3.
+struct TvZParams {
+  const float *x;       // padded x^{t+1} (halo >= 2 valid)
+  float *zv, *zh;       // padded, in place on tile (+) 1
+  TileGeom g;
+  int ny, nx;
+  float b, s, tau;      // kappa/rho, sqrt(2 kappa), kappa beta
+  uint32_t seed_lo, seed_hi, t1;
 };
 
 // z1 block of the Poisson posterior (readings R32-R34): on tile (+) r_H (inside the image)
@@ -107,6 +122,7 @@ struct CnnChunkParams {
 // Launchers (return cudaGetLastError()).
 cudaError_t launch_update(const UpdateParams &p, cudaStream_t s);
 cudaError_t launch_z1_update(const Z1Params &p, cudaStream_t s);
+cudaError_t launch_tv_z_update(const TvZParams &p, cudaStream_t s);
 cudaError_t launch_copy_jobs(const CopyJob *d_jobs, int njobs, int max_rows, cudaStream_t s);
 cudaError_t launch_fill(float *p, float v, size_t n, cudaStream_t s);
 cudaError_t launch_finalize(const FinalizeParams &p, cudaStream_t s);

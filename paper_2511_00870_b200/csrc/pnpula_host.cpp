@@ -69,6 +69,7 @@ struct pnpula_ctx {
   double sigma2 = 1, alpha = 0, eps = 1, lambda = 0, c_lo = 0, c_hi = 1, rho = 0, kappa = 0,
          z_lo = 0, z_hi = 0, gamma = 0;
   double eta = 1, rho1 = 0, kappa1 = 0;   // OP_POISSON
+  double tv_beta = 0;                     // > 0: TV prior (z = (z_v, z_h) ~ D x in td.z, td.z1)
   int flags = 0;
   int n_layers = 0, channels = 0;   // 0 layers = no CNN
   int h = 0;
@@ -313,8 +314,10 @@ UpdateParams make_update_params(pnpula_ctx *c, TileDev &td, int buf) {
     for (size_t i = 0; i < c->kx.size(); ++i) p.kx[i] = c->kx[i];
   }
   p.a_g = poisson ? (float)(c->gamma * c->eta / c->rho1) : (float)(c->gamma / c->sigma2);
-  p.has_z = c->rho > 0;
-  p.a_rho = p.has_z ? (float)(c->gamma / c->rho) : 0.f;
+  p.has_tv = c->tv_beta > 0;
+  p.has_z = c->rho > 0 && !p.has_tv;   // TV: z ~ D x is updated by its own kernel after the exchange
+  if (p.has_tv) { p.a_tv = (float)(c->gamma / c->rho); p.zv = td.z; p.zh = td.z1; }
+  p.a_rho = p.has_z ? (float)(c->gamma / c->rho) : 0.f;   // (TV: a_tv)
   p.has_G = c->n_layers > 0;
   p.a_d = p.has_G ? (float)(c->alpha * c->gamma / (c->eps * c->eps)) : 0.f;
   p.has_box = c->lambda > 0;
@@ -351,6 +354,28 @@ pnpula_status step(pnpula_ctx *c) {
   }
   pnpula_status s = exchange(c, buf ^ 1);
   if (s) return s;
+  if (c->tv_beta > 0) {
+    // TV z block (R37, R38): x^{t+1} (halo now valid) -> z = (z_v, z_h) on tile (+) 1
+    for (auto &td : c->tiles) {
+      TvZParams q{};
+      q.x = td.x[buf ^ 1];
+      q.zv = td.z;
+      q.zh = td.z1;
+      q.g = td.g;
+      q.ny = c->ny; q.nx = c->nx;
+      q.b = (float)(c->kappa / c->rho);
+      q.s = (float)std::sqrt(2.0 * c->kappa);
+      q.tau = (float)(c->kappa * c->tv_beta);
+      q.seed_lo = (uint32_t)c->seed;
+      q.seed_hi = (uint32_t)(c->seed >> 32);
+      q.t1 = (uint32_t)t1;
+      cudaEvent_t end;
+      timer_begin(c, c->tm_update, &end);
+      CU(c, launch_tv_z_update(q, c->stream));
+      c->n_launches++;
+      timer_end(c, end);
+    }
+  }
   if (c->op == PNPULA_OP_POISSON) {
     // line 11-13 for the z1 block: x^{t+1} (halo now valid) -> z1 on tile (+) r_H (R33, R34)
     for (auto &td : c->tiles) {
@@ -576,6 +601,10 @@ pnpula_status pnpula_create(const pnpula_config *cfg, pnpula_ctx **out) {
   }
   if (f.rho > 0 && !(f.kappa > 0 && f.kappa < f.rho)) { set_error("kappa must lie in (0, rho)"); return PNPULA_E_INVALID_ARG; }
   const bool use_cnn = f.den && f.alpha != 0.0;
+  const bool tv = f.tv_beta > 0;
+  if (tv && (poisson || !(f.rho > 0) || use_cnn || f.lambda > 0)) {
+    set_error("TV prior needs OP_CONV/OP_MASK, rho > 0, no denoiser and lambda <= 0"); return PNPULA_E_INVALID_ARG;
+  }
   if (use_cnn) {
     if (f.den->n_layers < 2 || !f.den->weights || !f.den->biases) { set_error("denoiser needs >= 2 layers and weights"); return PNPULA_E_INVALID_ARG; }
     if (f.den->channels != 16 && f.den->channels != 32 && f.den->channels != 64) {
@@ -593,6 +622,7 @@ pnpula_status pnpula_create(const pnpula_config *cfg, pnpula_ctx **out) {
   c->c_lo = f.c_lo; c->c_hi = f.c_hi; c->rho = f.rho; c->kappa = f.kappa;
   c->z_lo = f.z_lo; c->z_hi = f.z_hi; c->gamma = f.gamma;
   if (poisson) { c->eta = f.eta; c->rho1 = f.rho1; c->kappa1 = f.kappa1; }
+  if (tv) c->tv_beta = f.tv_beta;
   if (f.op != PNPULA_OP_MASK) {
     c->kh = f.kh; c->kw = f.kw; c->ry = f.kh / 2; c->rx = f.kw / 2;
     c->separable = (f.kernel_y && f.kernel_x) ? 1 : 0;
@@ -605,6 +635,7 @@ pnpula_status pnpula_create(const pnpula_config *cfg, pnpula_ctx **out) {
   }
   if (use_cnn) { c->n_layers = f.den->n_layers; c->channels = f.den->channels; }
   c->h = pnpula_halo_width(f.op, f.kh, f.kw, c->n_layers);
+  if (tv) c->h = std::max(c->h, 2);   // D^T D x needs x at distance 1, z on tile (+) 1 needs 2 (R38)
   c->ntiles = ntiles;
   c->n_local = ntiles / f.world_size;
   c->first_tile = f.rank * c->n_local;
@@ -634,7 +665,9 @@ pnpula_status pnpula_create(const pnpula_config *cfg, pnpula_ctx **out) {
       if (poisson) L_h2 = s * s / f.rho1;
     }
     const double lam = f.lambda > 0 ? f.lambda : 1e300;
-    int32_t bad = pnpula_check_stepsizes(L, (f.rho > 0 ? 1.0 / f.rho : 0.0) + L_h2, use_cnn ? f.alpha : 0.0,
+    // ||H2||^2 / rho: H2 = I (1/rho), TV H2 = D (||D||^2 <= 8, R35), plus the Poisson z1 block
+    const double h2 = f.rho > 0 ? (tv ? 8.0 : 1.0) / f.rho : 0.0;
+    int32_t bad = pnpula_check_stepsizes(L, h2 + L_h2, use_cnn ? f.alpha : 0.0,
                                          use_cnn ? f.eps : 1.0, f.lipschitz_LD, lam, f.gamma);
     if (bad) set_error("warning: eq:stepsize_cond violated (mask %d) -- continuing", bad);
   }
@@ -722,7 +755,7 @@ pnpula_status pnpula_create(const pnpula_config *cfg, pnpula_ctx **out) {
     CUB(cudaMalloc(&td.mean, n * sizeof(float)));
     CUB(cudaMalloc(&td.m2, n * sizeof(float)));
     if (c->rho > 0) CUB(cudaMalloc(&td.z, n * sizeof(float)));
-    if (poisson) {
+    if (poisson || tv) {   // Poisson z1 block, or the TV horizontal component z_h
       CUB(cudaMalloc(&td.z1, n * sizeof(float)));
       CUB(cudaMemsetAsync(td.z1, 0, n * sizeof(float), c->stream));
     }
@@ -1006,7 +1039,9 @@ pnpula_status pnpula_get_state(pnpula_ctx *c, float *x, float *z, int64_t *t, in
 pnpula_status pnpula_get_z1(pnpula_ctx *c, float *z1, int32_t scope) {
   pnpula_status s = check_ctx(c);
   if (s) return s;
-  if (c->op != PNPULA_OP_POISSON) { set_error("z1 exists only for OP_POISSON"); return PNPULA_E_STATE; }
+  if (c->op != PNPULA_OP_POISSON && !(c->tv_beta > 0)) {
+    set_error("z1 exists only for OP_POISSON (z1 block) or the TV prior (z_h)"); return PNPULA_E_STATE;
+  }
   CU(c, cudaSetDevice(c->device));
   std::vector<const float *> zs;
   for (auto &td : c->tiles) zs.push_back(td.z1);

@@ -123,6 +123,28 @@ __device__ __forceinline__ void ula_load(const UpdateParams &p, int gi, int gj4,
   }
 }
 
+// D^T (D x - z) at the 4 pixels of a quad (R35, R37):
+//   g_v[i-1,j] [i >= 1] - g_v[i,j] [i < ny-1] + g_h[i,j-1] [j >= 1] - g_h[i,j] [j < nx-1],
+//   g_v = (x[i+1,j] - x[i,j]) - z_v, g_h = (x[i,j+1] - x[i,j]) - z_h.  Neighbours come from the
+// padded x (halo >= 2) and z (valid on tile (+) 1), through L1.
+__device__ __forceinline__ void tv_term(const UpdateParams &p, int gi, int gj4, const float *xc, float out[4]) {
+  const TileGeom &g = p.g;
+  const int64_t base = pidx(g, gi, gj4);
+  const int64_t pitch = g.pitch;
+#pragma unroll
+  for (int l = 0; l < 4; ++l) {
+    const int gj = gj4 + l;
+    if (gj >= p.nx) { out[l] = 0.f; continue; }
+    const int64_t n = base + l;
+    float s = 0.f;
+    if (gi >= 1) s += (xc[l] - __ldg(p.x + n - pitch)) - __ldg(p.zv + n - pitch);
+    if (gi < p.ny - 1) s -= (__ldg(p.x + n + pitch) - xc[l]) - __ldg(p.zv + n);
+    if (gj >= 1) s += (xc[l] - __ldg(p.x + n - 1)) - __ldg(p.zh + n - 1);
+    if (gj < p.nx - 1) s -= (__ldg(p.x + n + 1) - xc[l]) - __ldg(p.zh + n);
+    out[l] = s;
+  }
+}
+
 __device__ __forceinline__ void ula_finish(const UpdateParams &p, int gi, int gj4, const float gr[4], QuadIn &q) {
   const TileGeom &g = p.g;
   const int64_t base = pidx(g, gi, gj4);
@@ -131,6 +153,8 @@ __device__ __forceinline__ void ula_finish(const UpdateParams &p, int gi, int gj
   float *mv = q.m, *sv = q.s;
   float xi[4];
   normals4(p.seed_lo, p.seed_hi, (uint32_t)gj4 >> 2, (uint32_t)gi, p.t1, 0u, xi);
+  float dtv[4] = {0.f, 0.f, 0.f, 0.f};
+  if (p.has_tv) tv_term(p, gi, gj4, xv, dtv);
   float xn[4];
 #pragma unroll
   for (int l = 0; l < 4; ++l) {
@@ -138,8 +162,9 @@ __device__ __forceinline__ void ula_finish(const UpdateParams &p, int gi, int gj
     if (p.has_z) v -= p.a_rho * (xv[l] - zv[l]);
     if (p.has_G) v += p.a_d * (-Gv[l]);
     if (p.has_box) v += p.a_lam * (fminf(fmaxf(xv[l], p.c_lo), p.c_hi) - xv[l]);
+    if (p.has_tv) v -= p.a_tv * dtv[l];
     v += p.a_xi * xi[l];
-    xn[l] = v;
+    xn[l] = p.has_tv ? fmaxf(v, 0.f) : v;   // TV: PSGLA projection onto R+ after the step (R37)
   }
   float zn[4];
   if (p.has_z) {
@@ -617,6 +642,40 @@ __global__ void __launch_bounds__(NTHREADS) z1_sep_kernel(const __grid_constant_
   }
 }
 
+// ---------------------------------------------------------------- TV z block (R37, R38)
+// One thread per column quad of tile (+) 1 (global quads: the Philox calls match the oracle's
+// (stream, pixel) counters); D x+ from the padded x+ (halo >= 2), block soft threshold per pixel.
+__global__ void __launch_bounds__(NTHREADS) tv_z_kernel(const __grid_constant__ TvZParams p) {
+  const TileGeom &g = p.g;
+  const int r0 = max(g.i0 - 1, 0), r1 = min(g.i0 + g.th + 1, p.ny);
+  const int c0 = max(g.j0 - 1, 0), c1 = min(g.j0 + g.tw + 1, p.nx);
+  const int q0 = c0 >> 2, nq = ((c1 + 3) >> 2) - q0;
+  const int64_t total = (int64_t)nq * (r1 - r0);
+  for (int64_t e = (int64_t)blockIdx.x * NTHREADS + threadIdx.x; e < total; e += (int64_t)gridDim.x * NTHREADS) {
+    const int gi = r0 + (int)(e / nq);
+    const int gj4 = 4 * (q0 + (int)(e % nq));
+    float zev[4], zeh[4];
+    normals4(p.seed_lo, p.seed_hi, (uint32_t)gj4 >> 2, (uint32_t)gi, p.t1, 1u, zev);
+    normals4(p.seed_lo, p.seed_hi, (uint32_t)gj4 >> 2, (uint32_t)gi, p.t1, 3u, zeh);
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+      const int gj = gj4 + l;
+      if (gj < c0 || gj >= c1) continue;
+      const int64_t n = pidx(g, gi, gj);
+      const float xc = __ldg(p.x + n);
+      const float dv = gi < p.ny - 1 ? __ldg(p.x + n + g.pitch) - xc : 0.f;
+      const float dh = gj < p.nx - 1 ? __ldg(p.x + n + 1) - xc : 0.f;
+      const float zv = p.zv[n], zh = p.zh[n];
+      const float vv = zv - p.b * (zv - dv) + p.s * zev[l];
+      const float vh = zh - p.b * (zh - dh) + p.s * zeh[l];
+      const float nrm = sqrtf(vv * vv + vh * vh);
+      const float sc = nrm > p.tau ? 1.f - p.tau / nrm : 0.f;
+      p.zv[n] = vv * sc;
+      p.zh[n] = vh * sc;
+    }
+  }
+}
+
 // ---------------------------------------------------------------- mask K7 (no stencil)
 __global__ void __launch_bounds__(NTHREADS) update_mask_kernel(const __grid_constant__ UpdateParams p) {
   const TileGeom &g = p.g;
@@ -774,6 +833,19 @@ cudaError_t launch_z1_update(const Z1Params &p, cudaStream_t s) {
   if (blocks > 148 * 16) blocks = 148 * 16;
   if (blocks < 1) blocks = 1;
   z1_update_kernel<<<(unsigned)blocks, NTHREADS, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tv_z_update(const TvZParams &p, cudaStream_t s) {
+  const int r0 = p.g.i0 - 1 < 0 ? 0 : p.g.i0 - 1;
+  const int r1 = p.g.i0 + p.g.th + 1 > p.ny ? p.ny : p.g.i0 + p.g.th + 1;
+  const int c0 = p.g.j0 - 1 < 0 ? 0 : p.g.j0 - 1;
+  const int c1 = p.g.j0 + p.g.tw + 1 > p.nx ? p.nx : p.g.j0 + p.g.tw + 1;
+  const int64_t total = (int64_t)(((c1 + 3) >> 2) - (c0 >> 2)) * (r1 - r0);
+  int64_t blocks = (total + NTHREADS - 1) / NTHREADS;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks < 1) blocks = 1;
+  tv_z_kernel<<<(unsigned)blocks, NTHREADS, 0, s>>>(p);
   return cudaGetLastError();
 }
 

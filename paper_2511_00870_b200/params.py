@@ -11,6 +11,8 @@ poisson_pnp: P:777-782 (Poisson noise, PnP prior, AXDA blocks z1 ~ eta H x, z2 ~
   lambda = 0.99 / (4 ||eta H||^2/rho1 + 4/rho2 + 2 alpha L_D/eps^2),
   gamma  = 0.99 / (3 (alpha L_D/eps^2 + ||eta H||^2/rho1 + 1/rho2 + 1/lambda)),
   kappa1 = 0.99 rho1, kappa2 = 0.99 rho2.
+tv_gaussian: P:802-809 (Gaussian noise, TV prior, z ~ D x): rho = 1e-5, beta = 40,
+  gamma = 0.99 (||H||^2/sigma^2 + ||D||^2/rho)^-1, kappa = 0.99 rho ||D||^-2, ||D||^2 <= 8.
 """
 from __future__ import annotations
 
@@ -42,3 +44,9 @@ def poisson_pnp(eta: float, normH2: float = 1.0, L_D: float = 1.0, alpha: float 
     gamma = 0.99 / (3 * (alpha * L_D / eps ** 2 + h2 + 1 / rho2 + 1 / lam))
     return dict(alpha=alpha, eps=eps, lam=lam, gamma=gamma, eta=eta, rho1=rho1, kappa1=0.99 * rho1,
                 rho=rho2, kappa=0.99 * rho2)
+
+
+def tv_gaussian(sigma2: float, normH2: float = 1.0, rho: float = 1e-5, beta: float = 40.0,
+                normD2: float = 8.0) -> dict:
+    gamma = 0.99 / (normH2 / sigma2 + normD2 / rho)
+    return dict(gamma=gamma, rho=rho, kappa=0.99 * rho / normD2, tv_beta=beta)

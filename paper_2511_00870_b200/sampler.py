@@ -27,7 +27,7 @@ class Sampler:
                  x0: Optional[np.ndarray] = None, in_rect=None, tiles=(1, 1),
                  rank: int = 0, world_size: int = 1, device: int = 0, nccl_uid: Optional[bytes] = None,
                  stream: int = 0, flags: int = 0, lipschitz_L: float = 0.0, lipschitz_LD: float = 0.0,
-                 eta: float = 0.0, rho1: float = 0.0, kappa1: float = 0.0):
+                 eta: float = 0.0, rho1: float = 0.0, kappa1: float = 0.0, tv_beta: float = 0.0):
         lib = L.load()
         keep = []
         cfg = L.Config()
@@ -80,6 +80,7 @@ class Sampler:
         cfg.lipschitz_L, cfg.lipschitz_LD = lipschitz_L, lipschitz_LD
         cfg.flags = flags
         cfg.eta, cfg.rho1, cfg.kappa1 = eta, rho1, kappa1
+        cfg.tv_beta = tv_beta
         h = C.c_void_p()
         L.check(lib.pnpula_create(C.byref(cfg), C.byref(h)))
         self.warning = L.last_error()
@@ -131,7 +132,7 @@ class Sampler:
         return x, z, t.value
 
     def z1(self, scope: int = L.SCOPE_LOCAL):
-        """OP_POISSON: the AXDA block z1 (~ eta H x)."""
+        """OP_POISSON: the AXDA block z1 (~ eta H x); TV prior: z_h."""
         shp = self._out_shape(scope)
         out = np.zeros(shp, np.float32) if shp else None
         L.check(self._lib.pnpula_get_z1(self._h, L._ptr(out), scope))

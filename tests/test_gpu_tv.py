@@ -1,0 +1,81 @@
+"""GPU parity for the TV-prior iteration (item:prior_choice:tv P:786-809; DESIGN.md readings
+R35-R38): the C-ABI library (tv_beta > 0: PSGLA x-step on R+, z = (z_v, z_h) ~ D x with the
+l2,1 prox, z on tile (+) 1) against the pinned oracle, and bitwise tiling invariance."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from gpu_common import rel_l2
+from paper_2511_00870_b200 import Sampler, params
+from paper_2511_00870_b200._lib import FLAG_HALO_VIA_NCCL
+
+pytestmark = pytest.mark.gpu
+
+
+def tv_problem(ny, nx, *, op="conv", kernel="gauss9", rho=1e-3, beta=40.0):
+    if op == "conv":
+        if kernel.startswith("gauss"):
+            L = int(kernel[5:])
+            ky, kx = synth.gaussian_factors(L, 1.0 if L == 5 else 2.0)
+            k2 = synth.outer(ky, kx)
+            ks, ko = dict(kernel_sep=(ky, kx)), dict(ksep=(ky, kx))
+        else:
+            L = int(kernel[6:])
+            k = synth.random_kernel(L, L, seed=L)
+            k2 = k.astype(np.float64)
+            ks, ko = dict(kernel=k), dict(kernel=k)
+        s2 = synth.noise_sigma2_blur(ny, nx, k2, 25.0)
+        y = synth.observe_blur(ny, nx, k2, s2)
+        extra_s, extra_o = dict(op="conv", **ks), dict(op="conv", **ko)
+    else:
+        s2 = synth.noise_sigma2_mask(ny, nx, 15.0)
+        y, m = synth.observe_mask(ny, nx, s2)
+        extra_s, extra_o = dict(op="mask", mask=m), dict(op="mask", mask=m)
+    hp = params.tv_gaussian(s2, rho=rho, beta=beta)
+    common = dict(sigma2=s2, gamma=hp["gamma"], rho=hp["rho"], kappa=hp["kappa"], tv_beta=hp["tv_beta"],
+                  x0=(synth.ground_truth(ny, nx) * 0.8 + 0.1).astype(np.float32))
+    kw = dict(ny=ny, nx=nx, y=y, **extra_s, **common)
+    pb = oracle.Problem(y=y, **extra_o, **common)
+    return kw, pb
+
+
+def gpu_tv(kw, n_iter, burn_in, seed, tiles=(1, 1), flags=0):
+    s = Sampler(**kw, tiles=tiles, flags=flags)
+    try:
+        s.run(n_iter, burn_in, seed)
+        x, zv, _ = s.state()
+        zh = s.z1()
+        mean, var, _ = s.moments()
+        return dict(x=x, z=zv, z1=zh, mean=mean, var=var)
+    finally:
+        s.close()
+
+
+@pytest.mark.parametrize("op,kernel,shape", [("conv", "gauss9", (70, 83)), ("conv", "random5", (61, 57)),
+                                             ("mask", None, (64, 66))])
+def test_tv_chain_fp32_path_vs_oracle(op, kernel, shape):
+    ny, nx = shape
+    kw, pb = tv_problem(ny, nx, op=op, kernel=kernel or "gauss9")
+    g = gpu_tv(kw, 50, 10, seed=872)
+    o = oracle.run(pb, 50, 10, seed=872)
+    for k in ("x", "z", "z1", "mean"):
+        assert rel_l2(g[k], o[k]) <= 1e-5, k
+    assert rel_l2(g["var"], o["var"]) <= 1e-4
+    assert np.all(g["x"] >= 0)
+
+
+@pytest.mark.parametrize("tiles,flags", [((2, 2), 0), ((3, 1), 0), ((1, 3), FLAG_HALO_VIA_NCCL)])
+def test_tv_tiled_bitwise(tiles, flags):
+    kw, _ = tv_problem(66, 75, kernel="random5")
+    a = gpu_tv(kw, 12, 4, seed=6)
+    b = gpu_tv(kw, 12, 4, seed=6, tiles=tiles, flags=flags)
+    for k in ("x", "z", "z1", "mean", "var"):
+        np.testing.assert_array_equal(a[k], b[k], err_msg=k)
+
+
+def test_tv_rejects_denoiser():
+    kw, _ = tv_problem(40, 40, kernel="gauss5")
+    w, b = synth.dncnn_weights(4, 16)
+    with pytest.raises(Exception):
+        Sampler(**kw, weights=w, biases=b, n_layers=4, channels=16, alpha=1.0, eps=0.1)
