@@ -42,7 +42,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=60)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--workload", default="c5", choices=["c5", "c2", "c3", "c4", "c1", "p5"])
+    ap.add_argument("--workload", default="c5", choices=["c5", "c2", "c3", "c4", "c1", "p5", "t5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -66,6 +66,12 @@ def workload(name, n):
         return dict(name="p5", desc="weak scaling as c5, Poisson deconvolution (eta = 250, 9x9 Gaussian), "
                     "AXDA z1 ~ eta H x (KL prox) + z2 ~ x (R+), DnCNN-lite 8x32", ny=ny, nx=nx, tiles=(n, 1),
                     op="poisson", L=9, sb=2.0, cnn=(8, 32), z=True, scaling="weak")
+    if name == "t5":
+        shapes = {1: (4096, 8192), 2: (8192, 8192), 4: (8192, 16384), 8: (16384, 16384)}
+        ny, nx = shapes.get(n, (4096 * n, 8192))
+        return dict(name="t5", desc="weak scaling as c5, 9x9 Gaussian deblur 25 dB with the TV prior "
+                    "(beta = 40, rho = 1e-5; PSGLA on R+, z ~ D x)", ny=ny, nx=nx, tiles=(n, 1), op="conv", L=9,
+                    sb=2.0, cnn=None, z=True, tv=True, scaling="weak")
     if name == "c2":
         return dict(name="c2", desc="1024x1024 deblur, 9x9 Gaussian blur, DnCNN-lite 8x32", ny=1024, nx=1024,
                     tiles=(n, 1), op="conv", L=9, sb=2.0, cnn=(8, 32), z=False, scaling="strong")
@@ -115,7 +121,10 @@ def build_inputs(wl, rect, pinned=False):
         s2 = synth.noise_sigma2_mask(ny, nx, 15.0)
         y, m = synth.observe_mask(ny, nx, s2, rect=rect)
         kw.update(op="mask", mask=m)
-    if wl["name"] == "c4":
+    if wl.get("tv"):
+        hp = params.tv_gaussian(s2)
+        kw.update(rho=hp["rho"], kappa=hp["kappa"], tv_beta=hp["tv_beta"])
+    elif wl["name"] == "c4":
         hp = dict(gamma=0.99 / 120, lam=0.05)
         s2 = 1e-2
         kw.update(lam=0.05, c_lo=0.5, c_hi=0.5)
@@ -218,7 +227,7 @@ def oracle_crop_problem(wl, size):
     kw = build_inputs(wl, (i0, j0, size, size))
     okw = {k: v for k, v in kw.items() if k in ("sigma2", "gamma", "mask", "weights", "biases", "n_layers",
                                                 "channels", "alpha", "eps", "lam", "c_lo", "c_hi", "rho", "kappa",
-                                                "z_lo", "z_hi", "eta", "rho1", "kappa1")}
+                                                "z_lo", "z_hi", "eta", "rho1", "kappa1", "tv_beta")}
     if wl["op"] == "poisson":
         okw.update(op="poisson", ksep=kw["kernel_sep"])
     elif "kernel_sep" in kw:
@@ -384,6 +393,8 @@ def main():
                 "algorithmic": f"2*{cnn_macs(Kc, P)} FLOP/px (2 MAC) x {own_px} px per evaluation",
                 "peak_source": peak_src + " bf16_tflops_sustained"}
     upd_bytes_px = 32 + (8 if wl["z"] else 0) - (4 if not wl["cnn"] else 0) + (1 if wl["op"] == "mask" else 0)
+    if wl.get("tv"):
+        upd_bytes_px = 28 + 8 + 20   # x-update 28 (no G) + z_v, z_h read; z kernel: x+ 4, z_v/z_h 16
     if wl["op"] == "poisson":
         upd_bytes_px += 16   # z1 block kernel: y + z1 read, z1 written, x+ (stencil, once from HBM)
     upd_ach = upd_bytes_px * own_px * K / (upd_ms * 1e-3) / 1e9 if upd_ms else None
