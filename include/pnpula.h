@@ -198,6 +198,18 @@ pnpula_status pnpula_get_state(pnpula_ctx *ctx, float *x, float *z, int64_t *t, 
  * TV prior: the horizontal component z_h of z ~ D x.  LOCAL bbox or, on root, the whole image. */
 pnpula_status pnpula_get_z1(pnpula_ctx *ctx, float *z1, int32_t scope);
 
+/* Checkpoint / resume.  The blob holds this rank's complete chain state:
+ * t, burn-in, seed and, per owned tile, the padded buffers (interior + ghost frame) of x^t,
+ * the z blocks (z; z1 for OP_POISSON / z_h for TV) and the Welford mean / M2, so that
+ * load + advance(n) is bitwise identical to never having stopped.  Host memory, caller-owned.
+ * pnpula_checkpoint_bytes: size of the blob.  pnpula_save_checkpoint: writes it (bytes must be
+ * >= the size, else E_INVALID_ARG).  pnpula_load_checkpoint: restores a blob saved by a context
+ * created with the same configuration, tile grid and rank (E_SHAPE if the header differs); it
+ * replaces pnpula_reset. */
+pnpula_status pnpula_checkpoint_bytes(pnpula_ctx *ctx, uint64_t *bytes);
+pnpula_status pnpula_save_checkpoint(pnpula_ctx *ctx, void *buf, uint64_t bytes);
+pnpula_status pnpula_load_checkpoint(pnpula_ctx *ctx, const void *buf, uint64_t bytes);
+
 /* Number of tiles owned by this rank; halo width h; the i-th owned tile's rectangle. */
 pnpula_status pnpula_tile_info(pnpula_ctx *ctx, int32_t local_index, pnpula_rect *rect,
                                int32_t *n_local_tiles, int32_t *halo);
@@ -228,6 +240,12 @@ void pnpula_partition(int64_t n, int64_t parts, int64_t p, int64_t *lo, int64_t 
 
 /* Halo width h = max(2 r_H, K) (receptive-field strategy, R5). */
 int32_t pnpula_halo_width(int32_t op, int32_t kh, int32_t kw, int32_t n_layers);
+
+/* Host helper for the step sizes: upper bound of ||H||_2^2 for the same-size,
+ * zero-boundary convolution with the kh x kw kernel k (host, row-major): max over a grid x grid
+ * DFT of |K(w)|^2 (the zero-boundary operator is a restriction of the full convolution, whose
+ * norm is sup |K(w)|; grid >= max(kh, kw), e.g. 256).  Returns PNPULA_E_INVALID_ARG on bad sizes. */
+pnpula_status pnpula_conv_norm2_bound(const float *k, int32_t kh, int32_t kw, int32_t grid, double *out);
 
 /* One ghost-region message: the global rectangle `rect` of tile src's interior
  * that tile dst stores in its ghost frame (Fig. 2(b)). */

@@ -88,6 +88,10 @@ def load():
         "pnpula_get_moments": ([vp, vp, vp, C.POINTER(i64), i32], C.c_int),
         "pnpula_get_state": ([vp, vp, vp, C.POINTER(i64), i32], C.c_int),
         "pnpula_get_z1": ([vp, vp, i32], C.c_int),
+        "pnpula_checkpoint_bytes": ([vp, C.POINTER(u64)], C.c_int),
+        "pnpula_save_checkpoint": ([vp, vp, u64], C.c_int),
+        "pnpula_load_checkpoint": ([vp, vp, u64], C.c_int),
+        "pnpula_conv_norm2_bound": ([vp, i32, i32, i32, C.POINTER(d)], C.c_int),
         "pnpula_tile_info": ([vp, i32, C.POINTER(Rect), C.POINTER(i32), C.POINTER(i32)], C.c_int),
         "pnpula_get_padded_x": ([vp, i32, vp], C.c_int),
         "pnpula_get_denoiser_residual": ([vp, vp], C.c_int),
@@ -112,7 +116,8 @@ EXPORTED = ["pnpula_version", "pnpula_last_error", "pnpula_get_unique_id", "pnpu
             "pnpula_advance", "pnpula_run", "pnpula_synchronize", "pnpula_local_bbox", "pnpula_get_moments",
             "pnpula_get_state", "pnpula_get_z1", "pnpula_tile_info", "pnpula_get_padded_x", "pnpula_get_denoiser_residual",
             "pnpula_set_timing", "pnpula_kernel_time", "pnpula_destroy", "pnpula_partition",
-            "pnpula_halo_width", "pnpula_plan_halo", "pnpula_check_stepsizes"]
+            "pnpula_halo_width", "pnpula_plan_halo", "pnpula_check_stepsizes", "pnpula_checkpoint_bytes",
+            "pnpula_save_checkpoint", "pnpula_load_checkpoint", "pnpula_conv_norm2_bound"]
 
 
 def last_error() -> str:
@@ -155,6 +160,15 @@ def pnpula_plan_halo(ny, nx, tiles_y, tiles_x, h):
 
 def pnpula_check_stepsizes(L, h2_over_rho, alpha, eps, L_D, lam, gamma) -> int:
     return int(load().pnpula_check_stepsizes(L, h2_over_rho, alpha, eps, L_D, lam, gamma))
+
+
+def pnpula_conv_norm2_bound(k, grid: int = 256) -> float:
+    """Upper bound of ||H||^2 for the zero-boundary convolution with kernel k (max |DFT|^2)."""
+    import numpy as np
+    kk = np.ascontiguousarray(k, dtype=np.float32)
+    out = C.c_double()
+    check(load().pnpula_conv_norm2_bound(kk.ctypes.data, kk.shape[0], kk.shape[1], grid, C.byref(out)))
+    return out.value
 
 
 def pnpula_get_unique_id() -> bytes:

@@ -1048,6 +1048,113 @@ pnpula_status pnpula_get_z1(pnpula_ctx *c, float *z1, int32_t scope) {
   return gather_padded_interiors(c, zs, z1, scope == PNPULA_SCOPE_GLOBAL_ON_ROOT);
 }
 
+namespace {
+constexpr uint64_t kCkptMagic = 0x31544b504c554e50ull;   // "PNULPKT1"
+struct CkptHeader {
+  uint64_t magic;
+  int64_t t, burn_in;
+  uint64_t seed;
+  int32_t ny, nx, tiles_y, tiles_x, rank, world, n_local, nfields;
+  uint64_t elems_total;   // floats after the header
+};
+// the fields of one tile, in blob order (x^t first)
+std::vector<float *> ckpt_fields(pnpula_ctx *c, TileDev &td) {
+  std::vector<float *> f{td.x[c->cur], td.mean, td.m2};
+  if (td.z) f.push_back(td.z);
+  if (td.z1) f.push_back(td.z1);
+  return f;
+}
+uint64_t ckpt_bytes(pnpula_ctx *c) {
+  uint64_t n = 0;
+  for (auto &td : c->tiles) n += (uint64_t)geom_elems(td.g) * ckpt_fields(c, td).size();
+  return sizeof(CkptHeader) + n * sizeof(float);
+}
+}  // namespace
+
+pnpula_status pnpula_checkpoint_bytes(pnpula_ctx *c, uint64_t *bytes) {
+  pnpula_status s = check_ctx(c);
+  if (s) return s;
+  if (!bytes) { set_error("null output"); return PNPULA_E_INVALID_ARG; }
+  *bytes = ckpt_bytes(c);
+  return PNPULA_OK;
+}
+
+pnpula_status pnpula_save_checkpoint(pnpula_ctx *c, void *buf, uint64_t bytes) {
+  pnpula_status s = check_ctx(c);
+  if (s) return s;
+  if (!c->have_reset) { set_error("no chain to checkpoint (pnpula_reset first)"); return PNPULA_E_STATE; }
+  if (!buf || bytes < ckpt_bytes(c)) { set_error("checkpoint buffer too small"); return PNPULA_E_INVALID_ARG; }
+  CU(c, cudaSetDevice(c->device));
+  CkptHeader h{kCkptMagic, c->t, c->burn_in, c->seed, c->ny, c->nx, c->tiles_y, c->tiles_x, c->rank, c->world,
+               c->n_local, (int32_t)(c->tiles.empty() ? 0 : ckpt_fields(c, c->tiles[0]).size()),
+               (ckpt_bytes(c) - sizeof(CkptHeader)) / sizeof(float)};
+  memcpy(buf, &h, sizeof(h));
+  float *dst = reinterpret_cast<float *>(static_cast<char *>(buf) + sizeof(h));
+  for (auto &td : c->tiles) {
+    const size_t n = geom_elems(td.g);
+    for (float *f : ckpt_fields(c, td)) {
+      CU(c, cudaMemcpyAsync(dst, f, n * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+      dst += n;
+    }
+  }
+  CU(c, cudaStreamSynchronize(c->stream));
+  return PNPULA_OK;
+}
+
+pnpula_status pnpula_load_checkpoint(pnpula_ctx *c, const void *buf, uint64_t bytes) {
+  pnpula_status s = check_ctx(c);
+  if (s) return s;
+  if (!buf || bytes < sizeof(CkptHeader)) { set_error("checkpoint buffer too small"); return PNPULA_E_INVALID_ARG; }
+  CkptHeader h;
+  memcpy(&h, buf, sizeof(h));
+  c->cur = 0;   // the restored x^t goes to buffer 0
+  const uint64_t need = ckpt_bytes(c);
+  if (h.magic != kCkptMagic || h.ny != c->ny || h.nx != c->nx || h.tiles_y != c->tiles_y || h.tiles_x != c->tiles_x ||
+      h.rank != c->rank || h.world != c->world || h.n_local != c->n_local ||
+      h.elems_total != (need - sizeof(CkptHeader)) / sizeof(float) ||
+      h.nfields != (int32_t)(c->tiles.empty() ? 0 : ckpt_fields(c, c->tiles[0]).size())) {
+    set_error("checkpoint does not match this context (geometry, rank or state fields)");
+    return PNPULA_E_SHAPE;
+  }
+  if (bytes < need) { set_error("checkpoint truncated"); return PNPULA_E_INVALID_ARG; }
+  CU(c, cudaSetDevice(c->device));
+  const float *src = reinterpret_cast<const float *>(static_cast<const char *>(buf) + sizeof(h));
+  for (auto &td : c->tiles) {
+    const size_t n = geom_elems(td.g);
+    for (float *f : ckpt_fields(c, td)) {
+      CU(c, cudaMemcpyAsync(f, src, n * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+      src += n;
+    }
+  }
+  CU(c, cudaStreamSynchronize(c->stream));
+  c->t = h.t;
+  c->burn_in = h.burn_in;
+  c->seed = h.seed;
+  c->have_reset = true;
+  return PNPULA_OK;
+}
+
+pnpula_status pnpula_conv_norm2_bound(const float *k, int32_t kh, int32_t kw, int32_t grid, double *out) {
+  if (!k || !out || kh <= 0 || kw <= 0 || grid < std::max(kh, kw)) {
+    set_error("bad kernel / grid"); return PNPULA_E_INVALID_ARG;
+  }
+  double best = 0;
+  const double w0 = 2.0 * M_PI / grid;
+  for (int u = 0; u < grid; ++u)
+    for (int v = 0; v < grid; ++v) {
+      double re = 0, im = 0;
+      for (int p = 0; p < kh; ++p)
+        for (int q = 0; q < kw; ++q) {
+          const double ph = w0 * ((double)u * p + (double)v * q);
+          re += k[p * kw + q] * std::cos(ph);
+          im -= k[p * kw + q] * std::sin(ph);
+        }
+      best = std::max(best, re * re + im * im);
+    }
+  *out = best;
+  return PNPULA_OK;
+}
+
 pnpula_status pnpula_get_padded_x(pnpula_ctx *c, int32_t li, float *out) {
   pnpula_status s = check_ctx(c);
   if (s) return s;

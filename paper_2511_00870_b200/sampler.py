@@ -138,6 +138,18 @@ class Sampler:
         L.check(self._lib.pnpula_get_z1(self._h, L._ptr(out), scope))
         return out
 
+    def save_checkpoint(self) -> bytes:
+        """This rank's complete chain state (resume with load_checkpoint on an identical context)."""
+        n = C.c_uint64()
+        L.check(self._lib.pnpula_checkpoint_bytes(self._h, C.byref(n)))
+        buf = (C.c_uint8 * n.value)()
+        L.check(self._lib.pnpula_save_checkpoint(self._h, buf, n.value))
+        return bytes(buf)
+
+    def load_checkpoint(self, blob: bytes):
+        buf = (C.c_uint8 * len(blob)).from_buffer_copy(blob)
+        L.check(self._lib.pnpula_load_checkpoint(self._h, buf, len(blob)))
+
     def tile_info(self, i: int):
         r = L.Rect()
         L.check(self._lib.pnpula_tile_info(self._h, i, C.byref(r), None, None))

@@ -140,3 +140,41 @@ def test_chain_50_with_cnn():
     assert rel_l2(g["x"], o["x"]) <= 2e-2
     assert rel_l2(g["mean"], o["mean"]) <= 2e-2
     assert rel_l2(g["x"], o16["x"]) <= 2e-3
+
+
+@pytest.mark.parametrize("case", ["cnn", "poisson", "tv"])
+def test_checkpoint_resume_is_bitwise(case):
+    """save after 9 iterations, load into a fresh context, advance 11: identical to 20 straight
+    (x, z blocks, moments) -- SURVEY 8(f) rank 4 resume."""
+    if case == "cnn":
+        kw, _ = make_problem(45, 52, kernel="gauss5", cnn=(4, 16), z=True)
+    elif case == "poisson":
+        from test_gpu_poisson import poisson_problem
+        kw, _ = poisson_problem(47, 50, kernel="random5", cnn=(4, 16))
+    else:
+        from test_gpu_tv import tv_problem
+        kw, _ = tv_problem(47, 50, kernel="random5")
+    ref = Sampler(**kw, tiles=(2, 1))
+    ref.run(20, 4, 77)
+    want_x, want_z, _ = ref.state()
+    want_m, want_v, _ = ref.moments()
+    want_z1 = ref.z1() if case != "cnn" else None
+    ref.close()
+    a = Sampler(**kw, tiles=(2, 1))
+    a.reset(4, 77)
+    a.advance(9)
+    blob = a.save_checkpoint()
+    a.close()
+    b = Sampler(**kw, tiles=(2, 1))
+    b.load_checkpoint(blob)
+    b.advance(11)
+    x, z, t = b.state()
+    m, v, _ = b.moments()
+    assert t == 20
+    np.testing.assert_array_equal(x, want_x)
+    np.testing.assert_array_equal(z, want_z)
+    np.testing.assert_array_equal(m, want_m)
+    np.testing.assert_array_equal(v, want_v)
+    if want_z1 is not None:
+        np.testing.assert_array_equal(b.z1(), want_z1)
+    b.close()
