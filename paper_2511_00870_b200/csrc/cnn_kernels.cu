@@ -64,7 +64,13 @@ __host__ __device__ constexpr int mma_warps(int nl) { return nl < kMmaWarps ? nl
 __host__ __device__ constexpr int epi_groups(int nl) { return nl < kEpiGroups ? nl : kEpiGroups; }
 __host__ __device__ constexpr int epi0(int nl) { return kMma0 + mma_warps(nl); }
 __host__ __device__ constexpr int block_threads(int nl) { return 32 * (epi0(nl) + 4 * epi_groups(nl)); }
-constexpr int kRing = 4;                        // input-row ring slots per layer
+constexpr int kRing = 4;                        // input-row ring slots of layer 0 (one per producer warp)
+#ifndef PNPULA_RING_ACT
+#define PNPULA_RING_ACT 4
+#endif
+constexpr int kRingAct = PNPULA_RING_ACT;       // ring slots of the epilogue-fed layers l >= 1
+static_assert(kRingAct >= 3 && kRingAct <= 8, "input ring slots");
+__host__ __device__ constexpr uint32_t ring_slots(int l) { return l == 0 ? (uint32_t)kRing : (uint32_t)kRingAct; }
 constexpr int kAcc = 4;                         // accumulator-row slots per layer (TMEM)
 #ifndef PNPULA_LAG
 #define PNPULA_LAG 3
@@ -96,7 +102,7 @@ __host__ __device__ inline SmemLayout make_layout(int P, int nl, int first, int 
   for (int l = 0; l < nl; ++l) {
     L.slot_bytes[l] = (l == 0 && first) ? 2u * 128u * 16u : act_slot;
     L.ring_off[l] = off;
-    off = align_up(off + kRing * L.slot_bytes[l], 128);
+    off = align_up(off + ring_slots(l) * L.slot_bytes[l], 128);
   }
   for (int l = 0; l < nl; ++l) {
     const int cin = (l == 0 && first) ? 1 : P;
@@ -104,8 +110,8 @@ __host__ __device__ inline SmemLayout make_layout(int P, int nl, int first, int 
     L.w_off[l] = off;
     off = align_up(off + packed_layer_elems(cout, cin) * 2u, 128);
   }
-  L.bar_off = off;   // per layer: full[4], empty[4], tfull[4], tempty[4]
-  off = align_up(off + (uint32_t)nl * 16u * 8u, 128);
+  L.bar_off = off;   // per layer: full[8], empty[8], tfull[4], tempty[4]
+  off = align_up(off + (uint32_t)nl * 24u * 8u, 128);
   L.misc_off = off;  // tmem address, abort flag, drain barrier, per-layer table {ring, slot, w, 0},
                      // folded last layer's warp-edge exchange [2][4 warps][6] floats
   off += 16 + 16u * (uint32_t)nl + 192u;
@@ -298,10 +304,11 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t sbase = smem_u32(smem);
   const uint32_t bar0 = sbase + L.bar_off;
-  auto bar_full = [&](int l, uint32_t s) { return bar0 + (uint32_t)(l * 16 + s) * 8u; };
-  auto bar_empty = [&](int l, uint32_t s) { return bar0 + (uint32_t)(l * 16 + 4 + s) * 8u; };
-  auto bar_tfull = [&](int l, uint32_t s) { return bar0 + (uint32_t)(l * 16 + 8 + s) * 8u; };
-  auto bar_tempty = [&](int l, uint32_t s) { return bar0 + (uint32_t)(l * 16 + 12 + s) * 8u; };
+  // per layer: full[8], empty[8] (input ring), tfull[4], tempty[4] (accumulator ring)
+  auto bar_full = [&](int l, uint32_t s) { return bar0 + (uint32_t)(l * 24 + s) * 8u; };
+  auto bar_empty = [&](int l, uint32_t s) { return bar0 + (uint32_t)(l * 24 + 8 + s) * 8u; };
+  auto bar_tfull = [&](int l, uint32_t s) { return bar0 + (uint32_t)(l * 24 + 16 + s) * 8u; };
+  auto bar_tempty = [&](int l, uint32_t s) { return bar0 + (uint32_t)(l * 24 + 20 + s) * 8u; };
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + L.misc_off);
   volatile int *abort_flag = reinterpret_cast<volatile int *>(smem + L.misc_off + 4);
   const uint32_t bar_done = sbase + L.misc_off + 8;
@@ -321,17 +328,20 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
     uint4 *dst = reinterpret_cast<uint4 *>(smem + L.w_off[l]);
     for (uint32_t e = threadIdx.x; e < n16; e += kThreads) dst[e] = src[e];
     uint4 *r = reinterpret_cast<uint4 *>(smem + L.ring_off[l]);
-    const uint32_t nr = kRing * L.slot_bytes[l] / 16;
+    const uint32_t nr = ring_slots(l) * L.slot_bytes[l] / 16;
     for (uint32_t e = threadIdx.x; e < nr; e += kThreads) r[e] = make_uint4(0, 0, 0, 0);
   }
   if (threadIdx.x == 0) {
-    for (int l = 0; l < NL; ++l)
-      for (int s = 0; s < 4; ++s) {
+    for (int l = 0; l < NL; ++l) {
+      for (int s = 0; s < (int)ring_slots(l); ++s) {
         mbar_init(bar_full(l, s), (l == 0) ? 1 : 4);   // producer lane, or the 4 warps of one group
         mbar_init(bar_empty(l, s), 1);
+      }
+      for (int s = 0; s < kAcc; ++s) {
         mbar_init(bar_tfull(l, s), 1);
         mbar_init(bar_tempty(l, s), 4);
       }
+    }
     mbar_init(bar_done, kMmaWarps);
     *abort_flag = 0;
     uint4 *tab = reinterpret_cast<uint4 *>(smem + L.misc_off + 16);
@@ -486,7 +496,8 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
           const bool netlast = (l == NL - 1) && last && !im2col;
           const uint32_t Fg = Fcnt(l) + (uint32_t)f;
           trace_ev(p.trace, tr_on && lane == 0, 3, s, l);
-          ok = mbar_wait(bar_full(l, Fg & 3), (Fg >> 2) & 1, abort_flag, p.err, 2);
+          const uint32_t nring = ring_slots(l), rs = Fg % nring;
+          ok = mbar_wait(bar_full(l, rs), (Fg / nring) & 1, abort_flag, p.err, 2);
           trace_ev(p.trace, tr_on && lane == 0, 14, s, l);
           // output row that receives its first contribution (im2col: the only one)
           const uint32_t O0 = Ocnt(l);
@@ -502,7 +513,7 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
           const uint4 lt = ltab[l];
           const uint32_t acc0 = tmem_base + (uint32_t)(l * kAcc * P);
           const uint32_t wbase = sbase + lt.z;
-          const uint32_t slot = sbase + lt.x + (Fg & 3) * lt.y;
+          const uint32_t slot = sbase + lt.x + rs * lt.y;
           if (im2col) {
             const uint64_t ad = make_desc(slot, 2048, 128);
             const uint64_t bd = make_desc(wbase, (uint32_t)P * 16, 128);
@@ -551,7 +562,7 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
           }
           __syncwarp();
           if (elect_one()) {
-            mma_commit(bar_empty(l, Fg & 3));            // input row consumed
+            mma_commit(bar_empty(l, rs));                // input row consumed
             if (netlast) {
               mma_commit(bar_tfull(l, Fg & 1));          // this fill's tap sums
             } else {
@@ -666,10 +677,10 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
             if (lane == 0) mbar_arrive(bar_tempty(l, Ig & 3));
             if (l < NL - 1) {
               const uint32_t Fg = Fcnt(l + 1) + (uint32_t)ic;
-              if (Fg >= 4 && !mbar_wait(bar_empty(l + 1, Fg & 3), ((Fg >> 2) - 1) & 1, abort_flag, p.err, 5))
+              if (Fg >= kRingAct && !mbar_wait(bar_empty(l + 1, Fg % kRingAct), ((Fg / kRingAct) - 1) & 1, abort_flag, p.err, 5))
                 return false;
               __syncwarp();
-              if (lane == 0) mbar_arrive(bar_full(l + 1, Fg & 3));
+              if (lane == 0) mbar_arrive(bar_full(l + 1, Fg % kRingAct));
             }
             return true;
           }
@@ -719,17 +730,17 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
           if (l < NL - 1) {
             // next layer's input fill = this layer's output row index ic
             const uint32_t Fg = Fcnt(l + 1) + (uint32_t)ic;
-            if (Fg >= 4 && !mbar_wait(bar_empty(l + 1, Fg & 3), ((Fg >> 2) - 1) & 1, abort_flag, p.err, 5))
+            if (Fg >= kRingAct && !mbar_wait(bar_empty(l + 1, Fg % kRingAct), ((Fg / kRingAct) - 1) & 1, abort_flag, p.err, 5))
               return false;
             trace_ev(p.trace, trw, 9, s, l);
             const uint4 lt = ltab[l + 1];
-            uint8_t *slot = smem + lt.x + (Fg & 3) * lt.y + (m + 1) * 16;
+            uint8_t *slot = smem + lt.x + (Fg % kRingAct) * lt.y + (m + 1) * 16;
 #pragma unroll
             for (int gq = 0; gq < G; ++gq)
               *reinterpret_cast<uint4 *>(slot + gq * GS) = make_uint4(w[4 * gq], w[4 * gq + 1], w[4 * gq + 2], w[4 * gq + 3]);
             fence_proxy_async();
             __syncwarp();
-            if (lane == 0) mbar_arrive(bar_full(l + 1, Fg & 3));
+            if (lane == 0) mbar_arrive(bar_full(l + 1, Fg % kRingAct));
           } else if (col_valid) {
             // chunk output (activations for the next launch), valid columns only
 #pragma unroll
