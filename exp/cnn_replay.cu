@@ -119,9 +119,24 @@ __global__ void __launch_bounds__(512, 1) replay(int S, long long *out) {
           const uint32_t slot = sb + ringl + ((l - 1) * 4 + (f & 3)) * SLOT;
           const uint32_t wb = sb + wl + (l - 1) * 9 * P * P * 2;
           const int Ilo = f - 2;
+          const uint64_t ad0 = make_desc(slot, GS, 128), bd0 = make_desc(wb, 3u * P * 16u, 128);
+          if (SPLIT >= 2) {
+            // SPLIT 2: wrap steps as one N=128 MMA per (dx,ks) (zero block for the draining slot);
+            // SPLIT 3: same + one N=32 accumulate=0 MMA zeroing the fresh row's slot per step
+            const bool wrap = (Ilo & 3) >= 2;
+            if (SPLIT == 3) mma(acc0 + (f & 3) * P, ad0, bd0, make_idesc(P), 0);
+            const uint32_t d1 = wrap ? acc0 : acc0 + (Ilo & 3) * P, id1 = make_idesc(wrap ? 4 * P : 3 * P);
+#pragma unroll
+            for (int dx = 0; dx < 3; ++dx)
+#pragma unroll
+              for (int ks = 0; ks < KS; ++ks) {
+                const uint64_t ad = ad0 + (uint64_t)((2 * ks * GS + dx * 16) >> 4);
+                const uint64_t bd = bd0 + (uint64_t)((dx * KS + ks) * 3u * P * 2u);
+                mma(d1, ad, bd, id1, 1);
+              }
+          } else {
           const int n1 = SPLIT ? (4 - (Ilo & 3) < 3 ? 4 - (Ilo & 3) : 3) : 3;
           const int n2 = 3 - n1;
-          const uint64_t ad0 = make_desc(slot, GS, 128), bd0 = make_desc(wb, 3u * P * 16u, 128);
           const uint32_t d1 = acc0 + (SPLIT ? (Ilo & 3) * P : 0), id1 = make_idesc(n1 * P), id2 = make_idesc((n2 ? n2 : 1) * P);
 #pragma unroll
           for (int dx = 0; dx < 3; ++dx)
@@ -132,6 +147,7 @@ __global__ void __launch_bounds__(512, 1) replay(int S, long long *out) {
               mma(d1, ad, bd, id1, 1);
               if (n2 > 0) mma(acc0, ad, bd + (uint64_t)(n1 * P), id2, 1);
             }
+          }
         }
       }
       __syncwarp();
@@ -216,6 +232,8 @@ int main() {
   run<1, 1>("1 issuer, split at wrap");
   run<1, 0>("1 issuer, no split");
   run<2, 1>("4 warps elect+sync, split");
+  run<2, 2>("... wrap as N=128");
+  run<2, 3>("... wrap as N=128 + zero MMA");
   run<2, 1, 0, 1>("... random bf16 data");
   run<2, 1, 5>("... + sleeping waiters on commits");
   run<2, 1, 6>("... + sleeping waiters elsewhere");
