@@ -55,6 +55,7 @@ class _Config(C.Structure):
         ("tiles_y", C.c_int32), ("tiles_x", C.c_int32),
         ("i_off", C.c_int64), ("j_off", C.c_int64),
         ("eta", C.c_double), ("rho1", C.c_double), ("kappa1", C.c_double),
+        ("den_kind", C.c_int32), ("ddfb_gammas", C.c_void_p), ("ht_eps", C.c_double),
         ("tv_beta", C.c_double),
     ]
 
@@ -86,6 +87,10 @@ def _load():
         _lib.or_grad2d.argtypes = [vp, i32, i32, vp, vp]
         _lib.or_grad2d_adj.argtypes = [vp, vp, i32, i32, vp]
         _lib.or_prox_l21.argtypes = [d, d, d, C.POINTER(d), C.POINTER(d)]
+        _lib.or_ddfb_residual.argtypes = [vp, i32, i32, i32, i32, vp, vp, d, i32, vp]
+        _lib.or_ddfb_residual.restype = C.c_int
+        _lib.or_ddfb_param_count.argtypes = [i32, i32, i32]
+        _lib.or_ddfb_param_count.restype = i64
     return _lib
 
 
@@ -153,6 +158,22 @@ def dncnn_residual(x, weights, biases, n_layers: int, channels: int, bf16_emulat
     return G
 
 
+def ddfb_residual(x, weights, gammas, n_layers: int, channels: int, ht_eps: float, bf16_emulate: bool = False):
+    """G = v - D(v) for the DDFB denoiser (eq:ddfb_operator, eq:dfb_operator:T; readings R39-R42)."""
+    x = _f64(x)
+    w, g = _f32(weights), _f32(gammas)
+    G = np.zeros_like(x)
+    e = _load().or_ddfb_residual(x.ctypes.data, x.shape[0], x.shape[1], n_layers, channels, w.ctypes.data,
+                                 g.ctypes.data, ht_eps, int(bf16_emulate), G.ctypes.data)
+    if e:
+        raise ValueError("or_ddfb_residual failed")
+    return G
+
+
+def ddfb_param_count(n_layers: int, channels: int, image_channels: int) -> int:
+    return int(_load().or_ddfb_param_count(n_layers, channels, image_channels))
+
+
 def dncnn_param_count(n_layers: int, channels: int, image_channels: int) -> int:
     return int(_load().or_dncnn_param_count(n_layers, channels, image_channels))
 
@@ -216,6 +237,9 @@ class Problem:
     rho1: float = 0.0
     kappa1: float = 0.0
     tv_beta: float = 0.0                  # > 0: TV prior, z ~ D x (z = vertical, z1 = horizontal)
+    den_kind: str = "dncnn"               # "dncnn" | "ddfb"
+    ddfb_gammas: Optional[np.ndarray] = None
+    ht_eps: float = 0.0
     extra: dict = field(default_factory=dict)
 
 
@@ -248,9 +272,17 @@ def run(pb: Problem, n_iter: int, burn_in: int, seed: int, tiles=(1, 1), bf16_em
     cfg.y = y.ctypes.data
     cfg.sigma2 = pb.sigma2
     if pb.n_layers and pb.alpha != 0.0:
-        w, b = _f32(pb.weights), _f32(pb.biases)
-        keep += [w, b]
-        cfg.weights, cfg.biases = w.ctypes.data, b.ctypes.data
+        w = _f32(pb.weights)
+        keep.append(w)
+        cfg.weights = w.ctypes.data
+        if pb.den_kind == "ddfb":
+            gm = _f32(pb.ddfb_gammas)
+            keep.append(gm)
+            cfg.den_kind, cfg.ddfb_gammas, cfg.ht_eps = 1, gm.ctypes.data, pb.ht_eps
+        else:
+            b = _f32(pb.biases)
+            keep.append(b)
+            cfg.biases = b.ctypes.data
         cfg.n_layers, cfg.channels = pb.n_layers, pb.channels
     cfg.alpha, cfg.eps, cfg.bf16_emulate = pb.alpha, pb.eps, int(bf16_emulate)
     cfg.lam, cfg.c_lo, cfg.c_hi = pb.lam, pb.c_lo, pb.c_hi

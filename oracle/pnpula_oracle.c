@@ -25,6 +25,8 @@
  *                       z-update eq:sgs_pnp_ula_psgla:psgla, online moments
  *   or_run (tiles>1)    same chain, every tile computed from its own padded copy S_b x
  *                       (Def. prop:localselection P:135-152, ghost regions P:494-498)
+ *   or_ddfb_residual    DDFB denoiser G = v - D(v) (Example sec:denoiser:cnn:ddfb, eq:ddfb_operator
+ *                       P:382-385, eq:dfb_operator:T P:390-393), C = 1 (readings R39-R42)
  *   or_check_stepsizes  eq:stepsize_cond P:581-587 (reading R11: ||H2||^2 -> ||H2||^2/rho)
  *   or_prox_kl          prox of kappa KL(y || .) for the Poisson likelihood (eq:poisson:f2 P:737-741;
  *                       closed form = the positive root of u^2 - (v - kappa) u - kappa y = 0, reading R31)
@@ -221,6 +223,105 @@ int or_dncnn_residual(const double *x, int32_t ny, int32_t nx, int32_t n_layers,
 }
 
 /* ------------------------------------------------------------------ */
+/* DDFB (eq:ddfb_operator P:382-385, eq:dfb_operator:T P:390-393), C = 1 image channel, P features:
+ *   W_k : R^N -> R^{P x N},  (W_k v)_c[i,j] = sum_{u,v=-1..1} w_k[c][u+1][v+1] v[i+u][j+v]
+ *         (PyTorch conv2d cross-correlation, zero boundary; weights [P][1][3][3], reading R39)
+ *   W_k^*: its adjoint,     (W_k^* a)[i,j] = sum_c sum_{u,v} w_k[c][u+1][v+1] a_c[i-u][j-v]
+ *   T_k(u) = HT( u + gamma_k W_k proj_[0,1](v - W_k^* u) ),  HT = clamp to [-ht_eps, ht_eps] (R40)
+ *   D(v)   = proj_[0,1]( v - gamma_K W_K^* T_{K-1}( ... T_1( W_K v ) ) )
+ * Output G = v - D(v), so that the x-update's -G term is D(v) - v.
+ * bf16_emulate rounds at the GPU's points (R41): the conv weights as bf16(w_K) in u0 = W_K v,
+ * bf16(gamma_k w_k) in T_k, bf16(w_k) in W_k^* (k < K), bf16(gamma_K w_K) in the final adjoint;
+ * v and p at every W_k input; u after u0 and after every T_k.  Accumulation stays fp64. */
+static void or_ddfb_w(const double *v, int ny, int nx, int P, const float *w, double scale, int emul, double *out) {
+  int64_t npx = (int64_t)ny * nx;
+  for (int c = 0; c < P; c++)
+    for (int i = 0; i < ny; i++)
+      for (int j = 0; j < nx; j++) {
+        double s = 0.0;
+        for (int u = -1; u <= 1; u++)
+          for (int q = -1; q <= 1; q++) {
+            int ii = i + u, jj = j + q;
+            if (ii < 0 || ii >= ny || jj < 0 || jj >= nx) continue;
+            double wt = scale * (double)w[(c * 3 + (u + 1)) * 3 + (q + 1)];
+            if (emul) wt = or_bf16(wt);
+            double a = v[(int64_t)ii * nx + jj];
+            if (emul) a = or_bf16(a);
+            s += wt * a;
+          }
+        out[(int64_t)c * npx + (int64_t)i * nx + j] = s;
+      }
+}
+
+static void or_ddfb_wadj(const double *a, int ny, int nx, int P, const float *w, double scale, int emul, double *out) {
+  int64_t npx = (int64_t)ny * nx;
+  for (int i = 0; i < ny; i++)
+    for (int j = 0; j < nx; j++) {
+      double s = 0.0;
+      for (int c = 0; c < P; c++)
+        for (int u = -1; u <= 1; u++)
+          for (int q = -1; q <= 1; q++) {
+            int ii = i - u, jj = j - q;
+            if (ii < 0 || ii >= ny || jj < 0 || jj >= nx) continue;
+            double wt = scale * (double)w[(c * 3 + (u + 1)) * 3 + (q + 1)];
+            if (emul) wt = or_bf16(wt);
+            s += wt * a[(int64_t)c * npx + (int64_t)ii * nx + jj];
+          }
+      out[(int64_t)i * nx + j] = s;
+    }
+}
+
+int64_t or_ddfb_param_count(int32_t K, int32_t P, int32_t C) { return (int64_t)K * P * C * 9; }
+
+/* in != NULL: only pixels with in[n] != 0 belong to the image (a worker's padded crop, reading
+ * R8): u and p are zero elsewhere, exactly as the global image's zero boundary. */
+static int or_ddfb_masked(const double *v, int32_t ny, int32_t nx, int32_t K, int32_t P, const float *weights,
+                          const float *gammas, double ht_eps, int32_t emul, const uint8_t *in, double *G) {
+  if (K < 1 || P < 1) return OR_E_INVALID;
+  int64_t npx = (int64_t)ny * nx;
+  double *u = (double *)calloc((size_t)(npx * P), sizeof(double));
+  double *t = (double *)calloc((size_t)(npx * P), sizeof(double));
+  double *a = (double *)calloc((size_t)npx, sizeof(double));
+  double *pp = (double *)calloc((size_t)npx, sizeof(double));
+  if (!u || !t || !a || !pp) { free(u); free(t); free(a); free(pp); return OR_E_INVALID; }
+  const float *wK = weights + (int64_t)(K - 1) * P * 9;
+  or_ddfb_w(v, ny, nx, P, wK, 1.0, emul, u);                      /* u0 = W_K v */
+  for (int64_t n = 0; n < npx * P; n++) {
+    if (emul) u[n] = or_bf16(u[n]);
+    if (in && !in[n % npx]) u[n] = 0.0;
+  }
+  for (int k = 1; k <= K - 1; k++) {                               /* u <- T_k(u) */
+    const float *wk = weights + (int64_t)(k - 1) * P * 9;
+    or_ddfb_wadj(u, ny, nx, P, wk, 1.0, emul, a);
+    for (int64_t n = 0; n < npx; n++) {
+      double q = v[n] - a[n];
+      pp[n] = q < 0.0 ? 0.0 : (q > 1.0 ? 1.0 : q);                 /* proj_[0,1] */
+      if (in && !in[n]) pp[n] = 0.0;
+    }
+    or_ddfb_w(pp, ny, nx, P, wk, (double)gammas[k - 1], emul, t);
+    for (int64_t n = 0; n < npx * P; n++) {
+      double q = u[n] + t[n];
+      q = q < -ht_eps ? -ht_eps : (q > ht_eps ? ht_eps : q);      /* HT_eps */
+      u[n] = emul ? or_bf16(q) : q;
+      if (in && !in[n % npx]) u[n] = 0.0;
+    }
+  }
+  or_ddfb_wadj(u, ny, nx, P, wK, (double)gammas[K - 1], emul, a);  /* gamma_K W_K^* u */
+  for (int64_t n = 0; n < npx; n++) {
+    double q = v[n] - a[n];
+    double d = q < 0.0 ? 0.0 : (q > 1.0 ? 1.0 : q);
+    G[n] = v[n] - d;
+  }
+  free(u); free(t); free(a); free(pp);
+  return OR_OK;
+}
+
+int or_ddfb_residual(const double *v, int32_t ny, int32_t nx, int32_t K, int32_t P, const float *weights,
+                     const float *gammas, double ht_eps, int32_t emul, double *G) {
+  return or_ddfb_masked(v, ny, nx, K, P, weights, gammas, ht_eps, emul, NULL, G);
+}
+
+/* ------------------------------------------------------------------ */
 /* Step-size conditions eq:stepsize_cond, with ||H2||^2 read as
  * ||H2||^2/rho (reading R11).  Returns bit 0 set if the first inequality fails,
  * bit 1 if the second fails.  h2_over_rho = ||H2||^2/rho (0 when AXDA is off). */
@@ -309,6 +410,10 @@ typedef struct {
                                     the noise is indexed by global pixel (reading R9), so a crop
                                     of a larger image draws the same xi/zeta at the same pixel */
   double eta, rho1, kappa1;      /* op = 2: Poisson scale and the z1 block's coupling / step */
+  int32_t den_kind;              /* 0 = DnCNN (weights/biases), 1 = DDFB (weights [K][P][1][3][3],
+                                    ddfb_gammas[K], ht_eps; biases unused) */
+  const float *ddfb_gammas;
+  double ht_eps;
   double tv_beta;                /* > 0: TV prior: the z block is z ~ D x (two
                                     components) with f2 = tv_beta ||.||_{2,1} and x moves by PSGLA
                                     with p = 1_{R+}; requires rho > 0, no CNN, no box term */
@@ -349,8 +454,11 @@ static int or_step_global(const or_config *c, const double *k, const double *yd,
   /* line 8: D_eps(x) - x = -G_eps(x) */
   int use_cnn = c->n_layers > 0 && c->alpha != 0.0;
   if (use_cnn) {
-    int e = or_dncnn_residual(x, ny, nx, c->n_layers, c->channels, c->weights, c->biases,
-                              c->bf16_emulate, G);
+    int e = c->den_kind == 1
+                ? or_ddfb_residual(x, ny, nx, c->n_layers, c->channels, c->weights, c->ddfb_gammas, c->ht_eps,
+                                   c->bf16_emulate, G)
+                : or_dncnn_residual(x, ny, nx, c->n_layers, c->channels, c->weights, c->biases,
+                                    c->bf16_emulate, G);
     if (e) return e;
   }
   double sq2g = sqrt(2.0 * c->gamma);
@@ -437,7 +545,8 @@ static int or_step_tiled(const or_config *c, const double *k, const double *yd, 
   int ry = c->kh / 2, rx = c->kw / 2;
   int use_cnn = c->n_layers > 0 && c->alpha != 0.0;
   int hr = (c->op != 1) ? 2 * (ry > rx ? ry : rx) : 0;
-  int h = use_cnn && c->n_layers > hr ? c->n_layers : hr;
+  int rf = use_cnn ? (c->den_kind == 1 ? 2 * c->n_layers : c->n_layers) : 0;   /* DDFB: 2 convs per layer */
+  int h = rf > hr ? rf : hr;
   if (c->tv_beta > 0.0 && h < 2) h = 2;   /* D^T D x needs x at distance 1; z on tile (+) 1 needs 2 */
   for (int ty = 0; ty < c->tiles_y; ty++)
     for (int tx = 0; tx < c->tiles_x; tx++) {
@@ -497,7 +606,24 @@ static int or_step_tiled(const or_config *c, const double *k, const double *yd, 
       }
       for (int64_t n = 0; n < (int64_t)th * tw; n++)
         gl[n] = c->op == 2 ? c->eta * gl[n] / c->rho1 : gl[n] / c->sigma2;
-      if (use_cnn) {
+      if (use_cnn && c->den_kind == 1) {
+        /* DDFB on the worker's padded crop with the image mask; tile pixels are >= 2K from the
+         * crop edge, so they see exactly the global computation */
+        uint8_t *inm = (uint8_t *)calloc((size_t)ph * pw, 1);
+        double *Gp = (double *)calloc((size_t)ph * pw, sizeof(double));
+        if (!inm || !Gp) { free(inm); free(Gp); free(xp); free(rp); free(gl); free(Gl); return OR_E_INVALID; }
+        for (int a = 0; a < ph; a++)
+          for (int b = 0; b < pw; b++) {
+            int64_t gi = i0 - h + a, gj = j0 - h + b;
+            inm[(int64_t)a * pw + b] = (gi >= 0 && gi < ny && gj >= 0 && gj < nx) ? 1 : 0;
+          }
+        int e = or_ddfb_masked(xp, ph, pw, c->n_layers, c->channels, c->weights, c->ddfb_gammas, c->ht_eps,
+                               c->bf16_emulate, inm, Gp);
+        for (int a = 0; a < th; a++)
+          for (int b = 0; b < tw; b++) Gl[(int64_t)a * tw + b] = Gp[(int64_t)(a + h) * pw + (b + h)];
+        free(inm); free(Gp);
+        if (e) { free(xp); free(rp); free(gl); free(Gl); return e; }
+      } else if (use_cnn) {
         /* receptive-field strategy: layer k is evaluated on tile (+) (K-k),
          * activations outside the image are zero at every layer input (reading R8). */
         int K = c->n_layers, P = c->channels;

@@ -165,6 +165,10 @@ def test_dncnn_linear_construction():
 
 def test_param_counts_table1():
     for row in _rows("dncnn_param_counts.txt"):
+        if row[0] == "ddfb":
+            K, F, C, n = map(int, row[1:])
+            assert oracle.ddfb_param_count(K, F, C) == n
+            continue
         K, F, C, n = map(int, row)
         assert oracle.dncnn_param_count(K, F, C) == n
     w, b = synth.dncnn_weights(8, 32)
