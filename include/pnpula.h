@@ -81,13 +81,23 @@ typedef struct {
   int32_t i0, j0, h, w; /* rectangle of global pixel coordinates: rows [i0, i0+h), cols [j0, j0+w) */
 } pnpula_rect;
 
-/* DnCNN-style denoiser weights, fp32, copied at create and stored as bf16. */
+enum { PNPULA_DEN_DNCNN = 0, PNPULA_DEN_DDFB = 1 };
+
+/* Denoiser weights, fp32, copied at create and stored as bf16.
+ * PNPULA_DEN_DNCNN: DnCNN-style, D = Id - G.
+ * PNPULA_DEN_DDFB (Example sec:denoiser:cnn:ddfb P:378-395; R39-R42): unrolled dual
+ *   forward-backward, D(v) = proj_[0,1](v - gamma_K W_K^* T_{K-1}(...T_1(W_K v))), T_k(u) =
+ *   HT(u + gamma_k W_k proj_[0,1](v - W_k^* u)), HT = clamp to [-ht_eps, ht_eps]. */
 typedef struct {
-  int32_t n_layers;      /* K >= 2 */
+  int32_t n_layers;      /* K >= 2 (DnCNN), >= 1 (DDFB) */
   int32_t channels;      /* P, one of 16, 32, 64 */
-  const float *weights;  /* host; OIHW per layer, layers concatenated:
-                            [P][1][3][3], (K-2) x [P][P][3][3], [1][P][3][3] */
-  const float *biases;   /* host; P per layer for layers 1..K-1, then 1 */
+  const float *weights;  /* host; DnCNN: OIHW per layer, layers concatenated:
+                            [P][1][3][3], (K-2) x [P][P][3][3], [1][P][3][3];
+                            DDFB: K x [P][1][3][3] (W_k : 1 -> P, PyTorch conv2d convention) */
+  const float *biases;   /* host; DnCNN: P per layer for layers 1..K-1, then 1; DDFB: unused */
+  int32_t kind;          /* PNPULA_DEN_DNCNN (0) or PNPULA_DEN_DDFB */
+  const float *ddfb_gammas;  /* DDFB: K steps gamma_k in (0, 2/||W_k||^2) */
+  double ht_eps;         /* DDFB: hard-tanh level > 0 */
 } pnpula_denoiser;
 
 typedef struct {

@@ -34,9 +34,13 @@ class Rect(C.Structure):
         return (self.i0, self.j0, self.h, self.w)
 
 
+DEN_DNCNN, DEN_DDFB = 0, 1
+
+
 class Denoiser(C.Structure):
     _fields_ = [("n_layers", C.c_int32), ("channels", C.c_int32),
-                ("weights", C.c_void_p), ("biases", C.c_void_p)]
+                ("weights", C.c_void_p), ("biases", C.c_void_p),
+                ("kind", C.c_int32), ("ddfb_gammas", C.c_void_p), ("ht_eps", C.c_double)]
 
 
 class Config(C.Structure):

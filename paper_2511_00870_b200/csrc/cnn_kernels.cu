@@ -652,7 +652,16 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
           if (ic >= 0 && ic < nout(l) && col_valid) {
             const int o = r_lo - (NL - 1 - l) + ic;
             const TileGeom &g = p.gg;
-            p.G[(int64_t)(o - (g.i0 - g.h)) * g.pitch + (cm - (g.j0 - g.hx))] = row_done + p.bias[l][0];
+            const int64_t gidx = (int64_t)(o - (g.i0 - g.h)) * g.pitch + (cm - (g.j0 - g.hx));
+            if (NL != 1 || p.mode < 2) {   // DDFB modes only exist for single-operator launches
+              p.G[gidx] = row_done + p.bias[l][0];
+            } else if (o >= 0 && o < p.ny && cm >= 0 && cm < p.nx) {
+              // DDFB adjoint step (R39): q = proj_[0,1](v - W_k^* u); final: G = v - q
+              const TileGeom &xg = p.xg;
+              const float v = p.x[(int64_t)(o - (xg.i0 - xg.h)) * xg.pitch + (cm - (xg.j0 - xg.hx))];
+              const float q = fminf(fmaxf(v - row_done, 0.f), 1.f);
+              p.G[gidx] = p.mode == 4 ? v - q : q;
+            }
           }
           trace_ev(p.trace, trw, 8, s, l);
           return true;
@@ -704,6 +713,37 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
           }
           const uint32_t ta = taddr + (Ig & 3) * (uint32_t)P;
           uint32_t w[P / 2];
+          if (NL == 1 && (p.mode == 1 || p.mode == 3)) {
+            // DDFB im2col layers (R39, R40): mode 1 u0 = W_K v (no bias, no activation);
+            // mode 3 u' = HT(u + gamma_k W_k p) with u read (bf16) at the same pixel
+            uint32_t uin[P / 2];
+            if (p.mode == 3) {
+              const int64_t ab = ((int64_t)(o - p.a_i0) * p.a_cols + (cm - p.a_j0)) * 8;
+#pragma unroll
+              for (int gq = 0; gq < G; ++gq) {
+                const uint4 t = inside ? *reinterpret_cast<const uint4 *>(p.ain + (int64_t)gq * p.a_rows * p.a_cols * 8 + ab)
+                                       : make_uint4(0, 0, 0, 0);
+                uin[4 * gq] = t.x; uin[4 * gq + 1] = t.y; uin[4 * gq + 2] = t.z; uin[4 * gq + 3] = t.w;
+              }
+            }
+            const float ht = p.ht_eps;
+#pragma unroll
+            for (int h = 0; h < P; h += 16) {
+              float v[16];
+              tmem_load<16>(ta + h, v);
+              tmem_wait_ld();
+#pragma unroll
+              for (int c = 0; c < 16; c += 2) {
+                float a0 = v[c], a1 = v[c + 1];
+                if (p.mode == 3) {
+                  const uint32_t pr = uin[(h + c) / 2];
+                  a0 = fminf(fmaxf(__uint_as_float(pr << 16) + a0, -ht), ht);
+                  a1 = fminf(fmaxf(__uint_as_float(pr & 0xffff0000u) + a1, -ht), ht);
+                }
+                w[(h + c) / 2] = pack_bf16(inside ? a0 : 0.f, inside ? a1 : 0.f);
+              }
+            }
+          } else {
           // 16 channels at a time (tcgen05.ld -> +bias, ReLU -> bf16 pairs): keeps at most 16
           // accumulator values live next to the bias registers
 #pragma unroll
@@ -717,6 +757,7 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
               w[(h + c) / 2] = pack_bf16(inside ? fmaxf(v[c] + b4.x, 0.f) : 0.f, inside ? fmaxf(v[c + 1] + b4.y, 0.f) : 0.f);
               w[(h + c) / 2 + 1] = pack_bf16(inside ? fmaxf(v[c + 2] + b4.z, 0.f) : 0.f, inside ? fmaxf(v[c + 3] + b4.w, 0.f) : 0.f);
             }
+          }
           }
           if (!im2col) {       // im2col MMAs overwrite (accumulate = 0): no re-zeroing needed
 #pragma unroll

@@ -117,6 +117,9 @@ struct CnnChunkParams {
   int units;             // strips * row blocks
   int *err;              // device error flag (watchdog)
   unsigned long long *trace;   // optional pipeline trace (CTA 0, first unit): [0] = count, then records
+  int mode;              // 0 DnCNN; DDFB (R39-R42): 1 u0 = W_K v, 2 p = proj(v - W^* u), 3 u = HT(u + gamma W p),
+                         // 4 G = v - proj(v - gamma_K W_K^* u)
+  float ht_eps;          // DDFB hard-tanh level
 };
 
 // Launchers (return cudaGetLastError()).

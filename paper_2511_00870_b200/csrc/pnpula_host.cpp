@@ -44,6 +44,7 @@ struct TileDev {
   uint8_t *mask = nullptr;
   float *z = nullptr, *mean = nullptr, *m2 = nullptr, *G = nullptr;
   float *z1 = nullptr;     // OP_POISSON: z1 block, valid on tile (+) r_H (reading R33)
+  float *pbuf = nullptr;   // DDFB: p = proj(v - W_k^* u), fp32 padded geometry, zero outside the image
   uint16_t *act[2] = {nullptr, nullptr};   // inter-chunk activations
 };
 
@@ -72,6 +73,12 @@ struct pnpula_ctx {
   double tv_beta = 0;                     // > 0: TV prior (z = (z_v, z_h) ~ D x in td.z, td.z1)
   int flags = 0;
   int n_layers = 0, channels = 0;   // 0 layers = no CNN
+  int den_kind = 0;                 // PNPULA_DEN_DNCNN / PNPULA_DEN_DDFB
+  double ht_eps = 0;
+  // DDFB operator images (R39-R42): W_K (im2col) for u0, gamma_k W_k (im2col) for T_k,
+  // flipped W_k (folded P -> 1) for W_k^*, flipped gamma_K W_K for the final adjoint
+  uint16_t *ddfb_u0 = nullptr, *ddfb_fin = nullptr;
+  std::vector<uint16_t *> ddfb_t, ddfb_adj;
   int h = 0;
 
   cudaStream_t stream = nullptr;
@@ -204,7 +211,82 @@ pnpula_status upload_padded(pnpula_ctx *c, T *dst, const TileGeom &g, const T *h
   return PNPULA_OK;
 }
 
+// DDFB (R39-R42): 2K single-operator launches per tile on shrinking regions tile (+) e:
+//   u0 = W_K v (e = 2K-1); for k < K: p = proj(v - W_k^* u) (e = 2K-2k), u = HT(u + gamma_k W_k p)
+//   (e = 2K-2k-1); G = v - proj(v - gamma_K W_K^* u) (e = 0).
+pnpula_status run_ddfb(pnpula_ctx *c, int buf) {
+  const int K = c->n_layers, P = c->channels;
+  for (auto &td : c->tiles) {
+    const TileGeom &g = td.g;
+    int cur = 0;   // act buffer holding the current u
+    auto base = [&](int mode, int ext) {
+      CnnChunkParams p{};
+      p.P = P;
+      p.nl = 1;
+      p.mode = mode;
+      p.ht_eps = (float)c->ht_eps;
+      p.x = td.x[buf];
+      p.xg = g;
+      p.oi0 = g.i0 - ext; p.oj0 = g.j0 - ext;
+      p.oh = g.th + 2 * ext; p.ow = g.tw + 2 * ext;
+      p.ny = c->ny; p.nx = c->nx;
+      p.err = c->d_err;
+      return p;
+    };
+    auto set_ain = [&](CnnChunkParams &p, int ext) {   // u on tile (+) ext
+      p.ain = td.act[cur];
+      p.a_i0 = g.i0 - ext; p.a_j0 = g.j0 - ext;
+      p.a_rows = g.th + 2 * ext; p.a_cols = g.tw + 2 * ext;
+    };
+    auto set_aout = [&](CnnChunkParams &p, int b) {
+      p.aout = td.act[b];
+      p.o_i0 = p.oi0; p.o_j0 = p.oj0; p.o_rows = p.oh; p.o_cols = p.ow;
+    };
+    auto launch = [&](const CnnChunkParams &p) -> pnpula_status {
+      cudaEvent_t end;
+      timer_begin(c, c->tm_cnn, &end);
+      CU(c, launch_cnn_chunk(p, c->num_sms, c->stream));
+      c->n_launches++;
+      timer_end(c, end);
+      return PNPULA_OK;
+    };
+    pnpula_status s;
+    {   // u0 = W_K v on tile (+) 2K-1
+      CnnChunkParams p = base(1, 2 * K - 1);
+      p.first_is_input = 1;
+      p.w[0] = c->ddfb_u0;
+      set_aout(p, cur);
+      if ((s = launch(p))) return s;
+    }
+    for (int k = 1; k < K; ++k) {
+      const int eu = 2 * K - 2 * k + 1;   // u lives on tile (+) eu
+      CnnChunkParams pa = base(2, eu - 1);   // p = proj(v - W_k^* u)
+      pa.last_is_output = 1;
+      pa.w[0] = c->ddfb_adj[k - 1];
+      set_ain(pa, eu);
+      pa.G = td.pbuf; pa.gg = g;
+      if ((s = launch(pa))) return s;
+      CnnChunkParams pt = base(3, eu - 2);   // u = HT(u + gamma_k W_k p)
+      pt.first_is_input = 1;
+      pt.x = td.pbuf;                        // im2col input = p (the v it needs came through p)
+      pt.w[0] = c->ddfb_t[k - 1];
+      set_ain(pt, eu);
+      set_aout(pt, cur ^ 1);
+      if ((s = launch(pt))) return s;
+      cur ^= 1;
+    }
+    CnnChunkParams pf = base(4, 0);          // G = v - proj(v - gamma_K W_K^* u)
+    pf.last_is_output = 1;
+    pf.w[0] = c->ddfb_fin;
+    set_ain(pf, 1);
+    pf.G = td.G; pf.gg = g;
+    if ((s = launch(pf))) return s;
+  }
+  return PNPULA_OK;
+}
+
 pnpula_status run_cnn(pnpula_ctx *c, int buf) {
+  if (c->den_kind == PNPULA_DEN_DDFB) return run_ddfb(c, buf);
   for (auto &td : c->tiles) {
     for (size_t ci = 0; ci < c->chunks.size(); ++ci) {
       const CnnChunk &ch = c->chunks[ci];
@@ -605,7 +687,12 @@ pnpula_status pnpula_create(const pnpula_config *cfg, pnpula_ctx **out) {
   if (tv && (poisson || !(f.rho > 0) || use_cnn || f.lambda > 0)) {
     set_error("TV prior needs OP_CONV/OP_MASK, rho > 0, no denoiser and lambda <= 0"); return PNPULA_E_INVALID_ARG;
   }
-  if (use_cnn) {
+  const bool ddfb = use_cnn && f.den->kind == PNPULA_DEN_DDFB;
+  if (use_cnn && f.den->kind != PNPULA_DEN_DNCNN && !ddfb) { set_error("unknown denoiser kind"); return PNPULA_E_INVALID_ARG; }
+  if (ddfb && (f.den->n_layers < 1 || !f.den->weights || !f.den->ddfb_gammas || !(f.den->ht_eps > 0))) {
+    set_error("DDFB needs >= 1 layer, weights, gammas and ht_eps > 0"); return PNPULA_E_INVALID_ARG;
+  }
+  if (use_cnn && !ddfb) {
     if (f.den->n_layers < 2 || !f.den->weights || !f.den->biases) { set_error("denoiser needs >= 2 layers and weights"); return PNPULA_E_INVALID_ARG; }
     if (f.den->channels != 16 && f.den->channels != 32 && f.den->channels != 64) {
       set_error("denoiser channels must be 16, 32 or 64"); return PNPULA_E_UNSUPPORTED;
@@ -634,7 +721,9 @@ pnpula_status pnpula_create(const pnpula_config *cfg, pnpula_ctx **out) {
     }
   }
   if (use_cnn) { c->n_layers = f.den->n_layers; c->channels = f.den->channels; }
-  c->h = pnpula_halo_width(f.op, f.kh, f.kw, c->n_layers);
+  if (ddfb) { c->den_kind = PNPULA_DEN_DDFB; c->ht_eps = f.den->ht_eps; }
+  // receptive field of the prior: K 3x3 layers (DnCNN), or two 3x3 operators per DDFB layer
+  c->h = pnpula_halo_width(f.op, f.kh, f.kw, ddfb ? 2 * c->n_layers : c->n_layers);
   if (tv) c->h = std::max(c->h, 2);   // D^T D x needs x at distance 1, z on tile (+) 1 needs 2 (R38)
   c->ntiles = ntiles;
   c->n_local = ntiles / f.world_size;
@@ -780,8 +869,57 @@ pnpula_status pnpula_create(const pnpula_config *cfg, pnpula_ctx **out) {
       if (s) return bail(s);
     }
   }
+  // DDFB operator images and buffers
+  if (ddfb) {
+    const int K = c->n_layers, P = c->channels;
+    auto upload = [&](const std::vector<float> &wt, int cout, int cin, uint16_t **dst) -> pnpula_status {
+      std::vector<uint16_t> packed(cnn_packed_layer_elems(cout, cin));
+      cnn_pack_layer(wt.data(), cout, cin, packed.data());
+      cudaError_t e2 = cudaMalloc(dst, packed.size() * sizeof(uint16_t));
+      if (e2 == cudaSuccess) e2 = cudaMemcpy(*dst, packed.data(), packed.size() * sizeof(uint16_t), cudaMemcpyHostToDevice);
+      if (e2 != cudaSuccess) { fail_cuda(nullptr, e2, "DDFB weights", __LINE__); return PNPULA_E_CUDA; }
+      return PNPULA_OK;
+    };
+    // W_k as a 1 -> P conv [P][1][3][3] (scaled), and W_k^* as a P -> 1 conv [1][P][3][3]:
+    // w'[0][c][a][b] = s * w_k[c][0][2-a][2-b] (the adjoint of a cross-correlation)
+    auto wk = [&](int k, double sc) {
+      std::vector<float> o((size_t)P * 9);
+      for (size_t i = 0; i < o.size(); ++i) o[i] = (float)(sc * f.den->weights[(size_t)(k - 1) * P * 9 + i]);
+      return o;
+    };
+    auto wadj = [&](int k, double sc) {
+      std::vector<float> o((size_t)P * 9);
+      for (int ch = 0; ch < P; ++ch)
+        for (int a = 0; a < 3; ++a)
+          for (int b = 0; b < 3; ++b)
+            o[((size_t)ch * 3 + a) * 3 + b] = (float)(sc * f.den->weights[(size_t)(k - 1) * P * 9 + ((size_t)ch * 3 + (2 - a)) * 3 + (2 - b)]);
+      return o;
+    };
+    pnpula_status s = upload(wk(K, 1.0), P, 1, &c->ddfb_u0);
+    if (s) return bail(s);
+    for (int k = 1; k < K; ++k) {
+      uint16_t *t = nullptr, *a = nullptr;
+      s = upload(wk(k, f.den->ddfb_gammas[k - 1]), P, 1, &t);
+      if (!s) s = upload(wadj(k, 1.0), 1, P, &a);
+      c->ddfb_t.push_back(t);
+      c->ddfb_adj.push_back(a);
+      if (s) return bail(s);
+    }
+    s = upload(wadj(K, f.den->ddfb_gammas[K - 1]), 1, P, &c->ddfb_fin);
+    if (s) return bail(s);
+    for (auto &td : c->tiles) {
+      const size_t n = geom_elems(td.g);
+      CUB(cudaMalloc(&td.pbuf, n * sizeof(float)));
+      CUB(cudaMemsetAsync(td.pbuf, 0, n * sizeof(float), c->stream));
+      const size_t act = (size_t)(td.g.th + 2 * (2 * K - 1)) * (td.g.tw + 2 * (2 * K - 1)) * P;
+      for (int b2 = 0; b2 < 2; ++b2) {
+        CUB(cudaMalloc(&td.act[b2], act * sizeof(uint16_t)));
+        CUB(cudaMemsetAsync(td.act[b2], 0, act * sizeof(uint16_t), c->stream));
+      }
+    }
+  }
   // CNN weights
-  if (c->n_layers > 0) {
+  if (c->n_layers > 0 && !ddfb) {
     plan_cnn_chunks(c);
     const int K = c->n_layers, P = c->channels;
     const float *w = f.den->weights;
@@ -1219,11 +1357,14 @@ pnpula_status pnpula_destroy(pnpula_ctx *c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (auto &td : c->tiles) {
     cudaFree(td.x[0]); cudaFree(td.x[1]); cudaFree(td.x0); cudaFree(td.y); cudaFree(td.mask);
-    cudaFree(td.z); cudaFree(td.z1); cudaFree(td.mean); cudaFree(td.m2); cudaFree(td.G);
+    cudaFree(td.z); cudaFree(td.z1); cudaFree(td.mean); cudaFree(td.m2); cudaFree(td.G); cudaFree(td.pbuf);
     cudaFree(td.act[0]); cudaFree(td.act[1]);
   }
   for (auto p : c->d_w) cudaFree(p);
   for (auto p : c->d_b) cudaFree(p);
+  cudaFree(c->ddfb_u0); cudaFree(c->ddfb_fin);
+  for (auto p : c->ddfb_t) cudaFree(p);
+  for (auto p : c->ddfb_adj) cudaFree(p);
   for (int b = 0; b < 2; ++b) {
     cudaFree(c->d_local_jobs[b]); cudaFree(c->d_pack_jobs[b]); cudaFree(c->d_unpack_jobs[b]);
   }

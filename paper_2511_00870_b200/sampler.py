@@ -27,7 +27,8 @@ class Sampler:
                  x0: Optional[np.ndarray] = None, in_rect=None, tiles=(1, 1),
                  rank: int = 0, world_size: int = 1, device: int = 0, nccl_uid: Optional[bytes] = None,
                  stream: int = 0, flags: int = 0, lipschitz_L: float = 0.0, lipschitz_LD: float = 0.0,
-                 eta: float = 0.0, rho1: float = 0.0, kappa1: float = 0.0, tv_beta: float = 0.0):
+                 eta: float = 0.0, rho1: float = 0.0, kappa1: float = 0.0, tv_beta: float = 0.0,
+                 den_kind: str = "dncnn", ddfb_gammas: Optional[np.ndarray] = None, ht_eps: float = 0.0):
         lib = L.load()
         keep = []
         cfg = L.Config()
@@ -68,9 +69,16 @@ class Sampler:
             raise ValueError(f"y has shape {yy.shape}, in_rect is {r}")
         cfg.sigma2 = sigma2
         if n_layers and alpha != 0.0:
-            w, b = _f32(weights), _f32(biases)
-            keep += [w, b]
-            den = L.Denoiser(n_layers, channels, w.ctypes.data, b.ctypes.data)
+            w = _f32(weights)
+            keep.append(w)
+            if den_kind == "ddfb":
+                gm = _f32(ddfb_gammas)
+                keep.append(gm)
+                den = L.Denoiser(n_layers, channels, w.ctypes.data, None, L.DEN_DDFB, gm.ctypes.data, ht_eps)
+            else:
+                b = _f32(biases)
+                keep.append(b)
+                den = L.Denoiser(n_layers, channels, w.ctypes.data, b.ctypes.data, L.DEN_DNCNN, None, 0.0)
             keep.append(den)
             cfg.den = C.pointer(den)
         cfg.alpha, cfg.eps = alpha, eps
