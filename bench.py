@@ -42,7 +42,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=60)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--workload", default="c5", choices=["c5", "c2", "c3", "c4", "c1", "p5", "t5"])
+    ap.add_argument("--workload", default="c5", choices=["c5", "c2", "c3", "c4", "c1", "p5", "t5", "d5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -66,6 +66,12 @@ def workload(name, n):
         return dict(name="p5", desc="weak scaling as c5, Poisson deconvolution (eta = 250, 9x9 Gaussian), "
                     "AXDA z1 ~ eta H x (KL prox) + z2 ~ x (R+), DnCNN-lite 8x32", ny=ny, nx=nx, tiles=(n, 1),
                     op="poisson", L=9, sb=2.0, cnn=(8, 32), z=True, scaling="weak")
+    if name == "d5":
+        shapes = {1: (4096, 8192), 2: (8192, 8192), 4: (8192, 16384), 8: (16384, 16384)}
+        ny, nx = shapes.get(n, (4096 * n, 8192))
+        return dict(name="d5", desc="weak scaling as c5, 9x9 Gaussian deblur 25 dB with the DDFB prior "
+                    "(K = 4, F = 64, the paper's light denoiser)", ny=ny, nx=nx, tiles=(n, 1), op="conv", L=9,
+                    sb=2.0, cnn=(4, 64), ddfb=True, z=False, scaling="weak")
     if name == "t5":
         shapes = {1: (4096, 8192), 2: (8192, 8192), 4: (8192, 16384), 8: (16384, 16384)}
         ny, nx = shapes.get(n, (4096 * n, 8192))
@@ -133,7 +139,12 @@ def build_inputs(wl, rect, pinned=False):
         kw.update(lam=hp["lam"], c_lo=0.0, c_hi=1.0)
         if wl["z"]:
             kw.update(rho=hp["rho"], kappa=hp["kappa"], z_lo=0.0, z_hi=1.0)
-    if wl["cnn"]:
+    if wl["cnn"] and wl.get("ddfb"):
+        K, P = wl["cnn"]
+        w, g, ht = synth.ddfb_weights(K, P)
+        kw.update(weights=w, n_layers=K, channels=P, alpha=1.0, eps=float(np.sqrt(s2)), den_kind="ddfb",
+                  ddfb_gammas=g, ht_eps=ht)
+    elif wl["cnn"]:
         K, P = wl["cnn"]
         w, b = synth.dncnn_weights(K, P)
         kw.update(weights=w, biases=b, n_layers=K, channels=P, alpha=1.0, eps=float(np.sqrt(s2)))
@@ -227,7 +238,8 @@ def oracle_crop_problem(wl, size):
     kw = build_inputs(wl, (i0, j0, size, size))
     okw = {k: v for k, v in kw.items() if k in ("sigma2", "gamma", "mask", "weights", "biases", "n_layers",
                                                 "channels", "alpha", "eps", "lam", "c_lo", "c_hi", "rho", "kappa",
-                                                "z_lo", "z_hi", "eta", "rho1", "kappa1", "tv_beta")}
+                                                "z_lo", "z_hi", "eta", "rho1", "kappa1", "tv_beta",
+                                                "den_kind", "ddfb_gammas", "ht_eps")}
     if wl["op"] == "poisson":
         okw.update(op="poisson", ksep=kw["kernel_sep"])
     elif "kernel_sep" in kw:
@@ -381,7 +393,19 @@ def main():
     if traffic.get("workload") != wl["name"]:
         traffic = {}   # the committed ncu capture is for another workload
     roof = None
-    if wl["cnn"] and cnn_n:
+    if wl["cnn"] and cnn_n and wl.get("ddfb"):
+        # DDFB: 2K single-operator launches with a 1 <-> P channel structure (4.6 kFLOP/px): HBM-bound on
+        # the P-channel state u (bf16, 2P B/px per read or write); algorithmic bytes per pixel:
+        # W_K v (x 4 + u 2P) + (K-1) x [proj(v - W^*u) (u 2P + x 4 + p 4) + HT(u + W p) (p 4 + u 4P)]
+        # + final (u 2P + x 4 + G 4)
+        Kc, P = wl["cnn"]
+        bpp = (4 + 2 * P) + (Kc - 1) * ((2 * P + 8) + (4 + 4 * P)) + (2 * P + 8)
+        ach = bpp * own_px * K / (cnn_ms * 1e-3) / 1e9
+        roof = {"kernel": "cnn_chunk_kernel DDFB modes (tcgen05, %d launches/iteration)" % (cnn_n // K),
+                "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm, "traffic": None,
+                "share_of_step": cnn_ms / ms if ms else None,
+                "algorithmic": f"{bpp} B/px x {own_px} px per evaluation ({2 * Kc * P * 9} MAC/px)"}
+    elif wl["cnn"] and cnn_n:
         Kc, P = wl["cnn"]
         flops = 2.0 * cnn_macs(Kc, P) * own_px * K
         ach = flops / (cnn_ms * 1e-3) / 1e12
