@@ -80,7 +80,7 @@ def _load():
         _lib.or_check_stepsizes.restype = C.c_int
         _lib.or_run.argtypes = [C.POINTER(_Config), vp, vp, vp, vp, C.POINTER(i64)]
         _lib.or_run.restype = C.c_int
-        _lib.or_run_ex.argtypes = [C.POINTER(_Config), vp, vp, vp, vp, vp, C.POINTER(i64)]
+        _lib.or_run_ex.argtypes = [C.POINTER(_Config), vp, vp, vp, vp, vp, vp, C.POINTER(i64)]
         _lib.or_run_ex.restype = C.c_int
         _lib.or_prox_kl.argtypes = [d, d, d]
         _lib.or_prox_kl.restype = d
@@ -236,7 +236,7 @@ class Problem:
     eta: float = 0.0                      # op "poisson": y ~ Poisson(eta H x), z1 ~ eta H x
     rho1: float = 0.0
     kappa1: float = 0.0
-    tv_beta: float = 0.0                  # > 0: TV prior, z ~ D x (z = vertical, z1 = horizontal)
+    tv_beta: float = 0.0                  # > 0: TV prior, z ~ D x (z = vertical, zh = horizontal)
     den_kind: str = "dncnn"               # "dncnn" | "ddfb"
     ddfb_gammas: Optional[np.ndarray] = None
     ht_eps: float = 0.0
@@ -297,14 +297,14 @@ def run(pb: Problem, n_iter: int, burn_in: int, seed: int, tiles=(1, 1), bf16_em
     cfg.i_off, cfg.j_off = origin
     cfg.eta, cfg.rho1, cfg.kappa1 = pb.eta, pb.rho1, pb.kappa1
     cfg.tv_beta = pb.tv_beta
-    x = np.zeros((ny, nx)); z = np.zeros((ny, nx)); z1 = np.zeros((ny, nx))
+    x = np.zeros((ny, nx)); z = np.zeros((ny, nx)); z1 = np.zeros((ny, nx)); zh = np.zeros((ny, nx))
     mean = np.zeros((ny, nx)); var = np.zeros((ny, nx))
     n = C.c_int64()
     have_mean = n_iter > burn_in
     have_var = want_var and n_iter - burn_in >= 2
-    e = lib.or_run_ex(C.byref(cfg), x.ctypes.data, z.ctypes.data, z1.ctypes.data,
+    e = lib.or_run_ex(C.byref(cfg), x.ctypes.data, z.ctypes.data, z1.ctypes.data, zh.ctypes.data,
                       mean.ctypes.data if have_mean else None, var.ctypes.data if have_var else None, C.byref(n))
     if e:
         raise ValueError(f"or_run failed with status {e}")
-    return {"x": x, "z": z, "z1": z1, "mean": mean if have_mean else None, "var": var if have_var else None,
+    return {"x": x, "z": z, "z1": z1, "zh": zh, "mean": mean if have_mean else None, "var": var if have_var else None,
             "n": n.value}

@@ -428,8 +428,8 @@ static void or_kernel2d(const or_config *c, double *k) {
 
 /* One untiled iteration of Algorithm 1 (lines 5-13) on global arrays. */
 static int or_step_global(const or_config *c, const double *k, const double *yd, uint64_t t,
-                          const double *x, const double *z, const double *z1, double *xn, double *zn,
-                          double *z1n, double *r, double *g, double *G) {
+                          const double *x, const double *z, const double *z1, const double *zh, double *xn,
+                          double *zn, double *z1n, double *zhn, double *r, double *g, double *G) {
   int ny = c->ny, nx = c->nx;
   int64_t npx = (int64_t)ny * nx;
   /* line 6: u1 = H1^T grad f1(H1 x),  f1(v) = ||y - v||^2/(2 sigma^2) (eq:potential_gaussian_likelihood) */
@@ -470,7 +470,7 @@ static int or_step_global(const or_config *c, const double *k, const double *yd,
     double *dt = (double *)malloc(sizeof(double) * (size_t)npx);
     if (!dv || !dh || !dt) { free(dv); free(dh); free(dt); return OR_E_INVALID; }
     or_grad2d(x, ny, nx, dv, dh);
-    for (int64_t n = 0; n < npx; n++) { dv[n] -= z[n]; dh[n] -= z1[n]; }
+    for (int64_t n = 0; n < npx; n++) { dv[n] -= z[n]; dh[n] -= zh[n]; }
     or_grad2d_adj(dv, dh, ny, nx, dt);
     for (int64_t i = 0; i < ny; i++)
       for (int64_t j = 0; j < nx; j++) {
@@ -488,13 +488,12 @@ static int or_step_global(const or_config *c, const double *k, const double *yd,
         int64_t n = i * nx + j;
         double vv = z[n] - (c->kappa / c->rho) * (z[n] - dv[n]) +
                     sq2k * or_normal(c->seed, (uint32_t)(t + 1), i + c->i_off, j + c->j_off, 1);
-        double vh = z1[n] - (c->kappa / c->rho) * (z1[n] - dh[n]) +
+        double vh = zh[n] - (c->kappa / c->rho) * (zh[n] - dh[n]) +
                     sq2k * or_normal(c->seed, (uint32_t)(t + 1), i + c->i_off, j + c->j_off, 3);
-        or_prox_l21(vv, vh, c->kappa * c->tv_beta, &zn[n], &z1n[n]);
+        or_prox_l21(vv, vh, c->kappa * c->tv_beta, &zn[n], &zhn[n]);
       }
     free(dv); free(dh); free(dt);
-    return OR_OK;
-  }
+  } else {
   for (int64_t i = 0; i < ny; i++)
     for (int64_t j = 0; j < nx; j++) {
       int64_t n = i * nx + j;
@@ -520,6 +519,7 @@ static int or_step_global(const or_config *c, const double *k, const double *yd,
         zn[n] = v < c->z_lo ? c->z_lo : (v > c->z_hi ? c->z_hi : v);
       }
   }
+  }   /* end of the non-TV x / z updates */
   if (c->op == 2) {
     /* lines 11-13 for the z1 block: H2,1 = eta H, prox of kappa1 KL(y || .), stream 2 */
     or_conv_fwd(xn, ny, nx, k, c->kh, c->kw, r);
@@ -539,8 +539,8 @@ static int or_step_global(const or_config *c, const double *k, const double *yd,
  * from S_b x only (the tile plus a ghost frame of width h, zero outside the
  * image), exactly as worker b of Algorithm 1 would after line 5. */
 static int or_step_tiled(const or_config *c, const double *k, const double *yd, uint64_t t,
-                         const double *x, const double *z, const double *z1, double *xn, double *zn,
-                         double *z1n) {
+                         const double *x, const double *z, const double *z1, const double *zh, double *xn,
+                         double *zn, double *z1n, double *zhn) {
   int ny = c->ny, nx = c->nx;
   int ry = c->kh / 2, rx = c->kw / 2;
   int use_cnn = c->n_layers > 0 && c->alpha != 0.0;
@@ -681,8 +681,8 @@ static int or_step_tiled(const or_config *c, const double *k, const double *yd, 
             double s = 0.0;
             if (gi >= 1) s += (xc[0] - xc[-pw]) - z[n - nx];          /* g_v[i-1,j] */
             if (gi < ny - 1) s -= (xc[pw] - xc[0]) - z[n];            /* g_v[i,j]   */
-            if (gj >= 1) s += (xc[0] - xc[-1]) - z1[n - 1];           /* g_h[i,j-1] */
-            if (gj < nx - 1) s -= (xc[1] - xc[0]) - z1[n];            /* g_h[i,j]   */
+            if (gj >= 1) s += (xc[0] - xc[-1]) - zh[n - 1];           /* g_h[i,j-1] */
+            if (gj < nx - 1) s -= (xc[1] - xc[0]) - zh[n];            /* g_h[i,j]   */
             double v = xc[0] - c->gamma * gl[(int64_t)a * tw + b] - (c->gamma / c->rho) * s +
                        sq2g * or_normal(c->seed, (uint32_t)(t + 1), gi + c->i_off, gj + c->j_off, 0);
             xn[n] = v < 0.0 ? 0.0 : v;
@@ -729,9 +729,9 @@ static int or_step_tiled(const or_config *c, const double *k, const double *yd, 
             double dh = (gj < nx - 1) ? xn[n + 1] - xn[n] : 0.0;
             double vv = z[n] - (c->kappa / c->rho) * (z[n] - dv) +
                         sq2k * or_normal(c->seed, (uint32_t)(t + 1), gi + c->i_off, gj + c->j_off, 1);
-            double vh = z1[n] - (c->kappa / c->rho) * (z1[n] - dh) +
+            double vh = zh[n] - (c->kappa / c->rho) * (zh[n] - dh) +
                         sq2k * or_normal(c->seed, (uint32_t)(t + 1), gi + c->i_off, gj + c->j_off, 3);
-            or_prox_l21(vv, vh, c->kappa * c->tv_beta, &zn[n], &z1n[n]);
+            or_prox_l21(vv, vh, c->kappa * c->tv_beta, &zn[n], &zhn[n]);
           }
       }
   }
@@ -770,19 +770,19 @@ static int or_step_tiled(const or_config *c, const double *k, const double *yd, 
   return OR_OK;
 }
 
-/* Full chain.  Outputs (each ny*nx, any may be NULL): final x, final z (z2 block for
- * op = 2; vertical component of z ~ D x for TV), final z1 (op = 2; horizontal TV component), MMSE mean and variance (M2/(n-1), reading R15) of x^{(t)},
+/* Full chain.  Outputs (each ny*nx, any may be NULL): final x, final z (the H2 = I block, or
+ * the vertical component of z ~ D x for TV), final z1 (op = 2), final z_h (TV horizontal), MMSE mean and variance (M2/(n-1), reading R15) of x^{(t)},
  * t = burn_in+1..n_iter (reading R14), accumulated with Welford's update (P:839 footnote). */
-int or_run_ex(const or_config *c, double *x_out, double *z_out, double *z1_out, double *mean_out,
-              double *var_out, int64_t *n_samples) {
+int or_run_ex(const or_config *c, double *x_out, double *z_out, double *z1_out, double *zh_out,
+              double *mean_out, double *var_out, int64_t *n_samples) {
   if (c->ny <= 0 || c->nx <= 0 || c->gamma <= 0.0) return OR_E_INVALID;
   if (c->op != 2 && c->sigma2 <= 0.0) return OR_E_INVALID;
   if (c->op != 1 && (c->kh % 2 == 0 || c->kw % 2 == 0)) return OR_E_INVALID;
   if (c->rho > 0.0 && !(c->kappa > 0.0 && c->kappa < c->rho)) return OR_E_INVALID;
   if (c->op == 2 && !(c->eta > 0.0 && c->rho1 > 0.0 && c->kappa1 > 0.0 && c->kappa1 < c->rho1))
     return OR_E_INVALID;
-  if (c->tv_beta > 0.0 && (c->op == 2 || !(c->rho > 0.0) || (c->n_layers > 0 && c->alpha != 0.0) || c->lambda > 0.0))
-    return OR_E_INVALID;   /* TV: Gaussian likelihood, z block on, no CNN, no box term */
+  if (c->tv_beta > 0.0 && (!(c->rho > 0.0) || (c->n_layers > 0 && c->alpha != 0.0) || c->lambda > 0.0))
+    return OR_E_INVALID;   /* TV: z block on (the TV block), no CNN, no box term; any likelihood */
   int64_t npx = (int64_t)c->ny * c->nx;
   double *k = (double *)calloc((size_t)(c->kh > 0 ? c->kh * c->kw : 1), sizeof(double));
   double *yd = (double *)malloc(sizeof(double) * (size_t)npx);
@@ -792,13 +792,15 @@ int or_run_ex(const or_config *c, double *x_out, double *z_out, double *z1_out, 
   double *zn = (double *)calloc((size_t)npx, sizeof(double));
   double *z1 = (double *)calloc((size_t)npx, sizeof(double));
   double *z1n = (double *)calloc((size_t)npx, sizeof(double));
+  double *zh = (double *)calloc((size_t)npx, sizeof(double));
+  double *zhn = (double *)calloc((size_t)npx, sizeof(double));
   double *r = (double *)calloc((size_t)npx, sizeof(double));
   double *g = (double *)calloc((size_t)npx, sizeof(double));
   double *G = (double *)calloc((size_t)npx, sizeof(double));
   double *mu = (double *)calloc((size_t)npx, sizeof(double));
   double *m2 = (double *)calloc((size_t)npx, sizeof(double));
   int err = OR_OK;
-  if (!k || !yd || !x || !xn || !z || !zn || !z1 || !z1n || !r || !g || !G || !mu || !m2) {
+  if (!k || !yd || !x || !xn || !z || !zn || !z1 || !z1n || !zh || !zhn || !r || !g || !G || !mu || !m2) {
     err = OR_E_INVALID;
     goto done;
   }
@@ -810,9 +812,9 @@ int or_run_ex(const or_config *c, double *x_out, double *z_out, double *z1_out, 
   int64_t cnt = 0;
   for (int64_t t = 0; t < c->n_iter; t++) {
     if (c->tiles_y > 1 || c->tiles_x > 1)
-      err = or_step_tiled(c, k, yd, (uint64_t)t, x, z, z1, xn, zn, z1n);
+      err = or_step_tiled(c, k, yd, (uint64_t)t, x, z, z1, zh, xn, zn, z1n, zhn);
     else
-      err = or_step_global(c, k, yd, (uint64_t)t, x, z, z1, xn, zn, z1n, r, g, G);
+      err = or_step_global(c, k, yd, (uint64_t)t, x, z, z1, zh, xn, zn, z1n, zhn, r, g, G);
     if (err) goto done;
     if (t + 1 > c->burn_in) {
       cnt++;
@@ -824,11 +826,13 @@ int or_run_ex(const or_config *c, double *x_out, double *z_out, double *z1_out, 
     }
     double *tt = x; x = xn; xn = tt;
     if (c->rho > 0.0) { tt = z; z = zn; zn = tt; }
-    if (c->op == 2 || c->tv_beta > 0.0) { tt = z1; z1 = z1n; z1n = tt; }
+    if (c->op == 2) { tt = z1; z1 = z1n; z1n = tt; }
+    if (c->tv_beta > 0.0) { tt = zh; zh = zhn; zhn = tt; }
   }
   if (x_out) memcpy(x_out, x, sizeof(double) * (size_t)npx);
   if (z_out) memcpy(z_out, z, sizeof(double) * (size_t)npx);
   if (z1_out) memcpy(z1_out, z1, sizeof(double) * (size_t)npx);
+  if (zh_out) memcpy(zh_out, zh, sizeof(double) * (size_t)npx);
   if (n_samples) *n_samples = cnt;
   if (mean_out) {
     if (cnt < 1) { err = OR_E_STATS_EMPTY; goto done; }
@@ -839,12 +843,12 @@ int or_run_ex(const or_config *c, double *x_out, double *z_out, double *z1_out, 
     for (int64_t n = 0; n < npx; n++) var_out[n] = m2[n] / (double)(cnt - 1);
   }
 done:
-  free(k); free(yd); free(x); free(xn); free(z); free(zn); free(z1); free(z1n);
+  free(k); free(yd); free(x); free(xn); free(z); free(zn); free(z1); free(z1n); free(zh); free(zhn);
   free(r); free(g); free(G); free(mu); free(m2);
   return err;
 }
 
 int or_run(const or_config *c, double *x_out, double *z_out, double *mean_out, double *var_out,
            int64_t *n_samples) {
-  return or_run_ex(c, x_out, z_out, NULL, mean_out, var_out, n_samples);
+  return or_run_ex(c, x_out, z_out, NULL, NULL, mean_out, var_out, n_samples);
 }

@@ -132,7 +132,7 @@ def test_tv_iterations_against_dense_matrices(n_iter):
     out = oracle.run(pb, n_iter=n_iter, burn_in=n_iter, seed=seed)
     np.testing.assert_allclose(out["x"].ravel(), x, rtol=0, atol=1e-12)
     np.testing.assert_allclose(out["z"].ravel(), zv, rtol=0, atol=1e-12)
-    np.testing.assert_allclose(out["z1"].ravel(), zh, rtol=0, atol=1e-12)
+    np.testing.assert_allclose(out["zh"].ravel(), zh, rtol=0, atol=1e-12)
 
 
 @pytest.mark.parametrize("tiles", [(2, 2), (3, 1), (1, 3)])
@@ -146,6 +146,45 @@ def test_tv_tiled_equals_untiled(tiles):
                         tv_beta=40.0)
     a = oracle.run(pb, n_iter=6, burn_in=2, seed=870)
     t = oracle.run(pb, n_iter=6, burn_in=2, seed=870, tiles=tiles)
-    for key in ("x", "z", "z1", "mean", "var"):
+    for key in ("x", "z", "zh", "mean", "var"):
         np.testing.assert_array_equal(a[key], t[key])
     assert np.all(a["x"] >= 0)
+
+
+def test_poisson_tv_iteration_against_dense_matrices():
+    """Poisson noise with the TV prior: f1 = 0, z1 ~ eta H x (KL prox, stream 2),
+    z = (z_v, z_h) ~ D x (l2,1 prox, streams 1 / 3), x by PSGLA on R+."""
+    ny, nx = 6, 7
+    rng = np.random.default_rng(12)
+    k = rng.uniform(0, 1, size=(3, 3))
+    k /= k.sum()
+    eta = 30.0
+    y = rng.poisson(eta * convolve2d(rng.uniform(0.1, 1, (ny, nx)), k, mode="same")).astype(np.float32)
+    pb = oracle.Problem(y=y, sigma2=1.0, gamma=1e-3, op="poisson", kernel=k.astype(np.float32), eta=eta,
+                        rho1=10.0, kappa1=9.9, rho=0.05, kappa=0.05 * 0.99 / 8, tv_beta=3.0,
+                        x0=rng.uniform(0, 1, (ny, nx)).astype(np.float32))
+    seed = 17
+    H = _dense_conv(ny, nx, np.asarray(pb.kernel, np.float64))
+    Dv, Dh = _dense_D(ny, nx)
+    x = np.asarray(pb.x0, np.float64).ravel()
+    yy = np.asarray(y, np.float64).ravel()
+    z1, zv, zh = np.zeros(ny * nx), np.zeros(ny * nx), np.zeros(ny * nx)
+    g, r, kp, tau, e, r1, k1 = pb.gamma, pb.rho, pb.kappa, pb.kappa * pb.tv_beta, eta, pb.rho1, pb.kappa1
+    for t in range(2):
+        xi, zev, zeh, ze1 = (oracle.normal_field(seed, t + 1, ny, nx, s).ravel() for s in (0, 1, 3, 2))
+        v = (x - (g / r1) * e * H.T @ (e * H @ x - z1) - (g / r) * (Dv.T @ (Dv @ x - zv) + Dh.T @ (Dh @ x - zh))
+             + np.sqrt(2 * g) * xi)
+        x = np.maximum(v, 0.0)
+        wv = zv - (kp / r) * (zv - Dv @ x) + np.sqrt(2 * kp) * zev
+        wh = zh - (kp / r) * (zh - Dh @ x) + np.sqrt(2 * kp) * zeh
+        nrm = np.hypot(wv, wh)
+        sc = np.where(nrm > tau, 1 - tau / np.where(nrm > 0, nrm, 1), 0.0)
+        zv, zh = wv * sc, wh * sc
+        w1 = z1 - (k1 / r1) * (z1 - e * H @ x) + np.sqrt(2 * k1) * ze1
+        z1 = 0.5 * ((w1 - k1) + np.sqrt((w1 - k1) ** 2 + 4 * k1 * yy))
+    out = oracle.run(pb, n_iter=2, burn_in=2, seed=seed)
+    for key, ref in (("x", x), ("z", zv), ("zh", zh), ("z1", z1)):
+        np.testing.assert_allclose(out[key].ravel(), ref, rtol=0, atol=1e-11, err_msg=key)
+    t2 = oracle.run(pb, n_iter=2, burn_in=2, seed=seed, tiles=(2, 1))
+    for key in ("x", "z", "zh", "z1"):
+        np.testing.assert_array_equal(out[key], t2[key])
