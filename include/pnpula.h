@@ -152,8 +152,8 @@ typedef struct {
    * tv_beta > 0 turns the z block into z = (z_v, z_h) ~ D x (2-D forward differences) with
    * f2 = tv_beta ||.||_{2,1} (coupling rho, step kappa), and x moves by PSGLA with p = 1_{R+}:
    * x+ = max(x - gamma grad f1 - (gamma/rho) D^T (D x - z) + sqrt(2 gamma) xi, 0).
-   * Requires OP_CONV or OP_MASK, rho > 0, no denoiser, lambda <= 0.  pnpula_get_state returns
-   * z_v, pnpula_get_z1 z_h. */
+   * Requires rho > 0, no denoiser, lambda <= 0; with OP_POISSON the z1 block is kept
+   * and f1 = 0.  pnpula_get_state returns z_v, pnpula_get_tv_zh z_h. */
   double tv_beta;
 } pnpula_config;
 
@@ -204,9 +204,13 @@ pnpula_status pnpula_get_moments(pnpula_ctx *ctx, float *mean, float *var, int64
 /* [collective for GLOBAL scope] Current state x^t, z^t (either may be NULL) and t. */
 pnpula_status pnpula_get_state(pnpula_ctx *ctx, float *x, float *z, int64_t *t, int32_t scope);
 
-/* [collective for GLOBAL scope] OP_POISSON: current z1 block (the AXDA variable ~ eta H x);
- * TV prior: the horizontal component z_h of z ~ D x.  LOCAL bbox or, on root, the whole image. */
+/* [collective for GLOBAL scope] OP_POISSON: current z1 block (the AXDA variable ~ eta H x), on
+ * the LOCAL bbox or, on root, the whole image. */
 pnpula_status pnpula_get_z1(pnpula_ctx *ctx, float *z1, int32_t scope);
+
+/* [collective for GLOBAL scope] TV prior: the horizontal component z_h of z ~ D x (z_v is the z of
+ * pnpula_get_state). */
+pnpula_status pnpula_get_tv_zh(pnpula_ctx *ctx, float *zh, int32_t scope);
 
 /* Checkpoint / resume.  The blob holds this rank's complete chain state:
  * t, burn-in, seed and, per owned tile, the padded buffers (interior + ghost frame) of x^t,

@@ -92,6 +92,7 @@ def load():
         "pnpula_get_moments": ([vp, vp, vp, C.POINTER(i64), i32], C.c_int),
         "pnpula_get_state": ([vp, vp, vp, C.POINTER(i64), i32], C.c_int),
         "pnpula_get_z1": ([vp, vp, i32], C.c_int),
+        "pnpula_get_tv_zh": ([vp, vp, i32], C.c_int),
         "pnpula_checkpoint_bytes": ([vp, C.POINTER(u64)], C.c_int),
         "pnpula_save_checkpoint": ([vp, vp, u64], C.c_int),
         "pnpula_load_checkpoint": ([vp, vp, u64], C.c_int),
@@ -118,7 +119,7 @@ def load():
 # names exported by include/pnpula.h (tests check the .so exports every one)
 EXPORTED = ["pnpula_version", "pnpula_last_error", "pnpula_get_unique_id", "pnpula_create", "pnpula_reset",
             "pnpula_advance", "pnpula_run", "pnpula_synchronize", "pnpula_local_bbox", "pnpula_get_moments",
-            "pnpula_get_state", "pnpula_get_z1", "pnpula_tile_info", "pnpula_get_padded_x", "pnpula_get_denoiser_residual",
+            "pnpula_get_state", "pnpula_get_z1", "pnpula_get_tv_zh", "pnpula_tile_info", "pnpula_get_padded_x", "pnpula_get_denoiser_residual",
             "pnpula_set_timing", "pnpula_kernel_time", "pnpula_destroy", "pnpula_partition",
             "pnpula_halo_width", "pnpula_plan_halo", "pnpula_check_stepsizes", "pnpula_checkpoint_bytes",
             "pnpula_save_checkpoint", "pnpula_load_checkpoint", "pnpula_conv_norm2_bound"]

@@ -44,6 +44,7 @@ struct TileDev {
   uint8_t *mask = nullptr;
   float *z = nullptr, *mean = nullptr, *m2 = nullptr, *G = nullptr;
   float *z1 = nullptr;     // OP_POISSON: z1 block, valid on tile (+) r_H (reading R33)
+  float *zh = nullptr;     // TV prior: horizontal component z_h of z ~ D x (z_v lives in z)
   float *pbuf = nullptr;   // DDFB: p = proj(v - W_k^* u), fp32 padded geometry, zero outside the image
   uint16_t *act[2] = {nullptr, nullptr};   // inter-chunk activations
 };
@@ -398,7 +399,7 @@ UpdateParams make_update_params(pnpula_ctx *c, TileDev &td, int buf) {
   p.a_g = poisson ? (float)(c->gamma * c->eta / c->rho1) : (float)(c->gamma / c->sigma2);
   p.has_tv = c->tv_beta > 0;
   p.has_z = c->rho > 0 && !p.has_tv;   // TV: z ~ D x is updated by its own kernel after the exchange
-  if (p.has_tv) { p.a_tv = (float)(c->gamma / c->rho); p.zv = td.z; p.zh = td.z1; }
+  if (p.has_tv) { p.a_tv = (float)(c->gamma / c->rho); p.zv = td.z; p.zh = td.zh; }
   p.a_rho = p.has_z ? (float)(c->gamma / c->rho) : 0.f;   // (TV: a_tv)
   p.has_G = c->n_layers > 0;
   p.a_d = p.has_G ? (float)(c->alpha * c->gamma / (c->eps * c->eps)) : 0.f;
@@ -442,7 +443,7 @@ pnpula_status step(pnpula_ctx *c) {
       TvZParams q{};
       q.x = td.x[buf ^ 1];
       q.zv = td.z;
-      q.zh = td.z1;
+      q.zh = td.zh;
       q.g = td.g;
       q.ny = c->ny; q.nx = c->nx;
       q.b = (float)(c->kappa / c->rho);
@@ -684,8 +685,8 @@ pnpula_status pnpula_create(const pnpula_config *cfg, pnpula_ctx **out) {
   if (f.rho > 0 && !(f.kappa > 0 && f.kappa < f.rho)) { set_error("kappa must lie in (0, rho)"); return PNPULA_E_INVALID_ARG; }
   const bool use_cnn = f.den && f.alpha != 0.0;
   const bool tv = f.tv_beta > 0;
-  if (tv && (poisson || !(f.rho > 0) || use_cnn || f.lambda > 0)) {
-    set_error("TV prior needs OP_CONV/OP_MASK, rho > 0, no denoiser and lambda <= 0"); return PNPULA_E_INVALID_ARG;
+  if (tv && (!(f.rho > 0) || use_cnn || f.lambda > 0)) {
+    set_error("TV prior needs rho > 0 (its z block), no denoiser and lambda <= 0"); return PNPULA_E_INVALID_ARG;
   }
   const bool ddfb = use_cnn && f.den->kind == PNPULA_DEN_DDFB;
   if (use_cnn && f.den->kind != PNPULA_DEN_DNCNN && !ddfb) { set_error("unknown denoiser kind"); return PNPULA_E_INVALID_ARG; }
@@ -844,7 +845,11 @@ pnpula_status pnpula_create(const pnpula_config *cfg, pnpula_ctx **out) {
     CUB(cudaMalloc(&td.mean, n * sizeof(float)));
     CUB(cudaMalloc(&td.m2, n * sizeof(float)));
     if (c->rho > 0) CUB(cudaMalloc(&td.z, n * sizeof(float)));
-    if (poisson || tv) {   // Poisson z1 block, or the TV horizontal component z_h
+    if (tv) {
+      CUB(cudaMalloc(&td.zh, n * sizeof(float)));
+      CUB(cudaMemsetAsync(td.zh, 0, n * sizeof(float), c->stream));
+    }
+    if (poisson) {   // Poisson z1 block
       CUB(cudaMalloc(&td.z1, n * sizeof(float)));
       CUB(cudaMemsetAsync(td.z1, 0, n * sizeof(float), c->stream));
     }
@@ -978,6 +983,7 @@ pnpula_status pnpula_reset(pnpula_ctx *c, int64_t burn_in, uint64_t seed) {
     CU(c, cudaMemcpyAsync(td.x[1], td.x0, n, cudaMemcpyDeviceToDevice, c->stream));
     if (td.z) CU(c, cudaMemsetAsync(td.z, 0, n, c->stream));
     if (td.z1) CU(c, cudaMemsetAsync(td.z1, 0, n, c->stream));
+    if (td.zh) CU(c, cudaMemsetAsync(td.zh, 0, n, c->stream));
     CU(c, cudaMemsetAsync(td.mean, 0, n, c->stream));
     CU(c, cudaMemsetAsync(td.m2, 0, n, c->stream));
   }
@@ -1177,9 +1183,7 @@ pnpula_status pnpula_get_state(pnpula_ctx *c, float *x, float *z, int64_t *t, in
 pnpula_status pnpula_get_z1(pnpula_ctx *c, float *z1, int32_t scope) {
   pnpula_status s = check_ctx(c);
   if (s) return s;
-  if (c->op != PNPULA_OP_POISSON && !(c->tv_beta > 0)) {
-    set_error("z1 exists only for OP_POISSON (z1 block) or the TV prior (z_h)"); return PNPULA_E_STATE;
-  }
+  if (c->op != PNPULA_OP_POISSON) { set_error("z1 exists only for OP_POISSON"); return PNPULA_E_STATE; }
   CU(c, cudaSetDevice(c->device));
   std::vector<const float *> zs;
   for (auto &td : c->tiles) zs.push_back(td.z1);
@@ -1200,6 +1204,7 @@ std::vector<float *> ckpt_fields(pnpula_ctx *c, TileDev &td) {
   std::vector<float *> f{td.x[c->cur], td.mean, td.m2};
   if (td.z) f.push_back(td.z);
   if (td.z1) f.push_back(td.z1);
+  if (td.zh) f.push_back(td.zh);
   return f;
 }
 uint64_t ckpt_bytes(pnpula_ctx *c) {
@@ -1293,6 +1298,16 @@ pnpula_status pnpula_conv_norm2_bound(const float *k, int32_t kh, int32_t kw, in
   return PNPULA_OK;
 }
 
+pnpula_status pnpula_get_tv_zh(pnpula_ctx *c, float *zh, int32_t scope) {
+  pnpula_status s = check_ctx(c);
+  if (s) return s;
+  if (!(c->tv_beta > 0)) { set_error("z_h exists only with the TV prior"); return PNPULA_E_STATE; }
+  CU(c, cudaSetDevice(c->device));
+  std::vector<const float *> zs;
+  for (auto &td : c->tiles) zs.push_back(td.zh);
+  return gather_padded_interiors(c, zs, zh, scope == PNPULA_SCOPE_GLOBAL_ON_ROOT);
+}
+
 pnpula_status pnpula_get_padded_x(pnpula_ctx *c, int32_t li, float *out) {
   pnpula_status s = check_ctx(c);
   if (s) return s;
@@ -1357,7 +1372,7 @@ pnpula_status pnpula_destroy(pnpula_ctx *c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (auto &td : c->tiles) {
     cudaFree(td.x[0]); cudaFree(td.x[1]); cudaFree(td.x0); cudaFree(td.y); cudaFree(td.mask);
-    cudaFree(td.z); cudaFree(td.z1); cudaFree(td.mean); cudaFree(td.m2); cudaFree(td.G); cudaFree(td.pbuf);
+    cudaFree(td.z); cudaFree(td.z1); cudaFree(td.zh); cudaFree(td.mean); cudaFree(td.m2); cudaFree(td.G); cudaFree(td.pbuf);
     cudaFree(td.act[0]); cudaFree(td.act[1]);
   }
   for (auto p : c->d_w) cudaFree(p);

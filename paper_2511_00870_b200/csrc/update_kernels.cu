@@ -581,7 +581,10 @@ template <int R>
 __global__ void __launch_bounds__(NTHREADS) z1_sep_kernel(const __grid_constant__ Z1Params p,
                                                         const __grid_constant__ CUtensorMap tmx, int r0, int q0,
                                                         int nbx) {
-  constexpr int XR = TY + 2 * R, XC = TX + 2 * R;
+  // the staged columns start 16-B aligned (XL = R rounded up to 4): TMA tile loads need a
+  // 16-B aligned inner start coordinate
+  constexpr int XL = (R + 3) / 4 * 4;
+  constexpr int XR = TY + 2 * R, XC = TX + 2 * XL;
   static_assert((XC * 4) % 16 == 0, "TMA row bytes");
   __shared__ __align__(128) float X[XR * XC];
   __shared__ __align__(16) float T[XR * TX];
@@ -598,11 +601,11 @@ __global__ void __launch_bounds__(NTHREADS) z1_sep_kernel(const __grid_constant_
     asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(b),
                  "r"((uint32_t)(XR * XC * 4))
                  : "memory");
-    tma_load_2d((uint32_t)__cvta_generic_to_shared(X), &tmx, bj0 - R - (g.j0 - g.hx), bi0 - R - (g.i0 - g.h), b);
+    tma_load_2d((uint32_t)__cvta_generic_to_shared(X), &tmx, bj0 - XL - (g.j0 - g.hx), bi0 - R - (g.i0 - g.h), b);
   }
   __syncthreads();
   mbar_wait_parity(b, 0);
-  // horizontal: T[a][c] = sum_q kx[q+R] X[a][c + R - q]   (x+ column bj0 + c - q)
+  // horizontal: T[a][c] = sum_q kx[q+R] X[a][c + XL - q]   (x+ column bj0 + c - q)
   for (int e = tid; e < XR * (TX / 4); e += NTHREADS) {
     const int a = e / (TX / 4), c4 = 4 * (e - a * (TX / 4));
     float o[4];
@@ -610,7 +613,7 @@ __global__ void __launch_bounds__(NTHREADS) z1_sep_kernel(const __grid_constant_
     for (int j = 0; j < 4; ++j) {
       float s = 0.f;
 #pragma unroll
-      for (int q = -R; q <= R; ++q) s = fmaf(kxs[q + R], X[a * XC + c4 + j + R - q], s);
+      for (int q = -R; q <= R; ++q) s = fmaf(kxs[q + R], X[a * XC + c4 + j + XL - q], s);
       o[j] = s;
     }
     *reinterpret_cast<float4 *>(T + a * TX + 4 * (e - a * (TX / 4))) = make_float4(o[0], o[1], o[2], o[3]);
@@ -823,7 +826,7 @@ cudaError_t launch_z1_update(const Z1Params &p, cudaStream_t s) {
     const int R = p.ry, q0 = c0 >> 2;
     const int nbx = (((c1 + 3) >> 2) - q0 + 15) / 16, nby = (r1 - r0 + TY - 1) / TY;
     CUtensorMap tmx;
-    if (!encode_padded_2d(&tmx, p.x, p.g, TX + 2 * R, TY + 2 * R)) return cudaErrorInvalidValue;
+    if (!encode_padded_2d(&tmx, p.x, p.g, TX + 2 * ((R + 3) / 4 * 4), TY + 2 * R)) return cudaErrorInvalidValue;
     if (R == 4) z1_sep_kernel<4><<<nbx * nby, NTHREADS, 0, s>>>(p, tmx, r0, q0, nbx);
     else z1_sep_kernel<2><<<nbx * nby, NTHREADS, 0, s>>>(p, tmx, r0, q0, nbx);
     return cudaGetLastError();

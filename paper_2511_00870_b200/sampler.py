@@ -140,10 +140,17 @@ class Sampler:
         return x, z, t.value
 
     def z1(self, scope: int = L.SCOPE_LOCAL):
-        """OP_POISSON: the AXDA block z1 (~ eta H x); TV prior: z_h."""
+        """OP_POISSON: the AXDA block z1 (~ eta H x)."""
         shp = self._out_shape(scope)
         out = np.zeros(shp, np.float32) if shp else None
         L.check(self._lib.pnpula_get_z1(self._h, L._ptr(out), scope))
+        return out
+
+    def tv_zh(self, scope: int = L.SCOPE_LOCAL):
+        """TV prior: the horizontal component z_h of z ~ D x."""
+        shp = self._out_shape(scope)
+        out = np.zeros(shp, np.float32) if shp else None
+        L.check(self._lib.pnpula_get_tv_zh(self._h, L._ptr(out), scope))
         return out
 
     def save_checkpoint(self) -> bytes:

@@ -39,7 +39,7 @@ def _crop_oracle(wl, si, sj, bf16):
     okw.update(op="poisson" if wl["op"] == "poisson" else "conv", ksep=kw["kernel_sep"])
     pb = oracle.Problem(y=kw["y"], **okw)
     out = oracle.run(pb, N_ITER, 0, SEED, bf16_emulate=bf16, origin=(i0, j0))
-    return {k: out[k][si - i0, sj - j0] for k in ("x", "z", "z1", "mean")}
+    return {k: out[k][si - i0, sj - j0] for k in ("x", "z", "z1", "zh", "mean")}
 
 
 @pytest.mark.parametrize("name,bf16,atol", [("c5", True, 2e-3), ("p5", True, 2e-3), ("t5", False, 1e-5)])
@@ -53,7 +53,8 @@ def test_full_size_sampled_parity(name, bf16, atol):
         s.run(N_ITER, 0, SEED)
         x, z, _ = s.state()
         mean, _, _ = s.moments(want_var=False)
-        z1 = s.z1() if (wl["op"] == "poisson" or wl.get("tv")) else None
+        z1 = s.z1() if wl["op"] == "poisson" else None
+        zh = s.tv_zh() if wl.get("tv") else None
     finally:
         s.close()
     assert np.isfinite(x).all()
@@ -65,3 +66,5 @@ def test_full_size_sampled_parity(name, bf16, atol):
             assert abs(float(z[si, sj]) - o["z"]) <= atol * max(1.0, abs(o["z"])), (si, sj, z[si, sj], o["z"])
         if z1 is not None:
             assert abs(float(z1[si, sj]) - o["z1"]) <= atol * max(1.0, abs(o["z1"])), (si, sj, z1[si, sj], o["z1"])
+        if zh is not None:
+            assert abs(float(zh[si, sj]) - o["zh"]) <= atol * max(1.0, abs(o["zh"])), (si, sj, zh[si, sj], o["zh"])

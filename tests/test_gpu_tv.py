@@ -45,9 +45,10 @@ def gpu_tv(kw, n_iter, burn_in, seed, tiles=(1, 1), flags=0):
     try:
         s.run(n_iter, burn_in, seed)
         x, zv, _ = s.state()
-        zh = s.z1()
+        zh = s.tv_zh()
+        z1 = s.z1() if kw.get("op") == "poisson" else None
         mean, var, _ = s.moments()
-        return dict(x=x, z=zv, z1=zh, mean=mean, var=var)
+        return dict(x=x, z=zv, zh=zh, z1=z1, mean=mean, var=var)
     finally:
         s.close()
 
@@ -59,7 +60,7 @@ def test_tv_chain_fp32_path_vs_oracle(op, kernel, shape):
     kw, pb = tv_problem(ny, nx, op=op, kernel=kernel or "gauss9")
     g = gpu_tv(kw, 50, 10, seed=872)
     o = oracle.run(pb, 50, 10, seed=872)
-    for k in ("x", "z", "z1", "mean"):
+    for k in ("x", "z", "zh", "mean"):
         assert rel_l2(g[k], o[k]) <= 1e-5, k
     assert rel_l2(g["var"], o["var"]) <= 1e-4
     assert np.all(g["x"] >= 0)
@@ -70,7 +71,7 @@ def test_tv_tiled_bitwise(tiles, flags):
     kw, _ = tv_problem(66, 75, kernel="random5")
     a = gpu_tv(kw, 12, 4, seed=6)
     b = gpu_tv(kw, 12, 4, seed=6, tiles=tiles, flags=flags)
-    for k in ("x", "z", "z1", "mean", "var"):
+    for k in ("x", "z", "zh", "mean", "var"):
         np.testing.assert_array_equal(a[k], b[k], err_msg=k)
 
 
@@ -79,3 +80,23 @@ def test_tv_rejects_denoiser():
     w, b = synth.dncnn_weights(4, 16)
     with pytest.raises(Exception):
         Sampler(**kw, weights=w, biases=b, n_layers=4, channels=16, alpha=1.0, eps=0.1)
+
+
+def test_poisson_tv_chain_vs_oracle_and_tiling():
+    """Poisson noise with the TV prior: z1 KL block + z ~ D x, x by PSGLA on R+."""
+    ny, nx = 58, 61
+    ky, kx = synth.gaussian_factors(5, 1.0)
+    y = synth.observe_poisson(ny, nx, synth.outer(ky, kx), 250.0)
+    hp = params.poisson_pnp(250.0)
+    gamma = 0.99 / (250.0 ** 2 / hp["rho1"] + 8.0 / 1e-3)
+    common = dict(gamma=gamma, eta=250.0, rho1=hp["rho1"], kappa1=hp["kappa1"], rho=1e-3, kappa=0.99e-3 / 8,
+                  tv_beta=13.0, x0=(synth.ground_truth(ny, nx) * 0.8 + 0.1).astype(np.float32))
+    kw = dict(ny=ny, nx=nx, y=y, sigma2=1.0, op="poisson", kernel_sep=(ky, kx), **common)
+    pb = oracle.Problem(y=y, sigma2=1.0, op="poisson", ksep=(ky, kx), **common)
+    g = gpu_tv(kw, 40, 8, seed=874)
+    o = oracle.run(pb, 40, 8, seed=874)
+    for k in ("x", "z", "zh", "z1", "mean"):
+        assert rel_l2(g[k], o[k]) <= 1e-5, k
+    t = gpu_tv(kw, 40, 8, seed=874, tiles=(2, 2))
+    for k in ("x", "z", "zh", "z1", "mean", "var"):
+        np.testing.assert_array_equal(g[k], t[k], err_msg=k)
