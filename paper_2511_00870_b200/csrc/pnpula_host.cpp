@@ -115,6 +115,10 @@ struct pnpula_ctx {
   bool have_reset = false;
   bool poisoned = false;
 
+  // device scratch reused by the result gathers (no cudaMalloc/cudaFree per call)
+  void *scratch = nullptr;
+  size_t scratch_bytes = 0;
+
   // timing
   bool timing = false;
   Timer tm_cnn, tm_update, tm_halo;
@@ -1075,13 +1079,21 @@ pnpula_status gather_fields(pnpula_ctx *c, const std::vector<float *> &d_tile_bu
                h.data() + (size_t)f * r.h * r.w + (size_t)a * r.w, (size_t)r.w * sizeof(float));
     }
   };
+  // own tiles: one strided device -> host copy per field straight into the caller's buffer
+  // (full-rate DMA when the buffer is pinned; no staging vector, no per-row memcpy)
   for (int li = 0; li < c->n_local; ++li) {
     const TileGeom &g = c->tiles[li].g;
-    std::vector<float> h((size_t)g.th * g.tw * nf);
-    CU(c, cudaMemcpyAsync(h.data(), d_tile_bufs[li], h.size() * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
-    CU(c, cudaStreamSynchronize(c->stream));
-    if (!global || c->rank == 0) place({g.i0, g.j0, g.th, g.tw}, h);
+    if (global && c->rank != 0) break;
+    for (int f = 0; f < nf; ++f) {
+      float *o = host_out[f];
+      if (!o) continue;
+      CU(c, cudaMemcpy2DAsync(o + (size_t)(g.i0 - dst_rect.i0) * dst_rect.w + (g.j0 - dst_rect.j0),
+                              (size_t)dst_rect.w * sizeof(float), d_tile_bufs[li] + (size_t)f * g.th * g.tw,
+                              (size_t)g.tw * sizeof(float), (size_t)g.tw * sizeof(float), g.th,
+                              cudaMemcpyDeviceToHost, c->stream));
+    }
   }
+  CU(c, cudaStreamSynchronize(c->stream));
   if (!global || c->world == 1) return PNPULA_OK;
   // remote tiles -> rank 0
   if (c->rank == 0) {
@@ -1108,23 +1120,40 @@ pnpula_status gather_fields(pnpula_ctx *c, const std::vector<float *> &d_tile_bu
   return PNPULA_OK;
 }
 
+// per-tile contiguous staging in the context's reusable device scratch (grown on demand)
+pnpula_status tile_staging(pnpula_ctx *c, int nf, std::vector<float *> &bufs) {
+  size_t total = 0;
+  for (auto &td : c->tiles) total += (size_t)td.g.th * td.g.tw * nf;
+  if (total * sizeof(float) > c->scratch_bytes) {
+    if (c->scratch) CU(c, cudaFree(c->scratch));
+    c->scratch = nullptr;
+    c->scratch_bytes = 0;
+    CU(c, cudaMalloc(&c->scratch, total * sizeof(float)));
+    c->scratch_bytes = total * sizeof(float);
+  }
+  float *d = static_cast<float *>(c->scratch);
+  bufs.clear();
+  for (auto &td : c->tiles) {
+    bufs.push_back(d);
+    d += (size_t)td.g.th * td.g.tw * nf;
+  }
+  return PNPULA_OK;
+}
+
 pnpula_status gather_padded_interiors(pnpula_ctx *c, const std::vector<const float *> &src, float *host,
                                       bool global) {
   // pack interiors to contiguous, then gather
   std::vector<float *> bufs;
+  pnpula_status s = tile_staging(c, 1, bufs);
+  if (s) return s;
   for (int li = 0; li < c->n_local; ++li) {
     const TileGeom &g = c->tiles[li].g;
-    float *d = nullptr;
-    CU(c, cudaMalloc(&d, (size_t)g.th * g.tw * sizeof(float)));
-    CU(c, cudaMemcpy2DAsync(d, (size_t)g.tw * sizeof(float), src[li] + (size_t)g.h * g.pitch + g.hx,
+    CU(c, cudaMemcpy2DAsync(bufs[li], (size_t)g.tw * sizeof(float), src[li] + (size_t)g.h * g.pitch + g.hx,
                             (size_t)g.pitch * sizeof(float), (size_t)g.tw * sizeof(float), g.th,
                             cudaMemcpyDeviceToDevice, c->stream));
-    bufs.push_back(d);
   }
   pnpula_rect dst = global ? pnpula_rect{0, 0, c->ny, c->nx} : c->bbox;
-  pnpula_status s = gather_fields(c, bufs, 1, {host}, dst, global);
-  for (float *d : bufs) cudaFree(d);
-  return s;
+  return gather_fields(c, bufs, 1, {host}, dst, global);
 }
 
 }  // namespace
@@ -1142,21 +1171,20 @@ pnpula_status pnpula_get_moments(pnpula_ctx *c, float *mean, float *var, int64_t
   if ((mean && n < 1) || (var && n < 2)) { set_error("not enough post-burn-in samples (%lld)", (long long)n); return PNPULA_E_STATS_EMPTY; }
   if (global && c->rank == 0 && c->world > 1 && ((mean && false) || false)) {}
   std::vector<float *> bufs;
-  for (auto &td : c->tiles) {
+  s = tile_staging(c, 2, bufs);
+  if (s) return s;
+  for (size_t li = 0; li < c->tiles.size(); ++li) {
+    auto &td = c->tiles[li];
     const TileGeom &g = td.g;
-    float *d = nullptr;
-    CU(c, cudaMalloc(&d, (size_t)g.th * g.tw * 2 * sizeof(float)));
+    float *d = bufs[li];
     FinalizeParams p{};
     p.mean = td.mean; p.m2 = td.m2; p.g = g;
     p.out_mean = d; p.out_var = d + (size_t)g.th * g.tw;
     p.inv_nm1 = n >= 2 ? (float)(1.0 / (double)(n - 1)) : 0.f;
     CU(c, launch_finalize(p, c->stream));
-    bufs.push_back(d);
   }
   pnpula_rect dst = global ? pnpula_rect{0, 0, c->ny, c->nx} : c->bbox;
-  s = gather_fields(c, bufs, 2, {mean, var}, dst, global);
-  for (float *d : bufs) cudaFree(d);
-  return s;
+  return gather_fields(c, bufs, 2, {mean, var}, dst, global);
 }
 
 pnpula_status pnpula_get_state(pnpula_ctx *c, float *x, float *z, int64_t *t, int32_t scope) {
@@ -1377,6 +1405,7 @@ pnpula_status pnpula_destroy(pnpula_ctx *c) {
   }
   for (auto p : c->d_w) cudaFree(p);
   for (auto p : c->d_b) cudaFree(p);
+  if (c->scratch) cudaFree(c->scratch);
   cudaFree(c->ddfb_u0); cudaFree(c->ddfb_fin);
   for (auto p : c->ddfb_t) cudaFree(p);
   for (auto p : c->ddfb_adj) cudaFree(p);

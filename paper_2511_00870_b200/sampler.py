@@ -123,10 +123,14 @@ class Sampler:
             return (self.ny, self.nx) if self.rank == 0 else None
         return (self.bbox[2], self.bbox[3])
 
-    def moments(self, scope: int = L.SCOPE_LOCAL, want_var: bool = True):
+    def moments(self, scope: int = L.SCOPE_LOCAL, want_var: bool = True, out=None):
+        """out: optional (mean, var) host arrays (e.g. pinned) to write into."""
         shp = self._out_shape(scope)
-        mean = np.zeros(shp, np.float32) if shp else None
-        var = np.zeros(shp, np.float32) if (shp and want_var) else None
+        if out is not None:
+            mean, var = out
+        else:
+            mean = np.zeros(shp, np.float32) if shp else None
+            var = np.zeros(shp, np.float32) if (shp and want_var) else None
         n = C.c_int64()
         L.check(self._lib.pnpula_get_moments(self._h, L._ptr(mean), L._ptr(var), C.byref(n), scope))
         return mean, var, n.value
