@@ -59,7 +59,7 @@ typedef enum {
   PNPULA_OK = 0,
   PNPULA_E_INVALID_ARG = 1,        /* null pointer, non-positive step, even kernel, kappa not in (0, rho) */
   PNPULA_E_SHAPE = 2,              /* in_rect does not cover the rank's tiles (+) r_H, bad sizes */
-  PNPULA_E_PARTITION_TOO_FINE = 3, /* a tile extent < halo width h (Def. 1 (i)) */
+  PNPULA_E_PARTITION_TOO_FINE = 3, /* a tile extent < halo width h along an axis with >= 2 tiles (Def. 1 (i)) */
   PNPULA_E_STEPSIZE = 4,           /* reserved: eq:stepsize_cond violations are warnings only */
   PNPULA_E_STATS_EMPTY = 5,        /* fewer than 1 (mean) / 2 (variance) post-burn-in samples */
   PNPULA_E_STATE = 6,              /* context poisoned by an earlier CUDA/NCCL error, or wrong call order */
@@ -271,7 +271,7 @@ typedef struct {
 /* All messages of one exchange for a tiles_y x tiles_x grid and halo h, in the
  * canonical (src_tile, dst_tile) order used to post NCCL sends/receives.
  * Writes at most cap messages to out (out may be NULL) and returns the total count,
- * or -1 if a tile extent is smaller than h. */
+ * or -1 if a tile extent is smaller than h along an axis split into >= 2 tiles. */
 int32_t pnpula_plan_halo(int32_t ny, int32_t nx, int32_t tiles_y, int32_t tiles_x, int32_t h,
                          pnpula_halo_msg *out, int32_t cap);
 

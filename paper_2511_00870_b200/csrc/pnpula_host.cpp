@@ -614,7 +614,9 @@ int32_t pnpula_plan_halo(int32_t ny, int32_t nx, int32_t tiles_y, int32_t tiles_
   std::vector<pnpula_rect> rects(nt);
   for (int t = 0; t < nt; ++t) {
     tile_rect(ny, nx, tiles_y, tiles_x, t, &rects[t]);
-    if (rects[t].h < h || rects[t].w < h) return -1;
+    // a tile narrower than h would need ghost rows from beyond its neighbour; along an axis with
+    // a single tile there is no neighbour, so any extent works there
+    if ((tiles_y > 1 && rects[t].h < h) || (tiles_x > 1 && rects[t].w < h)) return -1;
   }
   if (h == 0) return 0;
   int count = 0;
@@ -773,7 +775,7 @@ pnpula_status pnpula_create(const pnpula_config *cfg, pnpula_ctx **out) {
   for (int li = 0; li < c->n_local; ++li) {
     pnpula_rect r;
     tile_rect(f.ny, f.nx, f.tiles_y, f.tiles_x, c->first_tile + li, &r);
-    if (r.h < c->h || r.w < c->h) {
+    if ((f.tiles_y > 1 && r.h < c->h) || (f.tiles_x > 1 && r.w < c->h)) {
       set_error("tile %dx%d smaller than halo width %d", r.h, r.w, c->h);
       delete c;
       return PNPULA_E_PARTITION_TOO_FINE;
