@@ -255,6 +255,13 @@ void pnpula_partition(int64_t n, int64_t parts, int64_t p, int64_t *lo, int64_t 
 /* Halo width h = max(2 r_H, K) (receptive-field strategy, R5). */
 int32_t pnpula_halo_width(int32_t op, int32_t kh, int32_t kw, int32_t n_layers);
 
+/* [collective] ||H||_2^2 of this context's forward operator (the same-size, zero-boundary
+ * convolution over the whole image, every tile and rank) by `iters` >= 2 power iterations on the
+ * GPU (v <- H^T H v / ||.||, Rayleigh quotient of the last unit iterate; start vector = fixed
+ * Philox normals).  OP_MASK returns 1.  Uses the idle x buffer as scratch: call between
+ * iterations only (the chain state is untouched).  SURVEY 8(f) rank 4 (step sizes P:774/P:782). */
+pnpula_status pnpula_opnorm2(pnpula_ctx *ctx, int32_t iters, double *out);
+
 /* Host helper for the step sizes: upper bound of ||H||_2^2 for the same-size,
  * zero-boundary convolution with the kh x kw kernel k (host, row-major): max over a grid x grid
  * DFT of |K(w)|^2 (the zero-boundary operator is a restriction of the full convolution, whose

@@ -97,6 +97,7 @@ def load():
         "pnpula_save_checkpoint": ([vp, vp, u64], C.c_int),
         "pnpula_load_checkpoint": ([vp, vp, u64], C.c_int),
         "pnpula_conv_norm2_bound": ([vp, i32, i32, i32, C.POINTER(d)], C.c_int),
+        "pnpula_opnorm2": ([vp, i32, C.POINTER(d)], C.c_int),
         "pnpula_tile_info": ([vp, i32, C.POINTER(Rect), C.POINTER(i32), C.POINTER(i32)], C.c_int),
         "pnpula_get_padded_x": ([vp, i32, vp], C.c_int),
         "pnpula_get_denoiser_residual": ([vp, vp], C.c_int),
@@ -122,7 +123,7 @@ EXPORTED = ["pnpula_version", "pnpula_last_error", "pnpula_get_unique_id", "pnpu
             "pnpula_get_state", "pnpula_get_z1", "pnpula_get_tv_zh", "pnpula_tile_info", "pnpula_get_padded_x", "pnpula_get_denoiser_residual",
             "pnpula_set_timing", "pnpula_kernel_time", "pnpula_destroy", "pnpula_partition",
             "pnpula_halo_width", "pnpula_plan_halo", "pnpula_check_stepsizes", "pnpula_checkpoint_bytes",
-            "pnpula_save_checkpoint", "pnpula_load_checkpoint", "pnpula_conv_norm2_bound"]
+            "pnpula_save_checkpoint", "pnpula_load_checkpoint", "pnpula_conv_norm2_bound", "pnpula_opnorm2"]
 
 
 def last_error() -> str:

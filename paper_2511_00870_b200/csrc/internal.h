@@ -125,6 +125,19 @@ struct CnnChunkParams {
 // Launchers (return cudaGetLastError()).
 cudaError_t launch_update(const UpdateParams &p, cudaStream_t s);
 cudaError_t launch_z1_update(const Z1Params &p, cudaStream_t s);
+
+// power iteration for ||H||^2 (pnpula_opnorm2)
+struct OpNormParams {
+  float *v;          // padded iterate (halo exchanged)
+  float *w;          // padded H v on tile (+) r_H
+  float *u;          // padded H^T H v on the tile
+  double *acc;       // [0] sum u^2, [1] sum u.v (device, accumulated over tiles)
+  TileGeom g;
+  int ny, nx, ry, rx;
+  float k2d[kMaxTaps * kMaxTaps];
+};
+// which: 0 init v, 1 w = H v, 2 u = H^T w (+ sums), 3 v = u * (*scale)
+cudaError_t launch_opnorm(int which, const OpNormParams &p, const double *scale, cudaStream_t s);
 cudaError_t launch_tv_z_update(const TvZParams &p, cudaStream_t s);
 cudaError_t launch_copy_jobs(const CopyJob *d_jobs, int njobs, int max_rows, cudaStream_t s);
 cudaError_t launch_fill(float *p, float v, size_t n, cudaStream_t s);

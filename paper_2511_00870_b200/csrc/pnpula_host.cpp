@@ -1307,6 +1307,78 @@ pnpula_status pnpula_load_checkpoint(pnpula_ctx *c, const void *buf, uint64_t by
   return PNPULA_OK;
 }
 
+pnpula_status pnpula_opnorm2(pnpula_ctx *c, int32_t iters, double *out) {
+  pnpula_status s = check_ctx(c);
+  if (s) return s;
+  if (!out || iters < 2) { set_error("need an output and iters >= 2"); return PNPULA_E_INVALID_ARG; }
+  if (c->op == PNPULA_OP_MASK) { *out = 1.0; return PNPULA_OK; }   // diag(m), m in {0, 1}
+  CU(c, cudaSetDevice(c->device));
+  const int vb = c->cur ^ 1;   // the iterate lives in the idle x buffer (rewritten by the next step)
+  std::vector<float *> tmp;
+  double *d_acc = nullptr;
+  auto cleanup = [&]() {
+    for (float *t : tmp) cudaFree(t);
+    if (d_acc) cudaFree(d_acc);
+  };
+  auto params = [&](TileDev &td, int li) {
+    OpNormParams q{};
+    q.v = td.x[vb];
+    q.w = tmp[2 * li];
+    q.u = tmp[2 * li + 1];
+    q.acc = d_acc;
+    q.g = td.g;
+    q.ny = c->ny; q.nx = c->nx; q.ry = c->ry; q.rx = c->rx;
+    const int kh = 2 * c->ry + 1, kw = 2 * c->rx + 1;
+    for (int a = 0; a < kh; ++a)
+      for (int b = 0; b < kw; ++b) q.k2d[a * kw + b] = c->separable ? c->ky[a] * c->kx[b] : c->k2d[a * kw + b];
+    return q;
+  };
+  for (auto &td : c->tiles) {
+    const size_t n = geom_elems(td.g) * sizeof(float);
+    for (int i = 0; i < 2; ++i) {
+      float *t = nullptr;
+      cudaError_t e = cudaMalloc(&t, n);
+      if (e == cudaSuccess) e = cudaMemsetAsync(t, 0, n, c->stream);
+      if (e != cudaSuccess) { cleanup(); return fail_cuda(c, e, "opnorm buffers", __LINE__); }
+      tmp.push_back(t);
+    }
+  }
+  cudaError_t e = cudaMalloc(&d_acc, 3 * sizeof(double));
+  if (e != cudaSuccess) { cleanup(); return fail_cuda(c, e, "opnorm acc", __LINE__); }
+  double lam = 0.0;
+  for (int li = 0; li < c->n_local; ++li) {
+    e = launch_opnorm(0, params(c->tiles[li], li), nullptr, c->stream);
+    if (e != cudaSuccess) { cleanup(); return fail_cuda(c, e, "opnorm init", __LINE__); }
+  }
+  s = exchange(c, vb);
+  for (int it = 0; it < iters && !s; ++it) {
+    e = cudaMemsetAsync(d_acc, 0, 2 * sizeof(double), c->stream);
+    for (int li = 0; li < c->n_local && e == cudaSuccess; ++li) e = launch_opnorm(1, params(c->tiles[li], li), nullptr, c->stream);
+    for (int li = 0; li < c->n_local && e == cudaSuccess; ++li) e = launch_opnorm(2, params(c->tiles[li], li), nullptr, c->stream);
+    if (e != cudaSuccess) { cleanup(); return fail_cuda(c, e, "opnorm iteration", __LINE__); }
+    if (c->world > 1) {
+      ncclResult_t r = ncclAllReduce(d_acc, d_acc, 2, ncclFloat64, ncclSum, c->comm, c->stream);
+      if (r != ncclSuccess) { cleanup(); return fail_nccl(c, r, "ncclAllReduce", __LINE__); }
+    }
+    double h[2];
+    e = cudaMemcpyAsync(h, d_acc, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    if (e != cudaSuccess) { cleanup(); return fail_cuda(c, e, "opnorm sums", __LINE__); }
+    // v has unit norm from the second iteration on: Rayleigh quotient u.v = v^T H^T H v
+    if (it > 0) lam = h[1];
+    const double sc = h[0] > 0 ? 1.0 / std::sqrt(h[0]) : 0.0;
+    e = cudaMemcpyAsync(d_acc + 2, &sc, sizeof(double), cudaMemcpyHostToDevice, c->stream);
+    for (int li = 0; li < c->n_local && e == cudaSuccess; ++li) e = launch_opnorm(3, params(c->tiles[li], li), d_acc + 2, c->stream);
+    if (e != cudaSuccess) { cleanup(); return fail_cuda(c, e, "opnorm scale", __LINE__); }
+    s = exchange(c, vb);
+    if (!s) { e = cudaStreamSynchronize(c->stream); if (e != cudaSuccess) { cleanup(); return fail_cuda(c, e, "opnorm sync", __LINE__); } }
+  }
+  cleanup();
+  if (s) return s;
+  *out = lam;
+  return PNPULA_OK;
+}
+
 pnpula_status pnpula_conv_norm2_bound(const float *k, int32_t kh, int32_t kw, int32_t grid, double *out) {
   if (!k || !out || kh <= 0 || kw <= 0 || grid < std::max(kh, kw)) {
     set_error("bad kernel / grid"); return PNPULA_E_INVALID_ARG;

@@ -679,6 +679,93 @@ __global__ void __launch_bounds__(NTHREADS) tv_z_kernel(const __grid_constant__ 
   }
 }
 
+// ---------------------------------------------------------------- power iteration for ||H||^2
+// (step sizes of P:774 / P:782 need ||H||^2).  v: padded with a valid halo
+// (>= 2 r_H).  Pass 1: w = H v on tile (+) r_H, zero outside the image.  Pass 2: u = H^T w on the
+// tile, written in place of v's interior is NOT allowed (v is read by neighbours' pass 1), so into
+// the padded u buffer; per-block partial sums of u^2 and u.v go to acc[0], acc[1] (fp64 atomics).
+__global__ void __launch_bounds__(NTHREADS) opnorm_fwd_kernel(const __grid_constant__ OpNormParams p) {
+  const TileGeom &g = p.g;
+  const int ry = p.ry, rx = p.rx, kw = 2 * rx + 1;
+  const int r0 = max(g.i0 - ry, 0), r1 = min(g.i0 + g.th + ry, p.ny);
+  const int c0 = max(g.j0 - rx, 0), c1 = min(g.j0 + g.tw + rx, p.nx);
+  const int w = c1 - c0;
+  const int64_t total = (int64_t)w * (r1 - r0);
+  for (int64_t e = (int64_t)blockIdx.x * NTHREADS + threadIdx.x; e < total; e += (int64_t)gridDim.x * NTHREADS) {
+    const int gi = r0 + (int)(e / w), gj = c0 + (int)(e % w);
+    float s = 0.f;
+    for (int a = 0; a < 2 * ry + 1; ++a) {
+      const float *vr = p.v + pidx(g, gi - (a - ry), gj + rx);
+      const float *kr = p.k2d + a * kw;
+      for (int b = 0; b < kw; ++b) s = fmaf(kr[b], __ldg(vr - b), s);
+    }
+    p.w[pidx(g, gi, gj)] = s;
+  }
+}
+
+__global__ void __launch_bounds__(NTHREADS) opnorm_adj_kernel(const __grid_constant__ OpNormParams p) {
+  const TileGeom &g = p.g;
+  const int ry = p.ry, rx = p.rx, kw = 2 * rx + 1;
+  const int64_t total = (int64_t)g.th * g.tw;
+  double su = 0.0, suv = 0.0;
+  for (int64_t e = (int64_t)blockIdx.x * NTHREADS + threadIdx.x; e < total; e += (int64_t)gridDim.x * NTHREADS) {
+    const int gi = g.i0 + (int)(e / g.tw), gj = g.j0 + (int)(e % g.tw);
+    float s = 0.f;   // (H^T w)[i][j] = sum_{a,b} k[a][b] w[i + (a - ry)][j + (b - rx)], w = 0 outside the image
+    for (int a = 0; a < 2 * ry + 1; ++a) {
+      const int ii = gi + (a - ry);
+      if (ii < 0 || ii >= p.ny) continue;
+      for (int b = 0; b < kw; ++b) {
+        const int jj = gj + (b - rx);
+        if (jj < 0 || jj >= p.nx) continue;
+        s = fmaf(p.k2d[a * kw + b], p.w[pidx(g, ii, jj)], s);
+      }
+    }
+    const int64_t n = pidx(g, gi, gj);
+    p.u[n] = s;
+    su += (double)s * s;
+    suv += (double)s * p.v[n];
+  }
+  // block reduction then one fp64 atomic per block and quantity
+  __shared__ double red[2][NTHREADS / 32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    su += __shfl_down_sync(0xffffffffu, su, o);
+    suv += __shfl_down_sync(0xffffffffu, suv, o);
+  }
+  if ((threadIdx.x & 31) == 0) { red[0][threadIdx.x >> 5] = su; red[1][threadIdx.x >> 5] = suv; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int i = 0; i < NTHREADS / 32; ++i) { a += red[0][i]; b += red[1][i]; }
+    atomicAdd(p.acc, a);
+    atomicAdd(p.acc + 1, b);
+  }
+}
+
+// v <- u * scale on the tile interior (the halo is refreshed by the exchange)
+__global__ void opnorm_scale_kernel(const __grid_constant__ OpNormParams p, const double *scale) {
+  const TileGeom &g = p.g;
+  const float sc = (float)*scale;
+  const int64_t total = (int64_t)g.th * g.tw;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int gi = g.i0 + (int)(e / g.tw), gj = g.j0 + (int)(e % g.tw);
+    const int64_t n = pidx(g, gi, gj);
+    p.v[n] = p.u[n] * sc;
+  }
+}
+
+// deterministic start vector: Philox normals (stream 7, iteration 0) on the interior
+__global__ void opnorm_init_kernel(const __grid_constant__ OpNormParams p) {
+  const TileGeom &g = p.g;
+  const int64_t total = (int64_t)g.th * g.tw;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int gi = g.i0 + (int)(e / g.tw), gj = g.j0 + (int)(e % g.tw);
+    float z[4];
+    normals4(0x2511u, 0x870u, (uint32_t)gj >> 2, (uint32_t)gi, 0u, 7u, z);
+    p.v[pidx(g, gi, gj)] = z[gj & 3];
+  }
+}
+
 // ---------------------------------------------------------------- mask K7 (no stencil)
 __global__ void __launch_bounds__(NTHREADS) update_mask_kernel(const __grid_constant__ UpdateParams p) {
   const TileGeom &g = p.g;
@@ -849,6 +936,17 @@ cudaError_t launch_tv_z_update(const TvZParams &p, cudaStream_t s) {
   if (blocks > 148 * 16) blocks = 148 * 16;
   if (blocks < 1) blocks = 1;
   tv_z_kernel<<<(unsigned)blocks, NTHREADS, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_opnorm(int which, const OpNormParams &p, const double *scale, cudaStream_t s) {
+  const int blocks = 148 * 4;
+  switch (which) {
+    case 0: opnorm_init_kernel<<<blocks, NTHREADS, 0, s>>>(p); break;
+    case 1: opnorm_fwd_kernel<<<blocks, NTHREADS, 0, s>>>(p); break;
+    case 2: opnorm_adj_kernel<<<blocks, NTHREADS, 0, s>>>(p); break;
+    default: opnorm_scale_kernel<<<blocks, NTHREADS, 0, s>>>(p, scale); break;
+  }
   return cudaGetLastError();
 }
 

@@ -157,6 +157,12 @@ class Sampler:
         L.check(self._lib.pnpula_get_tv_zh(self._h, L._ptr(out), scope))
         return out
 
+    def opnorm2(self, iters: int = 100) -> float:
+        """||H||^2 by power iteration on the GPU (collective)."""
+        out = C.c_double()
+        L.check(self._lib.pnpula_opnorm2(self._h, iters, C.byref(out)))
+        return out.value
+
     def save_checkpoint(self) -> bytes:
         """This rank's complete chain state (resume with load_checkpoint on an identical context)."""
         n = C.c_uint64()

@@ -86,3 +86,43 @@ def test_single_post_burn_in_sample_and_large_seed():
         s.close()
     o = oracle.run(pb, 7, 6, seed, want_var=False)
     assert rel_l2(x, o["x"]) <= 1e-5
+
+
+@pytest.mark.parametrize("tiles", [(1, 1), (2, 2)])
+def test_opnorm2_power_iteration(tiles):
+    """||H||^2 on the GPU (power iteration over the tiled operator) vs the largest eigenvalue of
+    H^T H from a dense matrix built with scipy (zero-boundary same-size convolution)."""
+    from scipy.signal import convolve2d
+    ny, nx = 30, 27
+    k = synth.random_kernel(5, 5, seed=4) - 0.02
+    H = np.zeros((ny * nx, ny * nx))
+    for n in range(ny * nx):
+        e = np.zeros(ny * nx)
+        e[n] = 1.0
+        H[:, n] = convolve2d(e.reshape(ny, nx), k, mode="same").ravel()
+    lam = np.linalg.eigvalsh(H.T @ H)[-1]
+    kw, _ = _conv_problem(ny, nx, k)
+    s = Sampler(**kw, tiles=tiles)
+    try:
+        est = s.opnorm2(400)
+    finally:
+        s.close()
+    # Rayleigh quotients never exceed lambda_max; the top of this spectrum is clustered
+    # (0.24656, 0.24630, 0.24486, ...), so 400 iterations land within ~1 % of it
+    assert lam * 0.99 <= est <= lam * (1 + 1e-5)
+    # a kernel with a well-separated top eigenvalue: 2 taps, converges fast
+    k2 = np.zeros((3, 3))
+    k2[1, 1], k2[1, 2] = 1.0, 0.9
+    H2 = np.zeros((ny * nx, ny * nx))
+    for n in range(ny * nx):
+        e = np.zeros(ny * nx)
+        e[n] = 1.0
+        H2[:, n] = convolve2d(e.reshape(ny, nx), k2, mode="same").ravel()
+    lam2 = np.linalg.eigvalsh(H2.T @ H2)[-1]
+    kw2, _ = _conv_problem(ny, nx, k2)
+    s = Sampler(**kw2, tiles=tiles)
+    try:
+        est2 = s.opnorm2(3000)
+    finally:
+        s.close()
+    assert lam2 * 0.999 <= est2 <= lam2 * (1 + 1e-5)
