@@ -75,7 +75,9 @@ enum { PNPULA_SCOPE_LOCAL = 0, PNPULA_SCOPE_GLOBAL_ON_ROOT = 1 };
 /* flags */
 #define PNPULA_FLAG_HALO_VIA_NCCL 0x1  /* route same-rank halos through NCCL self send/recv (tests) */
 #define PNPULA_FLAG_CNN_LAYERWISE 0x2  /* one CNN layer per launch instead of fused layer chains */
-#define PNPULA_FLAG_NO_GRAPH      0x4  /* reserved (kernels are always launched directly) */
+#define PNPULA_FLAG_NO_GRAPH      0x4  /* launch every kernel directly (default: after the first iteration, each
+                                         iteration replays a captured CUDA graph when it is single-rank and
+                                         untimed; env PNPULA_GRAPHS=0 does the same) */
 
 typedef struct {
   int32_t i0, j0, h, w; /* rectangle of global pixel coordinates: rows [i0, i0+h), cols [j0, j0+w) */

@@ -18,6 +18,16 @@ struct TileGeom {
   int pitch;            // floats per padded row (multiple of 32)
 };
 
+// Iteration state on the device for CUDA-graph replays (the graph of one iteration is replayed
+// with unchanged parameters).  Two slots: the graph for x-buffer parity b reads slot b (this
+// iteration's scalars) and its first update kernel writes slot b^1 (the next iteration's).
+struct IterState {
+  long long t1;           // iteration index t+1
+  long long burn_in;
+  int accumulate;         // t1 > burn_in
+  float inv_n;            // 1 / (t1 - burn_in)
+};
+
 // K7: fused data-fidelity stencil + Moreau box + AXDA coupling + ULA update +
 // Philox/Box-Muller noise + z PSGLA step + Welford moments, one tile.
 struct UpdateParams {
@@ -48,6 +58,8 @@ struct UpdateParams {
   int has_tv;                      // TV prior (R37): - a_tv D^T (D x - z) and x+ = max(., 0)
   float a_tv;                      // gamma / rho
   const float *zv, *zh;            // padded z = (z_v, z_h) ~ D x, valid on tile (+) 1
+  const IterState *it;             // non-null: t1 / accumulate / inv_n from here (graph replay)
+  IterState *it_next;              // non-null: block 0 writes the next iteration's scalars here
 };
 
 // TV z block (R37, R38): on tile (+) 1 inside the image
@@ -60,6 +72,7 @@ struct TvZParams {
   int ny, nx;
   float b, s, tau;      // kappa/rho, sqrt(2 kappa), kappa beta
   uint32_t seed_lo, seed_hi, t1;
+  const IterState *it;  // non-null: t1 from here (graph replay)
 };
 
 // z1 block of the Poisson posterior (readings R32-R34): on tile (+) r_H (inside the image)
@@ -77,6 +90,7 @@ struct Z1Params {
   float ky[kMaxTaps], kx[kMaxTaps];
   float eta, b1, s1, kappa1;        // eta, kappa1/rho1, sqrt(2 kappa1), kappa1
   uint32_t seed_lo, seed_hi, t1;
+  const IterState *it;              // non-null: t1 from here (graph replay)
 };
 
 // One rectangular copy between pitched fp32 buffers (halo exchange, pack/unpack).

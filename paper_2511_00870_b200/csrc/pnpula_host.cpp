@@ -124,6 +124,14 @@ struct pnpula_ctx {
   Timer tm_cnn, tm_update, tm_halo;
   int64_t n_launches = 0;   // kernels of this library launched (all classes)
   bool traced = false;      // PNPULA_CNN_TRACE written
+
+  // CUDA graphs of one iteration, one per x-buffer parity (see step())
+  IterState *d_iter = nullptr;     // [2], see IterState
+  cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+  int64_t glaunches[2] = {0, 0};   // kernels per replay
+  int64_t dev_t = -1;              // iteration count held by d_iter (-1: unknown)
+  bool graphs_off = false;         // PNPULA_FLAG_NO_GRAPH or PNPULA_GRAPHS=0
+  bool warm = false;               // one direct iteration done (modules loaded, attributes set)
 };
 
 namespace {
@@ -419,8 +427,10 @@ UpdateParams make_update_params(pnpula_ctx *c, TileDev &td, int buf) {
   return p;
 }
 
-pnpula_status step(pnpula_ctx *c) {
-  const int buf = c->cur;
+// Enqueue one iteration reading x[buf]. it == nullptr: the iteration scalars go by value
+// (t1 = c->t + 1); otherwise every kernel reads them from it = d_iter[buf] and the first
+// update launch writes the next iteration's into d_iter[buf ^ 1] (graph capture).
+pnpula_status enqueue_step(pnpula_ctx *c, int buf, const IterState *it) {
   if (c->n_layers > 0) {
     pnpula_status s = run_cnn(c, buf);
     if (s) return s;
@@ -433,6 +443,8 @@ pnpula_status step(pnpula_ctx *c) {
     p.t1 = (uint32_t)t1;
     p.accumulate = acc;
     p.inv_n = (float)(1.0 / k);
+    p.it = it;
+    p.it_next = (it && &td == &c->tiles[0]) ? c->d_iter + (buf ^ 1) : nullptr;
     cudaEvent_t end;
     timer_begin(c, c->tm_update, &end);
     CU(c, launch_update(p, c->stream));
@@ -456,6 +468,7 @@ pnpula_status step(pnpula_ctx *c) {
       q.seed_lo = (uint32_t)c->seed;
       q.seed_hi = (uint32_t)(c->seed >> 32);
       q.t1 = (uint32_t)t1;
+      q.it = it;
       cudaEvent_t end;
       timer_begin(c, c->tm_update, &end);
       CU(c, launch_tv_z_update(q, c->stream));
@@ -489,12 +502,67 @@ pnpula_status step(pnpula_ctx *c) {
       q.seed_lo = (uint32_t)c->seed;
       q.seed_hi = (uint32_t)(c->seed >> 32);
       q.t1 = (uint32_t)t1;
+      q.it = it;
       cudaEvent_t end;
       timer_begin(c, c->tm_update, &end);
       CU(c, launch_z1_update(q, c->stream));
       c->n_launches++;
       timer_end(c, end);
     }
+  }
+  return PNPULA_OK;
+}
+
+void drop_graphs(pnpula_ctx *c) {
+  for (int b = 0; b < 2; ++b) {
+    if (c->gexec[b]) cudaGraphExecDestroy(c->gexec[b]);
+    c->gexec[b] = nullptr;
+  }
+  c->dev_t = -1;
+}
+
+// Replays are used when nothing in the iteration needs the host between kernels: no per-kernel
+// timing events, no pipeline trace, no NCCL messages (single rank, device-copy exchange).
+bool graph_eligible(const pnpula_ctx *c) {
+  return c->warm && !c->graphs_off && !c->timing && c->sends.empty() && c->recvs.empty() && !getenv("PNPULA_CNN_TRACE");
+}
+
+pnpula_status step(pnpula_ctx *c) {
+  const int buf = c->cur;
+  if (graph_eligible(c)) {
+    if (!c->gexec[buf]) {
+      // capture: every scalar of the iteration read from d_iter[buf]
+      const int64_t n0 = c->n_launches;
+      cudaGraph_t g = nullptr;
+      CU(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeRelaxed));
+      pnpula_status s = enqueue_step(c, buf, c->d_iter + buf);
+      const cudaError_t e2 = cudaStreamEndCapture(c->stream, &g);
+      if (s) { if (g) cudaGraphDestroy(g); return s; }
+      CU(c, e2);
+      const cudaError_t e3 = cudaGraphInstantiate(&c->gexec[buf], g, 0);
+      cudaGraphDestroy(g);
+      CU(c, e3);
+      c->glaunches[buf] = c->n_launches - n0;
+      c->n_launches = n0;
+    }
+    if (c->dev_t != c->t) {   // d_iter[buf] does not hold iteration t+1 (reset, load, direct steps)
+      const int64_t t1 = c->t + 1;
+      const bool acc = t1 > c->burn_in;
+      IterState h{};
+      h.t1 = t1;
+      h.burn_in = c->burn_in;
+      h.accumulate = acc;
+      h.inv_n = (float)(1.0 / (acc ? (double)(t1 - c->burn_in) : 1.0));
+      CU(c, cudaMemcpyAsync(c->d_iter + buf, &h, sizeof(h), cudaMemcpyHostToDevice, c->stream));
+      CU(c, cudaStreamSynchronize(c->stream));   // h is a stack (pageable) buffer
+    }
+    CU(c, cudaGraphLaunch(c->gexec[buf], c->stream));
+    c->n_launches += c->glaunches[buf];
+    c->dev_t = c->t + 1;   // d_iter[buf ^ 1] now holds iteration t+2
+  } else {
+    pnpula_status s = enqueue_step(c, buf, nullptr);
+    if (s) return s;
+    c->warm = true;
   }
   c->cur ^= 1;
   c->t += 1;
@@ -824,6 +892,11 @@ pnpula_status pnpula_create(const pnpula_config *cfg, pnpula_ctx **out) {
   } while (0)
   CUB(cudaMalloc(&c->d_err, sizeof(int)));
   CUB(cudaMemsetAsync(c->d_err, 0, sizeof(int), c->stream));
+  CUB(cudaMalloc(&c->d_iter, 2 * sizeof(IterState)));
+  {
+    const char *ge = getenv("PNPULA_GRAPHS");
+    c->graphs_off = (f.flags & PNPULA_FLAG_NO_GRAPH) != 0 || (ge && atoi(ge) == 0);
+  }
 
   if (f.world_size > 1) {
     if (!f.nccl_uid) { set_error("nccl_uid required when world_size > 1"); return bail(PNPULA_E_INVALID_ARG); }
@@ -993,6 +1066,7 @@ pnpula_status pnpula_reset(pnpula_ctx *c, int64_t burn_in, uint64_t seed) {
     CU(c, cudaMemsetAsync(td.mean, 0, n, c->stream));
     CU(c, cudaMemsetAsync(td.m2, 0, n, c->stream));
   }
+  drop_graphs(c);
   c->cur = 0;
   c->t = 0;
   c->burn_in = burn_in;
@@ -1300,6 +1374,7 @@ pnpula_status pnpula_load_checkpoint(pnpula_ctx *c, const void *buf, uint64_t by
     }
   }
   CU(c, cudaStreamSynchronize(c->stream));
+  drop_graphs(c);
   c->t = h.t;
   c->burn_in = h.burn_in;
   c->seed = h.seed;
@@ -1487,6 +1562,8 @@ pnpula_status pnpula_destroy(pnpula_ctx *c) {
     cudaFree(c->d_local_jobs[b]); cudaFree(c->d_pack_jobs[b]); cudaFree(c->d_unpack_jobs[b]);
   }
   cudaFree(c->d_sendbuf); cudaFree(c->d_recvbuf); cudaFree(c->d_err);
+  drop_graphs(c);
+  cudaFree(c->d_iter);
   for (Timer *t : {&c->tm_cnn, &c->tm_update, &c->tm_halo})
     for (auto &e : t->ev) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
   if (c->comm) ncclCommDestroy(c->comm);

@@ -77,6 +77,26 @@ __device__ __forceinline__ void normals4(uint32_t seed_lo, uint32_t seed_hi, uin
   out[0] = a.x; out[1] = a.y; out[2] = b.x; out[3] = b.y;
 }
 
+// Iteration scalars: by value (direct launches) or from the device IterState (CUDA-graph
+// replays; see IterState).
+template <class P> __device__ __forceinline__ uint32_t it_t1(const P &p) {
+  return p.it ? (uint32_t)__ldg(&p.it->t1) : p.t1;
+}
+// (read-only loads: nothing in the kernel writes *p.it, so the compiler may keep them in registers)
+__device__ __forceinline__ int it_acc(const UpdateParams &p) { return p.it ? __ldg(&p.it->accumulate) : p.accumulate; }
+__device__ __forceinline__ float it_inv_n(const UpdateParams &p) { return p.it ? __ldg(&p.it->inv_n) : p.inv_n; }
+// next iteration's scalars (same fp64 -> fp32 rounding of 1 / (t+2 - burn_in) as the host's)
+__device__ __forceinline__ void it_advance(const UpdateParams &p) {
+  if (p.it_next && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+    const long long t1 = p.it->t1 + 1, b = p.it->burn_in;
+    const bool acc = t1 > b;
+    p.it_next->t1 = t1;
+    p.it_next->burn_in = b;
+    p.it_next->accumulate = acc;
+    p.it_next->inv_n = (float)(1.0 / (acc ? (double)(t1 - b) : 1.0));
+  }
+}
+
 __device__ __forceinline__ int64_t pidx(const TileGeom &g, int gi, int gj) {
   return (int64_t)(gi - (g.i0 - g.h)) * g.pitch + (gj - (g.j0 - g.hx));
 }
@@ -106,7 +126,7 @@ __device__ __forceinline__ void ula_load(const UpdateParams &p, int gi, int gj4,
       const float4 b = *reinterpret_cast<const float4 *>(p.z + base);
       q.z[0] = b.x; q.z[1] = b.y; q.z[2] = b.z; q.z[3] = b.w;
     }
-    if (p.accumulate) {
+    if (it_acc(p)) {
       const float4 a2 = *reinterpret_cast<const float4 *>(p.mean + base);
       const float4 b2 = *reinterpret_cast<const float4 *>(p.m2 + base);
       q.m[0] = a2.x; q.m[1] = a2.y; q.m[2] = a2.z; q.m[3] = a2.w;
@@ -118,7 +138,7 @@ __device__ __forceinline__ void ula_load(const UpdateParams &p, int gi, int gj4,
       q.x[l] = p.x[base + l];
       if (p.has_G) q.G[l] = p.G[base + l];
       if (p.has_z) q.z[l] = p.z[base + l];
-      if (p.accumulate) { q.m[l] = p.mean[base + l]; q.s[l] = p.m2[base + l]; }
+      if (it_acc(p)) { q.m[l] = p.mean[base + l]; q.s[l] = p.m2[base + l]; }
     }
   }
 }
@@ -152,7 +172,7 @@ __device__ __forceinline__ void ula_finish(const UpdateParams &p, int gi, int gj
   const float *xv = q.x, *Gv = q.G, *zv = q.z;
   float *mv = q.m, *sv = q.s;
   float xi[4];
-  normals4(p.seed_lo, p.seed_hi, (uint32_t)gj4 >> 2, (uint32_t)gi, p.t1, 0u, xi);
+  normals4(p.seed_lo, p.seed_hi, (uint32_t)gj4 >> 2, (uint32_t)gi, it_t1(p), 0u, xi);
   float dtv[4] = {0.f, 0.f, 0.f, 0.f};
   if (p.has_tv) tv_term(p, gi, gj4, xv, dtv);
   float xn[4];
@@ -169,25 +189,25 @@ __device__ __forceinline__ void ula_finish(const UpdateParams &p, int gi, int gj
   float zn[4];
   if (p.has_z) {
     float ze[4];
-    normals4(p.seed_lo, p.seed_hi, (uint32_t)gj4 >> 2, (uint32_t)gi, p.t1, 1u, ze);
+    normals4(p.seed_lo, p.seed_hi, (uint32_t)gj4 >> 2, (uint32_t)gi, it_t1(p), 1u, ze);
 #pragma unroll
     for (int l = 0; l < 4; ++l) {
       const float v = zv[l] - p.b_rho * (zv[l] - xn[l]) + p.b_zeta * ze[l];
       zn[l] = fminf(fmaxf(v, p.z_lo), p.z_hi);
     }
   }
-  if (p.accumulate) {
+  if (it_acc(p)) {
 #pragma unroll
     for (int l = 0; l < 4; ++l) {
       const float d = xn[l] - mv[l];
-      mv[l] = mv[l] + d * p.inv_n;
+      mv[l] = mv[l] + d * it_inv_n(p);
       sv[l] = sv[l] + d * (xn[l] - mv[l]);
     }
   }
   if (full) {
     *reinterpret_cast<float4 *>(p.xn + base) = make_float4(xn[0], xn[1], xn[2], xn[3]);
     if (p.has_z) *reinterpret_cast<float4 *>(p.z + base) = make_float4(zn[0], zn[1], zn[2], zn[3]);
-    if (p.accumulate) {
+    if (it_acc(p)) {
       *reinterpret_cast<float4 *>(p.mean + base) = make_float4(mv[0], mv[1], mv[2], mv[3]);
       *reinterpret_cast<float4 *>(p.m2 + base) = make_float4(sv[0], sv[1], sv[2], sv[3]);
     }
@@ -198,7 +218,7 @@ __device__ __forceinline__ void ula_finish(const UpdateParams &p, int gi, int gj
       if (gj < g.j0 || gj >= g.j0 + g.tw) continue;
       p.xn[base + l] = xn[l];
       if (p.has_z) p.z[base + l] = zn[l];
-      if (p.accumulate) { p.mean[base + l] = mv[l]; p.m2[base + l] = sv[l]; }
+      if (it_acc(p)) { p.mean[base + l] = mv[l]; p.m2[base + l] = sv[l]; }
     }
   }
 }
@@ -215,6 +235,7 @@ template <int RY_, int RX_, bool SEP>
 __global__ void __launch_bounds__(NTHREADS)
 update_conv_kernel(const __grid_constant__ UpdateParams p) {
   extern __shared__ float smem[];
+  it_advance(p);
   const int RY = RY_ >= 0 ? RY_ : p.ry;
   const int RX = RX_ >= 0 ? RX_ : p.rx;
   const TileGeom &g = p.g;
@@ -378,6 +399,7 @@ update_sep_kernel(const __grid_constant__ UpdateParams p, const __grid_constant_
   static_assert(RC % 4 == 0 && XC % 4 == 0 && NW % 4 == 0, "R must be even");
   static_assert(RR * TX <= XR * XC, "T2 reuses the x buffer");
   extern __shared__ __align__(128) float sm[];
+  it_advance(p);
   // TMA completion barrier per staging buffer, after the float regions (no static shared
   // memory: the dynamic region then starts 1024-B aligned, as the TMA destinations need)
   uint64_t *const full_bar = reinterpret_cast<uint64_t *>(sm + Gm::floats);
@@ -552,7 +574,7 @@ __global__ void __launch_bounds__(NTHREADS) z1_update_kernel(const __grid_consta
     const int gi = r0 + (int)(e / nq);
     const int gj4 = 4 * (q0 + (int)(e % nq));
     float ze[4];
-    normals4(p.seed_lo, p.seed_hi, (uint32_t)gj4 >> 2, (uint32_t)gi, p.t1, 2u, ze);
+    normals4(p.seed_lo, p.seed_hi, (uint32_t)gj4 >> 2, (uint32_t)gi, it_t1(p), 2u, ze);
 #pragma unroll
     for (int l = 0; l < 4; ++l) {
       const int gj = gj4 + l;
@@ -628,7 +650,7 @@ __global__ void __launch_bounds__(NTHREADS) z1_sep_kernel(const __grid_constant_
     const int a = 2 * a2 + r, gi = bi0 + a;
     if (gi < rlo || gi >= rhi || gj4 >= chi || gj4 + 4 <= clo) continue;
     float ze[4];
-    normals4(p.seed_lo, p.seed_hi, (uint32_t)gj4 >> 2, (uint32_t)gi, p.t1, 2u, ze);
+    normals4(p.seed_lo, p.seed_hi, (uint32_t)gj4 >> 2, (uint32_t)gi, it_t1(p), 2u, ze);
 #pragma unroll
     for (int l = 0; l < 4; ++l) {
       const int gj = gj4 + l;
@@ -658,8 +680,8 @@ __global__ void __launch_bounds__(NTHREADS) tv_z_kernel(const __grid_constant__ 
     const int gi = r0 + (int)(e / nq);
     const int gj4 = 4 * (q0 + (int)(e % nq));
     float zev[4], zeh[4];
-    normals4(p.seed_lo, p.seed_hi, (uint32_t)gj4 >> 2, (uint32_t)gi, p.t1, 1u, zev);
-    normals4(p.seed_lo, p.seed_hi, (uint32_t)gj4 >> 2, (uint32_t)gi, p.t1, 3u, zeh);
+    normals4(p.seed_lo, p.seed_hi, (uint32_t)gj4 >> 2, (uint32_t)gi, it_t1(p), 1u, zev);
+    normals4(p.seed_lo, p.seed_hi, (uint32_t)gj4 >> 2, (uint32_t)gi, it_t1(p), 3u, zeh);
 #pragma unroll
     for (int l = 0; l < 4; ++l) {
       const int gj = gj4 + l;
@@ -768,6 +790,7 @@ __global__ void opnorm_init_kernel(const __grid_constant__ OpNormParams p) {
 
 // ---------------------------------------------------------------- mask K7 (no stencil)
 __global__ void __launch_bounds__(NTHREADS) update_mask_kernel(const __grid_constant__ UpdateParams p) {
+  it_advance(p);
   const TileGeom &g = p.g;
   const int nq = ((g.j0 + g.tw + 3) >> 2) - (g.j0 >> 2);
   const int64_t total = (int64_t)nq * g.th;
