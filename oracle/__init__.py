@@ -11,7 +11,8 @@ file with gcc and marshals numpy arrays through ctypes.
 
 Parity status per function:
   partition, philox, normal, conv fwd/adj, mask, dncnn residual, step-size
-  check, run (untiled + tiled), KL prox, Poisson run: pinned (tests/test_oracle_*.py).
+  check, run (untiled + tiled), KL prox, Poisson run, TV, DDFB, C-channel (RGB) run and
+  residual: pinned (tests/test_oracle_*.py).
 """
 from __future__ import annotations
 
@@ -57,6 +58,7 @@ class _Config(C.Structure):
         ("eta", C.c_double), ("rho1", C.c_double), ("kappa1", C.c_double),
         ("den_kind", C.c_int32), ("ddfb_gammas", C.c_void_p), ("ht_eps", C.c_double),
         ("tv_beta", C.c_double),
+        ("n_chan", C.c_int32),
     ]
 
 
@@ -74,6 +76,8 @@ def _load():
         _lib.or_conv_adj.argtypes = [vp, i32, i32, vp, i32, i32, vp]
         _lib.or_dncnn_residual.argtypes = [vp, i32, i32, i32, i32, vp, vp, i32, vp]
         _lib.or_dncnn_residual.restype = C.c_int
+        _lib.or_dncnn_residual_c.argtypes = [vp, i32, i32, i32, i32, i32, vp, vp, i32, vp]
+        _lib.or_dncnn_residual_c.restype = C.c_int
         _lib.or_dncnn_param_count.argtypes = [i32, i32, i32]
         _lib.or_dncnn_param_count.restype = i64
         _lib.or_check_stepsizes.argtypes = [d, d, d, d, d, d, d]
@@ -148,11 +152,13 @@ def conv_adj(r, k) -> np.ndarray:
 
 
 def dncnn_residual(x, weights, biases, n_layers: int, channels: int, bf16_emulate: bool = False):
+    """x: (ny, nx) grayscale or (C, ny, nx) planes (layer 1 C -> P, layer K P -> C; R43)."""
     x = _f64(x)
     w, b = _f32(weights), _f32(biases)
     G = np.zeros_like(x)
-    e = _load().or_dncnn_residual(x.ctypes.data, x.shape[0], x.shape[1], n_layers, channels,
-                                  w.ctypes.data, b.ctypes.data, int(bf16_emulate), G.ctypes.data)
+    nc = x.shape[0] if x.ndim == 3 else 1
+    e = _load().or_dncnn_residual_c(x.ctypes.data, x.shape[-2], x.shape[-1], nc, n_layers, channels,
+                                    w.ctypes.data, b.ctypes.data, int(bf16_emulate), G.ctypes.data)
     if e:
         raise ValueError("or_dncnn_residual failed")
     return G
@@ -246,10 +252,12 @@ class Problem:
 def run(pb: Problem, n_iter: int, burn_in: int, seed: int, tiles=(1, 1), bf16_emulate=False,
         want_var: bool = True, origin=(0, 0)) -> dict:
     """Run the chain.  origin = global coordinates of pixel (0, 0) when pb is a crop of a
-    larger image (only the noise indexing uses it)."""
+    larger image (only the noise indexing uses it).  pb.y of shape (C, ny, nx) runs a C-channel
+    image (R43); the returned fields then have that shape too."""
     lib = _load()
     y = _f32(pb.y)
-    ny, nx = y.shape
+    nc = y.shape[0] if y.ndim == 3 else 1
+    ny, nx = y.shape[-2:]
     keep = [y]
     cfg = _Config()
     cfg.ny, cfg.nx = ny, nx
@@ -297,8 +305,10 @@ def run(pb: Problem, n_iter: int, burn_in: int, seed: int, tiles=(1, 1), bf16_em
     cfg.i_off, cfg.j_off = origin
     cfg.eta, cfg.rho1, cfg.kappa1 = pb.eta, pb.rho1, pb.kappa1
     cfg.tv_beta = pb.tv_beta
-    x = np.zeros((ny, nx)); z = np.zeros((ny, nx)); z1 = np.zeros((ny, nx)); zh = np.zeros((ny, nx))
-    mean = np.zeros((ny, nx)); var = np.zeros((ny, nx))
+    cfg.n_chan = nc
+    shp = y.shape
+    x = np.zeros(shp); z = np.zeros(shp); z1 = np.zeros(shp); zh = np.zeros(shp)
+    mean = np.zeros(shp); var = np.zeros(shp)
     n = C.c_int64()
     have_mean = n_iter > burn_in
     have_var = want_var and n_iter - burn_in >= 2

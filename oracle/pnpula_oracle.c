@@ -172,25 +172,27 @@ int64_t or_dncnn_param_count(int32_t n_layers, int32_t P, int32_t C) {
   return w + b;
 }
 
-/* CNN residual G_eps(x) for C = 1 (D_eps = Id - G_eps).
+/* CNN residual G_eps(x) for C image channels (D_eps = Id - G_eps; C = 3 for the
+ * colour DnCNN of P:843, reading R43): layer 1 is C -> P, layer K is P -> C; x and G are C planes.
  * Layer k: a^k_{c'}[i,j] = eta_k( b_k[c'] + sum_c sum_{u,v=-1..1} W_k[c'][c][u+1][v+1] a^{k-1}_c[i+u][j+v] )
  * (PyTorch conv2d cross-correlation, half padding, reading R2/R8: zero outside
  * the image at every layer input); eta = ReLU for k < K, identity for k = K.
  * weights: fp32 OIHW, layers concatenated; biases: per layer, concatenated.     */
-int or_dncnn_residual(const double *x, int32_t ny, int32_t nx, int32_t n_layers, int32_t P,
-                      const float *weights, const float *biases, int32_t bf16_emulate, double *G) {
-  if (n_layers < 2 || P < 1) return OR_E_INVALID;
+int or_dncnn_residual_c(const double *x, int32_t ny, int32_t nx, int32_t C, int32_t n_layers, int32_t P,
+                        const float *weights, const float *biases, int32_t bf16_emulate, double *G) {
+  if (n_layers < 2 || P < 1 || C < 1) return OR_E_INVALID;
   int64_t npx = (int64_t)ny * nx;
-  double *a = (double *)calloc((size_t)(npx * P), sizeof(double));
-  double *b = (double *)calloc((size_t)(npx * P), sizeof(double));
+  int64_t wide = P > C ? P : C;
+  double *a = (double *)calloc((size_t)(npx * wide), sizeof(double));
+  double *b = (double *)calloc((size_t)(npx * wide), sizeof(double));
   if (!a || !b) { free(a); free(b); return OR_E_INVALID; }
-  /* a^0 = x (one channel) */
-  for (int64_t n = 0; n < npx; n++) a[n] = bf16_emulate ? or_bf16(x[n]) : x[n];
-  int cin = 1;
+  /* a^0 = x (C channels) */
+  for (int64_t n = 0; n < npx * C; n++) a[n] = bf16_emulate ? or_bf16(x[n]) : x[n];
+  int cin = C;
   const float *w = weights;
   const float *bb = biases;
   for (int k = 1; k <= n_layers; k++) {
-    int cout = (k == n_layers) ? 1 : P;
+    int cout = (k == n_layers) ? C : P;
     for (int co = 0; co < cout; co++)
       for (int i = 0; i < ny; i++)
         for (int j = 0; j < nx; j++) {
@@ -216,10 +218,15 @@ int or_dncnn_residual(const double *x, int32_t ny, int32_t nx, int32_t n_layers,
     double *t = a; a = b; b = t;
     cin = cout;
   }
-  for (int64_t n = 0; n < npx; n++) G[n] = a[n];
+  for (int64_t n = 0; n < npx * C; n++) G[n] = a[n];
   free(a);
   free(b);
   return OR_OK;
+}
+
+int or_dncnn_residual(const double *x, int32_t ny, int32_t nx, int32_t n_layers, int32_t P,
+                      const float *weights, const float *biases, int32_t bf16_emulate, double *G) {
+  return or_dncnn_residual_c(x, ny, nx, 1, n_layers, P, weights, biases, bf16_emulate, G);
 }
 
 /* ------------------------------------------------------------------ */
@@ -417,7 +424,13 @@ typedef struct {
   double tv_beta;                /* > 0: TV prior: the z block is z ~ D x (two
                                     components) with f2 = tv_beta ||.||_{2,1} and x moves by PSGLA
                                     with p = 1_{R+}; requires rho > 0, no CNN, no box term */
+  int32_t n_chan;                /* image channels C (0 or 1 = grayscale; 3 = RGB, reading R43): y, x0
+                                    and every state array are C planes [C][ny][nx]; H acts on each
+                                    plane, the mask is shared, channel c draws Philox streams 4c + s;
+                                    C > 1: untiled, DnCNN or no prior, no TV */
 } or_config;
+
+static int or_nchan(const or_config *c) { return c->n_chan > 1 ? c->n_chan : 1; }
 
 static void or_kernel2d(const or_config *c, double *k) {
   for (int p = 0; p < c->kh; p++)
@@ -426,10 +439,12 @@ static void or_kernel2d(const or_config *c, double *k) {
                                    : (double)c->kernel[p * c->kw + q];
 }
 
-/* One untiled iteration of Algorithm 1 (lines 5-13) on global arrays. */
-static int or_step_global(const or_config *c, const double *k, const double *yd, uint64_t t,
-                          const double *x, const double *z, const double *z1, const double *zh, double *xn,
-                          double *zn, double *z1n, double *zhn, double *r, double *g, double *G) {
+/* One untiled iteration of Algorithm 1 (lines 5-13) for one image channel (plane) on global
+ * arrays, given the channel's CNN residual G; the channel draws Philox streams sb + s (R43). */
+static int or_step_plane(const or_config *c, const double *k, const double *yd, uint64_t t,
+                         const double *x, const double *z, const double *z1, const double *zh, double *xn,
+                         double *zn, double *z1n, double *zhn, double *r, double *g, const double *G,
+                         uint32_t sb) {
   int ny = c->ny, nx = c->nx;
   int64_t npx = (int64_t)ny * nx;
   /* line 6: u1 = H1^T grad f1(H1 x),  f1(v) = ||y - v||^2/(2 sigma^2) (eq:potential_gaussian_likelihood) */
@@ -451,16 +466,8 @@ static int or_step_global(const or_config *c, const double *k, const double *yd,
     or_conv_adj(r, ny, nx, k, c->kh, c->kw, g);
     for (int64_t n = 0; n < npx; n++) g[n] = c->eta * g[n] / c->rho1;
   }
-  /* line 8: D_eps(x) - x = -G_eps(x) */
+  /* line 8: D_eps(x) - x = -G_eps(x), G given */
   int use_cnn = c->n_layers > 0 && c->alpha != 0.0;
-  if (use_cnn) {
-    int e = c->den_kind == 1
-                ? or_ddfb_residual(x, ny, nx, c->n_layers, c->channels, c->weights, c->ddfb_gammas, c->ht_eps,
-                                   c->bf16_emulate, G)
-                : or_dncnn_residual(x, ny, nx, c->n_layers, c->channels, c->weights, c->biases,
-                                    c->bf16_emulate, G);
-    if (e) return e;
-  }
   double sq2g = sqrt(2.0 * c->gamma);
   if (c->tv_beta > 0.0) {
     /* TV prior: x^{t+1} = proj_{R+}( x - gamma grad f1(H1 x) - (gamma/rho) D^T (D x - z)
@@ -476,7 +483,7 @@ static int or_step_global(const or_config *c, const double *k, const double *yd,
       for (int64_t j = 0; j < nx; j++) {
         int64_t n = i * nx + j;
         double v = x[n] - c->gamma * g[n] - (c->gamma / c->rho) * dt[n] +
-                   sq2g * or_normal(c->seed, (uint32_t)(t + 1), i + c->i_off, j + c->j_off, 0);
+                   sq2g * or_normal(c->seed, (uint32_t)(t + 1), i + c->i_off, j + c->j_off, sb + 0);
         xn[n] = v < 0.0 ? 0.0 : v;
       }
     /* lines 11-13: z^{t+1} = prox_{kappa beta ||.||_{2,1}}( z - (kappa/rho)(z - D x^{t+1}) + sqrt(2 kappa) zeta ),
@@ -487,9 +494,9 @@ static int or_step_global(const or_config *c, const double *k, const double *yd,
       for (int64_t j = 0; j < nx; j++) {
         int64_t n = i * nx + j;
         double vv = z[n] - (c->kappa / c->rho) * (z[n] - dv[n]) +
-                    sq2k * or_normal(c->seed, (uint32_t)(t + 1), i + c->i_off, j + c->j_off, 1);
+                    sq2k * or_normal(c->seed, (uint32_t)(t + 1), i + c->i_off, j + c->j_off, sb + 1);
         double vh = zh[n] - (c->kappa / c->rho) * (zh[n] - dh[n]) +
-                    sq2k * or_normal(c->seed, (uint32_t)(t + 1), i + c->i_off, j + c->j_off, 3);
+                    sq2k * or_normal(c->seed, (uint32_t)(t + 1), i + c->i_off, j + c->j_off, sb + 3);
         or_prox_l21(vv, vh, c->kappa * c->tv_beta, &zn[n], &zhn[n]);
       }
     free(dv); free(dh); free(dt);
@@ -505,7 +512,7 @@ static int or_step_global(const or_config *c, const double *k, const double *yd,
         double pc = x[n] < c->c_lo ? c->c_lo : (x[n] > c->c_hi ? c->c_hi : x[n]);
         v += (c->gamma / c->lambda) * (pc - x[n]);
       }
-      v += sq2g * or_normal(c->seed, (uint32_t)(t + 1), i + c->i_off, j + c->j_off, 0);
+      v += sq2g * or_normal(c->seed, (uint32_t)(t + 1), i + c->i_off, j + c->j_off, sb + 0);
       xn[n] = v;
     }
   if (c->rho > 0.0) {
@@ -515,7 +522,7 @@ static int or_step_global(const or_config *c, const double *k, const double *yd,
         int64_t n = i * nx + j;
         /* lines 12-13 / eq:sgs_pnp_ula_psgla:psgla with H2 = I, prox = projection onto [z_lo,z_hi] */
         double v = z[n] - (c->kappa / c->rho) * (z[n] - xn[n]) +
-                   sq2k * or_normal(c->seed, (uint32_t)(t + 1), i + c->i_off, j + c->j_off, 1);
+                   sq2k * or_normal(c->seed, (uint32_t)(t + 1), i + c->i_off, j + c->j_off, sb + 1);
         zn[n] = v < c->z_lo ? c->z_lo : (v > c->z_hi ? c->z_hi : v);
       }
   }
@@ -528,9 +535,33 @@ static int or_step_global(const or_config *c, const double *k, const double *yd,
       for (int64_t j = 0; j < nx; j++) {
         int64_t n = i * nx + j;
         double v = z1[n] - (c->kappa1 / c->rho1) * (z1[n] - c->eta * r[n]) +
-                   sq2k1 * or_normal(c->seed, (uint32_t)(t + 1), i + c->i_off, j + c->j_off, 2);
+                   sq2k1 * or_normal(c->seed, (uint32_t)(t + 1), i + c->i_off, j + c->j_off, sb + 2);
         z1n[n] = or_prox_kl(v, yd[n], c->kappa1);
       }
+  }
+  return OR_OK;
+}
+
+/* One untiled iteration on C channel planes: line 8 (the CNN couples the channels) once, then
+ * lines 5-13 per channel (H, the mask, the box and the z blocks act channel by channel). */
+static int or_step_global(const or_config *c, const double *k, const double *yd, uint64_t t,
+                          const double *x, const double *z, const double *z1, const double *zh, double *xn,
+                          double *zn, double *z1n, double *zhn, double *r, double *g, double *G) {
+  const int nc = or_nchan(c);
+  const int64_t npx = (int64_t)c->ny * c->nx;
+  if (c->n_layers > 0 && c->alpha != 0.0) {
+    int e = c->den_kind == 1
+                ? or_ddfb_residual(x, c->ny, c->nx, c->n_layers, c->channels, c->weights, c->ddfb_gammas,
+                                   c->ht_eps, c->bf16_emulate, G)
+                : or_dncnn_residual_c(x, c->ny, c->nx, nc, c->n_layers, c->channels, c->weights, c->biases,
+                                      c->bf16_emulate, G);
+    if (e) return e;
+  }
+  for (int ch = 0; ch < nc; ch++) {
+    const int64_t o = (int64_t)ch * npx;
+    int e = or_step_plane(c, k, yd + o, t, x + o, z + o, z1 + o, zh + o, xn + o, zn + o, z1n + o, zhn + o, r, g,
+                          G + o, 4u * (uint32_t)ch);
+    if (e) return e;
   }
   return OR_OK;
 }
@@ -783,7 +814,9 @@ int or_run_ex(const or_config *c, double *x_out, double *z_out, double *z1_out, 
     return OR_E_INVALID;
   if (c->tv_beta > 0.0 && (!(c->rho > 0.0) || (c->n_layers > 0 && c->alpha != 0.0) || c->lambda > 0.0))
     return OR_E_INVALID;   /* TV: z block on (the TV block), no CNN, no box term; any likelihood */
-  int64_t npx = (int64_t)c->ny * c->nx;
+  const int nc = or_nchan(c);
+  if (nc > 1 && (c->tiles_y > 1 || c->tiles_x > 1 || c->tv_beta > 0.0 || c->den_kind == 1)) return OR_E_INVALID;
+  int64_t npx = (int64_t)c->ny * c->nx * nc;   /* all C planes */
   double *k = (double *)calloc((size_t)(c->kh > 0 ? c->kh * c->kw : 1), sizeof(double));
   double *yd = (double *)malloc(sizeof(double) * (size_t)npx);
   double *x = (double *)calloc((size_t)npx, sizeof(double));

@@ -133,11 +133,11 @@ def _blur_valid(xext: np.ndarray, k2d: np.ndarray) -> np.ndarray:
     return fftconvolve(xext.astype(np.float64), k2d, mode="valid")
 
 
-def blurred_truth(ny, nx, k2d, rect=None) -> np.ndarray:
+def blurred_truth(ny, nx, k2d, rect=None, gt_seed=GT_SEED) -> np.ndarray:
     """conv(x̄, K) (same size, zero boundary) on rect, via scipy FFT convolution."""
     i0, j0, h, w = rect if rect is not None else (0, 0, ny, nx)
     ry, rx = k2d.shape[0] // 2, k2d.shape[1] // 2
-    xe = ground_truth(ny, nx, (i0 - ry, j0 - rx, h + 2 * ry, w + 2 * rx))
+    xe = ground_truth(ny, nx, (i0 - ry, j0 - rx, h + 2 * ry, w + 2 * rx), seed=gt_seed)
     return _blur_valid(xe, k2d)
 
 
@@ -157,9 +157,9 @@ def noise_sigma2_mask(ny, nx, snr_db=15.0) -> float:
     return float(np.mean(xb ** 2) / 10 ** (snr_db / 10))
 
 
-def observe_blur(ny, nx, k2d, sigma2, rect=None) -> np.ndarray:
+def observe_blur(ny, nx, k2d, sigma2, rect=None, gt_seed=GT_SEED, noise_seed=NOISE_SEED) -> np.ndarray:
     rect = rect if rect is not None else (0, 0, ny, nx)
-    y = blurred_truth(ny, nx, k2d, rect) + np.sqrt(sigma2) * white_noise(ny, nx, rect)
+    y = blurred_truth(ny, nx, k2d, rect, gt_seed) + np.sqrt(sigma2) * white_noise(ny, nx, rect, noise_seed)
     i0, j0, h, w = rect
     y[:max(0, -i0), :] = 0
     y[:, :max(0, -j0)] = 0
@@ -200,6 +200,31 @@ def observe_mask(ny, nx, sigma2, p=0.3, rect=None):
     return y.astype(np.float32), m
 
 
+# ---------------------------------------------------------------- colour (C = 3; reading R43)
+def rgb_seeds(c: int):
+    """(ground-truth seed, noise seed) of colour channel c: one texture and one noise field per plane."""
+    return GT_SEED + 17 * c, NOISE_SEED + 17 * c
+
+
+def ground_truth_rgb(ny, nx, rect=None, C=3) -> np.ndarray:
+    """Planes [C][h][w]: channel c is the procedural texture with seed rgb_seeds(c)[0]."""
+    return np.stack([ground_truth(ny, nx, rect, seed=rgb_seeds(c)[0]) for c in range(C)])
+
+
+def observe_blur_rgb(ny, nx, k2d, sigma2, rect=None, C=3) -> np.ndarray:
+    """y_c = conv(x̄_c, K) + sigma w_c per plane (the same blur on every channel)."""
+    return np.stack([observe_blur(ny, nx, k2d, sigma2, rect, *rgb_seeds(c)) for c in range(C)])
+
+
+def observe_mask_rgb(ny, nx, sigma2, p=0.3, rect=None, C=3):
+    """A per-pixel mask shared by the channels, y_c = m (x̄_c + sigma w_c)."""
+    rect = rect if rect is not None else (0, 0, ny, nx)
+    m = bernoulli_mask(ny, nx, p, rect)
+    y = np.stack([m * (ground_truth(ny, nx, rect, seed=rgb_seeds(c)[0]).astype(np.float64)
+                       + np.sqrt(sigma2) * white_noise(ny, nx, rect, rgb_seeds(c)[1])) for c in range(C)])
+    return y.astype(np.float32), m
+
+
 # ---------------------------------------------------------------- denoiser weights
 def _conv_spectral_norm(w: np.ndarray, grid: int = 64) -> float:
     """Largest singular value of the multichannel 3x3 circular convolution on a grid^2 torus
@@ -212,14 +237,15 @@ def _conv_spectral_norm(w: np.ndarray, grid: int = 64) -> float:
     return float(np.max(np.linalg.svd(F, compute_uv=False)))
 
 
-def dncnn_weights(n_layers: int, channels: int, seed: int = WEIGHT_SEED, target_norm: float = 0.9):
-    """Random-init DnCNN-style (1 -> P, (K-2) x P -> P, P -> 1; 3x3) weights, fp32 OIHW
+def dncnn_weights(n_layers: int, channels: int, seed: int = WEIGHT_SEED, target_norm: float = 0.9,
+                  image_channels: int = 1):
+    """Random-init DnCNN-style (C -> P, (K-2) x P -> P, P -> C; 3x3) weights, fp32 OIHW
     concatenated, and biases concatenated.  PyTorch-default-like U(-1/sqrt(fan_in), +)."""
     rng = np.random.default_rng(seed)
     ws, bs = [], []
-    cin = 1
+    cin = image_channels
     for k in range(1, n_layers + 1):
-        cout = 1 if k == n_layers else channels
+        cout = image_channels if k == n_layers else channels
         bound = 1.0 / np.sqrt(cin * 9)
         w = rng.uniform(-bound, bound, size=(cout, cin, 3, 3))
         w *= target_norm / _conv_spectral_norm(w)
