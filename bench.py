@@ -33,8 +33,8 @@ sys.path.insert(0, ROOT)
 CNN_MAC_PER_PX = {(8, 32): 55872, (4, 16): 4896}
 
 
-def cnn_macs(K, P):
-    return P * 9 + (K - 2) * P * P * 9 + P * 9
+def cnn_macs(K, P, C=1):
+    return C * P * 9 + (K - 2) * P * P * 9 + P * 9 * C
 
 
 def parse():
@@ -42,7 +42,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=60)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--workload", default="c5", choices=["c5", "c2", "c3", "c4", "c1", "p5", "t5", "d5"])
+    ap.add_argument("--workload", default="c5", choices=["c5", "c2", "c3", "c4", "c1", "p5", "t5", "d5", "r5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -72,6 +72,12 @@ def workload(name, n):
         return dict(name="d5", desc="weak scaling as c5, 9x9 Gaussian deblur 25 dB with the DDFB prior "
                     "(K = 4, F = 64, the paper's light denoiser)", ny=ny, nx=nx, tiles=(n, 1), op="conv", L=9,
                     sb=2.0, cnn=(4, 64), ddfb=True, z=False, scaling="weak")
+    if name == "r5":
+        shapes = {1: (4096, 8192), 2: (8192, 8192), 4: (8192, 16384), 8: (16384, 16384)}
+        ny, nx = shapes.get(n, (4096 * n, 8192))
+        return dict(name="r5", desc="weak scaling as c5, RGB (C = 3, planar) 9x9 Gaussian deblur 25 dB per "
+                    "channel, colour DnCNN-lite 8x32 (3 -> 32 ... 32 -> 3)", ny=ny, nx=nx, tiles=(n, 1), op="conv",
+                    L=9, sb=2.0, cnn=(8, 32), z=False, nc=3, scaling="weak")
     if name == "t5":
         shapes = {1: (4096, 8192), 2: (8192, 8192), 4: (8192, 16384), 8: (16384, 16384)}
         ny, nx = shapes.get(n, (4096 * n, 8192))
@@ -121,7 +127,10 @@ def build_inputs(wl, rect, pinned=False):
         ky, kx = synth.gaussian_factors(wl["L"], wl["sb"])
         k2 = synth.outer(ky, kx)
         s2 = synth.noise_sigma2_blur(ny, nx, k2, 25.0)
-        y = synth.observe_blur(ny, nx, k2, s2, rect)
+        if wl.get("nc", 1) > 1:
+            y = synth.observe_blur_rgb(ny, nx, k2, s2, rect, C=wl["nc"])
+        else:
+            y = synth.observe_blur(ny, nx, k2, s2, rect)
         kw.update(kernel_sep=(ky, kx))
     else:
         s2 = synth.noise_sigma2_mask(ny, nx, 15.0)
@@ -146,7 +155,7 @@ def build_inputs(wl, rect, pinned=False):
                   ddfb_gammas=g, ht_eps=ht)
     elif wl["cnn"]:
         K, P = wl["cnn"]
-        w, b = synth.dncnn_weights(K, P)
+        w, b = synth.dncnn_weights(K, P, image_channels=wl.get("nc", 1))
         kw.update(weights=w, biases=b, n_layers=K, channels=P, alpha=1.0, eps=float(np.sqrt(s2)))
     if pinned:
         import torch
@@ -366,8 +375,9 @@ def main():
         # pinned host buffers for the moments (D2H at full PCIe/NVLink-C2C rate)
         outs = None
         if world == 1:
-            pm = torch.empty((wl["ny"], wl["nx"]), dtype=torch.float32, pin_memory=True)
-            pv = torch.empty((wl["ny"], wl["nx"]), dtype=torch.float32, pin_memory=True)
+            shp = ((wl["nc"],) if wl.get("nc", 1) > 1 else ()) + (wl["ny"], wl["nx"])
+            pm = torch.empty(shp, dtype=torch.float32, pin_memory=True)
+            pv = torch.empty(shp, dtype=torch.float32, pin_memory=True)
             outs = (pm.numpy(), pv.numpy())
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -417,16 +427,17 @@ def main():
                 "algorithmic": f"{bpp} B/px x {own_px} px per evaluation ({2 * Kc * P * 9} MAC/px)"}
     elif wl["cnn"] and cnn_n:
         Kc, P = wl["cnn"]
-        flops = 2.0 * cnn_macs(Kc, P) * own_px * K
+        flops = 2.0 * cnn_macs(Kc, P, wl.get("nc", 1)) * own_px * K
         ach = flops / (cnn_ms * 1e-3) / 1e12
         tpp = traffic.get("cnn_bytes_per_px")
         roof = {"kernel": "cnn_chunk_kernel (tcgen05, %d launches/iteration)" % (cnn_n // K),
                 "bound": "tensor", "achieved": ach, "peak": tf_sus, "unit": "TFLOP/s", "frac": ach / tf_sus,
                 "traffic": (tpp * own_px) if tpp else None,
                 "share_of_step": cnn_ms / ms if ms else None,
-                "algorithmic": f"2*{cnn_macs(Kc, P)} FLOP/px (2 MAC) x {own_px} px per evaluation",
+                "algorithmic": f"2*{cnn_macs(Kc, P, wl.get("nc", 1))} FLOP/px (2 MAC) x {own_px} px per evaluation",
                 "peak_source": peak_src + " bf16_tflops_sustained"}
     upd_bytes_px = 32 + (8 if wl["z"] else 0) - (4 if not wl["cnn"] else 0) + (1 if wl["op"] == "mask" else 0)
+    upd_bytes_px *= wl.get("nc", 1)   # colour: every channel plane streams the same fields
     if wl.get("tv"):
         upd_bytes_px = 28 + 8 + 20   # x-update 28 (no G) + z_v, z_h read; z kernel: x+ 4, z_v/z_h 16
     if wl["op"] == "poisson":

@@ -104,7 +104,7 @@ typedef struct {
 
 typedef struct {
   /* geometry and SPMD identity */
-  int32_t ny, nx;                /* global image, C = 1 */
+  int32_t ny, nx;                /* global image (channels: img_channels below) */
   int32_t tiles_y, tiles_x;      /* tile grid; tiles_y*tiles_x must be a multiple of world_size */
   int32_t rank, world_size;      /* this process; world_size >= 1 */
   int32_t device;                /* CUDA device ordinal used by this rank */
@@ -157,6 +157,14 @@ typedef struct {
    * Requires rho > 0, no denoiser, lambda <= 0; with OP_POISSON the z1 block is kept
    * and f1 = 0.  pnpula_get_state returns z_v, pnpula_get_tv_zh z_h. */
   double tv_beta;
+
+  /* Image channels C (colour images; R43): 0 or 1 = grayscale, 3 = RGB.
+   * y, x0 and every per-pixel output (x, z, z1, mean, var, G) are C planes [C][h][w] (planar);
+   * the mask is one plane shared by the channels.  H, the box and the z blocks act on each
+   * channel; the DnCNN's first layer is C -> P and its last P -> C (weights OIHW as for C = 1,
+   * with I = C / O = C; needs channels P >= 32).  Channel c draws Philox streams 4c + s.
+   * Not with the TV prior or the DDFB denoiser (E_UNSUPPORTED). */
+  int32_t img_channels;
 } pnpula_config;
 
 typedef struct pnpula_ctx pnpula_ctx;
@@ -198,7 +206,7 @@ pnpula_status pnpula_local_bbox(pnpula_ctx *ctx, pnpula_rect *out);
 /* [collective for GLOBAL scope] Posterior mean (MMSE) and per-pixel variance
  * M2/(n-1) of x^{(t)}, t = burn_in+1 .. current t.  mean / var (either may be
  * NULL) are host buffers of the LOCAL bbox size, or ny*nx on rank 0 for
- * PNPULA_SCOPE_GLOBAL_ON_ROOT (other ranks may pass NULL).  Returns
+ * PNPULA_SCOPE_GLOBAL_ON_ROOT (other ranks may pass NULL); times C planes for C > 1.  Returns
  * PNPULA_E_STATS_EMPTY if n < 1 (mean) or n < 2 (var requested). */
 pnpula_status pnpula_get_moments(pnpula_ctx *ctx, float *mean, float *var, int64_t *n_samples,
                                  int32_t scope);

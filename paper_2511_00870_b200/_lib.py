@@ -60,6 +60,7 @@ class Config(C.Structure):
         ("flags", C.c_int32),
         ("eta", C.c_double), ("rho1", C.c_double), ("kappa1", C.c_double),
         ("tv_beta", C.c_double),
+        ("img_channels", C.c_int32),
     ]
 
 

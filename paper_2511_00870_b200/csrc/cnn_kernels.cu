@@ -89,32 +89,36 @@ struct SmemLayout {
 
 __host__ __device__ inline uint32_t align_up(uint32_t v, uint32_t a) { return (v + a - 1) / a * a; }
 
+// Image channels C (1 grayscale, 3 colour; reading R43) only touch the first layer (im2col:
+// 9C taps, K padded to 16 or 32) and the folded last layer (N = 16 per output channel).
+__host__ __device__ constexpr int im2col_k(int nc) { return 9 * nc <= 16 ? 16 : 32; }
+
 __host__ __device__ inline uint32_t packed_layer_elems(int cout, int cin) {
-  if (cin == 1) return 16u * (uint32_t)cout;
-  if (cout == 1) return 16u * (uint32_t)cin;   // folded P -> 1 layer: [K step][2][16 taps][8]
+  if (cin <= 3) return (uint32_t)im2col_k(cin) * (uint32_t)cout;   // im2col layer: [K/8][N][8]
+  if (cout <= 3) return 16u * (uint32_t)cout * (uint32_t)cin;      // folded P -> C: [K step][2][16 C][8]
   return 9u * (uint32_t)cin * (uint32_t)cout;
 }
 
-__host__ __device__ inline SmemLayout make_layout(int P, int nl, int first, int last) {
+__host__ __device__ inline SmemLayout make_layout(int P, int nl, int first, int last, int nc) {
   SmemLayout L{};
   uint32_t off = 0;
   const uint32_t act_slot = (uint32_t)(P / 8) * kRowPos * 16u;
   for (int l = 0; l < nl; ++l) {
-    L.slot_bytes[l] = (l == 0 && first) ? 2u * 128u * 16u : act_slot;
+    L.slot_bytes[l] = (l == 0 && first) ? (uint32_t)(im2col_k(nc) / 8) * 128u * 16u : act_slot;
     L.ring_off[l] = off;
     off = align_up(off + ring_slots(l) * L.slot_bytes[l], 128);
   }
   for (int l = 0; l < nl; ++l) {
-    const int cin = (l == 0 && first) ? 1 : P;
-    const int cout = (l == nl - 1 && last) ? 1 : P;
+    const int cin = (l == 0 && first) ? nc : P;
+    const int cout = (l == nl - 1 && last) ? nc : P;
     L.w_off[l] = off;
     off = align_up(off + packed_layer_elems(cout, cin) * 2u, 128);
   }
   L.bar_off = off;   // per layer: full[8], empty[8], tfull[4], tempty[4]
   off = align_up(off + (uint32_t)nl * 24u * 8u, 128);
   L.misc_off = off;  // tmem address, abort flag, drain barrier, per-layer table {ring, slot, w, 0},
-                     // folded last layer's warp-edge exchange [2][4 warps][6] floats
-  off += 16 + 16u * (uint32_t)nl + 192u;
+                     // folded last layer's warp-edge exchange [2][C][4 warps][6] floats
+  off += 16 + 16u * (uint32_t)nl + 192u * (uint32_t)nc;
   L.total = align_up(off, 128);
   return L;
 }
@@ -290,7 +294,7 @@ __device__ __forceinline__ void trace_ev(unsigned long long *tr, bool on, int co
 }
 
 // ---------------------------------------------------------------- the kernel
-template <int P, int NL>
+template <int P, int NL, int NC>
 __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const __grid_constant__ CnnChunkParams p) {
   constexpr int kMmaWarps = mma_warps(NL), kEpiGroups = epi_groups(NL), kEpi0 = epi0(NL);
   constexpr int kThreads = block_threads(NL);
@@ -300,7 +304,8 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
   constexpr uint32_t GS = kRowPos * 16; // bytes between channel groups in a ring row
   const bool first = p.first_is_input != 0;
   const bool last = p.last_is_output != 0;
-  const SmemLayout L = make_layout(P, NL, first, last);
+  const SmemLayout L = make_layout(P, NL, first, last, NC);
+  constexpr int K0 = im2col_k(NC);      // im2col K (9 NC taps, zero padded)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t sbase = smem_u32(smem);
   const uint32_t bar0 = sbase + L.bar_off;
@@ -321,8 +326,8 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
   // ---- one-time setup: weights, biases, zero rings, barriers, TMEM
 #pragma unroll
   for (int l = 0; l < NL; ++l) {
-    const int cin = (l == 0 && first) ? 1 : P;
-    const int cout = (l == NL - 1 && last) ? 1 : P;
+    const int cin = (l == 0 && first) ? NC : P;
+    const int cout = (l == NL - 1 && last) ? NC : P;
     const uint32_t n16 = packed_layer_elems(cout, cin) / 8;   // 16-byte chunks
     const uint4 *src = reinterpret_cast<const uint4 *>(p.w[l]);
     uint4 *dst = reinterpret_cast<uint4 *>(smem + L.w_off[l]);
@@ -419,29 +424,36 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
         trace_ev(p.trace, tr_on && lane == 0, 1, f, 0);
         uint8_t *slot = smem + ring0 + (Fg & 3) * slot0;
         if (first) {
-          // im2col row for layer-1 output row o: 9 taps of x (bf16), K padded to 16
+          // im2col row for layer-1 output row o: 9 taps per image channel of x (bf16), tap
+          // k = ch * 9 + (dy+1) * 3 + (dx+1), K padded to 16 (C = 1) or 32 (C = 3)
           const int o = r_lo - NL + f + 1;
           const TileGeom &g = p.xg;
           for (int m = lane; m < 128; m += 32) {
             const int cm = col0 + m;
-            float t[9];
+            float t[K0];
 #pragma unroll
-            for (int u2 = -1; u2 <= 1; ++u2) {
-              const int pr = o + u2 - (g.i0 - g.h);
-              const bool rok = pr >= 0 && pr < g.ph;
+            for (int k = 9 * NC; k < K0; ++k) t[k] = 0.f;
 #pragma unroll
-              for (int v2 = -1; v2 <= 1; ++v2) {
-                const int pc = cm + v2 - (g.j0 - g.hx);
-                float v = 0.f;
-                if (rok && pc >= 0 && pc < g.pitch) v = __ldg(p.x + (int64_t)pr * g.pitch + pc);
-                t[(u2 + 1) * 3 + (v2 + 1)] = v;
+            for (int ch = 0; ch < NC; ++ch) {
+              const float *xc = p.x + (int64_t)ch * p.xcs;
+#pragma unroll
+              for (int u2 = -1; u2 <= 1; ++u2) {
+                const int pr = o + u2 - (g.i0 - g.h);
+                const bool rok = pr >= 0 && pr < g.ph;
+#pragma unroll
+                for (int v2 = -1; v2 <= 1; ++v2) {
+                  const int pc = cm + v2 - (g.j0 - g.hx);
+                  float v = 0.f;
+                  if (rok && pc >= 0 && pc < g.pitch) v = __ldg(xc + (int64_t)pr * g.pitch + pc);
+                  t[ch * 9 + (u2 + 1) * 3 + (v2 + 1)] = v;
+                }
               }
             }
-            uint4 a0 = make_uint4(pack_bf16(t[0], t[1]), pack_bf16(t[2], t[3]), pack_bf16(t[4], t[5]),
-                                  pack_bf16(t[6], t[7]));
-            uint4 a1 = make_uint4(pack_bf16(t[8], 0.f), 0u, 0u, 0u);
-            *reinterpret_cast<uint4 *>(slot + m * 16) = a0;
-            *reinterpret_cast<uint4 *>(slot + 2048 + m * 16) = a1;
+#pragma unroll
+            for (int kg = 0; kg < K0 / 8; ++kg)
+              *reinterpret_cast<uint4 *>(slot + kg * 2048 + m * 16) =
+                  make_uint4(pack_bf16(t[kg * 8], t[kg * 8 + 1]), pack_bf16(t[kg * 8 + 2], t[kg * 8 + 3]),
+                             pack_bf16(t[kg * 8 + 4], t[kg * 8 + 5]), pack_bf16(t[kg * 8 + 6], t[kg * 8 + 7]));
           }
           fence_proxy_async();
           __syncwarp();
@@ -517,19 +529,25 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
           if (im2col) {
             const uint64_t ad = make_desc(slot, 2048, 128);
             const uint64_t bd = make_desc(wbase, (uint32_t)P * 16, 128);
-            if (elect_one()) mma_bf16(acc0 + (Ig & 3) * P, ad, bd, make_idesc(P), 0);
+            if (elect_one()) {
+#pragma unroll
+              for (int ks = 0; ks < K0 / 16; ++ks)   // K step = 2 core-matrix groups of A and B
+                mma_bf16(acc0 + (Ig & 3) * P, ad + (uint64_t)(ks * 256), bd + (uint64_t)(ks * 2 * P),
+                         make_idesc(P), ks > 0 ? 1u : 0u);
+            }
           } else if (netlast) {
             // P -> 1 layer: all nine taps folded into N = 16 (column n = q*3 + dxi, q = 1 - dy),
             // A unshifted (MMA row m = pixel col0 + m); the epilogue adds the dx-shifted columns
             // of neighbouring lanes and the dy rows of consecutive fills.  Fresh 16-column slot
             // per fill (accumulate = 0 on the first K step): no zeroing, no ring wrap.
+            // C output channels: 16 columns each (N = 16 C).
             const uint64_t ad0 = make_desc(slot + 16, GS, 128);
-            const uint64_t bd0 = make_desc(wbase, 16u * 16u, 128);
+            const uint64_t bd0 = make_desc(wbase, 16u * 16u * NC, 128);
             if (elect_one()) {
 #pragma unroll
               for (int ks = 0; ks < KS; ++ks)
-                mma_bf16(acc0 + (Fg & 1) * 16u, ad0 + (uint64_t)((2 * ks * GS) >> 4), bd0 + (uint64_t)(ks * 32),
-                         make_idesc(16), ks > 0 ? 1u : 0u);
+                mma_bf16(acc0 + (Fg & 1) * 16u * NC, ad0 + (uint64_t)((2 * ks * GS) >> 4),
+                         bd0 + (uint64_t)(ks * 32 * NC), make_idesc(16 * NC), ks > 0 ? 1u : 0u);
             }
           } else {
             // input row f contributes to output rows f-2 (dy=+1), f-1 (dy=0), f (dy=-1): B block q=0,1,2.
@@ -604,7 +622,9 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
       // d_{m-1}[q*3] + d_m[q*3+1] + d_{m+1}[q*3+2] (lanes m +- 1: shuffles, warp edges through
       // shared memory); a row is complete after its third fill.  Lanes 0 / 127 of the strip
       // are never valid output columns.
-      float nacc0 = 0.f, nacc1 = 0.f;   // running sums of output rows f-2 and f-1
+      float nacc0[NC], nacc1[NC];   // per output channel: running sums of output rows f-2 and f-1
+#pragma unroll
+      for (int co = 0; co < NC; ++co) { nacc0[co] = 0.f; nacc1[co] = 0.f; }
       float *const xch = reinterpret_cast<float *>(smem + L.misc_off + 16 + 16 * NL);
       auto netlast_fill = [&](const int l, const int f) -> bool {
           const int s = f + kLag * l;
@@ -612,55 +632,66 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
           if (!mbar_wait(bar_tfull(l, Fg & 1), (Fg >> 1) & 1, abort_flag, p.err, 4)) return false;
           trace_ev(p.trace, trw, 6, s, l);
           tc_fence_after();
-          float d[16];
-          tmem_load<16>(tmem_base + lane_base + (uint32_t)(l * kAcc * P) + (Fg & 1) * 16u, d);
+          float d[NC][16];
+#pragma unroll
+          for (int co = 0; co < NC; ++co)
+            tmem_load<16>(tmem_base + lane_base + (uint32_t)(l * kAcc * P) + (Fg & 1) * 16u * NC + co * 16u, d[co]);
           tmem_wait_ld();
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(bar_tempty(l, Fg & 1));
-          float lft[3], rgt[3];
+          float lft[NC][3], rgt[NC][3];
 #pragma unroll
-          for (int q = 0; q < 3; ++q) {
-            lft[q] = __shfl_up_sync(0xffffffffu, d[q * 3], 1);
-            rgt[q] = __shfl_down_sync(0xffffffffu, d[q * 3 + 2], 1);
-          }
-          float *xb = xch + (f & 1) * 24;   // [quarter][0-2: lane 31's left taps, 3-5: lane 0's right taps]
-          if (lane == 31) {
+          for (int co = 0; co < NC; ++co) {
 #pragma unroll
-            for (int q = 0; q < 3; ++q) xb[quarter * 6 + q] = d[q * 3];
-          }
-          if (lane == 0) {
+            for (int q = 0; q < 3; ++q) {
+              lft[co][q] = __shfl_up_sync(0xffffffffu, d[co][q * 3], 1);
+              rgt[co][q] = __shfl_down_sync(0xffffffffu, d[co][q * 3 + 2], 1);
+            }
+            // [parity][channel][quarter][0-2: lane 31's left taps, 3-5: lane 0's right taps]
+            float *xb = xch + ((f & 1) * NC + co) * 24;
+            if (lane == 31) {
 #pragma unroll
-            for (int q = 0; q < 3; ++q) xb[quarter * 6 + 3 + q] = d[q * 3 + 2];
+              for (int q = 0; q < 3; ++q) xb[quarter * 6 + q] = d[co][q * 3];
+            }
+            if (lane == 0) {
+#pragma unroll
+              for (int q = 0; q < 3; ++q) xb[quarter * 6 + 3 + q] = d[co][q * 3 + 2];
+            }
           }
           asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory");   // the group's 4 warps
-          if (lane == 0 && quarter > 0) {
-#pragma unroll
-            for (int q = 0; q < 3; ++q) lft[q] = xb[(quarter - 1) * 6 + q];
-          }
-          if (lane == 31 && quarter < 3) {
-#pragma unroll
-            for (int q = 0; q < 3; ++q) rgt[q] = xb[(quarter + 1) * 6 + 3 + q];
-          }
-          float c[3];
-#pragma unroll
-          for (int q = 0; q < 3; ++q) c[q] = (lft[q] + d[q * 3 + 1]) + rgt[q];
-          const float row_done = nacc0 + c[0];   // output row f-2 (dy = +1 is its last fill)
-          nacc0 = nacc1 + c[1];
-          nacc1 = c[2];
           const int ic = f - 2;
-          if (ic >= 0 && ic < nout(l) && col_valid) {
-            const int o = r_lo - (NL - 1 - l) + ic;
-            const TileGeom &g = p.gg;
-            const int64_t gidx = (int64_t)(o - (g.i0 - g.h)) * g.pitch + (cm - (g.j0 - g.hx));
-            if (NL != 1 || p.mode < 2) {   // DDFB modes only exist for single-operator launches
-              p.G[gidx] = row_done + p.bias[l][0];
-            } else if (o >= 0 && o < p.ny && cm >= 0 && cm < p.nx) {
-              // DDFB adjoint step (R39): q = proj_[0,1](v - W_k^* u); final: G = v - q
-              const TileGeom &xg = p.xg;
-              const float v = p.x[(int64_t)(o - (xg.i0 - xg.h)) * xg.pitch + (cm - (xg.j0 - xg.hx))];
-              const float q = fminf(fmaxf(v - row_done, 0.f), 1.f);
-              p.G[gidx] = p.mode == 4 ? v - q : q;
+          const int o = r_lo - (NL - 1 - l) + ic;
+          const TileGeom &g = p.gg;
+          const int64_t gidx = (int64_t)(o - (g.i0 - g.h)) * g.pitch + (cm - (g.j0 - g.hx));
+          const bool store = ic >= 0 && ic < nout(l) && col_valid;
+#pragma unroll
+          for (int co = 0; co < NC; ++co) {
+            const float *xb = xch + ((f & 1) * NC + co) * 24;
+            if (lane == 0 && quarter > 0) {
+#pragma unroll
+              for (int q = 0; q < 3; ++q) lft[co][q] = xb[(quarter - 1) * 6 + q];
+            }
+            if (lane == 31 && quarter < 3) {
+#pragma unroll
+              for (int q = 0; q < 3; ++q) rgt[co][q] = xb[(quarter + 1) * 6 + 3 + q];
+            }
+            float c[3];
+#pragma unroll
+            for (int q = 0; q < 3; ++q) c[q] = (lft[co][q] + d[co][q * 3 + 1]) + rgt[co][q];
+            const float row_done = nacc0[co] + c[0];   // output row f-2 (dy = +1 is its last fill)
+            nacc0[co] = nacc1[co] + c[1];
+            nacc1[co] = c[2];
+            if (store) {
+              if (NC > 1 || NL != 1 || p.mode < 2) {   // DDFB modes only exist for single-operator launches
+                p.G[(int64_t)co * p.gcs + gidx] = row_done + p.bias[l][co];
+              } else if (o >= 0 && o < p.ny && cm >= 0 && cm < p.nx) {
+                // DDFB adjoint step (R39): q = proj_[0,1](v - W_k^* u); final: G = v - q
+                const TileGeom &xg = p.xg;
+                const float v = p.x[(int64_t)(o - (xg.i0 - xg.h)) * xg.pitch + (cm - (xg.j0 - xg.hx))];
+                const float q = fminf(fmaxf(v - row_done, 0.f), 1.f);
+                p.G[gidx] = p.mode == 4 ? v - q : q;
+              }
             }
           }
           trace_ev(p.trace, trw, 8, s, l);
@@ -713,7 +744,7 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
           }
           const uint32_t ta = taddr + (Ig & 3) * (uint32_t)P;
           uint32_t w[P / 2];
-          if (NL == 1 && (p.mode == 1 || p.mode == 3)) {
+          if (NC == 1 && NL == 1 && (p.mode == 1 || p.mode == 3)) {
             // DDFB im2col layers (R39, R40): mode 1 u0 = W_K v (no bias, no activation);
             // mode 3 u' = HT(u + gamma_k W_k p) with u read (bf16) at the same pixel
             uint32_t uin[P / 2];
@@ -840,10 +871,10 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
   }
 }
 
-template <int P, int NL>
+template <int P, int NL, int NC>
 cudaError_t launch_pn(const CnnChunkParams &p0, int num_sms, cudaStream_t s) {
   CnnChunkParams p = p0;
-  const SmemLayout L = make_layout(P, NL, p.first_is_input, p.last_is_output);
+  const SmemLayout L = make_layout(P, NL, p.first_is_input, p.last_is_output, NC);
   const int Wv = kRowPos - 2 * ((p.last_is_output && NL < 2) ? 2 : NL);   // as in the kernel
   const int strips = (p.ow + Wv - 1) / Wv;
   // rows per unit: minimise (waves) x (rows per unit + pipeline fill) over row-block counts
@@ -861,7 +892,7 @@ cudaError_t launch_pn(const CnnChunkParams &p0, int num_sms, cudaStream_t s) {
   p.strips = strips;
   p.rows_per_unit = R;
   p.units = strips * ((p.oh + R - 1) / R);
-  auto kfn = cnn_chunk_kernel<P, NL>;
+  auto kfn = cnn_chunk_kernel<P, NL, NC>;
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
   if (e != cudaSuccess) return e;
   const int grid = p.units < num_sms ? p.units : num_sms;
@@ -872,23 +903,24 @@ cudaError_t launch_pn(const CnnChunkParams &p0, int num_sms, cudaStream_t s) {
 // compile-time chain lengths: TMEM (NL * 4 * P <= 512 columns) and 227 KB of shared memory
 constexpr int max_nl(int P) { return P == 16 ? 8 : P == 32 ? 4 : 1; }
 
-template <int P, int NL>
+template <int P, int NL, int NC>
 cudaError_t dispatch_nl(const CnnChunkParams &p, int num_sms, cudaStream_t s) {
   if constexpr (NL > max_nl(P)) {
     return cudaErrorInvalidValue;
   } else {
-    if (p.nl == NL) return launch_pn<P, NL>(p, num_sms, s);
-    if constexpr (NL < kMaxChunk) return dispatch_nl<P, NL + 1>(p, num_sms, s);
+    if (p.nl == NL) return launch_pn<P, NL, NC>(p, num_sms, s);
+    if constexpr (NL < kMaxChunk) return dispatch_nl<P, NL + 1, NC>(p, num_sms, s);
     return cudaErrorInvalidValue;
   }
 }
 
 }  // namespace
 
-size_t cnn_chunk_smem_bytes(int P, int nl, int first, int last) {
+size_t cnn_chunk_smem_bytes(int P, int nl, int first, int last, int nc) {
   if (nl < 1 || nl > kMaxChunk) return SIZE_MAX;
   if (nl > max_nl(P)) return SIZE_MAX;
-  return make_layout(P, nl, first, last).total;
+  if (nc != 1 && (nc != 3 || P < 32)) return SIZE_MAX;   // C = 3: N = 48 columns of the folded last layer
+  return make_layout(P, nl, first, last, nc).total;
 }
 
 size_t cnn_packed_layer_elems(int cout, int cin) { return packed_layer_elems(cout, cin); }
@@ -901,35 +933,38 @@ static uint16_t f32_to_bf16_rne(float f) {
   return (uint16_t)(u >> 16);
 }
 
-// B-operand image of one layer.  cin == 1: one K=16 block whose k index is the tap
-// (u+1)*3+(v+1).  cin == P: per (horizontal tap dx, K step ks) one block
+// B-operand image of one layer.  cin = C <= 3 (image): K = 16 or 32 whose k index is the tap
+// ci*9 + (u+1)*3+(v+1).  cin == P: per (horizontal tap dx, K step ks) one block
 // [2 halves][N3 = 3 Cb rows][8 cin] bf16 whose row n = q*Cb + co holds the weight of
-// vertical tap dy = 1 - q (q = 0, 1, 2 <-> dy = +1, 0, -1); Cb = cout, or 16 (zero padded)
-// for cout == 1.
+// vertical tap dy = 1 - q (q = 0, 1, 2 <-> dy = +1, 0, -1); Cb = cout.  cout = C <= 3: the
+// folded layer (all nine taps of output channel co in rows co*16 + q*3 + dxi).
 void cnn_pack_layer(const float *w, int cout, int cin, uint16_t *out) {
   const size_t n = packed_layer_elems(cout, cin);
   memset(out, 0, n * sizeof(uint16_t));
-  if (cin == 1) {
+  if (cin <= 3) {
+    // im2col layer: K index t = ci * 9 + tap (matching the producer's row), [K/8][N][8]
     const int N = cout;
     for (int co = 0; co < cout; ++co)
-      for (int t = 0; t < 9; ++t) {
+      for (int t = 0; t < 9 * cin; ++t) {
         const int g2 = t / 8, k8 = t % 8;
-        out[((size_t)g2 * N + co) * 8 + k8] = f32_to_bf16_rne(w[(size_t)co * 9 + t]);
+        out[((size_t)g2 * N + co) * 8 + k8] = f32_to_bf16_rne(w[(size_t)co * cin * 9 + t]);
       }
     return;
   }
   const int KS = cin / 16;
-  if (cout == 1) {
-    // folded P -> 1 layer: per K step one block [2 halves][16 taps][8 cin]; tap row
-    // n = q*3 + dxi holds W(dy = 1 - q, dx = dxi - 1); rows 9..15 zero
+  if (cout <= 3) {
+    // folded P -> C layer: per K step one block [2 halves][16 C taps][8 cin]; tap row
+    // n = co*16 + q*3 + dxi holds W_co(dy = 1 - q, dx = dxi - 1); rows co*16 + 9..15 zero
+    const size_t N = 16u * (size_t)cout;
     for (int ks = 0; ks < KS; ++ks)
-      for (int q = 0; q < 3; ++q)
-        for (int dxi = 0; dxi < 3; ++dxi)
-          for (int c = 0; c < 16; ++c) {
-            const int ci = ks * 16 + c, dyi = 2 - q;
-            out[(size_t)ks * 256 + ((size_t)(c / 8) * 16 + (size_t)(q * 3 + dxi)) * 8 + (c % 8)] =
-                f32_to_bf16_rne(w[(size_t)ci * 9 + dyi * 3 + dxi]);
-          }
+      for (int co = 0; co < cout; ++co)
+        for (int q = 0; q < 3; ++q)
+          for (int dxi = 0; dxi < 3; ++dxi)
+            for (int c = 0; c < 16; ++c) {
+              const int ci = ks * 16 + c, dyi = 2 - q;
+              out[(size_t)ks * 16 * N + ((size_t)(c / 8) * N + (size_t)(co * 16 + q * 3 + dxi)) * 8 + (c % 8)] =
+                  f32_to_bf16_rne(w[((size_t)co * cin + ci) * 9 + dyi * 3 + dxi]);
+            }
     return;
   }
   const int Cb = cout;
@@ -951,10 +986,20 @@ void cnn_pack_layer(const float *w, int cout, int cin, uint16_t *out) {
 }
 
 cudaError_t launch_cnn_chunk(const CnnChunkParams &p, int num_sms, cudaStream_t s) {
+  // image channels matter only to chunks holding the first or the last layer
+  const int nc = (p.first_is_input || p.last_is_output) && p.nc > 1 ? p.nc : 1;
+  if (nc == 3) {
+    switch (p.P) {
+      case 32: return dispatch_nl<32, 1, 3>(p, num_sms, s);
+      case 64: return dispatch_nl<64, 1, 3>(p, num_sms, s);
+      default: return cudaErrorInvalidValue;
+    }
+  }
+  if (nc != 1) return cudaErrorInvalidValue;
   switch (p.P) {
-    case 16: return dispatch_nl<16, 1>(p, num_sms, s);
-    case 32: return dispatch_nl<32, 1>(p, num_sms, s);
-    case 64: return dispatch_nl<64, 1>(p, num_sms, s);
+    case 16: return dispatch_nl<16, 1, 1>(p, num_sms, s);
+    case 32: return dispatch_nl<32, 1, 1>(p, num_sms, s);
+    case 64: return dispatch_nl<64, 1, 1>(p, num_sms, s);
     default: return cudaErrorInvalidValue;
   }
 }

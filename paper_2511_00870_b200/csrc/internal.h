@@ -60,6 +60,7 @@ struct UpdateParams {
   const float *zv, *zh;            // padded z = (z_v, z_h) ~ D x, valid on tile (+) 1
   const IterState *it;             // non-null: t1 / accumulate / inv_n from here (graph replay)
   IterState *it_next;              // non-null: block 0 writes the next iteration's scalars here
+  uint32_t sb;                     // Philox stream base of this image channel (4 c, reading R43)
 };
 
 // TV z block (R37, R38): on tile (+) 1 inside the image
@@ -91,6 +92,7 @@ struct Z1Params {
   float eta, b1, s1, kappa1;        // eta, kappa1/rho1, sqrt(2 kappa1), kappa1
   uint32_t seed_lo, seed_hi, t1;
   const IterState *it;              // non-null: t1 from here (graph replay)
+  uint32_t sb;                      // Philox stream base of this image channel (4 c)
 };
 
 // One rectangular copy between pitched fp32 buffers (halo exchange, pack/unpack).
@@ -134,6 +136,8 @@ struct CnnChunkParams {
   int mode;              // 0 DnCNN; DDFB (R39-R42): 1 u0 = W_K v, 2 p = proj(v - W^* u), 3 u = HT(u + gamma W p),
                          // 4 G = v - proj(v - gamma_K W_K^* u)
   float ht_eps;          // DDFB hard-tanh level
+  int nc;                // image channels C (1, or 3 with P >= 32; reading R43): planes of x / G
+  int64_t xcs, gcs;      // floats between the channel planes of x and of G
 };
 
 // Launchers (return cudaGetLastError()).
@@ -157,7 +161,7 @@ cudaError_t launch_copy_jobs(const CopyJob *d_jobs, int njobs, int max_rows, cud
 cudaError_t launch_fill(float *p, float v, size_t n, cudaStream_t s);
 cudaError_t launch_finalize(const FinalizeParams &p, cudaStream_t s);
 cudaError_t launch_cnn_chunk(const CnnChunkParams &p, int num_sms, cudaStream_t s);
-size_t cnn_chunk_smem_bytes(int P, int nl, int first_is_input, int last_is_output);
+size_t cnn_chunk_smem_bytes(int P, int nl, int first_is_input, int last_is_output, int nc);
 // Pack host fp32 OIHW weights of one layer into the device B-operand image (host side).
 void cnn_pack_layer(const float *w, int cout, int cin, uint16_t *out);
 size_t cnn_packed_layer_elems(int cout, int cin);

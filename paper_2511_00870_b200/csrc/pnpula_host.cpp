@@ -75,6 +75,7 @@ struct pnpula_ctx {
   int flags = 0;
   int n_layers = 0, channels = 0;   // 0 layers = no CNN
   int den_kind = 0;                 // PNPULA_DEN_DNCNN / PNPULA_DEN_DDFB
+  int nc = 1;                       // image channels (R43): state buffers hold nc planes
   double ht_eps = 0;
   // DDFB operator images (R39-R42): W_K (im2col) for u0, gamma_k W_k (im2col) for T_k,
   // flipped W_k (folded P -> 1) for W_k^*, flipped gamma_K W_K for the final adjoint
@@ -238,6 +239,7 @@ pnpula_status run_ddfb(pnpula_ctx *c, int buf) {
       p.nl = 1;
       p.mode = mode;
       p.ht_eps = (float)c->ht_eps;
+      p.nc = 1;
       p.x = td.x[buf];
       p.xg = g;
       p.oi0 = g.i0 - ext; p.oj0 = g.j0 - ext;
@@ -332,6 +334,8 @@ pnpula_status run_cnn(pnpula_ctx *c, int buf) {
         p.gg = g;
       }
       p.ny = c->ny; p.nx = c->nx;
+      p.nc = c->nc;
+      p.xcs = p.gcs = (int64_t)geom_elems(g);
       p.err = c->d_err;
       // optional pipeline trace of the first evaluation (diagnostics; env PNPULA_CNN_TRACE=<path prefix>)
       const char *trace_path = getenv("PNPULA_CNN_TRACE");
@@ -438,13 +442,21 @@ pnpula_status enqueue_step(pnpula_ctx *c, int buf, const IterState *it) {
   const uint64_t t1 = (uint64_t)c->t + 1;
   const bool acc = (int64_t)t1 > c->burn_in;
   const double k = acc ? (double)((int64_t)t1 - c->burn_in) : 1.0;
-  for (auto &td : c->tiles) {
+  for (auto &td : c->tiles)
+  for (int ch = 0; ch < c->nc; ++ch) {
     UpdateParams p = make_update_params(c, td, buf);
     p.t1 = (uint32_t)t1;
     p.accumulate = acc;
     p.inv_n = (float)(1.0 / k);
     p.it = it;
-    p.it_next = (it && &td == &c->tiles[0]) ? c->d_iter + (buf ^ 1) : nullptr;
+    p.it_next = (it && &td == &c->tiles[0] && ch == 0) ? c->d_iter + (buf ^ 1) : nullptr;
+    if (ch > 0) {   // channel plane ch (R43): same geometry, its own Philox streams 4 ch + s
+      const size_t o = (size_t)ch * geom_elems(td.g);
+      p.x += o; p.xn += o; p.y += o; p.mean += o; p.m2 += o;
+      if (p.G) p.G += o;
+      if (p.z) p.z += o;
+      p.sb = 4u * (uint32_t)ch;
+    }
     cudaEvent_t end;
     timer_begin(c, c->tm_update, &end);
     CU(c, launch_update(p, c->stream));
@@ -478,11 +490,14 @@ pnpula_status enqueue_step(pnpula_ctx *c, int buf, const IterState *it) {
   }
   if (c->op == PNPULA_OP_POISSON) {
     // line 11-13 for the z1 block: x^{t+1} (halo now valid) -> z1 on tile (+) r_H (R33, R34)
-    for (auto &td : c->tiles) {
+    for (auto &td : c->tiles)
+    for (int ch = 0; ch < c->nc; ++ch) {
+      const size_t o = (size_t)ch * geom_elems(td.g);
       Z1Params q{};
-      q.x = td.x[buf ^ 1];
-      q.y = td.y;
-      q.z1 = td.z1;
+      q.x = td.x[buf ^ 1] + o;
+      q.y = td.y + o;
+      q.z1 = td.z1 + o;
+      q.sb = 4u * (uint32_t)ch;
       q.g = td.g;
       q.ny = c->ny; q.nx = c->nx;
       q.ry = c->ry; q.rx = c->rx;
@@ -591,26 +606,30 @@ pnpula_status build_halo_plan(pnpula_ctx *c) {
     auto off = [](const TileGeom &g, int gi, int gj) {
       return (size_t)(gi - (g.i0 - g.h)) * g.pitch + (gj - (g.j0 - g.hx));
     };
-    if (src && dst && !force_nccl) {
-      for (int b = 0; b < 2; ++b)
-        lj[b].push_back({src->x[b] + off(src->g, r.i0, r.j0), dst->x[b] + off(dst->g, r.i0, r.j0),
-                         src->g.pitch, dst->g.pitch, r.h, r.w});
-      c->max_local = std::max(c->max_local, (int)cnt);
-      continue;
-    }
-    if (src) {
-      for (int b = 0; b < 2; ++b)
-        pj[b].push_back({src->x[b] + off(src->g, r.i0, r.j0), nullptr, src->g.pitch, r.w, r.h, r.w});
-      c->sends.push_back({owner(m.dst_tile), soff, cnt});
-      soff += cnt;
-      c->max_pack = std::max(c->max_pack, (int)cnt);
-    }
-    if (dst) {
-      for (int b = 0; b < 2; ++b)
-        uj[b].push_back({nullptr, dst->x[b] + off(dst->g, r.i0, r.j0), r.w, dst->g.pitch, r.h, r.w});
-      c->recvs.push_back({owner(m.src_tile), roff, cnt});
-      roff += cnt;
-      c->max_unpack = std::max(c->max_unpack, (int)cnt);
+    // one job / message per image channel plane (R43)
+    for (int ch = 0; ch < c->nc; ++ch) {
+      const size_t so = src ? (size_t)ch * geom_elems(src->g) : 0, dso = dst ? (size_t)ch * geom_elems(dst->g) : 0;
+      if (src && dst && !force_nccl) {
+        for (int b = 0; b < 2; ++b)
+          lj[b].push_back({src->x[b] + so + off(src->g, r.i0, r.j0), dst->x[b] + dso + off(dst->g, r.i0, r.j0),
+                           src->g.pitch, dst->g.pitch, r.h, r.w});
+        c->max_local = std::max(c->max_local, (int)cnt);
+        continue;
+      }
+      if (src) {
+        for (int b = 0; b < 2; ++b)
+          pj[b].push_back({src->x[b] + so + off(src->g, r.i0, r.j0), nullptr, src->g.pitch, r.w, r.h, r.w});
+        c->sends.push_back({owner(m.dst_tile), soff, cnt});
+        soff += cnt;
+        c->max_pack = std::max(c->max_pack, (int)cnt);
+      }
+      if (dst) {
+        for (int b = 0; b < 2; ++b)
+          uj[b].push_back({nullptr, dst->x[b] + dso + off(dst->g, r.i0, r.j0), r.w, dst->g.pitch, r.h, r.w});
+        c->recvs.push_back({owner(m.src_tile), roff, cnt});
+        roff += cnt;
+        c->max_unpack = std::max(c->max_unpack, (int)cnt);
+      }
     }
   }
   if (soff) CU(c, cudaMalloc(&c->d_sendbuf, soff * sizeof(float)));
@@ -650,7 +669,7 @@ void plan_cnn_chunks(pnpula_ctx *c) {
     int best = 1;
     const int maxnl = (c->flags & PNPULA_FLAG_CNN_LAYERWISE) ? 1 : kMaxChunk;
     for (int nl = 1; nl <= std::min(maxnl, K - l + 1); ++nl) {
-      if (cnn_chunk_smem_bytes(c->channels, nl, l == 1, l + nl - 1 == K) <= budget) best = nl;
+      if (cnn_chunk_smem_bytes(c->channels, nl, l == 1, l + nl - 1 == K, c->nc) <= budget) best = nl;
     }
     c->chunks.push_back({l, best, K - (l + best - 1)});
     l += best;
@@ -774,9 +793,16 @@ pnpula_status pnpula_create(const pnpula_config *cfg, pnpula_ctx **out) {
     }
     if (!(f.eps > 0)) { set_error("eps must be > 0"); return PNPULA_E_INVALID_ARG; }
   }
+  const int nc = f.img_channels > 1 ? f.img_channels : 1;
+  if (nc != 1 && nc != 3) { set_error("img_channels must be 1 or 3"); return PNPULA_E_UNSUPPORTED; }
+  if (nc > 1 && (tv || ddfb)) { set_error("colour images: TV prior and DDFB denoiser not supported"); return PNPULA_E_UNSUPPORTED; }
+  if (nc > 1 && use_cnn && f.den->channels < 32) {
+    set_error("colour DnCNN needs channels >= 32 (N = 48 folded output columns)"); return PNPULA_E_UNSUPPORTED;
+  }
   const pnpula_rect in = f.in_rect;
 
   pnpula_ctx *c = new pnpula_ctx();
+  c->nc = nc;
   c->ny = f.ny; c->nx = f.nx; c->tiles_y = f.tiles_y; c->tiles_x = f.tiles_x;
   c->rank = f.rank; c->world = f.world_size; c->device = f.device;
   c->op = f.op; c->flags = f.flags;
@@ -912,7 +938,8 @@ pnpula_status pnpula_create(const pnpula_config *cfg, pnpula_ctx **out) {
 
   // device buffers
   for (auto &td : c->tiles) {
-    const size_t n = geom_elems(td.g);
+    const size_t n1 = geom_elems(td.g);   // one plane
+    const size_t n = n1 * (size_t)nc;      // state fields: nc planes
     for (int b = 0; b < 2; ++b) {
       CUB(cudaMalloc(&td.x[b], n * sizeof(float)));
       CUB(cudaMemsetAsync(td.x[b], 0, n * sizeof(float), c->stream));
@@ -932,9 +959,9 @@ pnpula_status pnpula_create(const pnpula_config *cfg, pnpula_ctx **out) {
       CUB(cudaMalloc(&td.z1, n * sizeof(float)));
       CUB(cudaMemsetAsync(td.z1, 0, n * sizeof(float), c->stream));
     }
-    if (c->op == PNPULA_OP_MASK) {
-      CUB(cudaMalloc(&td.mask, n));
-      CUB(cudaMemsetAsync(td.mask, 0, n, c->stream));
+    if (c->op == PNPULA_OP_MASK) {   // one plane, shared by the channels
+      CUB(cudaMalloc(&td.mask, n1));
+      CUB(cudaMemsetAsync(td.mask, 0, n1, c->stream));
     }
     if (c->n_layers > 0) {
       CUB(cudaMalloc(&td.G, n * sizeof(float)));
@@ -942,11 +969,15 @@ pnpula_status pnpula_create(const pnpula_config *cfg, pnpula_ctx **out) {
     }
     const TileGeom &g = td.g;
     pnpula_status s;
-    s = upload_padded<float>(c, td.y, g, f.y, in, g.i0 - rH, g.j0 - rH, g.th + 2 * rH, g.tw + 2 * rH);
-    if (s) return bail(s);
-    if (f.x0) {
-      s = upload_padded<float>(c, td.x0, g, f.x0, in, g.i0, g.j0, g.th, g.tw);
+    const size_t in_plane = (size_t)in.h * in.w;
+    for (int ch = 0; ch < nc; ++ch) {
+      s = upload_padded<float>(c, td.y + ch * n1, g, f.y + ch * in_plane, in, g.i0 - rH, g.j0 - rH, g.th + 2 * rH,
+                               g.tw + 2 * rH);
       if (s) return bail(s);
+      if (f.x0) {
+        s = upload_padded<float>(c, td.x0 + ch * n1, g, f.x0 + ch * in_plane, in, g.i0, g.j0, g.th, g.tw);
+        if (s) return bail(s);
+      }
     }
     if (c->op == PNPULA_OP_MASK) {
       s = upload_padded<uint8_t>(c, td.mask, g, f.mask, in, g.i0, g.j0, g.th, g.tw);
@@ -1008,9 +1039,9 @@ pnpula_status pnpula_create(const pnpula_config *cfg, pnpula_ctx **out) {
     const int K = c->n_layers, P = c->channels;
     const float *w = f.den->weights;
     const float *b = f.den->biases;
-    int cin = 1;
+    int cin = nc;   // layer 1: C -> P, layer K: P -> C (R43)
     for (int l = 1; l <= K; ++l) {
-      const int cout = (l == K) ? 1 : P;
+      const int cout = (l == K) ? nc : P;
       std::vector<uint16_t> packed(cnn_packed_layer_elems(cout, cin));
       cnn_pack_layer(w, cout, cin, packed.data());
       uint16_t *dw = nullptr;
@@ -1057,7 +1088,7 @@ pnpula_status pnpula_reset(pnpula_ctx *c, int64_t burn_in, uint64_t seed) {
   if (burn_in < 0) { set_error("burn_in must be >= 0"); return PNPULA_E_INVALID_ARG; }
   CU(c, cudaSetDevice(c->device));
   for (auto &td : c->tiles) {
-    const size_t n = geom_elems(td.g) * sizeof(float);
+    const size_t n = geom_elems(td.g) * sizeof(float) * c->nc;
     CU(c, cudaMemcpyAsync(td.x[0], td.x0, n, cudaMemcpyDeviceToDevice, c->stream));
     CU(c, cudaMemcpyAsync(td.x[1], td.x0, n, cudaMemcpyDeviceToDevice, c->stream));
     if (td.z) CU(c, cudaMemsetAsync(td.z, 0, n, c->stream));
@@ -1216,8 +1247,8 @@ pnpula_status tile_staging(pnpula_ctx *c, int nf, std::vector<float *> &bufs) {
   return PNPULA_OK;
 }
 
-pnpula_status gather_padded_interiors(pnpula_ctx *c, const std::vector<const float *> &src, float *host,
-                                      bool global) {
+pnpula_status gather_padded_interiors1(pnpula_ctx *c, const std::vector<const float *> &src, float *host,
+                                       bool global) {
   // pack interiors to contiguous, then gather
   std::vector<float *> bufs;
   pnpula_status s = tile_staging(c, 1, bufs);
@@ -1230,6 +1261,21 @@ pnpula_status gather_padded_interiors(pnpula_ctx *c, const std::vector<const flo
   }
   pnpula_rect dst = global ? pnpula_rect{0, 0, c->ny, c->nx} : c->bbox;
   return gather_fields(c, bufs, 1, {host}, dst, global);
+}
+
+// all channel planes of a per-tile padded field -> host [C][h][w]
+pnpula_status gather_padded_interiors(pnpula_ctx *c, const std::vector<const float *> &src, float *host,
+                                      bool global, int planes = -1) {
+  if (planes < 0) planes = c->nc;
+  const pnpula_rect dst = global ? pnpula_rect{0, 0, c->ny, c->nx} : c->bbox;
+  for (int ch = 0; ch < planes; ++ch) {
+    std::vector<const float *> s2;
+    for (size_t li = 0; li < src.size(); ++li) s2.push_back(src[li] + (size_t)ch * geom_elems(c->tiles[li].g));
+    float *h = (host && (!global || c->rank == 0)) ? host + (size_t)ch * dst.h * dst.w : host;
+    pnpula_status s = gather_padded_interiors1(c, s2, h, global);
+    if (s) return s;
+  }
+  return PNPULA_OK;
 }
 
 }  // namespace
@@ -1249,18 +1295,26 @@ pnpula_status pnpula_get_moments(pnpula_ctx *c, float *mean, float *var, int64_t
   std::vector<float *> bufs;
   s = tile_staging(c, 2, bufs);
   if (s) return s;
-  for (size_t li = 0; li < c->tiles.size(); ++li) {
-    auto &td = c->tiles[li];
-    const TileGeom &g = td.g;
-    float *d = bufs[li];
-    FinalizeParams p{};
-    p.mean = td.mean; p.m2 = td.m2; p.g = g;
-    p.out_mean = d; p.out_var = d + (size_t)g.th * g.tw;
-    p.inv_nm1 = n >= 2 ? (float)(1.0 / (double)(n - 1)) : 0.f;
-    CU(c, launch_finalize(p, c->stream));
-  }
   pnpula_rect dst = global ? pnpula_rect{0, 0, c->ny, c->nx} : c->bbox;
-  return gather_fields(c, bufs, 2, {mean, var}, dst, global);
+  const size_t dplane = (size_t)dst.h * dst.w;
+  for (int ch = 0; ch < c->nc; ++ch) {   // one channel plane at a time (R43)
+    for (size_t li = 0; li < c->tiles.size(); ++li) {
+      auto &td = c->tiles[li];
+      const TileGeom &g = td.g;
+      const size_t o = (size_t)ch * geom_elems(g);
+      float *d = bufs[li];
+      FinalizeParams p{};
+      p.mean = td.mean + o; p.m2 = td.m2 + o; p.g = g;
+      p.out_mean = d; p.out_var = d + (size_t)g.th * g.tw;
+      p.inv_nm1 = n >= 2 ? (float)(1.0 / (double)(n - 1)) : 0.f;
+      CU(c, launch_finalize(p, c->stream));
+    }
+    const bool here = !global || c->rank == 0;
+    s = gather_fields(c, bufs, 2, {mean && here ? mean + ch * dplane : mean, var && here ? var + ch * dplane : var},
+                      dst, global);
+    if (s) return s;
+  }
+  return PNPULA_OK;
 }
 
 pnpula_status pnpula_get_state(pnpula_ctx *c, float *x, float *z, int64_t *t, int32_t scope) {
@@ -1279,7 +1333,7 @@ pnpula_status pnpula_get_state(pnpula_ctx *c, float *x, float *z, int64_t *t, in
     s = gather_padded_interiors(c, zs, z, global);
   } else if (z && (!global || c->rank == 0)) {
     pnpula_rect d = global ? pnpula_rect{0, 0, c->ny, c->nx} : c->bbox;
-    memset(z, 0, (size_t)d.h * d.w * sizeof(float));
+    memset(z, 0, (size_t)d.h * d.w * c->nc * sizeof(float));
   }
   return s;
 }
@@ -1313,7 +1367,7 @@ std::vector<float *> ckpt_fields(pnpula_ctx *c, TileDev &td) {
 }
 uint64_t ckpt_bytes(pnpula_ctx *c) {
   uint64_t n = 0;
-  for (auto &td : c->tiles) n += (uint64_t)geom_elems(td.g) * ckpt_fields(c, td).size();
+  for (auto &td : c->tiles) n += (uint64_t)geom_elems(td.g) * c->nc * ckpt_fields(c, td).size();
   return sizeof(CkptHeader) + n * sizeof(float);
 }
 }  // namespace
@@ -1338,7 +1392,7 @@ pnpula_status pnpula_save_checkpoint(pnpula_ctx *c, void *buf, uint64_t bytes) {
   memcpy(buf, &h, sizeof(h));
   float *dst = reinterpret_cast<float *>(static_cast<char *>(buf) + sizeof(h));
   for (auto &td : c->tiles) {
-    const size_t n = geom_elems(td.g);
+    const size_t n = geom_elems(td.g) * c->nc;
     for (float *f : ckpt_fields(c, td)) {
       CU(c, cudaMemcpyAsync(dst, f, n * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
       dst += n;
@@ -1367,7 +1421,7 @@ pnpula_status pnpula_load_checkpoint(pnpula_ctx *c, const void *buf, uint64_t by
   CU(c, cudaSetDevice(c->device));
   const float *src = reinterpret_cast<const float *>(static_cast<const char *>(buf) + sizeof(h));
   for (auto &td : c->tiles) {
-    const size_t n = geom_elems(td.g);
+    const size_t n = geom_elems(td.g) * c->nc;
     for (float *f : ckpt_fields(c, td)) {
       CU(c, cudaMemcpyAsync(f, src, n * sizeof(float), cudaMemcpyHostToDevice, c->stream));
       src += n;

@@ -172,7 +172,7 @@ __device__ __forceinline__ void ula_finish(const UpdateParams &p, int gi, int gj
   const float *xv = q.x, *Gv = q.G, *zv = q.z;
   float *mv = q.m, *sv = q.s;
   float xi[4];
-  normals4(p.seed_lo, p.seed_hi, (uint32_t)gj4 >> 2, (uint32_t)gi, it_t1(p), 0u, xi);
+  normals4(p.seed_lo, p.seed_hi, (uint32_t)gj4 >> 2, (uint32_t)gi, it_t1(p), p.sb + 0u, xi);
   float dtv[4] = {0.f, 0.f, 0.f, 0.f};
   if (p.has_tv) tv_term(p, gi, gj4, xv, dtv);
   float xn[4];
@@ -189,7 +189,7 @@ __device__ __forceinline__ void ula_finish(const UpdateParams &p, int gi, int gj
   float zn[4];
   if (p.has_z) {
     float ze[4];
-    normals4(p.seed_lo, p.seed_hi, (uint32_t)gj4 >> 2, (uint32_t)gi, it_t1(p), 1u, ze);
+    normals4(p.seed_lo, p.seed_hi, (uint32_t)gj4 >> 2, (uint32_t)gi, it_t1(p), p.sb + 1u, ze);
 #pragma unroll
     for (int l = 0; l < 4; ++l) {
       const float v = zv[l] - p.b_rho * (zv[l] - xn[l]) + p.b_zeta * ze[l];
@@ -574,7 +574,7 @@ __global__ void __launch_bounds__(NTHREADS) z1_update_kernel(const __grid_consta
     const int gi = r0 + (int)(e / nq);
     const int gj4 = 4 * (q0 + (int)(e % nq));
     float ze[4];
-    normals4(p.seed_lo, p.seed_hi, (uint32_t)gj4 >> 2, (uint32_t)gi, it_t1(p), 2u, ze);
+    normals4(p.seed_lo, p.seed_hi, (uint32_t)gj4 >> 2, (uint32_t)gi, it_t1(p), p.sb + 2u, ze);
 #pragma unroll
     for (int l = 0; l < 4; ++l) {
       const int gj = gj4 + l;
@@ -650,7 +650,7 @@ __global__ void __launch_bounds__(NTHREADS) z1_sep_kernel(const __grid_constant_
     const int a = 2 * a2 + r, gi = bi0 + a;
     if (gi < rlo || gi >= rhi || gj4 >= chi || gj4 + 4 <= clo) continue;
     float ze[4];
-    normals4(p.seed_lo, p.seed_hi, (uint32_t)gj4 >> 2, (uint32_t)gi, it_t1(p), 2u, ze);
+    normals4(p.seed_lo, p.seed_hi, (uint32_t)gj4 >> 2, (uint32_t)gi, it_t1(p), p.sb + 2u, ze);
 #pragma unroll
     for (int l = 0; l < 4; ++l) {
       const int gj = gj4 + l;

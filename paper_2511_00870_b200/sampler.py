@@ -65,7 +65,10 @@ class Sampler:
             cfg.x0 = xx.ctypes.data
         r = in_rect if in_rect is not None else (0, 0, ny, nx)
         cfg.in_rect = L.Rect(*r)
-        if yy.shape != (r[2], r[3]):
+        # colour images (R43): y / x0 as planes (C, h, w)
+        self.nc = yy.shape[0] if yy.ndim == 3 else 1
+        cfg.img_channels = self.nc
+        if yy.shape[-2:] != (r[2], r[3]) or yy.ndim not in (2, 3):
             raise ValueError(f"y has shape {yy.shape}, in_rect is {r}")
         cfg.sigma2 = sigma2
         if n_layers and alpha != 0.0:
@@ -118,10 +121,11 @@ class Sampler:
     def synchronize(self):
         L.check(self._lib.pnpula_synchronize(self._h))
 
-    def _out_shape(self, scope):
+    def _out_shape(self, scope, planes=None):
+        c = (self.nc if planes is None else planes,) if (self.nc > 1 and planes != 1) else ()
         if scope == L.SCOPE_GLOBAL_ON_ROOT:
-            return (self.ny, self.nx) if self.rank == 0 else None
-        return (self.bbox[2], self.bbox[3])
+            return c + (self.ny, self.nx) if self.rank == 0 else None
+        return c + (self.bbox[2], self.bbox[3])
 
     def moments(self, scope: int = L.SCOPE_LOCAL, want_var: bool = True, out=None):
         """out: optional (mean, var) host arrays (e.g. pinned) to write into."""
@@ -152,7 +156,7 @@ class Sampler:
 
     def tv_zh(self, scope: int = L.SCOPE_LOCAL):
         """TV prior: the horizontal component z_h of z ~ D x."""
-        shp = self._out_shape(scope)
+        shp = self._out_shape(scope, planes=1)
         out = np.zeros(shp, np.float32) if shp else None
         L.check(self._lib.pnpula_get_tv_zh(self._h, L._ptr(out), scope))
         return out
@@ -187,7 +191,7 @@ class Sampler:
         return out
 
     def denoiser_residual(self):
-        out = np.zeros((self.bbox[2], self.bbox[3]), np.float32)
+        out = np.zeros(self._out_shape(L.SCOPE_LOCAL), np.float32)
         L.check(self._lib.pnpula_get_denoiser_residual(self._h, out.ctypes.data))
         return out
 
