@@ -72,6 +72,7 @@ constexpr int kRingAct = PNPULA_RING_ACT;       // ring slots of the epilogue-fe
 static_assert(kRingAct >= 3 && kRingAct <= 8, "input ring slots");
 __host__ __device__ constexpr uint32_t ring_slots(int l) { return l == 0 ? (uint32_t)kRing : (uint32_t)kRingAct; }
 constexpr int kAcc = 4;                         // accumulator-row slots per layer (TMEM)
+constexpr int kXS = 136;                        // staged floats per x row (130 ring positions + alignment)
 #ifndef PNPULA_LAG
 #define PNPULA_LAG 3
 #endif
@@ -82,6 +83,7 @@ struct SmemLayout {
   uint32_t ring_off[kMaxChunk];
   uint32_t slot_bytes[kMaxChunk];
   uint32_t w_off[kMaxChunk];
+  uint32_t xs_off;      // first-layer x staging: [producer warp][3 C rows][kXS] fp32, then one mbarrier per warp
   uint32_t bar_off;
   uint32_t misc_off;
   uint32_t total;
@@ -113,6 +115,10 @@ __host__ __device__ inline SmemLayout make_layout(int P, int nl, int first, int 
     const int cout = (l == nl - 1 && last) ? nc : P;
     L.w_off[l] = off;
     off = align_up(off + packed_layer_elems(cout, cin) * 2u, 128);
+  }
+  if (first) {       // x rows of the im2col producer (TMA bulk copies), + one mbarrier per producer warp
+    L.xs_off = off;
+    off = align_up(off + (uint32_t)(kProdWarps * 3 * nc * kXS) * 4u + (uint32_t)kProdWarps * 8u, 128);
   }
   L.bar_off = off;   // per layer: full[8], empty[8], tfull[4], tempty[4]
   off = align_up(off + (uint32_t)nl * 24u * 8u, 128);
@@ -348,6 +354,8 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
       }
     }
     mbar_init(bar_done, kMmaWarps);
+    if (first)
+      for (int w = 0; w < kProdWarps; ++w) mbar_init(sbase + L.xs_off + (uint32_t)(kProdWarps * 3 * NC * kXS) * 4u + w * 8u, 1);
     *abort_flag = 0;
     uint4 *tab = reinterpret_cast<uint4 *>(smem + L.misc_off + 16);
     for (int l = 0; l < NL; ++l) tab[l] = make_uint4(L.ring_off[l], L.slot_bytes[l], L.w_off[l], 0u);
@@ -394,6 +402,7 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
   auto Fcnt = [&](int l) { return sumRn + kdone * (uint32_t)(2 * (NL - 1 - l) + (is_im2col(l) ? 0 : 2)); };
   auto Ocnt = [&](int l) { return sumRn + kdone * (uint32_t)(2 * (NL - 1 - l)); };
 
+  uint32_t xphase = 0;   // im2col producers: phase of this warp's x-staging mbarrier
   for (int u = blockIdx.x; u < units; u += gridDim.x) {
     if (*abort_flag) break;
     const int rb = u / strips, strip = u - (u / strips) * strips;
@@ -425,30 +434,53 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
         uint8_t *slot = smem + ring0 + (Fg & 3) * slot0;
         if (first) {
           // im2col row for layer-1 output row o: 9 taps per image channel of x (bf16), tap
-          // k = ch * 9 + (dy+1) * 3 + (dx+1), K padded to 16 (C = 1) or 32 (C = 3)
+          // k = ch * 9 + (dy+1) * 3 + (dx+1), K padded to 16 (C = 1) or 32 (C = 3).  The 3 C x
+          // rows (positions col0-1 .. col0+128) are first staged in shared memory by TMA bulk
+          // copies (one round trip per fill instead of one per 32 pixels), then read from there.
           const int o = r_lo - NL + f + 1;
           const TileGeom &g = p.xg;
+          float *xs = reinterpret_cast<float *>(smem + L.xs_off) + warp * 3 * NC * kXS;
+          const uint32_t xbar = sbase + L.xs_off + (uint32_t)(kProdWarps * 3 * NC * kXS) * 4u + warp * 8u;
+          const int pc0 = col0 - 1 - (g.j0 - g.hx);   // padded column of ring position 0 (>= 0: h >= K)
+          const int a0 = pc0 & ~3;                     // 16-byte aligned copy start
+          uint32_t total = 0;
+#pragma unroll
+          for (int r = 0; r < 3 * NC; ++r) {
+            const int pr = o + (r % 3) - 1 - (g.i0 - g.h);
+            const int nv = (pr >= 0 && pr < g.ph) ? min(kXS, g.pitch - a0) : 0;   // multiple of 4
+            for (int e = nv + lane; e < kXS; e += 32) xs[r * kXS + e] = 0.f;    // outside the buffer
+            total += (uint32_t)nv * 4u;
+          }
+          fence_proxy_async();   // earlier generic reads / the zero fill before the async-proxy writes
+          __syncwarp();
+          if (lane == 0) {
+            asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(xbar), "r"(total)
+                         : "memory");
+#pragma unroll
+            for (int r = 0; r < 3 * NC; ++r) {
+              const int pr = o + (r % 3) - 1 - (g.i0 - g.h);
+              const int nv = (pr >= 0 && pr < g.ph) ? min(kXS, g.pitch - a0) : 0;
+              if (nv > 0)
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                        smem_u32(xs + r * kXS)),
+                    "l"(p.x + (int64_t)(r / 3) * p.xcs + (int64_t)pr * g.pitch + a0), "r"(nv * 4), "r"(xbar)
+                    : "memory");
+            }
+          }
+          if (!mbar_wait(xbar, xphase, abort_flag, p.err, 7)) break;
+          xphase ^= 1u;
           for (int m = lane; m < 128; m += 32) {
-            const int cm = col0 + m;
             float t[K0];
 #pragma unroll
             for (int k = 9 * NC; k < K0; ++k) t[k] = 0.f;
+            const float *xm = xs + (pc0 - a0) + m;   // position m (= column cm - 1) of row 0
 #pragma unroll
-            for (int ch = 0; ch < NC; ++ch) {
-              const float *xc = p.x + (int64_t)ch * p.xcs;
+            for (int ch = 0; ch < NC; ++ch)
 #pragma unroll
-              for (int u2 = -1; u2 <= 1; ++u2) {
-                const int pr = o + u2 - (g.i0 - g.h);
-                const bool rok = pr >= 0 && pr < g.ph;
+              for (int u2 = 0; u2 < 3; ++u2)
 #pragma unroll
-                for (int v2 = -1; v2 <= 1; ++v2) {
-                  const int pc = cm + v2 - (g.j0 - g.hx);
-                  float v = 0.f;
-                  if (rok && pc >= 0 && pc < g.pitch) v = __ldg(xc + (int64_t)pr * g.pitch + pc);
-                  t[ch * 9 + (u2 + 1) * 3 + (v2 + 1)] = v;
-                }
-              }
-            }
+                for (int v2 = 0; v2 < 3; ++v2) t[ch * 9 + u2 * 3 + v2] = xm[(ch * 3 + u2) * kXS + v2];
 #pragma unroll
             for (int kg = 0; kg < K0 / 8; ++kg)
               *reinterpret_cast<uint4 *>(slot + kg * 2048 + m * 16) =
