@@ -149,18 +149,29 @@ __device__ __forceinline__ void ula_load(const UpdateParams &p, int gi, int gj4,
 // padded x (halo >= 2) and z (valid on tile (+) 1), through L1.
 __device__ __forceinline__ void tv_term(const UpdateParams &p, int gi, int gj4, const float *xc, float out[4]) {
   const TileGeom &g = p.g;
-  const int64_t base = pidx(g, gi, gj4);
+  const int64_t base = pidx(g, gi, gj4);   // 16-byte aligned (padded column of gj4 is a multiple of 4)
   const int64_t pitch = g.pitch;
+  // the quad's neighbourhood as 6 float4 + 2 scalar loads (x above / below, z_v above / here,
+  // z_h here, x left / right and z_h left); out-of-image terms are masked below
+  const float4 xu = __ldg(reinterpret_cast<const float4 *>(p.x + base - pitch));
+  const float4 xd = __ldg(reinterpret_cast<const float4 *>(p.x + base + pitch));
+  const float4 vu = __ldg(reinterpret_cast<const float4 *>(p.zv + base - pitch));
+  const float4 vc = __ldg(reinterpret_cast<const float4 *>(p.zv + base));
+  const float4 hc = __ldg(reinterpret_cast<const float4 *>(p.zh + base));
+  const float xl = __ldg(p.x + base - 1), xr = __ldg(p.x + base + 4), hl = __ldg(p.zh + base - 1);
+  const float xup[4] = {xu.x, xu.y, xu.z, xu.w}, xdn[4] = {xd.x, xd.y, xd.z, xd.w};
+  const float zvu[4] = {vu.x, vu.y, vu.z, vu.w}, zvc[4] = {vc.x, vc.y, vc.z, vc.w};
+  const float zhc[4] = {hc.x, hc.y, hc.z, hc.w};
 #pragma unroll
   for (int l = 0; l < 4; ++l) {
     const int gj = gj4 + l;
     if (gj >= p.nx) { out[l] = 0.f; continue; }
-    const int64_t n = base + l;
+    const float xlf = l > 0 ? xc[l - 1] : xl, xrt = l < 3 ? xc[l + 1] : xr, zhl = l > 0 ? zhc[l - 1] : hl;
     float s = 0.f;
-    if (gi >= 1) s += (xc[l] - __ldg(p.x + n - pitch)) - __ldg(p.zv + n - pitch);
-    if (gi < p.ny - 1) s -= (__ldg(p.x + n + pitch) - xc[l]) - __ldg(p.zv + n);
-    if (gj >= 1) s += (xc[l] - __ldg(p.x + n - 1)) - __ldg(p.zh + n - 1);
-    if (gj < p.nx - 1) s -= (__ldg(p.x + n + 1) - xc[l]) - __ldg(p.zh + n);
+    if (gi >= 1) s += (xc[l] - xup[l]) - zvu[l];
+    if (gi < p.ny - 1) s -= (xdn[l] - xc[l]) - zvc[l];
+    if (gj >= 1) s += (xc[l] - xlf) - zhl;
+    if (gj < p.nx - 1) s -= (xrt - xc[l]) - zhc[l];
     out[l] = s;
   }
 }
@@ -682,11 +693,37 @@ __global__ void __launch_bounds__(NTHREADS) tv_z_kernel(const __grid_constant__ 
     float zev[4], zeh[4];
     normals4(p.seed_lo, p.seed_hi, (uint32_t)gj4 >> 2, (uint32_t)gi, it_t1(p), 1u, zev);
     normals4(p.seed_lo, p.seed_hi, (uint32_t)gj4 >> 2, (uint32_t)gi, it_t1(p), 3u, zeh);
+    const int64_t n0 = pidx(g, gi, gj4);   // 16-byte aligned
+    if (gj4 >= c0 && gj4 + 4 <= c1) {
+      // whole quad inside: 4 float4 loads + 1 scalar (x right of the quad), 2 float4 stores
+      const float4 x4 = __ldg(reinterpret_cast<const float4 *>(p.x + n0));
+      const float4 d4 = __ldg(reinterpret_cast<const float4 *>(p.x + n0 + g.pitch));
+      const float xr = __ldg(p.x + n0 + 4);
+      const float4 v4 = *reinterpret_cast<const float4 *>(p.zv + n0);
+      const float4 h4 = *reinterpret_cast<const float4 *>(p.zh + n0);
+      const float xc[5] = {x4.x, x4.y, x4.z, x4.w, xr}, xd[4] = {d4.x, d4.y, d4.z, d4.w};
+      const float zv[4] = {v4.x, v4.y, v4.z, v4.w}, zh[4] = {h4.x, h4.y, h4.z, h4.w};
+      float ov[4], oh[4];
+#pragma unroll
+      for (int l = 0; l < 4; ++l) {
+        const float dv = gi < p.ny - 1 ? xd[l] - xc[l] : 0.f;
+        const float dh = gj4 + l < p.nx - 1 ? xc[l + 1] - xc[l] : 0.f;
+        const float vv = zv[l] - p.b * (zv[l] - dv) + p.s * zev[l];
+        const float vh = zh[l] - p.b * (zh[l] - dh) + p.s * zeh[l];
+        const float nrm = sqrtf(vv * vv + vh * vh);
+        const float sc = nrm > p.tau ? 1.f - p.tau / nrm : 0.f;
+        ov[l] = vv * sc;
+        oh[l] = vh * sc;
+      }
+      *reinterpret_cast<float4 *>(p.zv + n0) = make_float4(ov[0], ov[1], ov[2], ov[3]);
+      *reinterpret_cast<float4 *>(p.zh + n0) = make_float4(oh[0], oh[1], oh[2], oh[3]);
+      continue;
+    }
 #pragma unroll
     for (int l = 0; l < 4; ++l) {
       const int gj = gj4 + l;
       if (gj < c0 || gj >= c1) continue;
-      const int64_t n = pidx(g, gi, gj);
+      const int64_t n = n0 + l;
       const float xc = __ldg(p.x + n);
       const float dv = gi < p.ny - 1 ? __ldg(p.x + n + g.pitch) - xc : 0.f;
       const float dh = gj < p.nx - 1 ? __ldg(p.x + n + 1) - xc : 0.f;
