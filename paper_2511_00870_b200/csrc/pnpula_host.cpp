@@ -133,6 +133,12 @@ struct pnpula_ctx {
   int64_t dev_t = -1;              // iteration count held by d_iter (-1: unknown)
   bool graphs_off = false;         // PNPULA_FLAG_NO_GRAPH or PNPULA_GRAPHS=0
   bool warm = false;               // one direct iteration done (modules loaded, attributes set)
+
+  // halo-exchange overlap (row-strip tiles with NCCL messages): boundary bands first, then the
+  // exchange on comm_stream concurrently with the interior update
+  bool overlap = false;
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_bands = nullptr, ev_halo = nullptr;
 };
 
 namespace {
@@ -159,7 +165,7 @@ pnpula_status fail_nccl(pnpula_ctx *c, ncclResult_t e, const char *what, int lin
     if (_e != ncclSuccess) return fail_nccl((c), _e, #expr, __LINE__);    \
   } while (0)
 
-void timer_begin(pnpula_ctx *c, Timer &t, cudaEvent_t *end_out) {
+void timer_begin(pnpula_ctx *c, Timer &t, cudaEvent_t *end_out, cudaStream_t st = nullptr) {
   *end_out = nullptr;
   if (!c->timing) return;
   if (t.used == t.ev.size()) {
@@ -168,12 +174,12 @@ void timer_begin(pnpula_ctx *c, Timer &t, cudaEvent_t *end_out) {
     cudaEventCreate(&b);
     t.ev.push_back({a, b});
   }
-  cudaEventRecord(t.ev[t.used].first, c->stream);
+  cudaEventRecord(t.ev[t.used].first, st ? st : c->stream);
   *end_out = t.ev[t.used].second;
   t.used++;
 }
-void timer_end(pnpula_ctx *c, cudaEvent_t end) {
-  if (end) cudaEventRecord(end, c->stream);
+void timer_end(pnpula_ctx *c, cudaEvent_t end, cudaStream_t st = nullptr) {
+  if (end) cudaEventRecord(end, st ? st : c->stream);
 }
 void timer_collect(Timer &t) {
   for (size_t i = 0; i < t.used; ++i) {
@@ -373,20 +379,31 @@ pnpula_status run_cnn(pnpula_ctx *c, int buf) {
   return PNPULA_OK;
 }
 
-pnpula_status exchange(pnpula_ctx *c, int buf) {
+pnpula_status exchange(pnpula_ctx *c, int buf, cudaStream_t st = nullptr) {
+  if (!st) st = c->stream;
   cudaEvent_t end;
-  timer_begin(c, c->tm_halo, &end);
-  if (c->n_local_jobs) { CU(c, launch_copy_jobs(c->d_local_jobs[buf], c->n_local_jobs, c->max_local, c->stream)); c->n_launches++; }
+  timer_begin(c, c->tm_halo, &end, st);
+  if (c->n_local_jobs) { CU(c, launch_copy_jobs(c->d_local_jobs[buf], c->n_local_jobs, c->max_local, st)); c->n_launches++; }
   if (!c->sends.empty() || !c->recvs.empty()) {
-    if (c->n_pack) { CU(c, launch_copy_jobs(c->d_pack_jobs[buf], c->n_pack, c->max_pack, c->stream)); c->n_launches++; }
+    if (c->n_pack) { CU(c, launch_copy_jobs(c->d_pack_jobs[buf], c->n_pack, c->max_pack, st)); c->n_launches++; }
     NC(c, ncclGroupStart());
-    for (auto &m : c->sends) NC(c, ncclSend(c->d_sendbuf + m.off, m.count, ncclFloat32, m.peer, c->comm, c->stream));
-    for (auto &m : c->recvs) NC(c, ncclRecv(c->d_recvbuf + m.off, m.count, ncclFloat32, m.peer, c->comm, c->stream));
+    for (auto &m : c->sends) NC(c, ncclSend(c->d_sendbuf + m.off, m.count, ncclFloat32, m.peer, c->comm, st));
+    for (auto &m : c->recvs) NC(c, ncclRecv(c->d_recvbuf + m.off, m.count, ncclFloat32, m.peer, c->comm, st));
     NC(c, ncclGroupEnd());
-    if (c->n_unpack) { CU(c, launch_copy_jobs(c->d_unpack_jobs[buf], c->n_unpack, c->max_unpack, c->stream)); c->n_launches++; }
+    if (c->n_unpack) { CU(c, launch_copy_jobs(c->d_unpack_jobs[buf], c->n_unpack, c->max_unpack, st)); c->n_launches++; }
   }
-  timer_end(c, end);
+  timer_end(c, end, st);
   return PNPULA_OK;
+}
+
+// Rows [r0, r1) (tile-relative) of a tile as a geometry of its own: i0/th move, h grows by r0
+// so that i0 - h (the padded-buffer origin) and every padded index stay the same.
+TileGeom row_range(const TileGeom &g, int r0, int r1) {
+  TileGeom b = g;
+  b.i0 = g.i0 + r0;
+  b.th = r1 - r0;
+  b.h = g.h + r0;
+  return b;
 }
 
 UpdateParams make_update_params(pnpula_ctx *c, TileDev &td, int buf) {
@@ -442,29 +459,48 @@ pnpula_status enqueue_step(pnpula_ctx *c, int buf, const IterState *it) {
   const uint64_t t1 = (uint64_t)c->t + 1;
   const bool acc = (int64_t)t1 > c->burn_in;
   const double k = acc ? (double)((int64_t)t1 - c->burn_in) : 1.0;
-  for (auto &td : c->tiles)
-  for (int ch = 0; ch < c->nc; ++ch) {
-    UpdateParams p = make_update_params(c, td, buf);
-    p.t1 = (uint32_t)t1;
-    p.accumulate = acc;
-    p.inv_n = (float)(1.0 / k);
-    p.it = it;
-    p.it_next = (it && &td == &c->tiles[0] && ch == 0) ? c->d_iter + (buf ^ 1) : nullptr;
-    if (ch > 0) {   // channel plane ch (R43): same geometry, its own Philox streams 4 ch + s
-      const size_t o = (size_t)ch * geom_elems(td.g);
-      p.x += o; p.xn += o; p.y += o; p.mean += o; p.m2 += o;
-      if (p.G) p.G += o;
-      if (p.z) p.z += o;
-      p.sb = 4u * (uint32_t)ch;
+  // the x / z / moment update of rows [r0, r1) of every tile and channel
+  auto update_rows = [&](bool all, bool top_band, bool interior) -> pnpula_status {
+    for (auto &td : c->tiles)
+    for (int ch = 0; ch < c->nc; ++ch) {
+      UpdateParams p = make_update_params(c, td, buf);
+      p.t1 = (uint32_t)t1;
+      p.accumulate = acc;
+      p.inv_n = (float)(1.0 / k);
+      p.it = it;
+      p.it_next = (it && &td == &c->tiles[0] && ch == 0) ? c->d_iter + (buf ^ 1) : nullptr;
+      if (ch > 0) {   // channel plane ch (R43): same geometry, its own Philox streams 4 ch + s
+        const size_t o = (size_t)ch * geom_elems(td.g);
+        p.x += o; p.xn += o; p.y += o; p.mean += o; p.m2 += o;
+        if (p.G) p.G += o;
+        if (p.z) p.z += o;
+        p.sb = 4u * (uint32_t)ch;
+      }
+      const int h = td.g.h, th = td.g.th;
+      if (!all) p.g = interior ? row_range(td.g, h, th - h) : top_band ? row_range(td.g, 0, h) : row_range(td.g, th - h, th);
+      cudaEvent_t end;
+      timer_begin(c, c->tm_update, &end);
+      CU(c, launch_update(p, c->stream));
+      c->n_launches++;
+      timer_end(c, end);
     }
-    cudaEvent_t end;
-    timer_begin(c, c->tm_update, &end);
-    CU(c, launch_update(p, c->stream));
-    c->n_launches++;
-    timer_end(c, end);
+    return PNPULA_OK;
+  };
+  pnpula_status s;
+  if (c->overlap && !it) {
+    // boundary bands (the rows neighbours receive) first, then the exchange on the comm stream
+    // while the interior rows update (SURVEY 8(e) overlap); the next kernels wait for both
+    if ((s = update_rows(false, true, false)) || (s = update_rows(false, false, false))) return s;
+    CU(c, cudaEventRecord(c->ev_bands, c->stream));
+    CU(c, cudaStreamWaitEvent(c->comm_stream, c->ev_bands, 0));
+    if ((s = exchange(c, buf ^ 1, c->comm_stream))) return s;
+    CU(c, cudaEventRecord(c->ev_halo, c->comm_stream));
+    if ((s = update_rows(false, false, true))) return s;
+    CU(c, cudaStreamWaitEvent(c->stream, c->ev_halo, 0));
+  } else {
+    if ((s = update_rows(true, false, false))) return s;
+    if ((s = exchange(c, buf ^ 1))) return s;
   }
-  pnpula_status s = exchange(c, buf ^ 1);
-  if (s) return s;
   if (c->tv_beta > 0) {
     // TV z block (R37, R38): x^{t+1} (halo now valid) -> z = (z_v, z_h) on tile (+) 1
     for (auto &td : c->tiles) {
@@ -1075,6 +1111,19 @@ pnpula_status pnpula_create(const pnpula_config *cfg, pnpula_ctx **out) {
     pnpula_status s = build_halo_plan(c);
     if (s) return bail(s);
   }
+  // overlap the NCCL halo exchange with the interior update: row-strip grids (the messages are
+  // the h top / bottom rows of a tile) whose tiles have interior rows (env PNPULA_OVERLAP=0: off)
+  {
+    const char *oe = getenv("PNPULA_OVERLAP");
+    bool ok = !(oe && atoi(oe) == 0) && (!c->sends.empty() || !c->recvs.empty()) && c->tiles_x == 1 && c->h > 0;
+    for (auto &td : c->tiles) ok = ok && td.g.th > 2 * td.g.h;
+    if (ok) {
+      CUB(cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
+      CUB(cudaEventCreateWithFlags(&c->ev_bands, cudaEventDisableTiming));
+      CUB(cudaEventCreateWithFlags(&c->ev_halo, cudaEventDisableTiming));
+      c->overlap = true;
+    }
+  }
   CUB(cudaStreamSynchronize(c->stream));
   g_last_error = warn;
   *out = c;
@@ -1618,6 +1667,9 @@ pnpula_status pnpula_destroy(pnpula_ctx *c) {
   cudaFree(c->d_sendbuf); cudaFree(c->d_recvbuf); cudaFree(c->d_err);
   drop_graphs(c);
   cudaFree(c->d_iter);
+  if (c->comm_stream) { cudaStreamSynchronize(c->comm_stream); cudaStreamDestroy(c->comm_stream); }
+  if (c->ev_bands) cudaEventDestroy(c->ev_bands);
+  if (c->ev_halo) cudaEventDestroy(c->ev_halo);
   for (Timer *t : {&c->tm_cnn, &c->tm_update, &c->tm_halo})
     for (auto &e : t->ev) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
   if (c->comm) ncclCommDestroy(c->comm);
