@@ -47,15 +47,27 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1
   return c;
 }
 
-// ln(u), u = (U + 0.5) 2^-32, accurate for u near 0 and near 1: for u <= 1/2 the hardware
-// log2 (abs. error ~2^-22 on |log2 u| >= 1, i.e. relative 2^-22); for u > 1/2, log1p(-v)
-// with v = 1 - u formed exactly from the integer.
+// ln(u), u = (U + 0.5) 2^-32, accurate for u near 0 and near 1, without a data-dependent branch
+// (both halves are evaluated and selected, so a warp never runs two paths):
+//  * u <= 1/2: the hardware log2 (abs. error ~2^-22 on |log2 u| >= 1, i.e. relative 2^-22);
+//  * u > 1/2: ln(1 - v) = -2 atanh(z), z = v / (2 - v) in (0, 1/3], with v = 1 - u formed
+//    exactly from the integer; atanh(z) = z (1 + w/3 + w^2/5 + ... + w^7/15), w = z^2 <= 1/9
+//    (truncation < w^8/17 ~ 1e-9 relative; a few ulp of rounding).
 __device__ __forceinline__ float log_unit(uint32_t U) {
-  if (U < 0x80000000u) {
-    return __log2f(fmaf((float)U, 0x1p-32f, 0x1p-33f)) * 0.69314718055994531f;
-  }
+  const float lo = __log2f(fmaf((float)U, 0x1p-32f, 0x1p-33f)) * 0.69314718055994531f;
   const float v = fmaf((float)(~U), 0x1p-32f, 0x1p-33f);   // 1 - u
-  return log1pf(-v);
+  const float z = __fdividef(v, 2.0f - v);
+  const float w = z * z;
+  float a = 1.0f / 15.0f;
+  a = fmaf(a, w, 1.0f / 13.0f);
+  a = fmaf(a, w, 1.0f / 11.0f);
+  a = fmaf(a, w, 1.0f / 9.0f);
+  a = fmaf(a, w, 1.0f / 7.0f);
+  a = fmaf(a, w, 1.0f / 5.0f);
+  a = fmaf(a, w, 1.0f / 3.0f);
+  a = fmaf(a, w, 1.0f);
+  const float hi = -2.0f * z * a;
+  return U < 0x80000000u ? lo : hi;
 }
 
 // Box-Muller pair from (Ua, Ub): (rho cos theta, rho sin theta), theta = 2 pi (Ub+0.5) 2^-32,
@@ -78,13 +90,19 @@ __device__ __forceinline__ void normals4(uint32_t seed_lo, uint32_t seed_hi, uin
 }
 
 // Iteration scalars: by value (direct launches) or from the device IterState (CUDA-graph
-// replays; see IterState).
-template <class P> __device__ __forceinline__ uint32_t it_t1(const P &p) {
-  return p.it ? (uint32_t)__ldg(&p.it->t1) : p.t1;
+// replays; see IterState), read once per thread at kernel entry.
+struct IterScalars {
+  uint32_t t1;
+  int acc;
+  float inv_n;
+};
+template <class P> __device__ __forceinline__ uint32_t iter_t1(const P &p) {
+  return p.it ? (uint32_t)p.it->t1 : p.t1;
 }
-// (read-only loads: nothing in the kernel writes *p.it, so the compiler may keep them in registers)
-__device__ __forceinline__ int it_acc(const UpdateParams &p) { return p.it ? __ldg(&p.it->accumulate) : p.accumulate; }
-__device__ __forceinline__ float it_inv_n(const UpdateParams &p) { return p.it ? __ldg(&p.it->inv_n) : p.inv_n; }
+__device__ __forceinline__ IterScalars iter_scalars(const UpdateParams &p) {
+  if (p.it) return IterScalars{(uint32_t)p.it->t1, p.it->accumulate, p.it->inv_n};
+  return IterScalars{p.t1, p.accumulate, p.inv_n};
+}
 // next iteration's scalars (same fp64 -> fp32 rounding of 1 / (t+2 - burn_in) as the host's)
 __device__ __forceinline__ void it_advance(const UpdateParams &p) {
   if (p.it_next && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
@@ -109,7 +127,7 @@ struct QuadIn {
   float x[4], G[4], z[4], m[4], s[4];
 };
 
-__device__ __forceinline__ void ula_load(const UpdateParams &p, int gi, int gj4, QuadIn &q) {
+__device__ __forceinline__ void ula_load(const UpdateParams &p, const IterScalars &is, int gi, int gj4, QuadIn &q) {
   const TileGeom &g = p.g;
   const int64_t base = pidx(g, gi, gj4);
   const bool full = gj4 >= g.j0 && gj4 + 4 <= g.j0 + g.tw;
@@ -126,7 +144,7 @@ __device__ __forceinline__ void ula_load(const UpdateParams &p, int gi, int gj4,
       const float4 b = *reinterpret_cast<const float4 *>(p.z + base);
       q.z[0] = b.x; q.z[1] = b.y; q.z[2] = b.z; q.z[3] = b.w;
     }
-    if (it_acc(p)) {
+    if (is.acc) {
       const float4 a2 = *reinterpret_cast<const float4 *>(p.mean + base);
       const float4 b2 = *reinterpret_cast<const float4 *>(p.m2 + base);
       q.m[0] = a2.x; q.m[1] = a2.y; q.m[2] = a2.z; q.m[3] = a2.w;
@@ -138,7 +156,7 @@ __device__ __forceinline__ void ula_load(const UpdateParams &p, int gi, int gj4,
       q.x[l] = p.x[base + l];
       if (p.has_G) q.G[l] = p.G[base + l];
       if (p.has_z) q.z[l] = p.z[base + l];
-      if (it_acc(p)) { q.m[l] = p.mean[base + l]; q.s[l] = p.m2[base + l]; }
+      if (is.acc) { q.m[l] = p.mean[base + l]; q.s[l] = p.m2[base + l]; }
     }
   }
 }
@@ -176,14 +194,15 @@ __device__ __forceinline__ void tv_term(const UpdateParams &p, int gi, int gj4, 
   }
 }
 
-__device__ __forceinline__ void ula_finish(const UpdateParams &p, int gi, int gj4, const float gr[4], QuadIn &q) {
+__device__ __forceinline__ void ula_finish(const UpdateParams &p, const IterScalars &is, int gi, int gj4, const float gr[4],
+                                           QuadIn &q) {
   const TileGeom &g = p.g;
   const int64_t base = pidx(g, gi, gj4);
   const bool full = gj4 >= g.j0 && gj4 + 4 <= g.j0 + g.tw;
   const float *xv = q.x, *Gv = q.G, *zv = q.z;
   float *mv = q.m, *sv = q.s;
   float xi[4];
-  normals4(p.seed_lo, p.seed_hi, (uint32_t)gj4 >> 2, (uint32_t)gi, it_t1(p), p.sb + 0u, xi);
+  normals4(p.seed_lo, p.seed_hi, (uint32_t)gj4 >> 2, (uint32_t)gi, is.t1, p.sb + 0u, xi);
   float dtv[4] = {0.f, 0.f, 0.f, 0.f};
   if (p.has_tv) tv_term(p, gi, gj4, xv, dtv);
   float xn[4];
@@ -200,25 +219,25 @@ __device__ __forceinline__ void ula_finish(const UpdateParams &p, int gi, int gj
   float zn[4];
   if (p.has_z) {
     float ze[4];
-    normals4(p.seed_lo, p.seed_hi, (uint32_t)gj4 >> 2, (uint32_t)gi, it_t1(p), p.sb + 1u, ze);
+    normals4(p.seed_lo, p.seed_hi, (uint32_t)gj4 >> 2, (uint32_t)gi, is.t1, p.sb + 1u, ze);
 #pragma unroll
     for (int l = 0; l < 4; ++l) {
       const float v = zv[l] - p.b_rho * (zv[l] - xn[l]) + p.b_zeta * ze[l];
       zn[l] = fminf(fmaxf(v, p.z_lo), p.z_hi);
     }
   }
-  if (it_acc(p)) {
+  if (is.acc) {
 #pragma unroll
     for (int l = 0; l < 4; ++l) {
       const float d = xn[l] - mv[l];
-      mv[l] = mv[l] + d * it_inv_n(p);
+      mv[l] = mv[l] + d * is.inv_n;
       sv[l] = sv[l] + d * (xn[l] - mv[l]);
     }
   }
   if (full) {
     *reinterpret_cast<float4 *>(p.xn + base) = make_float4(xn[0], xn[1], xn[2], xn[3]);
     if (p.has_z) *reinterpret_cast<float4 *>(p.z + base) = make_float4(zn[0], zn[1], zn[2], zn[3]);
-    if (it_acc(p)) {
+    if (is.acc) {
       *reinterpret_cast<float4 *>(p.mean + base) = make_float4(mv[0], mv[1], mv[2], mv[3]);
       *reinterpret_cast<float4 *>(p.m2 + base) = make_float4(sv[0], sv[1], sv[2], sv[3]);
     }
@@ -229,15 +248,16 @@ __device__ __forceinline__ void ula_finish(const UpdateParams &p, int gi, int gj
       if (gj < g.j0 || gj >= g.j0 + g.tw) continue;
       p.xn[base + l] = xn[l];
       if (p.has_z) p.z[base + l] = zn[l];
-      if (it_acc(p)) { p.mean[base + l] = mv[l]; p.m2[base + l] = sv[l]; }
+      if (is.acc) { p.mean[base + l] = mv[l]; p.m2[base + l] = sv[l]; }
     }
   }
 }
 
-__device__ __forceinline__ void ula_quad(const UpdateParams &p, int gi, int gj4, const float gr[4]) {
+__device__ __forceinline__ void ula_quad(const UpdateParams &p, const IterScalars &is, int gi, int gj4,
+                                         const float gr[4]) {
   QuadIn q;
-  ula_load(p, gi, gj4, q);
-  ula_finish(p, gi, gj4, gr, q);
+  ula_load(p, is, gi, gj4, q);
+  ula_finish(p, is, gi, gj4, gr, q);
 }
 
 // ---------------------------------------------------------------- conv K7
@@ -247,6 +267,7 @@ __global__ void __launch_bounds__(NTHREADS)
 update_conv_kernel(const __grid_constant__ UpdateParams p) {
   extern __shared__ float smem[];
   it_advance(p);
+  const IterScalars is = iter_scalars(p);
   const int RY = RY_ >= 0 ? RY_ : p.ry;
   const int RX = RX_ >= 0 ? RX_ : p.rx;
   const TileGeom &g = p.g;
@@ -355,7 +376,7 @@ update_conv_kernel(const __grid_constant__ UpdateParams p) {
       }
       gr[l] = s;
     }
-    ula_quad(p, gi, gj4, gr);
+    ula_quad(p, is, gi, gj4, gr);
   }
 }
 
@@ -411,6 +432,7 @@ update_sep_kernel(const __grid_constant__ UpdateParams p, const __grid_constant_
   static_assert(RR * TX <= XR * XC, "T2 reuses the x buffer");
   extern __shared__ __align__(128) float sm[];
   it_advance(p);
+  const IterScalars is = iter_scalars(p);
   // TMA completion barrier per staging buffer, after the float regions (no static shared
   // memory: the dynamic region then starts 1024-B aligned, as the TMA destinations need)
   uint64_t *const full_bar = reinterpret_cast<uint64_t *>(sm + Gm::floats);
@@ -462,7 +484,7 @@ update_sep_kernel(const __grid_constant__ UpdateParams p, const __grid_constant_
     for (int r = 0; r < 2; ++r) {
       const int gi = bi0 + 2 * a2 + r;
       act[r] = !(gi >= g.i0 + g.th || gj4 >= g.j0 + g.tw || gj4 + 4 <= g.j0);
-      if (act[r]) ula_load(p, gi, gj4, qin[r]);
+      if (act[r]) ula_load(p, is, gi, gj4, qin[r]);
     }
     mbar_wait_parity((uint32_t)__cvta_generic_to_shared(&full_bar[buf]), (uint32_t)(k >> 1) & 1u);
 
@@ -563,7 +585,7 @@ update_sep_kernel(const __grid_constant__ UpdateParams p, const __grid_constant_
           for (int pp = -R; pp <= R; ++pp) s = fmaf(ky[pp + R], col[r + R + pp][j], s);
           gr[j] = s;
         }
-        ula_finish(p, bi0 + 2 * a2 + r, gj4, gr, qin[r]);
+        ula_finish(p, is, bi0 + 2 * a2 + r, gj4, gr, qin[r]);
       }
     }
     __syncthreads();   // buffer buf is restaged by the next iteration's prefetch
@@ -575,6 +597,7 @@ update_sep_kernel(const __grid_constant__ UpdateParams p, const __grid_constant_
 // so the Philox call is shared exactly as in the x-update), 2-D stencil of x+ read through L1.
 // Pixels outside tile (+) r_H or the image are skipped (z1 stays 0 outside the image).
 __global__ void __launch_bounds__(NTHREADS) z1_update_kernel(const __grid_constant__ Z1Params p) {
+  const uint32_t t1 = iter_t1(p);
   const TileGeom &g = p.g;
   const int ry = p.ry, rx = p.rx, kw = 2 * rx + 1;
   const int r0 = max(g.i0 - ry, 0), r1 = min(g.i0 + g.th + ry, p.ny);
@@ -585,7 +608,7 @@ __global__ void __launch_bounds__(NTHREADS) z1_update_kernel(const __grid_consta
     const int gi = r0 + (int)(e / nq);
     const int gj4 = 4 * (q0 + (int)(e % nq));
     float ze[4];
-    normals4(p.seed_lo, p.seed_hi, (uint32_t)gj4 >> 2, (uint32_t)gi, it_t1(p), p.sb + 2u, ze);
+    normals4(p.seed_lo, p.seed_hi, (uint32_t)gj4 >> 2, (uint32_t)gi, t1, p.sb + 2u, ze);
 #pragma unroll
     for (int l = 0; l < 4; ++l) {
       const int gj = gj4 + l;
@@ -614,6 +637,7 @@ template <int R>
 __global__ void __launch_bounds__(NTHREADS) z1_sep_kernel(const __grid_constant__ Z1Params p,
                                                         const __grid_constant__ CUtensorMap tmx, int r0, int q0,
                                                         int nbx) {
+  const uint32_t t1 = iter_t1(p);
   // the staged columns start 16-B aligned (XL = R rounded up to 4): TMA tile loads need a
   // 16-B aligned inner start coordinate
   constexpr int XL = (R + 3) / 4 * 4;
@@ -661,7 +685,7 @@ __global__ void __launch_bounds__(NTHREADS) z1_sep_kernel(const __grid_constant_
     const int a = 2 * a2 + r, gi = bi0 + a;
     if (gi < rlo || gi >= rhi || gj4 >= chi || gj4 + 4 <= clo) continue;
     float ze[4];
-    normals4(p.seed_lo, p.seed_hi, (uint32_t)gj4 >> 2, (uint32_t)gi, it_t1(p), p.sb + 2u, ze);
+    normals4(p.seed_lo, p.seed_hi, (uint32_t)gj4 >> 2, (uint32_t)gi, t1, p.sb + 2u, ze);
 #pragma unroll
     for (int l = 0; l < 4; ++l) {
       const int gj = gj4 + l;
@@ -682,6 +706,7 @@ __global__ void __launch_bounds__(NTHREADS) z1_sep_kernel(const __grid_constant_
 // One thread per column quad of tile (+) 1 (global quads: the Philox calls match the oracle's
 // (stream, pixel) counters); D x+ from the padded x+ (halo >= 2), block soft threshold per pixel.
 __global__ void __launch_bounds__(NTHREADS) tv_z_kernel(const __grid_constant__ TvZParams p) {
+  const uint32_t t1 = iter_t1(p);
   const TileGeom &g = p.g;
   const int r0 = max(g.i0 - 1, 0), r1 = min(g.i0 + g.th + 1, p.ny);
   const int c0 = max(g.j0 - 1, 0), c1 = min(g.j0 + g.tw + 1, p.nx);
@@ -691,8 +716,8 @@ __global__ void __launch_bounds__(NTHREADS) tv_z_kernel(const __grid_constant__ 
     const int gi = r0 + (int)(e / nq);
     const int gj4 = 4 * (q0 + (int)(e % nq));
     float zev[4], zeh[4];
-    normals4(p.seed_lo, p.seed_hi, (uint32_t)gj4 >> 2, (uint32_t)gi, it_t1(p), 1u, zev);
-    normals4(p.seed_lo, p.seed_hi, (uint32_t)gj4 >> 2, (uint32_t)gi, it_t1(p), 3u, zeh);
+    normals4(p.seed_lo, p.seed_hi, (uint32_t)gj4 >> 2, (uint32_t)gi, t1, 1u, zev);
+    normals4(p.seed_lo, p.seed_hi, (uint32_t)gj4 >> 2, (uint32_t)gi, t1, 3u, zeh);
     const int64_t n0 = pidx(g, gi, gj4);   // 16-byte aligned
     if (gj4 >= c0 && gj4 + 4 <= c1) {
       // whole quad inside: 4 float4 loads + 1 scalar (x right of the quad), 2 float4 stores
@@ -828,6 +853,7 @@ __global__ void opnorm_init_kernel(const __grid_constant__ OpNormParams p) {
 // ---------------------------------------------------------------- mask K7 (no stencil)
 __global__ void __launch_bounds__(NTHREADS) update_mask_kernel(const __grid_constant__ UpdateParams p) {
   it_advance(p);
+  const IterScalars is = iter_scalars(p);
   const TileGeom &g = p.g;
   const int nq = ((g.j0 + g.tw + 3) >> 2) - (g.j0 >> 2);
   const int64_t total = (int64_t)nq * g.th;
@@ -841,7 +867,7 @@ __global__ void __launch_bounds__(NTHREADS) update_mask_kernel(const __grid_cons
       const float m = p.mask[base + l] ? 1.f : 0.f;
       gr[l] = m * (m * p.x[base + l] - p.y[base + l]);
     }
-    ula_quad(p, gi, gj4, gr);
+    ula_quad(p, is, gi, gj4, gr);
   }
 }
 
