@@ -194,8 +194,11 @@ __device__ __forceinline__ void tv_term(const UpdateParams &p, int gi, int gj4, 
   }
 }
 
+// TVM: 0 = the TV term is compiled out (non-TV launches of the separable kernel), 1 = p.has_tv at run time
+template <int TVM = 1>
 __device__ __forceinline__ void ula_finish(const UpdateParams &p, const IterScalars &is, int gi, int gj4, const float gr[4],
                                            QuadIn &q) {
+  const bool has_tv = TVM != 0 && p.has_tv;
   const TileGeom &g = p.g;
   const int64_t base = pidx(g, gi, gj4);
   const bool full = gj4 >= g.j0 && gj4 + 4 <= g.j0 + g.tw;
@@ -204,7 +207,7 @@ __device__ __forceinline__ void ula_finish(const UpdateParams &p, const IterScal
   float xi[4];
   normals4(p.seed_lo, p.seed_hi, (uint32_t)gj4 >> 2, (uint32_t)gi, is.t1, p.sb + 0u, xi);
   float dtv[4] = {0.f, 0.f, 0.f, 0.f};
-  if (p.has_tv) tv_term(p, gi, gj4, xv, dtv);
+  if (has_tv) tv_term(p, gi, gj4, xv, dtv);
   float xn[4];
 #pragma unroll
   for (int l = 0; l < 4; ++l) {
@@ -212,9 +215,9 @@ __device__ __forceinline__ void ula_finish(const UpdateParams &p, const IterScal
     if (p.has_z) v -= p.a_rho * (xv[l] - zv[l]);
     if (p.has_G) v += p.a_d * (-Gv[l]);
     if (p.has_box) v += p.a_lam * (fminf(fmaxf(xv[l], p.c_lo), p.c_hi) - xv[l]);
-    if (p.has_tv) v -= p.a_tv * dtv[l];
+    if (has_tv) v -= p.a_tv * dtv[l];
     v += p.a_xi * xi[l];
-    xn[l] = p.has_tv ? fmaxf(v, 0.f) : v;   // TV: PSGLA projection onto R+ after the step (R37)
+    xn[l] = has_tv ? fmaxf(v, 0.f) : v;   // TV: PSGLA projection onto R+ after the step (R37)
   }
   float zn[4];
   if (p.has_z) {
@@ -422,7 +425,7 @@ struct SepGeom {
   static constexpr size_t bytes = floats * sizeof(float) + 16;   // + 2 mbarriers
 };
 
-template <int R>
+template <int R, int TVM>
 __global__ void __launch_bounds__(NTHREADS, 2)
 update_sep_kernel(const __grid_constant__ UpdateParams p, const __grid_constant__ CUtensorMap tmx,
                   const __grid_constant__ CUtensorMap tmy, int nbx, int nblk) {
@@ -585,7 +588,7 @@ update_sep_kernel(const __grid_constant__ UpdateParams p, const __grid_constant_
           for (int pp = -R; pp <= R; ++pp) s = fmaf(ky[pp + R], col[r + R + pp][j], s);
           gr[j] = s;
         }
-        ula_finish(p, is, bi0 + 2 * a2 + r, gj4, gr, qin[r]);
+        ula_finish<TVM>(p, is, bi0 + 2 * a2 + r, gj4, gr, qin[r]);
       }
     }
     __syncthreads();   // buffer buf is restaged by the next iteration's prefetch
@@ -969,9 +972,9 @@ cudaError_t launch_update(const UpdateParams &p, cudaStream_t s) {
       cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
       const int R = p.ry;
       const size_t smem = R == 4 ? SepGeom<4>::bytes : SepGeom<2>::bytes;
-      cudaError_t e = R == 4
-          ? cudaFuncSetAttribute(update_sep_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
-          : cudaFuncSetAttribute(update_sep_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      auto kfn = R == 4 ? (p.has_tv ? update_sep_kernel<4, 1> : update_sep_kernel<4, 0>)
+                        : (p.has_tv ? update_sep_kernel<2, 1> : update_sep_kernel<2, 0>);
+      cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
       // TMA maps of the padded x and y buffers (ph x pitch fp32), boxes = the staged regions
       CUtensorMap tmx, tmy;
@@ -979,8 +982,7 @@ cudaError_t launch_update(const UpdateParams &p, cudaStream_t s) {
       if (!encode_padded_2d(&tmx, p.x, p.g, XC, TY + 4 * R) || !encode_padded_2d(&tmy, p.y, p.g, XC, TY + 2 * R))
         return cudaErrorInvalidValue;
       const int grid = nblk < 2 * num_sms ? nblk : 2 * num_sms;
-      if (R == 4) update_sep_kernel<4><<<grid, NTHREADS, smem, s>>>(p, tmx, tmy, nbx, nblk);
-      else update_sep_kernel<2><<<grid, NTHREADS, smem, s>>>(p, tmx, tmy, nbx, nblk);
+      kfn<<<grid, NTHREADS, smem, s>>>(p, tmx, tmy, nbx, nblk);
       return cudaGetLastError();
     }
     return launch_conv<-1, -1, true>(p, s);
