@@ -606,10 +606,11 @@ __global__ void __launch_bounds__(NTHREADS) z1_update_kernel(const __grid_consta
   const int r0 = max(g.i0 - ry, 0), r1 = min(g.i0 + g.th + ry, p.ny);
   const int c0 = max(g.j0 - rx, 0), c1 = min(g.j0 + g.tw + rx, p.nx);
   const int q0 = c0 >> 2, nq = ((c1 + 3) >> 2) - q0;
-  const int64_t total = (int64_t)nq * (r1 - r0);
-  for (int64_t e = (int64_t)blockIdx.x * NTHREADS + threadIdx.x; e < total; e += (int64_t)gridDim.x * NTHREADS) {
-    const int gi = r0 + (int)(e / nq);
-    const int gj4 = 4 * (q0 + (int)(e % nq));
+  const uint32_t total = (uint32_t)nq * (uint32_t)(r1 - r0);   // < 2^31 quads per tile
+  for (uint32_t e = blockIdx.x * NTHREADS + threadIdx.x; e < total; e += gridDim.x * NTHREADS) {
+    const uint32_t qr = e / (uint32_t)nq;
+    const int gi = r0 + (int)qr;
+    const int gj4 = 4 * (q0 + (int)(e - qr * (uint32_t)nq));
     float ze[4];
     normals4(p.seed_lo, p.seed_hi, (uint32_t)gj4 >> 2, (uint32_t)gi, t1, p.sb + 2u, ze);
 #pragma unroll
@@ -714,10 +715,11 @@ __global__ void __launch_bounds__(NTHREADS) tv_z_kernel(const __grid_constant__ 
   const int r0 = max(g.i0 - 1, 0), r1 = min(g.i0 + g.th + 1, p.ny);
   const int c0 = max(g.j0 - 1, 0), c1 = min(g.j0 + g.tw + 1, p.nx);
   const int q0 = c0 >> 2, nq = ((c1 + 3) >> 2) - q0;
-  const int64_t total = (int64_t)nq * (r1 - r0);
-  for (int64_t e = (int64_t)blockIdx.x * NTHREADS + threadIdx.x; e < total; e += (int64_t)gridDim.x * NTHREADS) {
-    const int gi = r0 + (int)(e / nq);
-    const int gj4 = 4 * (q0 + (int)(e % nq));
+  const uint32_t total = (uint32_t)nq * (uint32_t)(r1 - r0);   // < 2^31 quads per tile
+  for (uint32_t e = blockIdx.x * NTHREADS + threadIdx.x; e < total; e += gridDim.x * NTHREADS) {
+    const uint32_t qr = e / (uint32_t)nq;
+    const int gi = r0 + (int)qr;
+    const int gj4 = 4 * (q0 + (int)(e - qr * (uint32_t)nq));
     float zev[4], zeh[4];
     normals4(p.seed_lo, p.seed_hi, (uint32_t)gj4 >> 2, (uint32_t)gi, t1, 1u, zev);
     normals4(p.seed_lo, p.seed_hi, (uint32_t)gj4 >> 2, (uint32_t)gi, t1, 3u, zeh);
@@ -738,8 +740,8 @@ __global__ void __launch_bounds__(NTHREADS) tv_z_kernel(const __grid_constant__ 
         const float dh = gj4 + l < p.nx - 1 ? xc[l + 1] - xc[l] : 0.f;
         const float vv = zv[l] - p.b * (zv[l] - dv) + p.s * zev[l];
         const float vh = zh[l] - p.b * (zh[l] - dh) + p.s * zeh[l];
-        const float nrm = sqrtf(vv * vv + vh * vh);
-        const float sc = nrm > p.tau ? 1.f - p.tau / nrm : 0.f;
+        const float n2 = fmaf(vv, vv, vh * vh);   // shrink: 1 - tau / ||(vv, vh)|| if the norm exceeds tau
+        const float sc = n2 > p.tau * p.tau ? 1.f - p.tau * rsqrtf(n2) : 0.f;
         ov[l] = vv * sc;
         oh[l] = vh * sc;
       }
@@ -758,8 +760,8 @@ __global__ void __launch_bounds__(NTHREADS) tv_z_kernel(const __grid_constant__ 
       const float zv = p.zv[n], zh = p.zh[n];
       const float vv = zv - p.b * (zv - dv) + p.s * zev[l];
       const float vh = zh - p.b * (zh - dh) + p.s * zeh[l];
-      const float nrm = sqrtf(vv * vv + vh * vh);
-      const float sc = nrm > p.tau ? 1.f - p.tau / nrm : 0.f;
+      const float n2 = fmaf(vv, vv, vh * vh);
+      const float sc = n2 > p.tau * p.tau ? 1.f - p.tau * rsqrtf(n2) : 0.f;
       p.zv[n] = vv * sc;
       p.zh[n] = vh * sc;
     }
@@ -859,9 +861,9 @@ __global__ void __launch_bounds__(NTHREADS) update_mask_kernel(const __grid_cons
   const IterScalars is = iter_scalars(p);
   const TileGeom &g = p.g;
   const int nq = ((g.j0 + g.tw + 3) >> 2) - (g.j0 >> 2);
-  const int64_t total = (int64_t)nq * g.th;
-  for (int64_t e = (int64_t)blockIdx.x * NTHREADS + threadIdx.x; e < total; e += (int64_t)gridDim.x * NTHREADS) {
-    const int rr = (int)(e / nq), q = (int)(e - (int64_t)rr * nq);
+  const uint32_t total = (uint32_t)nq * (uint32_t)g.th;   // < 2^31 quads per tile
+  for (uint32_t e = blockIdx.x * NTHREADS + threadIdx.x; e < total; e += gridDim.x * NTHREADS) {
+    const int rr = (int)(e / (uint32_t)nq), q = (int)(e - (uint32_t)rr * (uint32_t)nq);
     const int gi = g.i0 + rr, gj4 = (g.j0 & ~3) + 4 * q;
     const int64_t base = pidx(g, gi, gj4);
     float gr[4];
