@@ -8,6 +8,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -782,6 +783,15 @@ pnpula_status pnpula_get_unique_id(uint8_t out[128]) {
 pnpula_status pnpula_destroy(pnpula_ctx *c);
 
 pnpula_status pnpula_create(const pnpula_config *cfg, pnpula_ctx **out) {
+  // PNPULA_TIME_CREATE=1: per-phase wall times of create on stderr (diagnostics)
+  const bool tcre = getenv("PNPULA_TIME_CREATE") != nullptr;
+  auto tc0 = std::chrono::steady_clock::now();
+  auto phase = [&](const char *what) {
+    if (!tcre) return;
+    auto t = std::chrono::steady_clock::now();
+    fprintf(stderr, "[pnpula_create] %-28s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(t - tc0).count());
+    tc0 = t;
+  };
   g_last_error.clear();
   if (!cfg || !out) { set_error("null argument"); return PNPULA_E_INVALID_ARG; }
   *out = nullptr;
@@ -931,14 +941,17 @@ pnpula_status pnpula_create(const pnpula_config *cfg, pnpula_ctx **out) {
   auto bail = [&](pnpula_status s) { pnpula_destroy(c); return s; };
   cudaError_t e = cudaSetDevice(f.device);
   if (e != cudaSuccess) { fail_cuda(nullptr, e, "cudaSetDevice", __LINE__); return bail(PNPULA_E_CUDA); }
-  cudaDeviceProp prop;
-  e = cudaGetDeviceProperties(&prop, f.device);
-  if (e != cudaSuccess) { fail_cuda(nullptr, e, "cudaGetDeviceProperties", __LINE__); return bail(PNPULA_E_CUDA); }
-  if (prop.major != 10 || prop.minor != 0) {
-    set_error("device %d is sm_%d%d; this library is built for sm_100a only", f.device, prop.major, prop.minor);
+  // three attribute queries (cudaGetDeviceProperties fills every field: ~10 ms)
+  int cc_major = 0, cc_minor = 0, n_sms = 0;
+  e = cudaDeviceGetAttribute(&cc_major, cudaDevAttrComputeCapabilityMajor, f.device);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&cc_minor, cudaDevAttrComputeCapabilityMinor, f.device);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&n_sms, cudaDevAttrMultiProcessorCount, f.device);
+  if (e != cudaSuccess) { fail_cuda(nullptr, e, "cudaDeviceGetAttribute", __LINE__); return bail(PNPULA_E_CUDA); }
+  if (cc_major != 10 || cc_minor != 0) {
+    set_error("device %d is sm_%d%d; this library is built for sm_100a only", f.device, cc_major, cc_minor);
     return bail(PNPULA_E_CUDA);
   }
-  c->num_sms = prop.multiProcessorCount;
+  c->num_sms = n_sms;
   if (f.stream) {
     c->stream = (cudaStream_t)(uintptr_t)f.stream;
   } else {
@@ -952,6 +965,7 @@ pnpula_status pnpula_create(const pnpula_config *cfg, pnpula_ctx **out) {
     if (_e != cudaSuccess) { fail_cuda(nullptr, _e, #expr, __LINE__);          \
       return bail(_e == cudaErrorMemoryAllocation ? PNPULA_E_OOM : PNPULA_E_CUDA); } \
   } while (0)
+  phase("validation + stream");
   CUB(cudaMalloc(&c->d_err, sizeof(int)));
   CUB(cudaMemsetAsync(c->d_err, 0, sizeof(int), c->stream));
   CUB(cudaMalloc(&c->d_iter, 2 * sizeof(IterState)));
@@ -972,6 +986,7 @@ pnpula_status pnpula_create(const pnpula_config *cfg, pnpula_ctx **out) {
     if (r != ncclSuccess) { fail_nccl(nullptr, r, "ncclCommInitAll", __LINE__); return bail(PNPULA_E_NCCL); }
   }
 
+  phase("nccl / small buffers");
   // device buffers
   for (auto &td : c->tiles) {
     const size_t n1 = geom_elems(td.g);   // one plane
@@ -1020,6 +1035,7 @@ pnpula_status pnpula_create(const pnpula_config *cfg, pnpula_ctx **out) {
       if (s) return bail(s);
     }
   }
+  phase("tile buffers + uploads");
   // DDFB operator images and buffers
   if (ddfb) {
     const int K = c->n_layers, P = c->channels;
@@ -1070,6 +1086,7 @@ pnpula_status pnpula_create(const pnpula_config *cfg, pnpula_ctx **out) {
     }
   }
   // CNN weights
+  phase("ddfb");
   if (c->n_layers > 0 && !ddfb) {
     plan_cnn_chunks(c);
     const int K = c->n_layers, P = c->channels;
@@ -1103,11 +1120,13 @@ pnpula_status pnpula_create(const pnpula_config *cfg, pnpula_ctx **out) {
       for (auto &td : c->tiles)
         for (int b2 = 0; b2 < 2; ++b2) {
           CUB(cudaMalloc(&td.act[b2], maxact * sizeof(uint16_t)));
-          CUB(cudaMemsetAsync(td.act[b2], 0, maxact * sizeof(uint16_t), c->stream));
+          // no memset: every activation a chunk reads was written by the previous chunk of the same
+          // evaluation (positions outside the stored region are zero-filled by the producer)
         }
     }
   }
   {
+    phase("cnn weights + act buffers");
     pnpula_status s = build_halo_plan(c);
     if (s) return bail(s);
   }
@@ -1124,7 +1143,9 @@ pnpula_status pnpula_create(const pnpula_config *cfg, pnpula_ctx **out) {
       c->overlap = true;
     }
   }
+  phase("halo plan + overlap");
   CUB(cudaStreamSynchronize(c->stream));
+  phase("final sync");
   g_last_error = warn;
   *out = c;
   return PNPULA_OK;
