@@ -371,7 +371,7 @@ def main():
             dist.broadcast_object_list(obj, src=0)
             common["nccl_uid"] = obj[0]
             dist.barrier()
-        s.close()
+        s.close()   # its device memory returns to the library's pool (reused by the e2e context)
         # pinned host buffers for the moments (D2H at full PCIe/NVLink-C2C rate)
         outs = None
         if world == 1:
@@ -402,8 +402,9 @@ def main():
         d2h = (mean.nbytes + var.nbytes)
         e2e = {"value": px * K / dt / 1e6, "unit": "Mpx-it/s", "h2d_bytes_per_step": int(h2d * world // K),
                "d2h_bytes_per_step": int(d2h * world // K),
-               "timed": "create (H2D of y/weights from pinned host memory) + reset + K iterations + "
-                        "get_moments (D2H of mean and variance); wall clock, max over ranks"}
+               "timed": "create (H2D of y/weights from pinned host memory; device buffers from the library's "
+                        "memory pool, warm after the timed run) + reset + K iterations + get_moments (D2H of "
+                        "mean and variance); wall clock, max over ranks"}
     else:
         s.close()
 

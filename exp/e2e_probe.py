@@ -4,15 +4,16 @@ sys.path.insert(0, '/root/repo')
 import numpy as np, torch
 import bench
 from paper_2511_00870_b200 import Sampler
-wl = bench.workload("c5", 1)
+wl = bench.workload(sys.argv[1] if len(sys.argv) > 1 else "c5", 1)
 kw = bench.build_inputs(wl, (0, 0, wl["ny"], wl["nx"]), pinned=True)
 kw.pop("_pin")
-pm = torch.empty((wl["ny"], wl["nx"]), dtype=torch.float32, pin_memory=True).numpy()
-pv = torch.empty((wl["ny"], wl["nx"]), dtype=torch.float32, pin_memory=True).numpy()
+shp = ((wl["nc"],) if wl.get("nc", 1) > 1 else ()) + (wl["ny"], wl["nx"])
+pm = torch.empty(shp, dtype=torch.float32, pin_memory=True).numpy()
+pv = torch.empty(shp, dtype=torch.float32, pin_memory=True).numpy()
 for rep in range(2):
     torch.cuda.synchronize()
     t = [time.perf_counter()]
-    s = Sampler(**kw); t.append(time.perf_counter())
+    s = Sampler(**kw, tiles=wl["tiles"]); t.append(time.perf_counter())
     s.reset(0, 1); s.synchronize(); t.append(time.perf_counter())
     s.advance(1); s.synchronize(); t.append(time.perf_counter())
     s.advance(19); s.synchronize(); t.append(time.perf_counter())

@@ -254,8 +254,14 @@ pnpula_status pnpula_set_timing(pnpula_ctx *ctx, int32_t enable);
 pnpula_status pnpula_kernel_time(pnpula_ctx *ctx, const char *name, double *ms, int64_t *launches,
                                  int32_t reset);
 
-/* [collective] Free everything. */
+/* [collective] Free everything.  The per-tile state buffers (x, y, z blocks, moments, CNN
+ * activations) come from a per-process, per-device stream-ordered memory pool that keeps freed
+ * memory for the next context (env PNPULA_POOL=0 at create: plain cudaMalloc / cudaFree). */
 pnpula_status pnpula_destroy(pnpula_ctx *ctx);
+
+/* Return the pool's unused device memory of `device` to the driver (cudaMemPoolTrimTo 0).
+ * E_INVALID_ARG if the device has no pool. */
+pnpula_status pnpula_release_memory(int32_t device);
 
 /* ---------------- host-only planning helpers (no GPU needed) ---------------- */
 

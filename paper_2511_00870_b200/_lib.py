@@ -105,6 +105,7 @@ def load():
         "pnpula_set_timing": ([vp, i32], C.c_int),
         "pnpula_kernel_time": ([vp, C.c_char_p, C.POINTER(d), C.POINTER(i64), i32], C.c_int),
         "pnpula_destroy": ([vp], C.c_int),
+        "pnpula_release_memory": ([i32], C.c_int),
         "pnpula_partition": ([i64, i64, i64, C.POINTER(i64), C.POINTER(i64)], None),
         "pnpula_halo_width": ([i32, i32, i32, i32], i32),
         "pnpula_plan_halo": ([i32, i32, i32, i32, i32, C.POINTER(HaloMsg), i32], i32),
@@ -124,7 +125,8 @@ EXPORTED = ["pnpula_version", "pnpula_last_error", "pnpula_get_unique_id", "pnpu
             "pnpula_get_state", "pnpula_get_z1", "pnpula_get_tv_zh", "pnpula_tile_info", "pnpula_get_padded_x", "pnpula_get_denoiser_residual",
             "pnpula_set_timing", "pnpula_kernel_time", "pnpula_destroy", "pnpula_partition",
             "pnpula_halo_width", "pnpula_plan_halo", "pnpula_check_stepsizes", "pnpula_checkpoint_bytes",
-            "pnpula_save_checkpoint", "pnpula_load_checkpoint", "pnpula_conv_norm2_bound", "pnpula_opnorm2"]
+            "pnpula_save_checkpoint", "pnpula_load_checkpoint", "pnpula_conv_norm2_bound", "pnpula_opnorm2",
+            "pnpula_release_memory"]
 
 
 def last_error() -> str:

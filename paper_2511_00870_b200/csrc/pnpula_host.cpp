@@ -138,6 +138,7 @@ struct pnpula_ctx {
   // halo-exchange overlap (row-strip tiles with NCCL messages): boundary bands first, then the
   // exchange on comm_stream concurrently with the interior update
   bool overlap = false;
+  cudaMemPool_t pool = nullptr;    // stream-ordered pool of the per-tile buffers (see dmalloc)
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t ev_bands = nullptr, ev_halo = nullptr;
 };
@@ -203,6 +204,35 @@ TileGeom make_geom(int i0, int j0, int th, int tw, int h) {
 }
 
 size_t geom_elems(const TileGeom &g) { return (size_t)g.ph * g.pitch; }
+
+// Per-tile state buffers come from a process-wide stream-ordered pool per device that keeps
+// freed memory (release threshold = max): a context created after another was destroyed reuses
+// its memory without driver calls (fresh cudaMalloc of GBs stalls for 20-160 ms, measured).
+// Allocation and first use are ordered on the context stream.  PNPULA_POOL=0: plain cudaMalloc.
+cudaMemPool_t device_pool(int dev) {
+  static cudaMemPool_t pools[64] = {};
+  if (dev < 0 || dev >= 64) return nullptr;
+  if (!pools[dev]) {
+    cudaMemPoolProps pr{};
+    pr.allocType = cudaMemAllocationTypePinned;
+    pr.location.type = cudaMemLocationTypeDevice;
+    pr.location.id = dev;
+    if (cudaMemPoolCreate(&pools[dev], &pr) != cudaSuccess) { pools[dev] = nullptr; return nullptr; }
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  return pools[dev];
+}
+template <typename T>
+cudaError_t dmalloc(pnpula_ctx *c, T **p, size_t bytes) {
+  if (c->pool) return cudaMallocFromPoolAsync(reinterpret_cast<void **>(p), bytes, c->pool, c->stream);
+  return cudaMalloc(reinterpret_cast<void **>(p), bytes);
+}
+void dfree(pnpula_ctx *c, void *p) {
+  if (!p) return;
+  if (c->pool) cudaFreeAsync(p, c->stream);
+  else cudaFree(p);
+}
 
 void tile_rect(int ny, int nx, int ty_n, int tx_n, int tile, pnpula_rect *r) {
   int64_t a, b, c, d;
@@ -970,6 +1000,10 @@ pnpula_status pnpula_create(const pnpula_config *cfg, pnpula_ctx **out) {
   CUB(cudaMemsetAsync(c->d_err, 0, sizeof(int), c->stream));
   CUB(cudaMalloc(&c->d_iter, 2 * sizeof(IterState)));
   {
+    const char *pe = getenv("PNPULA_POOL");
+    if (!(pe && atoi(pe) == 0)) c->pool = device_pool(f.device);
+  }
+  {
     const char *ge = getenv("PNPULA_GRAPHS");
     c->graphs_off = (f.flags & PNPULA_FLAG_NO_GRAPH) != 0 || (ge && atoi(ge) == 0);
   }
@@ -992,34 +1026,35 @@ pnpula_status pnpula_create(const pnpula_config *cfg, pnpula_ctx **out) {
     const size_t n1 = geom_elems(td.g);   // one plane
     const size_t n = n1 * (size_t)nc;      // state fields: nc planes
     for (int b = 0; b < 2; ++b) {
-      CUB(cudaMalloc(&td.x[b], n * sizeof(float)));
+      CUB(dmalloc(c, &td.x[b], n * sizeof(float)));
       CUB(cudaMemsetAsync(td.x[b], 0, n * sizeof(float), c->stream));
     }
-    CUB(cudaMalloc(&td.x0, n * sizeof(float)));
+    CUB(dmalloc(c, &td.x0, n * sizeof(float)));
     CUB(cudaMemsetAsync(td.x0, 0, n * sizeof(float), c->stream));
-    CUB(cudaMalloc(&td.y, n * sizeof(float)));
+    CUB(dmalloc(c, &td.y, n * sizeof(float)));
     CUB(cudaMemsetAsync(td.y, 0, n * sizeof(float), c->stream));
-    CUB(cudaMalloc(&td.mean, n * sizeof(float)));
-    CUB(cudaMalloc(&td.m2, n * sizeof(float)));
-    if (c->rho > 0) CUB(cudaMalloc(&td.z, n * sizeof(float)));
+    CUB(dmalloc(c, &td.mean, n * sizeof(float)));
+    CUB(dmalloc(c, &td.m2, n * sizeof(float)));
+    if (c->rho > 0) CUB(dmalloc(c, &td.z, n * sizeof(float)));
     if (tv) {
-      CUB(cudaMalloc(&td.zh, n * sizeof(float)));
+      CUB(dmalloc(c, &td.zh, n * sizeof(float)));
       CUB(cudaMemsetAsync(td.zh, 0, n * sizeof(float), c->stream));
     }
     if (poisson) {   // Poisson z1 block
-      CUB(cudaMalloc(&td.z1, n * sizeof(float)));
+      CUB(dmalloc(c, &td.z1, n * sizeof(float)));
       CUB(cudaMemsetAsync(td.z1, 0, n * sizeof(float), c->stream));
     }
     if (c->op == PNPULA_OP_MASK) {   // one plane, shared by the channels
-      CUB(cudaMalloc(&td.mask, n1));
+      CUB(dmalloc(c, &td.mask, n1));
       CUB(cudaMemsetAsync(td.mask, 0, n1, c->stream));
     }
     if (c->n_layers > 0) {
-      CUB(cudaMalloc(&td.G, n * sizeof(float)));
+      CUB(dmalloc(c, &td.G, n * sizeof(float)));
       CUB(cudaMemsetAsync(td.G, 0, n * sizeof(float), c->stream));
     }
     const TileGeom &g = td.g;
     pnpula_status s;
+    phase("  tile malloc + memset");
     const size_t in_plane = (size_t)in.h * in.w;
     for (int ch = 0; ch < nc; ++ch) {
       s = upload_padded<float>(c, td.y + ch * n1, g, f.y + ch * in_plane, in, g.i0 - rH, g.j0 - rH, g.th + 2 * rH,
@@ -1076,11 +1111,11 @@ pnpula_status pnpula_create(const pnpula_config *cfg, pnpula_ctx **out) {
     if (s) return bail(s);
     for (auto &td : c->tiles) {
       const size_t n = geom_elems(td.g);
-      CUB(cudaMalloc(&td.pbuf, n * sizeof(float)));
+      CUB(dmalloc(c, &td.pbuf, n * sizeof(float)));
       CUB(cudaMemsetAsync(td.pbuf, 0, n * sizeof(float), c->stream));
       const size_t act = (size_t)(td.g.th + 2 * (2 * K - 1)) * (td.g.tw + 2 * (2 * K - 1)) * P;
       for (int b2 = 0; b2 < 2; ++b2) {
-        CUB(cudaMalloc(&td.act[b2], act * sizeof(uint16_t)));
+        CUB(dmalloc(c, &td.act[b2], act * sizeof(uint16_t)));
         CUB(cudaMemsetAsync(td.act[b2], 0, act * sizeof(uint16_t), c->stream));
       }
     }
@@ -1117,9 +1152,11 @@ pnpula_status pnpula_create(const pnpula_config *cfg, pnpula_ctx **out) {
         maxact = std::max(maxact, (size_t)(td.g.th + 2 * ch.ext) * (td.g.tw + 2 * ch.ext) * P);
     }
     if (maxact) {
+      // chunk ci writes act[ci & 1] and reads act[(ci + 1) & 1]: two chunks need one buffer
+      const int nact = c->chunks.size() > 2 ? 2 : 1;
       for (auto &td : c->tiles)
-        for (int b2 = 0; b2 < 2; ++b2) {
-          CUB(cudaMalloc(&td.act[b2], maxact * sizeof(uint16_t)));
+        for (int b2 = 0; b2 < nact; ++b2) {
+          CUB(dmalloc(c, &td.act[b2], maxact * sizeof(uint16_t)));
           // no memset: every activation a chunk reads was written by the previous chunk of the same
           // evaluation (positions outside the stored region are zero-filled by the producer)
         }
@@ -1302,10 +1339,10 @@ pnpula_status tile_staging(pnpula_ctx *c, int nf, std::vector<float *> &bufs) {
   size_t total = 0;
   for (auto &td : c->tiles) total += (size_t)td.g.th * td.g.tw * nf;
   if (total * sizeof(float) > c->scratch_bytes) {
-    if (c->scratch) CU(c, cudaFree(c->scratch));
+    dfree(c, c->scratch);
     c->scratch = nullptr;
     c->scratch_bytes = 0;
-    CU(c, cudaMalloc(&c->scratch, total * sizeof(float)));
+    CU(c, dmalloc(c, &c->scratch, total * sizeof(float)));
     c->scratch_bytes = total * sizeof(float);
   }
   float *d = static_cast<float *>(c->scratch);
@@ -1667,18 +1704,28 @@ pnpula_status pnpula_kernel_time(pnpula_ctx *c, const char *name, double *ms, in
   return PNPULA_OK;
 }
 
+pnpula_status pnpula_release_memory(int32_t device) {
+  cudaMemPool_t p = device_pool(device);
+  if (!p) { set_error("no memory pool for device %d", device); return PNPULA_E_INVALID_ARG; }
+  cudaError_t e = cudaMemPoolTrimTo(p, 0);
+  if (e != cudaSuccess) { set_error("cudaMemPoolTrimTo: %s", cudaGetErrorString(e)); return PNPULA_E_CUDA; }
+  return PNPULA_OK;
+}
+
 pnpula_status pnpula_destroy(pnpula_ctx *c) {
   if (!c) return PNPULA_OK;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (auto &td : c->tiles) {
-    cudaFree(td.x[0]); cudaFree(td.x[1]); cudaFree(td.x0); cudaFree(td.y); cudaFree(td.mask);
-    cudaFree(td.z); cudaFree(td.z1); cudaFree(td.zh); cudaFree(td.mean); cudaFree(td.m2); cudaFree(td.G); cudaFree(td.pbuf);
-    cudaFree(td.act[0]); cudaFree(td.act[1]);
+    for (void *q : {(void *)td.x[0], (void *)td.x[1], (void *)td.x0, (void *)td.y, (void *)td.mask, (void *)td.z,
+                    (void *)td.z1, (void *)td.zh, (void *)td.mean, (void *)td.m2, (void *)td.G, (void *)td.pbuf,
+                    (void *)td.act[0], (void *)td.act[1]})
+      dfree(c, q);
   }
   for (auto p : c->d_w) cudaFree(p);
   for (auto p : c->d_b) cudaFree(p);
-  if (c->scratch) cudaFree(c->scratch);
+  dfree(c, c->scratch);
+  if (c->pool && c->stream) cudaStreamSynchronize(c->stream);
   cudaFree(c->ddfb_u0); cudaFree(c->ddfb_fin);
   for (auto p : c->ddfb_t) cudaFree(p);
   for (auto p : c->ddfb_adj) cudaFree(p);
