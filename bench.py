@@ -415,12 +415,12 @@ def main():
         traffic = {}   # the committed ncu capture is for another workload
     roof = None
     if wl["cnn"] and cnn_n and wl.get("ddfb"):
-        # DDFB: 2K single-operator launches with a 1 <-> P channel structure (4.6 kFLOP/px): HBM-bound on
-        # the P-channel state u (bf16, 2P B/px per read or write); algorithmic bytes per pixel:
-        # W_K v (x 4 + u 2P) + (K-1) x [proj(v - W^*u) (u 2P + x 4 + p 4) + HT(u + W p) (p 4 + u 4P)]
-        # + final (u 2P + x 4 + G 4)
+        # DDFB: K two-operator launches (W_k then W_{k+1}^*, one chained kernel each) with a 1 <-> P
+        # channel structure (4.6 kFLOP/px): bound by the P-channel state u (bf16, 2P B/px per read or
+        # write); algorithmic bytes per pixel: first launch v 4 (im2col) + u0 2P (stored) + v 4 + p 4;
+        # each later launch p 4 + u 2P (residual) + u' 2P (stored) + v 4 + p' / G 4
         Kc, P = wl["cnn"]
-        bpp = (4 + 2 * P) + (Kc - 1) * ((2 * P + 8) + (4 + 4 * P)) + (2 * P + 8)
+        bpp = (12 + 2 * P) + (Kc - 1) * (12 + 4 * P)
         ach = bpp * own_px * K / (cnn_ms * 1e-3) / 1e9
         roof = {"kernel": "cnn_chunk_kernel DDFB modes (tcgen05, %d launches/iteration)" % (cnn_n // K),
                 "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm, "traffic": None,

@@ -312,6 +312,7 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
   const bool last = p.last_is_output != 0;
   const SmemLayout L = make_layout(P, NL, first, last, NC);
   constexpr int K0 = im2col_k(NC);      // im2col K (9 NC taps, zero padded)
+  constexpr bool kDdfb = NC == 1 && NL <= 2;   // DDFB operator modes compiled in (R39-R42)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t sbase = smem_u32(smem);
   const uint32_t bar0 = sbase + L.bar_off;
@@ -715,12 +716,12 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
             nacc0[co] = nacc1[co] + c[1];
             nacc1[co] = c[2];
             if (store) {
-              if (NC > 1 || NL != 1 || p.mode < 2) {   // DDFB modes only exist for single-operator launches
+              if (!kDdfb || p.mode < 2) {   // DDFB modes exist for 1- and 2-operator launches only
                 p.G[(int64_t)co * p.gcs + gidx] = row_done + p.bias[l][co];
               } else if (o >= 0 && o < p.ny && cm >= 0 && cm < p.nx) {
                 // DDFB adjoint step (R39): q = proj_[0,1](v - W_k^* u); final: G = v - q
                 const TileGeom &xg = p.xg;
-                const float v = p.x[(int64_t)(o - (xg.i0 - xg.h)) * xg.pitch + (cm - (xg.j0 - xg.hx))];
+                const float v = p.xv[(int64_t)(o - (xg.i0 - xg.h)) * xg.pitch + (cm - (xg.j0 - xg.hx))];
                 const float q = fminf(fmaxf(v - row_done, 0.f), 1.f);
                 p.G[gidx] = p.mode == 4 ? v - q : q;
               }
@@ -732,6 +733,21 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
       auto is_netlast = [&](int l) { return l == NL - 1 && last && !is_im2col(l); };
       // output row ic of layer l (completed at step s = f + kLag l, f = ic, or ic + 2 with the
       // dy fold); false on abort
+      // DDFB mode 3: u at the pixel of the next output row, loaded while this row is processed
+      // (the epilogue of a single im2col layer is otherwise latency-bound on these loads)
+      uint32_t upre[kDdfb ? P / 2 : 1];
+      int upre_ic = -1;
+      auto load_u = [&](int o2, uint32_t *dst) {
+        const bool in_a = col_in && o2 >= 0 && o2 < p.ny && o2 >= p.a_i0 && o2 < p.a_i0 + p.a_rows &&
+                          cm >= p.a_j0 && cm < p.a_j0 + p.a_cols;
+        const int64_t ab = ((int64_t)(o2 - p.a_i0) * p.a_cols + (cm - p.a_j0)) * 8;
+#pragma unroll
+        for (int gq = 0; gq < G; ++gq) {
+          const uint4 t = in_a ? *reinterpret_cast<const uint4 *>(p.ain + (int64_t)gq * p.a_rows * p.a_cols * 8 + ab)
+                               : make_uint4(0, 0, 0, 0);
+          dst[4 * gq] = t.x; dst[4 * gq + 1] = t.y; dst[4 * gq + 2] = t.z; dst[4 * gq + 3] = t.w;
+        }
+      };
       auto epi_step = [&](const int l, const int ic) -> bool {
           const bool im2col = is_im2col(l);
           const int s = (im2col ? ic : ic + 2) + kLag * l;
@@ -776,19 +792,12 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
           }
           const uint32_t ta = taddr + (Ig & 3) * (uint32_t)P;
           uint32_t w[P / 2];
-          if (NC == 1 && NL == 1 && (p.mode == 1 || p.mode == 3)) {
+          const int m0 = NL == 1 ? p.mode : p.mode0;   // DDFB mode of the im2col layer
+          if (kDdfb && is_im2col(l) && (m0 == 1 || m0 == 3)) {
             // DDFB im2col layers (R39, R40): mode 1 u0 = W_K v (no bias, no activation);
             // mode 3 u' = HT(u + gamma_k W_k p) with u read (bf16) at the same pixel
-            uint32_t uin[P / 2];
-            if (p.mode == 3) {
-              const int64_t ab = ((int64_t)(o - p.a_i0) * p.a_cols + (cm - p.a_j0)) * 8;
-#pragma unroll
-              for (int gq = 0; gq < G; ++gq) {
-                const uint4 t = inside ? *reinterpret_cast<const uint4 *>(p.ain + (int64_t)gq * p.a_rows * p.a_cols * 8 + ab)
-                                       : make_uint4(0, 0, 0, 0);
-                uin[4 * gq] = t.x; uin[4 * gq + 1] = t.y; uin[4 * gq + 2] = t.z; uin[4 * gq + 3] = t.w;
-              }
-            }
+            uint32_t *uin = upre;
+            if (m0 == 3 && upre_ic != ic) load_u(o, upre);   // not prefetched (first row of a unit)
             const float ht = p.ht_eps;
 #pragma unroll
             for (int h = 0; h < P; h += 16) {
@@ -798,13 +807,17 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
 #pragma unroll
               for (int c = 0; c < 16; c += 2) {
                 float a0 = v[c], a1 = v[c + 1];
-                if (p.mode == 3) {
+                if (m0 == 3) {
                   const uint32_t pr = uin[(h + c) / 2];
                   a0 = fminf(fmaxf(__uint_as_float(pr << 16) + a0, -ht), ht);
                   a1 = fminf(fmaxf(__uint_as_float(pr & 0xffff0000u) + a1, -ht), ht);
                 }
                 w[(h + c) / 2] = pack_bf16(inside ? a0 : 0.f, inside ? a1 : 0.f);
               }
+            }
+            if (m0 == 3) {
+              if (ic + 1 < nout(l)) { load_u(o + 1, upre); upre_ic = ic + 1; }
+              else upre_ic = -1;
             }
           } else {
           // 16 channels at a time (tcgen05.ld -> +bias, ReLU -> bf16 pairs): keeps at most 16
@@ -845,6 +858,16 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
             fence_proxy_async();
             __syncwarp();
             if (lane == 0) mbar_arrive(bar_full(l + 1, Fg % kRingAct));
+            if (kDdfb && NL == 2 && p.mode0 != 0 && o >= p.o_i0 && o < p.o_i0 + p.o_rows && cm >= p.o_j0 &&
+                cm < p.o_j0 + p.o_cols) {
+              // fused DDFB launch: u' also goes to HBM (the next launch's residual); positions two
+              // strips share are written twice with identical values
+#pragma unroll
+              for (int gq = 0; gq < G; ++gq) {
+                const int64_t idx = (((int64_t)gq * p.o_rows + (o - p.o_i0)) * p.o_cols + (cm - p.o_j0)) * 8;
+                *reinterpret_cast<uint4 *>(p.aout + idx) = make_uint4(w[4 * gq], w[4 * gq + 1], w[4 * gq + 2], w[4 * gq + 3]);
+              }
+            }
           } else if (col_valid) {
             // chunk output (activations for the next launch), valid columns only
 #pragma unroll
@@ -933,7 +956,7 @@ cudaError_t launch_pn(const CnnChunkParams &p0, int num_sms, cudaStream_t s) {
 }
 
 // compile-time chain lengths: TMEM (NL * 4 * P <= 512 columns) and 227 KB of shared memory
-constexpr int max_nl(int P) { return P == 16 ? 8 : P == 32 ? 4 : 1; }
+constexpr int max_nl(int P) { return P == 16 ? 8 : P == 32 ? 4 : 2; }
 
 template <int P, int NL, int NC>
 cudaError_t dispatch_nl(const CnnChunkParams &p, int num_sms, cudaStream_t s) {

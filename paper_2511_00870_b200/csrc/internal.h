@@ -136,6 +136,9 @@ struct CnnChunkParams {
   int mode;              // 0 DnCNN; DDFB (R39-R42): 1 u0 = W_K v, 2 p = proj(v - W^* u), 3 u = HT(u + gamma W p),
                          // 4 G = v - proj(v - gamma_K W_K^* u)
   float ht_eps;          // DDFB hard-tanh level
+  int mode0;             // DDFB two-operator launch (NL = 2): mode of the im2col layer (1 or 3); the folded
+                         // layer uses `mode` (2 or 4); u' of layer 0 is also stored to aout
+  const float *xv;       // DDFB: v (padded, geometry xg) for modes 2 / 4
   int nc;                // image channels C (1, or 3 with P >= 32; reading R43): planes of x / G
   int64_t xcs, gcs;      // floats between the channel planes of x and of G
 };

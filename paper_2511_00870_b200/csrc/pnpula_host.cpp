@@ -47,6 +47,7 @@ struct TileDev {
   float *z1 = nullptr;     // OP_POISSON: z1 block, valid on tile (+) r_H (reading R33)
   float *zh = nullptr;     // TV prior: horizontal component z_h of z ~ D x (z_v lives in z)
   float *pbuf = nullptr;   // DDFB: p = proj(v - W_k^* u), fp32 padded geometry, zero outside the image
+  float *pbuf2 = nullptr;  // DDFB fused launches: p alternates between pbuf and pbuf2
   uint16_t *act[2] = {nullptr, nullptr};   // inter-chunk activations
 };
 
@@ -262,77 +263,58 @@ pnpula_status upload_padded(pnpula_ctx *c, T *dst, const TileGeom &g, const T *h
   return PNPULA_OK;
 }
 
-// DDFB (R39-R42): 2K single-operator launches per tile on shrinking regions tile (+) e:
-//   u0 = W_K v (e = 2K-1); for k < K: p = proj(v - W_k^* u) (e = 2K-2k), u = HT(u + gamma_k W_k p)
-//   (e = 2K-2k-1); G = v - proj(v - gamma_K W_K^* u) (e = 0).
+// DDFB (R39-R42): K two-operator launches per tile (cnn_chunk_kernel<P, 2>: an im2col 1 -> P
+// layer feeding a folded P -> 1 layer through shared memory), on shrinking regions tile (+) e:
+//   j = 0:      u0 = W_K v (e = 2K-1, also stored)          -> p1 = proj(v - W_1^* u0) (e = 2K-2)
+//   0 < j < K:  u_j = HT(u_{j-1} + gamma_j W_j p_j) (stored) -> p_{j+1} = proj(v - W_{j+1}^* u_j)
+//   j = K-1:    the folded layer is G = v - proj(v - gamma_K W_K^* u_{K-1}) (e = 0)
+// (output extents e = 2K-2-2j; u_j on e+1).  p alternates between pbuf / pbuf2 and u between the
+// two activation buffers, so no launch reads what it writes.
 pnpula_status run_ddfb(pnpula_ctx *c, int buf) {
   const int K = c->n_layers, P = c->channels;
   for (auto &td : c->tiles) {
     const TileGeom &g = td.g;
-    int cur = 0;   // act buffer holding the current u
-    auto base = [&](int mode, int ext) {
+    int cur = 0;              // act buffer receiving u_j
+    float *pin = nullptr;     // p_j (im2col input of launch j > 0)
+    for (int j = 0; j < K; ++j) {
+      const int e = 2 * K - 2 - 2 * j;   // output extent; u_j on e + 1
       CnnChunkParams p{};
       p.P = P;
-      p.nl = 1;
-      p.mode = mode;
-      p.ht_eps = (float)c->ht_eps;
+      p.nl = 2;
       p.nc = 1;
-      p.x = td.x[buf];
+      p.first_is_input = 1;
+      p.last_is_output = 1;
+      p.mode0 = j == 0 ? 1 : 3;
+      p.mode = j == K - 1 ? 4 : 2;
+      p.ht_eps = (float)c->ht_eps;
+      p.w[0] = j == 0 ? c->ddfb_u0 : c->ddfb_t[j - 1];
+      p.w[1] = j == K - 1 ? c->ddfb_fin : c->ddfb_adj[j];
+      p.x = j == 0 ? td.x[buf] : pin;   // im2col input: v, then p_j
+      p.xv = td.x[buf];
       p.xg = g;
-      p.oi0 = g.i0 - ext; p.oj0 = g.j0 - ext;
-      p.oh = g.th + 2 * ext; p.ow = g.tw + 2 * ext;
+      p.oi0 = g.i0 - e; p.oj0 = g.j0 - e;
+      p.oh = g.th + 2 * e; p.ow = g.tw + 2 * e;
+      if (j > 0) {             // u_{j-1} on tile (+) e + 3 (read at the pixel by mode 3)
+        p.ain = td.act[cur ^ 1];
+        p.a_i0 = g.i0 - (e + 3); p.a_j0 = g.j0 - (e + 3);
+        p.a_rows = g.th + 2 * (e + 3); p.a_cols = g.tw + 2 * (e + 3);
+      }
+      p.aout = td.act[cur];     // u_j on tile (+) e + 1
+      p.o_i0 = g.i0 - (e + 1); p.o_j0 = g.j0 - (e + 1);
+      p.o_rows = g.th + 2 * (e + 1); p.o_cols = g.tw + 2 * (e + 1);
+      float *pout = (j % 2 == 0) ? td.pbuf : td.pbuf2;
+      p.G = j == K - 1 ? td.G : pout;
+      p.gg = g;
       p.ny = c->ny; p.nx = c->nx;
       p.err = c->d_err;
-      return p;
-    };
-    auto set_ain = [&](CnnChunkParams &p, int ext) {   // u on tile (+) ext
-      p.ain = td.act[cur];
-      p.a_i0 = g.i0 - ext; p.a_j0 = g.j0 - ext;
-      p.a_rows = g.th + 2 * ext; p.a_cols = g.tw + 2 * ext;
-    };
-    auto set_aout = [&](CnnChunkParams &p, int b) {
-      p.aout = td.act[b];
-      p.o_i0 = p.oi0; p.o_j0 = p.oj0; p.o_rows = p.oh; p.o_cols = p.ow;
-    };
-    auto launch = [&](const CnnChunkParams &p) -> pnpula_status {
       cudaEvent_t end;
       timer_begin(c, c->tm_cnn, &end);
       CU(c, launch_cnn_chunk(p, c->num_sms, c->stream));
       c->n_launches++;
       timer_end(c, end);
-      return PNPULA_OK;
-    };
-    pnpula_status s;
-    {   // u0 = W_K v on tile (+) 2K-1
-      CnnChunkParams p = base(1, 2 * K - 1);
-      p.first_is_input = 1;
-      p.w[0] = c->ddfb_u0;
-      set_aout(p, cur);
-      if ((s = launch(p))) return s;
-    }
-    for (int k = 1; k < K; ++k) {
-      const int eu = 2 * K - 2 * k + 1;   // u lives on tile (+) eu
-      CnnChunkParams pa = base(2, eu - 1);   // p = proj(v - W_k^* u)
-      pa.last_is_output = 1;
-      pa.w[0] = c->ddfb_adj[k - 1];
-      set_ain(pa, eu);
-      pa.G = td.pbuf; pa.gg = g;
-      if ((s = launch(pa))) return s;
-      CnnChunkParams pt = base(3, eu - 2);   // u = HT(u + gamma_k W_k p)
-      pt.first_is_input = 1;
-      pt.x = td.pbuf;                        // im2col input = p (the v it needs came through p)
-      pt.w[0] = c->ddfb_t[k - 1];
-      set_ain(pt, eu);
-      set_aout(pt, cur ^ 1);
-      if ((s = launch(pt))) return s;
+      pin = pout;
       cur ^= 1;
     }
-    CnnChunkParams pf = base(4, 0);          // G = v - proj(v - gamma_K W_K^* u)
-    pf.last_is_output = 1;
-    pf.w[0] = c->ddfb_fin;
-    set_ain(pf, 1);
-    pf.G = td.G; pf.gg = g;
-    if ((s = launch(pf))) return s;
   }
   return PNPULA_OK;
 }
@@ -1113,6 +1095,8 @@ pnpula_status pnpula_create(const pnpula_config *cfg, pnpula_ctx **out) {
       const size_t n = geom_elems(td.g);
       CUB(dmalloc(c, &td.pbuf, n * sizeof(float)));
       CUB(cudaMemsetAsync(td.pbuf, 0, n * sizeof(float), c->stream));
+      CUB(dmalloc(c, &td.pbuf2, n * sizeof(float)));
+      CUB(cudaMemsetAsync(td.pbuf2, 0, n * sizeof(float), c->stream));
       const size_t act = (size_t)(td.g.th + 2 * (2 * K - 1)) * (td.g.tw + 2 * (2 * K - 1)) * P;
       for (int b2 = 0; b2 < 2; ++b2) {
         CUB(dmalloc(c, &td.act[b2], act * sizeof(uint16_t)));
@@ -1718,7 +1702,7 @@ pnpula_status pnpula_destroy(pnpula_ctx *c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (auto &td : c->tiles) {
     for (void *q : {(void *)td.x[0], (void *)td.x[1], (void *)td.x0, (void *)td.y, (void *)td.mask, (void *)td.z,
-                    (void *)td.z1, (void *)td.zh, (void *)td.mean, (void *)td.m2, (void *)td.G, (void *)td.pbuf,
+                    (void *)td.z1, (void *)td.zh, (void *)td.mean, (void *)td.m2, (void *)td.G, (void *)td.pbuf, (void *)td.pbuf2,
                     (void *)td.act[0], (void *)td.act[1]})
       dfree(c, q);
   }
