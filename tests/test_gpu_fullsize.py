@@ -25,7 +25,7 @@ def _samples(ny, nx):
     pts += [(1000, 122 * k - 1) for k in (1, 7, 30)] + [(2047, 122 * k) for k in (2, 45)]
     rng = np.random.default_rng(7)
     pts += [(int(rng.integers(0, ny)), int(rng.integers(0, nx))) for _ in range(6)]
-    return pts
+    return [(i, j) for i, j in pts if i < ny and j < nx]
 
 
 def _crop_oracle(wl, si, sj, bf16):
@@ -35,8 +35,12 @@ def _crop_oracle(wl, si, sj, bf16):
     kw = bench.build_inputs(wl, (i0, j0, i1 - i0, j1 - j0))
     okw = {k: v for k, v in kw.items() if k in ("sigma2", "gamma", "mask", "weights", "biases", "n_layers",
                                                 "channels", "alpha", "eps", "lam", "c_lo", "c_hi", "rho", "kappa",
-                                                "z_lo", "z_hi", "eta", "rho1", "kappa1", "tv_beta")}
-    okw.update(op="poisson" if wl["op"] == "poisson" else "conv", ksep=kw["kernel_sep"])
+                                                "z_lo", "z_hi", "eta", "rho1", "kappa1", "tv_beta", "den_kind",
+                                                "ddfb_gammas", "ht_eps")}
+    if wl["op"] == "mask":
+        okw.update(op="mask")
+    else:
+        okw.update(op="poisson" if wl["op"] == "poisson" else "conv", ksep=kw["kernel_sep"])
     pb = oracle.Problem(y=kw["y"], **okw)
     out = oracle.run(pb, N_ITER, 0, SEED, bf16_emulate=bf16, origin=(i0, j0))
     return {k: out[k][..., si - i0, sj - j0] for k in ("x", "z", "z1", "zh", "mean")}
@@ -48,7 +52,7 @@ def _close(a, b, atol):
 
 
 @pytest.mark.parametrize("name,bf16,atol", [("c5", True, 2e-3), ("p5", True, 2e-3), ("t5", False, 1e-5),
-                                            ("r5", True, 2e-3)])
+                                            ("r5", True, 2e-3), ("c3", True, 2e-3), ("d5", True, 2e-3)])
 def test_full_size_sampled_parity(name, bf16, atol):
     wl = bench.workload(name, 1)
     ny, nx = wl["ny"], wl["nx"]
