@@ -664,6 +664,34 @@ __global__ void __launch_bounds__(NTHREADS) z1_sep_kernel(const __grid_constant_
                  : "memory");
     tma_load_2d((uint32_t)__cvta_generic_to_shared(X), &tmx, bj0 - XL - (g.j0 - g.hx), bi0 - R - (g.i0 - g.h), b);
   }
+  // this thread's outputs: 2 rows x 1 quad; z1 and y are requested now so their latency overlaps
+  // the TMA wait and the horizontal pass (float4 when the quad lies inside tile (+) r_H)
+  const int q = tid & 15, a2 = tid >> 4;
+  const int gj4 = bj0 + 4 * q;
+  const int rlo = g.i0 - p.ry < 0 ? 0 : g.i0 - p.ry, rhi = g.i0 + g.th + p.ry > p.ny ? p.ny : g.i0 + g.th + p.ry;
+  const int clo = g.j0 - p.rx < 0 ? 0 : g.j0 - p.rx, chi = g.j0 + g.tw + p.rx > p.nx ? p.nx : g.j0 + g.tw + p.rx;
+  bool act[2], full[2];
+  float zr[2][4], yr[2][4];
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const int gi = bi0 + 2 * a2 + r;
+    act[r] = !(gi < rlo || gi >= rhi || gj4 >= chi || gj4 + 4 <= clo);
+    full[r] = act[r] && gj4 >= clo && gj4 + 4 <= chi;
+    const int64_t n0 = pidx(g, gi, gj4);   // 16-byte aligned
+    if (full[r]) {
+      const float4 zv = *reinterpret_cast<const float4 *>(p.z1 + n0);
+      const float4 yv = __ldg(reinterpret_cast<const float4 *>(p.y + n0));
+      zr[r][0] = zv.x; zr[r][1] = zv.y; zr[r][2] = zv.z; zr[r][3] = zv.w;
+      yr[r][0] = yv.x; yr[r][1] = yv.y; yr[r][2] = yv.z; yr[r][3] = yv.w;
+    } else {
+#pragma unroll
+      for (int l = 0; l < 4; ++l) {
+        const bool in = act[r] && gj4 + l >= clo && gj4 + l < chi;
+        zr[r][l] = in ? p.z1[n0 + l] : 0.f;
+        yr[r][l] = in ? __ldg(p.y + n0 + l) : 0.f;
+      }
+    }
+  }
   __syncthreads();
   mbar_wait_parity(b, 0);
   // horizontal: T[a][c] = sum_q kx[q+R] X[a][c + XL - q]   (x+ column bj0 + c - q)
@@ -674,34 +702,37 @@ __global__ void __launch_bounds__(NTHREADS) z1_sep_kernel(const __grid_constant_
     for (int j = 0; j < 4; ++j) {
       float s = 0.f;
 #pragma unroll
-      for (int q = -R; q <= R; ++q) s = fmaf(kxs[q + R], X[a * XC + c4 + j + XL - q], s);
+      for (int q2 = -R; q2 <= R; ++q2) s = fmaf(kxs[q2 + R], X[a * XC + c4 + j + XL - q2], s);
       o[j] = s;
     }
     *reinterpret_cast<float4 *>(T + a * TX + 4 * (e - a * (TX / 4))) = make_float4(o[0], o[1], o[2], o[3]);
   }
   __syncthreads();
-  const int q = tid & 15, a2 = tid >> 4;
-  const int gj4 = bj0 + 4 * q;
-  const int rlo = g.i0 - p.ry < 0 ? 0 : g.i0 - p.ry, rhi = g.i0 + g.th + p.ry > p.ny ? p.ny : g.i0 + g.th + p.ry;
-  const int clo = g.j0 - p.rx < 0 ? 0 : g.j0 - p.rx, chi = g.j0 + g.tw + p.rx > p.nx ? p.nx : g.j0 + g.tw + p.rx;
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
+    if (!act[r]) continue;
     const int a = 2 * a2 + r, gi = bi0 + a;
-    if (gi < rlo || gi >= rhi || gj4 >= chi || gj4 + 4 <= clo) continue;
     float ze[4];
     normals4(p.seed_lo, p.seed_hi, (uint32_t)gj4 >> 2, (uint32_t)gi, t1, p.sb + 2u, ze);
+    float out[4];
 #pragma unroll
     for (int l = 0; l < 4; ++l) {
-      const int gj = gj4 + l;
-      if (gj < clo || gj >= chi) continue;
       float s = 0.f;   // vertical: sum_p ky[p+R] T[a + R - p][c]
 #pragma unroll
       for (int pp = -R; pp <= R; ++pp) s = fmaf(kys[pp + R], T[(a + R - pp) * TX + 4 * q + l], s);
-      const int64_t n = pidx(g, gi, gj);
-      const float z = p.z1[n];
+      const float z = zr[r][l];
       const float v = z - p.b1 * (z - p.eta * s) + p.s1 * ze[l];
       const float av = v - p.kappa1;
-      p.z1[n] = 0.5f * (av + sqrtf(fmaf(av, av, 4.0f * p.kappa1 * __ldg(p.y + n))));
+      const float r2 = fmaf(av, av, 4.0f * p.kappa1 * yr[r][l]);   // KL prox (R31): (av + sqrt(r2)) / 2
+      out[l] = 0.5f * (av + (r2 > 0.f ? r2 * rsqrtf(r2) : 0.f));
+    }
+    const int64_t n0 = pidx(g, gi, gj4);
+    if (full[r]) {
+      *reinterpret_cast<float4 *>(p.z1 + n0) = make_float4(out[0], out[1], out[2], out[3]);
+    } else {
+#pragma unroll
+      for (int l = 0; l < 4; ++l)
+        if (gj4 + l >= clo && gj4 + l < chi) p.z1[n0 + l] = out[l];
     }
   }
 }
