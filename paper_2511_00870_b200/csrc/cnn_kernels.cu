@@ -61,7 +61,9 @@ constexpr int kMma0 = kProdWarps;               // first MMA warp (also allocate
 // Per chain length NL: MMA warps MW and epilogue groups EG (at most one per layer), first
 // epilogue warp, block size -- producer warps, MMA warps, epilogue warps.
 __host__ __device__ constexpr int mma_warps(int nl) { return nl < kMmaWarps ? nl : kMmaWarps; }
-__host__ __device__ constexpr int epi_groups(int nl) { return nl < kEpiGroups ? nl : kEpiGroups; }
+// two-layer chains (DDFB operator pairs; P = 64 DnCNN chunks) give layer 0 two epilogue groups
+// (even / odd output rows): its P-channel epilogue, not the MMAs, bounds those launches
+__host__ __device__ constexpr int epi_groups(int nl) { return nl == 2 ? 3 : nl < kEpiGroups ? nl : kEpiGroups; }
 __host__ __device__ constexpr int epi0(int nl) { return kMma0 + mma_warps(nl); }
 __host__ __device__ constexpr int block_threads(int nl) { return 32 * (epi0(nl) + 4 * epi_groups(nl)); }
 constexpr int kRing = 4;                        // input-row ring slots of layer 0 (one per producer warp)
@@ -816,7 +818,8 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
               }
             }
             if (m0 == 3) {
-              if (ic + 1 < nout(l)) { load_u(o + 1, upre); upre_ic = ic + 1; }
+              constexpr int kStep = NL == 2 ? 2 : 1;   // next row this thread's group handles
+              if (ic + kStep < nout(l)) { load_u(o + kStep, upre); upre_ic = ic + kStep; }
               else upre_ic = -1;
             }
           } else {
@@ -879,7 +882,22 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
           trace_ev(p.trace, trw, 8, s, l);
           return true;
       };
-      if constexpr (NL <= kEpiGroups) {
+      if constexpr (NL == 2) {
+        // groups 0 / 1: layer 0, rows of their parity; group 2: layer 1
+        if (grp < 2) {
+          const int no = nout(0);
+          for (int ic = grp; ic < no; ic += 2)
+            if (!epi_step(0, ic)) break;
+        } else if (is_netlast(1)) {
+          const int nf = nfill(1);
+          for (int f = 0; f < nf; ++f)
+            if (!netlast_fill(1, f)) break;
+        } else {
+          const int no = nout(1);
+          for (int ic = 0; ic < no; ++ic)
+            if (!epi_step(1, ic)) break;
+        }
+      } else if constexpr (NL <= kEpiGroups) {
         // one layer per group: walk its output rows (or, folded last layer, its fills) directly
         if (is_netlast(grp)) {
           const int nf = nfill(grp);
