@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <mutex>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -212,7 +213,9 @@ size_t geom_elems(const TileGeom &g) { return (size_t)g.ph * g.pitch; }
 // Allocation and first use are ordered on the context stream.  PNPULA_POOL=0: plain cudaMalloc.
 cudaMemPool_t device_pool(int dev) {
   static cudaMemPool_t pools[64] = {};
+  static std::mutex mu;
   if (dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
   if (!pools[dev]) {
     cudaMemPoolProps pr{};
     pr.allocType = cudaMemAllocationTypePinned;
