@@ -127,7 +127,11 @@ struct QuadIn {
   float x[4], G[4], z[4], m[4], s[4];
 };
 
-__device__ __forceinline__ void ula_load(const UpdateParams &p, const IterScalars &is, int gi, int gj4, QuadIn &q) {
+// TVM (as for ula_finish): 2 = a TV launch, whose posterior has no denoiser G, no H2 = I z block
+// and no box term (create rejects those with the TV prior): their loads and terms compile out.
+// TVM = 2 is instantiated separately so the generic loader's code is unchanged.
+template <int TVM>
+__device__ __forceinline__ void ula_load_t(const UpdateParams &p, const IterScalars &is, int gi, int gj4, QuadIn &q) {
   const TileGeom &g = p.g;
   const int64_t base = pidx(g, gi, gj4);
   const bool full = gj4 >= g.j0 && gj4 + 4 <= g.j0 + g.tw;
@@ -136,11 +140,11 @@ __device__ __forceinline__ void ula_load(const UpdateParams &p, const IterScalar
   if (full) {
     const float4 a = __ldg(reinterpret_cast<const float4 *>(p.x + base));
     q.x[0] = a.x; q.x[1] = a.y; q.x[2] = a.z; q.x[3] = a.w;
-    if (p.has_G) {
+    if (TVM != 2 && p.has_G) {
       const float4 b = __ldg(reinterpret_cast<const float4 *>(p.G + base));
       q.G[0] = b.x; q.G[1] = b.y; q.G[2] = b.z; q.G[3] = b.w;
     }
-    if (p.has_z) {
+    if (TVM != 2 && p.has_z) {
       const float4 b = *reinterpret_cast<const float4 *>(p.z + base);
       q.z[0] = b.x; q.z[1] = b.y; q.z[2] = b.z; q.z[3] = b.w;
     }
@@ -154,11 +158,16 @@ __device__ __forceinline__ void ula_load(const UpdateParams &p, const IterScalar
 #pragma unroll
     for (int l = 0; l < 4; ++l) {
       q.x[l] = p.x[base + l];
-      if (p.has_G) q.G[l] = p.G[base + l];
-      if (p.has_z) q.z[l] = p.z[base + l];
+      if (TVM != 2 && p.has_G) q.G[l] = p.G[base + l];
+      if (TVM != 2 && p.has_z) q.z[l] = p.z[base + l];
       if (is.acc) { q.m[l] = p.mean[base + l]; q.s[l] = p.m2[base + l]; }
     }
   }
+}
+
+__device__ __forceinline__ void ula_load(const UpdateParams &p, const IterScalars &is, int gi, int gj4, QuadIn &q) {
+  if (p.has_tv) ula_load_t<2>(p, is, gi, gj4, q);
+  else ula_load_t<1>(p, is, gi, gj4, q);
 }
 
 // D^T (D x - z) at the 4 pixels of a quad (R35, R37):
@@ -212,15 +221,15 @@ __device__ __forceinline__ void ula_finish(const UpdateParams &p, const IterScal
 #pragma unroll
   for (int l = 0; l < 4; ++l) {
     float v = xv[l] - p.a_g * gr[l];
-    if (p.has_z) v -= p.a_rho * (xv[l] - zv[l]);
-    if (p.has_G) v += p.a_d * (-Gv[l]);
-    if (p.has_box) v += p.a_lam * (fminf(fmaxf(xv[l], p.c_lo), p.c_hi) - xv[l]);
+    if (TVM != 2 && p.has_z) v -= p.a_rho * (xv[l] - zv[l]);
+    if (TVM != 2 && p.has_G) v += p.a_d * (-Gv[l]);
+    if (TVM != 2 && p.has_box) v += p.a_lam * (fminf(fmaxf(xv[l], p.c_lo), p.c_hi) - xv[l]);
     if (has_tv) v -= p.a_tv * dtv[l];
     v += p.a_xi * xi[l];
     xn[l] = has_tv ? fmaxf(v, 0.f) : v;   // TV: PSGLA projection onto R+ after the step (R37)
   }
   float zn[4];
-  if (p.has_z) {
+  if (TVM != 2 && p.has_z) {
     float ze[4];
     normals4(p.seed_lo, p.seed_hi, (uint32_t)gj4 >> 2, (uint32_t)gi, is.t1, p.sb + 1u, ze);
 #pragma unroll
@@ -239,7 +248,7 @@ __device__ __forceinline__ void ula_finish(const UpdateParams &p, const IterScal
   }
   if (full) {
     *reinterpret_cast<float4 *>(p.xn + base) = make_float4(xn[0], xn[1], xn[2], xn[3]);
-    if (p.has_z) *reinterpret_cast<float4 *>(p.z + base) = make_float4(zn[0], zn[1], zn[2], zn[3]);
+    if (TVM != 2 && p.has_z) *reinterpret_cast<float4 *>(p.z + base) = make_float4(zn[0], zn[1], zn[2], zn[3]);
     if (is.acc) {
       *reinterpret_cast<float4 *>(p.mean + base) = make_float4(mv[0], mv[1], mv[2], mv[3]);
       *reinterpret_cast<float4 *>(p.m2 + base) = make_float4(sv[0], sv[1], sv[2], sv[3]);
@@ -250,7 +259,7 @@ __device__ __forceinline__ void ula_finish(const UpdateParams &p, const IterScal
       const int gj = gj4 + l;
       if (gj < g.j0 || gj >= g.j0 + g.tw) continue;
       p.xn[base + l] = xn[l];
-      if (p.has_z) p.z[base + l] = zn[l];
+      if (TVM != 2 && p.has_z) p.z[base + l] = zn[l];
       if (is.acc) { p.mean[base + l] = mv[l]; p.m2[base + l] = sv[l]; }
     }
   }
@@ -487,7 +496,7 @@ update_sep_kernel(const __grid_constant__ UpdateParams p, const __grid_constant_
     for (int r = 0; r < 2; ++r) {
       const int gi = bi0 + 2 * a2 + r;
       act[r] = !(gi >= g.i0 + g.th || gj4 >= g.j0 + g.tw || gj4 + 4 <= g.j0);
-      if (act[r]) ula_load(p, is, gi, gj4, qin[r]);
+      if (act[r]) ula_load_t<TVM == 2 ? 2 : 1>(p, is, gi, gj4, qin[r]);
     }
     mbar_wait_parity((uint32_t)__cvta_generic_to_shared(&full_bar[buf]), (uint32_t)(k >> 1) & 1u);
 
@@ -1005,8 +1014,8 @@ cudaError_t launch_update(const UpdateParams &p, cudaStream_t s) {
       cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
       const int R = p.ry;
       const size_t smem = R == 4 ? SepGeom<4>::bytes : SepGeom<2>::bytes;
-      auto kfn = R == 4 ? (p.has_tv ? update_sep_kernel<4, 1> : update_sep_kernel<4, 0>)
-                        : (p.has_tv ? update_sep_kernel<2, 1> : update_sep_kernel<2, 0>);
+      auto kfn = R == 4 ? (p.has_tv ? update_sep_kernel<4, 2> : update_sep_kernel<4, 0>)
+                        : (p.has_tv ? update_sep_kernel<2, 2> : update_sep_kernel<2, 0>);
       cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
       // TMA maps of the padded x and y buffers (ph x pitch fp32), boxes = the staged regions
