@@ -44,9 +44,6 @@ namespace {
 #ifndef PNPULA_EPI_GROUPS
 #define PNPULA_EPI_GROUPS 4
 #endif
-#ifndef PNPULA_EXP
-#define PNPULA_EXP 0   // timing experiments (exp/); 0 in every real build
-#endif
 constexpr int kRowPos = 130;                    // positions per ring row (128 MMA rows + 1 each side)
 constexpr int kEpiGroups = PNPULA_EPI_GROUPS;   // max epilogue groups (each: 4 warps = 4 TMEM lane quarters)
 #ifndef PNPULA_MMA_WARPS
@@ -551,7 +548,7 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
           const uint32_t Ig = O0 + (uint32_t)f;
           if (netlast) {   // 2-slot ring of per-fill accumulators: fill Fg-2 must have been read
             if (ok && Fg >= 2u) ok = mbar_wait(bar_tempty(l, Fg & 1), ((Fg >> 1) - 1) & 1, abort_flag, p.err, 3);
-          } else if (ok && f < no && Ig >= (uint32_t)kAcc && PNPULA_EXP != 7)
+          } else if (ok && f < no && Ig >= (uint32_t)kAcc)
             ok = mbar_wait(bar_tempty(l, Ig & 3), ((Ig >> 2) - 1) & 1, abort_flag, p.err, 3);
           ok = __shfl_sync(0xffffffffu, ok ? 1 : 0, 0) != 0;
           trace_ev(p.trace, tr_on && lane == 0, 4, s, l);
@@ -760,21 +757,6 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
           const uint32_t taddr = tmem_base + lane_base + (uint32_t)(l * kAcc * P);
           const int o = r_lo - (NL - 1 - l) + ic;      // global output row
           const bool inside = col_in && o >= 0 && o < p.ny;
-#if PNPULA_EXP == 8
-          // timing experiment only (wrong results): the epilogue only passes the barriers on
-          {
-            __syncwarp();
-            if (lane == 0) mbar_arrive(bar_tempty(l, Ig & 3));
-            if (l < NL - 1) {
-              const uint32_t Fg = Fcnt(l + 1) + (uint32_t)ic;
-              if (Fg >= kRingAct && !mbar_wait(bar_empty(l + 1, Fg % kRingAct), ((Fg / kRingAct) - 1) & 1, abort_flag, p.err, 5))
-                return false;
-              __syncwarp();
-              if (lane == 0) mbar_arrive(bar_full(l + 1, Fg % kRingAct));
-            }
-            return true;
-          }
-#endif
           if ((l == NL - 1) && last) {
             // network output G (no ReLU), column 0 of the 16-column slot
             float v[1];
