@@ -1,3 +1,4 @@
+# full round-end validation on one B200: smoke, deliverables (exp/deliv.sh), every bench workload
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
