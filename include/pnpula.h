@@ -189,7 +189,12 @@ pnpula_status pnpula_create(const pnpula_config *cfg, pnpula_ctx **out);
  * and set burn_in and seed for the following pnpula_advance calls. */
 pnpula_status pnpula_reset(pnpula_ctx *ctx, int64_t burn_in, uint64_t seed);
 
-/* [collective] Run n_iter further iterations (asynchronous on the context stream). */
+/* [collective] Run n_iter further iterations (asynchronous on the context stream).
+ * Execution (results are bitwise the same either way): after the first iteration, single-rank
+ * untimed iterations replay a captured CUDA graph per x-buffer parity (PNPULA_FLAG_NO_GRAPH /
+ * env PNPULA_GRAPHS=0: direct launches); with NCCL halo messages on a row-strip grid the update
+ * runs the h boundary rows of each tile first and the exchange, on a second stream, overlaps the
+ * interior rows (env PNPULA_OVERLAP=0 at create: serial). */
 pnpula_status pnpula_advance(pnpula_ctx *ctx, int64_t n_iter);
 
 /* [collective] pnpula_reset(burn_in, seed) then pnpula_advance(n_iter), then
