@@ -42,7 +42,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=60)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--workload", default="c5", choices=["c5", "c2", "c3", "c4", "c1", "p5", "t5", "d5", "r5"])
+    ap.add_argument("--workload", default="c5", choices=["c5", "c2", "c3", "c4", "c1", "p5", "t5", "d5", "r5", "pd"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -78,6 +78,13 @@ def workload(name, n):
         return dict(name="r5", desc="weak scaling as c5, RGB (C = 3, planar) 9x9 Gaussian deblur 25 dB per "
                     "channel, colour DnCNN-lite 8x32 (3 -> 32 ... 32 -> 3)", ny=ny, nx=nx, tiles=(n, 1), op="conv",
                     L=9, sb=2.0, cnn=(8, 32), z=False, nc=3, scaling="weak")
+    if name == "pd":
+        # context only (not a BASELINE.json config): the paper's own deblurring workload shape (P:843, P:761,
+        # RGB 2048^2, DnCNN K = 20 / 64 features, 353 ms per iteration on one V100) with a 15x15
+        # Gaussian blur (the largest this library supports; the paper uses a 65^2 motion blur)
+        return dict(name="pd", desc="context: paper-shaped RGB 2048^2 deblur, DnCNN 20x64 (3 -> 64 ... 64 -> 3), "
+                    "15x15 Gaussian blur", ny=2048 * max(n, 1), nx=2048, tiles=(n, 1), op="conv", L=15, sb=3.0,
+                    cnn=(20, 64), z=False, nc=3, scaling="weak")
     if name == "t5":
         shapes = {1: (4096, 8192), 2: (8192, 8192), 4: (8192, 16384), 8: (16384, 16384)}
         ny, nx = shapes.get(n, (4096 * n, 8192))
