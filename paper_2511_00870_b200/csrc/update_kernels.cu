@@ -480,7 +480,6 @@ update_sep_kernel(const __grid_constant__ UpdateParams p, const __grid_constant_
   for (int k = 0; blk < nblk; blk += gridDim.x, ++k) {
     const int buf = k & 1;
     const int nxt = blk + gridDim.x;
-    if (tid == 0 && nxt < nblk) stage(nxt, buf ^ 1);
     const int bi0 = g.i0 + (blk / nbx) * TY;
     const int bj0 = (g.j0 & ~3) + (blk - (blk / nbx) * nbx) * TX;
     float *const X = sm + buf * XR * XC;
@@ -520,6 +519,9 @@ update_sep_kernel(const __grid_constant__ UpdateParams p, const __grid_constant_
       *reinterpret_cast<float4 *>(T1 + a * RC + 4 * k4) = make_float4(o[0], o[1], o[2], o[3]);
     }
     __syncthreads();
+    // buffer buf ^ 1 (x / T2 and y of the previous block) is free once every thread has passed
+    // this barrier, so the next block's prefetch is issued here (no end-of-block barrier)
+    if (tid == 0 && nxt < nblk) stage(nxt, buf ^ 1);
     // phase 2: Rs[a][b] = sum_p ky[p+R] T1[a+R-p][b] - y, zero outside the image (4x4 per item)
     for (int e = tid; e < (RR / 4) * (RC / 4); e += NTHREADS) {
       const int a4 = e / (RC / 4), k4 = e - a4 * (RC / 4);
@@ -600,7 +602,6 @@ update_sep_kernel(const __grid_constant__ UpdateParams p, const __grid_constant_
         ula_finish<TVM>(p, is, bi0 + 2 * a2 + r, gj4, gr, qin[r]);
       }
     }
-    __syncthreads();   // buffer buf is restaged by the next iteration's prefetch
   }
 }
 
