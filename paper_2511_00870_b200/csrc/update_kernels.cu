@@ -89,6 +89,29 @@ __device__ __forceinline__ void normals4(uint32_t seed_lo, uint32_t seed_hi, uin
   out[0] = a.x; out[1] = a.y; out[2] = b.x; out[3] = b.y;
 }
 
+// normals4 for rows `row` and `row + 1` of the same quad, the two Philox chains advanced in one
+// loop (independent chains interleave: twice the instruction-level parallelism of two calls)
+__device__ __forceinline__ void normals4x2(uint32_t seed_lo, uint32_t seed_hi, uint32_t quad, uint32_t row,
+                                           uint32_t t1, uint32_t stream, float out[2][4]) {
+  uint4 c0 = make_uint4(quad, row, t1, stream), c1 = make_uint4(quad, row + 1u, t1, stream);
+  uint32_t k0 = seed_lo, k1 = seed_hi;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t lo0 = 0xD2511F53u * c0.x, hi0 = __umulhi(0xD2511F53u, c0.x);
+    const uint32_t lo1 = 0xCD9E8D57u * c0.z, hi1 = __umulhi(0xCD9E8D57u, c0.z);
+    const uint32_t lo2 = 0xD2511F53u * c1.x, hi2 = __umulhi(0xD2511F53u, c1.x);
+    const uint32_t lo3 = 0xCD9E8D57u * c1.z, hi3 = __umulhi(0xCD9E8D57u, c1.z);
+    c0 = make_uint4(hi1 ^ c0.y ^ k0, lo1, hi0 ^ c0.w ^ k1, lo0);
+    c1 = make_uint4(hi3 ^ c1.y ^ k0, lo3, hi2 ^ c1.w ^ k1, lo2);
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  const float2 a0 = box_muller(c0.x, c0.y), b0 = box_muller(c0.z, c0.w);
+  const float2 a1 = box_muller(c1.x, c1.y), b1 = box_muller(c1.z, c1.w);
+  out[0][0] = a0.x; out[0][1] = a0.y; out[0][2] = b0.x; out[0][3] = b0.y;
+  out[1][0] = a1.x; out[1][1] = a1.y; out[1][2] = b1.x; out[1][3] = b1.y;
+}
+
 // Iteration scalars: by value (direct launches) or from the device IterState (CUDA-graph
 // replays; see IterState), read once per thread at kernel entry.
 struct IterScalars {
@@ -206,7 +229,7 @@ __device__ __forceinline__ void tv_term(const UpdateParams &p, int gi, int gj4, 
 // TVM: 0 = the TV term is compiled out (non-TV launches of the separable kernel), 1 = p.has_tv at run time
 template <int TVM = 1>
 __device__ __forceinline__ void ula_finish(const UpdateParams &p, const IterScalars &is, int gi, int gj4, const float gr[4],
-                                           QuadIn &q) {
+                                           QuadIn &q, const float *xi_pre = nullptr) {
   const bool has_tv = TVM != 0 && p.has_tv;
   const TileGeom &g = p.g;
   const int64_t base = pidx(g, gi, gj4);
@@ -214,7 +237,12 @@ __device__ __forceinline__ void ula_finish(const UpdateParams &p, const IterScal
   const float *xv = q.x, *Gv = q.G, *zv = q.z;
   float *mv = q.m, *sv = q.s;
   float xi[4];
-  normals4(p.seed_lo, p.seed_hi, (uint32_t)gj4 >> 2, (uint32_t)gi, is.t1, p.sb + 0u, xi);
+  if (xi_pre) {
+#pragma unroll
+    for (int l = 0; l < 4; ++l) xi[l] = xi_pre[l];
+  } else {
+    normals4(p.seed_lo, p.seed_hi, (uint32_t)gj4 >> 2, (uint32_t)gi, is.t1, p.sb + 0u, xi);
+  }
   float dtv[4] = {0.f, 0.f, 0.f, 0.f};
   if (has_tv) tv_term(p, gi, gj4, xv, dtv);
   float xn[4];
@@ -588,6 +616,8 @@ update_sep_kernel(const __grid_constant__ UpdateParams p, const __grid_constant_
         const float4 t = *reinterpret_cast<const float4 *>(T2 + (2 * a2 + i) * TX + 4 * q4);
         col[i][0] = t.x; col[i][1] = t.y; col[i][2] = t.z; col[i][3] = t.w;
       }
+      float xi2[2][4];   // xi of both rows (rows outside the tile: computed, unused)
+      normals4x2(p.seed_lo, p.seed_hi, (uint32_t)gj4 >> 2, (uint32_t)(bi0 + 2 * a2), is.t1, p.sb + 0u, xi2);
 #pragma unroll
       for (int r = 0; r < 2; ++r) {
         if (!act[r]) continue;
@@ -599,7 +629,7 @@ update_sep_kernel(const __grid_constant__ UpdateParams p, const __grid_constant_
           for (int pp = -R; pp <= R; ++pp) s = fmaf(ky[pp + R], col[r + R + pp][j], s);
           gr[j] = s;
         }
-        ula_finish<TVM>(p, is, bi0 + 2 * a2 + r, gj4, gr, qin[r]);
+        ula_finish<TVM>(p, is, bi0 + 2 * a2 + r, gj4, gr, qin[r], xi2[r]);
       }
     }
   }
