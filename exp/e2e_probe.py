@@ -1,6 +1,6 @@
 """Diagnostics: where the end-to-end time goes (create / reset / advance / moments)."""
-import sys, time
-sys.path.insert(0, '/root/repo')
+import os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import bench
 from paper_2511_00870_b200 import Sampler

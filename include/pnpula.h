@@ -76,8 +76,8 @@ enum { PNPULA_SCOPE_LOCAL = 0, PNPULA_SCOPE_GLOBAL_ON_ROOT = 1 };
 #define PNPULA_FLAG_HALO_VIA_NCCL 0x1  /* route same-rank halos through NCCL self send/recv (tests) */
 #define PNPULA_FLAG_CNN_LAYERWISE 0x2  /* one CNN layer per launch instead of fused layer chains */
 #define PNPULA_FLAG_NO_GRAPH      0x4  /* launch every kernel directly (default: after the first iteration, each
-                                         iteration replays a captured CUDA graph when it is single-rank and
-                                         untimed; env PNPULA_GRAPHS=0 does the same) */
+                                         untimed iteration replays a captured CUDA graph, the NCCL halo group
+                                         included; env PNPULA_GRAPHS=0 does the same) */
 
 typedef struct {
   int32_t i0, j0, h, w; /* rectangle of global pixel coordinates: rows [i0, i0+h), cols [j0, j0+w) */
@@ -190,11 +190,13 @@ pnpula_status pnpula_create(const pnpula_config *cfg, pnpula_ctx **out);
 pnpula_status pnpula_reset(pnpula_ctx *ctx, int64_t burn_in, uint64_t seed);
 
 /* [collective] Run n_iter further iterations (asynchronous on the context stream).
- * Execution (results are bitwise the same either way): after the first iteration, single-rank
- * untimed iterations replay a captured CUDA graph per x-buffer parity (PNPULA_FLAG_NO_GRAPH /
- * env PNPULA_GRAPHS=0: direct launches); with NCCL halo messages on a row-strip grid the update
- * runs the h boundary rows of each tile first and the exchange, on a second stream, overlaps the
- * interior rows (env PNPULA_OVERLAP=0 at create: serial). */
+ * Execution (results are bitwise the same either way): after the first iteration, untimed
+ * iterations replay a captured CUDA graph per x-buffer parity, with the NCCL halo group of a
+ * multi-rank run captured inside it (PNPULA_FLAG_NO_GRAPH / env PNPULA_GRAPHS=0: direct
+ * launches); with NCCL halo messages on a row-strip grid the update runs the h boundary rows of
+ * each tile first and the exchange, on a second stream (a fork/join inside the graph), overlaps
+ * the interior rows (env PNPULA_OVERLAP=0 at create: serial).  Every rank must use the same
+ * graph setting (the captured NCCL calls are matched across ranks). */
 pnpula_status pnpula_advance(pnpula_ctx *ctx, int64_t n_iter);
 
 /* [collective] pnpula_reset(burn_in, seed) then pnpula_advance(n_iter), then
@@ -212,7 +214,9 @@ pnpula_status pnpula_local_bbox(pnpula_ctx *ctx, pnpula_rect *out);
  * M2/(n-1) of x^{(t)}, t = burn_in+1 .. current t.  mean / var (either may be
  * NULL) are host buffers of the LOCAL bbox size, or ny*nx on rank 0 for
  * PNPULA_SCOPE_GLOBAL_ON_ROOT (other ranks may pass NULL); times C planes for C > 1.  Returns
- * PNPULA_E_STATS_EMPTY if n < 1 (mean) or n < 2 (var requested). */
+ * PNPULA_E_STATS_EMPTY if n < 1 (mean) or n < 2 (var requested); GLOBAL_ON_ROOT with
+ * world_size > 1 returns it on every rank when n < 2, whatever pointers a rank passes (the
+ * outcome of a collective call must not differ between ranks). */
 pnpula_status pnpula_get_moments(pnpula_ctx *ctx, float *mean, float *var, int64_t *n_samples,
                                  int32_t scope);
 
@@ -267,6 +271,18 @@ pnpula_status pnpula_destroy(pnpula_ctx *ctx);
 /* Return the pool's unused device memory of `device` to the driver (cudaMemPoolTrimTo 0).
  * E_INVALID_ARG if the device has no pool. */
 pnpula_status pnpula_release_memory(int32_t device);
+
+/* Test hook for the noise of a6 (reading R9): the generator the update kernels use,
+ * evaluated on the device for n caller-chosen counters.  counters: host, n x 4 uint32
+ * (column quad j>>2, row i, iteration index t+1, stream) -- the Philox4x32-10 counter of R9 --
+ * under key (seed lo, seed hi).  words: host, n x 4, the raw Philox4x32-10 output words;
+ * normals: host, n x 4 fp32, the four Box-Muller normals of the quad (lanes j&3 = 0..3) exactly
+ * as the x / z updates draw them (the same device functions; reading R45 bounds their error
+ * against the fp64 definition).  Synchronous; allocates and frees its own device memory.
+ * PNPULA_E_STATE if the kernels' two normal paths (one and two Philox chains per thread)
+ * disagree in any bit. */
+pnpula_status pnpula_debug_philox(int32_t device, uint64_t seed, const uint32_t *counters, int64_t n,
+                                  uint32_t *words, float *normals);
 
 /* ---------------- host-only planning helpers (no GPU needed) ---------------- */
 

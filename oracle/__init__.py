@@ -31,9 +31,11 @@ _lib = None
 
 
 def build(force: bool = False) -> str:
-    """Compile the oracle with gcc (-O2, strict IEEE: no -ffast-math, no FMA contraction)."""
+    """Compile the oracle with gcc (-O2, strict IEEE: no -ffast-math, no FMA contraction; OpenMP
+    over output rows -- OMP_NUM_THREADS=1 for the single-thread timing; results do not depend on
+    the thread count)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        cmd = ["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-ffp-contract=off",
+        cmd = ["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-ffp-contract=off", "-fopenmp",
                "-D_DEFAULT_SOURCE", "-o", _LIB + ".tmp", _SRC, "-lm"]
         subprocess.check_call(cmd)
         os.replace(_LIB + ".tmp", _LIB)
@@ -111,6 +113,15 @@ def _f32(a) -> Optional[np.ndarray]:
 
 
 # ---------------------------------------------------------------- primitives
+def set_threads(n: int) -> int:
+    """OpenMP threads of the oracle's row loops (n <= 0: all host cores); returns the count set.
+    Results do not depend on it (see OR_PARALLEL_ROWS in pnpula_oracle.c)."""
+    _load()
+    n = n if n > 0 else (len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count())
+    C.CDLL("libgomp.so.1").omp_set_num_threads(int(n))
+    return int(n)
+
+
 def partition(n: int, parts: int, p: int) -> tuple[int, int]:
     lo, hi = C.c_int64(), C.c_int64()
     _load().or_partition(n, parts, p, C.byref(lo), C.byref(hi))

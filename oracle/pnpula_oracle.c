@@ -60,6 +60,18 @@ void or_partition(int64_t n, int64_t parts, int64_t p, int64_t *lo, int64_t *hi)
   *hi = ((p + 1) * n) / parts;
 }
 
+/* OpenMP over output rows (the oracle is timed single-thread and on all cores).
+ * Every parallelised loop writes disjoint outputs, each computed exactly as in the serial loop
+ * (same operands, same order), so results do not depend on the thread count; built without
+ * -fopenmp the pragmas vanish. */
+#ifdef _OPENMP
+#define OR_PARALLEL_ROWS _Pragma("omp parallel for schedule(static)")
+#define OR_PARALLEL_ROWS2 _Pragma("omp parallel for collapse(2) schedule(static)")
+#else
+#define OR_PARALLEL_ROWS
+#define OR_PARALLEL_ROWS2
+#endif
+
 /* ------------------------------------------------------------------ */
 /* Philox4x32-10 (Random123).  10 rounds; key schedule bumped between rounds. */
 static void or_mulhilo(uint32_t a, uint32_t b, uint32_t *hi, uint32_t *lo) {
@@ -118,6 +130,7 @@ void or_normal_field(uint64_t seed, uint32_t t1, int32_t ny, int32_t nx, uint32_
 void or_conv_fwd(const double *x, int32_t ny, int32_t nx, const double *k, int32_t kh, int32_t kw,
                  double *out) {
   int ry = kh / 2, rx = kw / 2;
+  OR_PARALLEL_ROWS
   for (int i = 0; i < ny; i++)
     for (int j = 0; j < nx; j++) {
       double s = 0.0;
@@ -136,6 +149,7 @@ void or_conv_fwd(const double *x, int32_t ny, int32_t nx, const double *k, int32
 void or_conv_adj(const double *r, int32_t ny, int32_t nx, const double *k, int32_t kh, int32_t kw,
                  double *out) {
   int ry = kh / 2, rx = kw / 2;
+  OR_PARALLEL_ROWS
   for (int i = 0; i < ny; i++)
     for (int j = 0; j < nx; j++) {
       double s = 0.0;
@@ -193,6 +207,7 @@ int or_dncnn_residual_c(const double *x, int32_t ny, int32_t nx, int32_t C, int3
   const float *bb = biases;
   for (int k = 1; k <= n_layers; k++) {
     int cout = (k == n_layers) ? C : P;
+    OR_PARALLEL_ROWS2
     for (int co = 0; co < cout; co++)
       for (int i = 0; i < ny; i++)
         for (int j = 0; j < nx; j++) {
@@ -242,6 +257,7 @@ int or_dncnn_residual(const double *x, int32_t ny, int32_t nx, int32_t n_layers,
  * v and p at every W_k input; u after u0 and after every T_k.  Accumulation stays fp64. */
 static void or_ddfb_w(const double *v, int ny, int nx, int P, const float *w, double scale, int emul, double *out) {
   int64_t npx = (int64_t)ny * nx;
+  OR_PARALLEL_ROWS2
   for (int c = 0; c < P; c++)
     for (int i = 0; i < ny; i++)
       for (int j = 0; j < nx; j++) {
@@ -262,6 +278,7 @@ static void or_ddfb_w(const double *v, int ny, int nx, int P, const float *w, do
 
 static void or_ddfb_wadj(const double *a, int ny, int nx, int P, const float *w, double scale, int emul, double *out) {
   int64_t npx = (int64_t)ny * nx;
+  OR_PARALLEL_ROWS
   for (int i = 0; i < ny; i++)
     for (int j = 0; j < nx; j++) {
       double s = 0.0;
@@ -501,6 +518,7 @@ static int or_step_plane(const or_config *c, const double *k, const double *yd, 
       }
     free(dv); free(dh); free(dt);
   } else {
+  OR_PARALLEL_ROWS
   for (int64_t i = 0; i < ny; i++)
     for (int64_t j = 0; j < nx; j++) {
       int64_t n = i * nx + j;
@@ -670,6 +688,7 @@ static int or_step_tiled(const or_config *c, const double *k, const double *yd, 
           int cout = (kk == K) ? 1 : P;
           int ext = K - kk;
           memset(B, 0, sizeof(double) * (size_t)plane * P);
+          OR_PARALLEL_ROWS2
           for (int co = 0; co < cout; co++)
             for (int a = h - ext; a < h + th + ext; a++)
               for (int b = h - ext; b < h + tw + ext; b++) {

@@ -106,6 +106,7 @@ def load():
         "pnpula_kernel_time": ([vp, C.c_char_p, C.POINTER(d), C.POINTER(i64), i32], C.c_int),
         "pnpula_destroy": ([vp], C.c_int),
         "pnpula_release_memory": ([i32], C.c_int),
+        "pnpula_debug_philox": ([i32, u64, vp, i64, vp, vp], C.c_int),
         "pnpula_partition": ([i64, i64, i64, C.POINTER(i64), C.POINTER(i64)], None),
         "pnpula_halo_width": ([i32, i32, i32, i32], i32),
         "pnpula_plan_halo": ([i32, i32, i32, i32, i32, C.POINTER(HaloMsg), i32], i32),
@@ -126,7 +127,7 @@ EXPORTED = ["pnpula_version", "pnpula_last_error", "pnpula_get_unique_id", "pnpu
             "pnpula_set_timing", "pnpula_kernel_time", "pnpula_destroy", "pnpula_partition",
             "pnpula_halo_width", "pnpula_plan_halo", "pnpula_check_stepsizes", "pnpula_checkpoint_bytes",
             "pnpula_save_checkpoint", "pnpula_load_checkpoint", "pnpula_conv_norm2_bound", "pnpula_opnorm2",
-            "pnpula_release_memory"]
+            "pnpula_release_memory", "pnpula_debug_philox"]
 
 
 def last_error() -> str:
@@ -178,6 +179,17 @@ def pnpula_conv_norm2_bound(k, grid: int = 256) -> float:
     out = C.c_double()
     check(load().pnpula_conv_norm2_bound(kk.ctypes.data, kk.shape[0], kk.shape[1], grid, C.byref(out)))
     return out.value
+
+
+def pnpula_debug_philox(seed: int, counters, device: int = 0):
+    """Test hook: raw Philox4x32-10 words and the four Box-Muller normals of each counter row
+    (column quad, row, t+1, stream), computed on the GPU by the update kernels' own functions."""
+    c = np.ascontiguousarray(counters, dtype=np.uint32).reshape(-1, 4)
+    words = np.zeros_like(c)
+    normals = np.zeros(c.shape, dtype=np.float32)
+    check(load().pnpula_debug_philox(device, seed, c.ctypes.data, c.shape[0], words.ctypes.data,
+                                     normals.ctypes.data))
+    return words, normals
 
 
 def pnpula_get_unique_id() -> bytes:

@@ -163,6 +163,9 @@ cudaError_t launch_tv_z_update(const TvZParams &p, cudaStream_t s);
 cudaError_t launch_copy_jobs(const CopyJob *d_jobs, int njobs, int max_rows, cudaStream_t s);
 cudaError_t launch_fill(float *p, float v, size_t n, cudaStream_t s);
 cudaError_t launch_finalize(const FinalizeParams &p, cudaStream_t s);
+// test hook: raw Philox words + normals of n counters (device arrays, n x 4 each)
+cudaError_t launch_debug_philox(uint64_t seed, const uint32_t *d_ctr, int64_t n, uint32_t *d_words, float *d_normals,
+                                int *d_bad, cudaStream_t s);
 cudaError_t launch_cnn_chunk(const CnnChunkParams &p, int num_sms, cudaStream_t s);
 size_t cnn_chunk_smem_bytes(int P, int nl, int first_is_input, int last_is_output, int nc);
 // Pack host fp32 OIHW weights of one layer into the device B-operand image (host side).

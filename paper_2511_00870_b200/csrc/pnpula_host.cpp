@@ -122,6 +122,8 @@ struct pnpula_ctx {
   // device scratch reused by the result gathers (no cudaMalloc/cudaFree per call)
   void *scratch = nullptr;
   size_t scratch_bytes = 0;
+  void *gather_buf = nullptr;   // root: remote tiles of a GLOBAL_ON_ROOT gather (grown on demand)
+  size_t gather_bytes = 0;
 
   // timing
   bool timing = false;
@@ -503,7 +505,7 @@ pnpula_status enqueue_step(pnpula_ctx *c, int buf, const IterState *it) {
     return PNPULA_OK;
   };
   pnpula_status s;
-  if (c->overlap && !it) {
+  if (c->overlap) {
     // boundary bands (the rows neighbours receive) first, then the exchange on the comm stream
     // while the interior rows update (SURVEY 8(e) overlap); the next kernels wait for both
     if ((s = update_rows(false, true, false)) || (s = update_rows(false, false, false))) return s;
@@ -589,9 +591,13 @@ void drop_graphs(pnpula_ctx *c) {
 }
 
 // Replays are used when nothing in the iteration needs the host between kernels: no per-kernel
-// timing events, no pipeline trace, no NCCL messages (single rank, device-copy exchange).
+// timing events and no pipeline trace.  The NCCL halo group (multi-rank, or FLAG_HALO_VIA_NCCL)
+// is captured into the graph like the kernels around it (NCCL supports stream capture); with the
+// overlap the comm stream forks from / joins the capturing stream through ev_bands / ev_halo, so
+// the replayed graph keeps the exchange concurrent with the interior update.  Every rank
+// captures the same sequence of NCCL calls per parity, so the replays stay matched across ranks.
 bool graph_eligible(const pnpula_ctx *c) {
-  return c->warm && !c->graphs_off && !c->timing && c->sends.empty() && c->recvs.empty() && !getenv("PNPULA_CNN_TRACE");
+  return c->warm && !c->graphs_off && !c->timing && !getenv("PNPULA_CNN_TRACE");
 }
 
 pnpula_status step(pnpula_ctx *c) {
@@ -967,6 +973,12 @@ pnpula_status pnpula_create(const pnpula_config *cfg, pnpula_ctx **out) {
     return bail(PNPULA_E_CUDA);
   }
   c->num_sms = n_sms;
+  {
+    // test hook: cap the CNN grid (persistent CTAs) so that small images give every CTA several
+    // work units -- exercises the cross-unit barrier-phase bookkeeping of the tcgen05 pipeline
+    const char *mc = getenv("PNPULA_MAX_CTAS");
+    if (mc && atoi(mc) > 0) c->num_sms = std::min(n_sms, atoi(mc));
+  }
   if (f.stream) {
     c->stream = (cudaStream_t)(uintptr_t)f.stream;
   } else {
@@ -1271,15 +1283,6 @@ namespace {
 pnpula_status gather_fields(pnpula_ctx *c, const std::vector<float *> &d_tile_bufs, int nf,
                             const std::vector<float *> &host_out, const pnpula_rect &dst_rect, bool global) {
   const int per_rank = c->ntiles / c->world;
-  auto place = [&](const pnpula_rect &r, const std::vector<float> &h) {
-    for (int f = 0; f < nf; ++f) {
-      float *o = host_out[f];
-      if (!o) continue;
-      for (int a = 0; a < r.h; ++a)
-        memcpy(o + (size_t)(r.i0 - dst_rect.i0 + a) * dst_rect.w + (r.j0 - dst_rect.j0),
-               h.data() + (size_t)f * r.h * r.w + (size_t)a * r.w, (size_t)r.w * sizeof(float));
-    }
-  };
   // own tiles: one strided device -> host copy per field straight into the caller's buffer
   // (full-rate DMA when the buffer is pinned; no staging vector, no per-row memcpy)
   for (int li = 0; li < c->n_local; ++li) {
@@ -1294,30 +1297,62 @@ pnpula_status gather_fields(pnpula_ctx *c, const std::vector<float *> &d_tile_bu
                               cudaMemcpyDeviceToHost, c->stream));
     }
   }
-  CU(c, cudaStreamSynchronize(c->stream));
-  if (!global || c->world == 1) return PNPULA_OK;
-  // remote tiles -> rank 0
+  if (!global || c->world == 1) {
+    CU(c, cudaStreamSynchronize(c->stream));
+    return PNPULA_OK;
+  }
+  // remote tiles -> rank 0: one NCCL group of receives into a device buffer that lives in the
+  // context's gather area (grown once, reused by later calls), then one strided D2H copy per
+  // tile and field straight into the caller's buffer (DMA at full rate when it is pinned), one
+  // synchronisation at the end.  Senders group their tiles the same way.
   if (c->rank == 0) {
+    size_t total = 0;
     for (int t = per_rank; t < c->ntiles; ++t) {
       pnpula_rect r;
       tile_rect(c->ny, c->nx, c->tiles_y, c->tiles_x, t, &r);
-      size_t cnt = (size_t)r.h * r.w * nf;
-      float *d = nullptr;
-      CU(c, cudaMalloc(&d, cnt * sizeof(float)));
-      NC(c, ncclRecv(d, cnt, ncclFloat32, t / per_rank, c->comm, c->stream));
-      std::vector<float> h(cnt);
-      CU(c, cudaMemcpyAsync(h.data(), d, cnt * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
-      CU(c, cudaStreamSynchronize(c->stream));
-      CU(c, cudaFree(d));
-      place(r, h);
+      total += (size_t)r.h * r.w * nf;
+    }
+    if (total * sizeof(float) > c->gather_bytes) {
+      dfree(c, c->gather_buf);
+      c->gather_buf = nullptr;
+      c->gather_bytes = 0;
+      CU(c, dmalloc(c, &c->gather_buf, total * sizeof(float)));
+      c->gather_bytes = total * sizeof(float);
+    }
+    float *d = static_cast<float *>(c->gather_buf);
+    NC(c, ncclGroupStart());
+    size_t off = 0;
+    for (int t = per_rank; t < c->ntiles; ++t) {
+      pnpula_rect r;
+      tile_rect(c->ny, c->nx, c->tiles_y, c->tiles_x, t, &r);
+      const size_t cnt = (size_t)r.h * r.w * nf;
+      NC(c, ncclRecv(d + off, cnt, ncclFloat32, t / per_rank, c->comm, c->stream));
+      off += cnt;
+    }
+    NC(c, ncclGroupEnd());
+    off = 0;
+    for (int t = per_rank; t < c->ntiles; ++t) {
+      pnpula_rect r;
+      tile_rect(c->ny, c->nx, c->tiles_y, c->tiles_x, t, &r);
+      for (int f = 0; f < nf; ++f) {
+        float *o = host_out[f];
+        if (!o) continue;
+        CU(c, cudaMemcpy2DAsync(o + (size_t)(r.i0 - dst_rect.i0) * dst_rect.w + (r.j0 - dst_rect.j0),
+                                (size_t)dst_rect.w * sizeof(float), d + off + (size_t)f * r.h * r.w,
+                                (size_t)r.w * sizeof(float), (size_t)r.w * sizeof(float), r.h,
+                                cudaMemcpyDeviceToHost, c->stream));
+      }
+      off += (size_t)r.h * r.w * nf;
     }
   } else {
+    NC(c, ncclGroupStart());
     for (int li = 0; li < c->n_local; ++li) {
       const TileGeom &g = c->tiles[li].g;
       NC(c, ncclSend(d_tile_bufs[li], (size_t)g.th * g.tw * nf, ncclFloat32, 0, c->comm, c->stream));
     }
-    CU(c, cudaStreamSynchronize(c->stream));
+    NC(c, ncclGroupEnd());
   }
+  CU(c, cudaStreamSynchronize(c->stream));
   return PNPULA_OK;
 }
 
@@ -1384,8 +1419,15 @@ pnpula_status pnpula_get_moments(pnpula_ctx *c, float *mean, float *var, int64_t
   CU(c, cudaSetDevice(c->device));
   const int64_t n = std::max<int64_t>(0, c->t - c->burn_in);
   if (n_samples) *n_samples = n;
-  if ((mean && n < 1) || (var && n < 2)) { set_error("not enough post-burn-in samples (%lld)", (long long)n); return PNPULA_E_STATS_EMPTY; }
-  if (global && c->rank == 0 && c->world > 1 && ((mean && false) || false)) {}
+  // GLOBAL scope with several ranks is collective: every rank gathers both fields, and its
+  // outcome must not depend on which pointers a rank passes (non-root ranks pass NULL), or the
+  // root would return while the other ranks block in ncclSend.  n is identical on every rank.
+  const bool collective = global && c->world > 1;
+  if ((collective && n < 2) || (mean && n < 1) || (var && n < 2)) {
+    set_error("not enough post-burn-in samples (%lld)%s", (long long)n,
+              collective ? "; GLOBAL_ON_ROOT with several ranks needs n >= 2 on every rank" : "");
+    return PNPULA_E_STATS_EMPTY;
+  }
   std::vector<float *> bufs;
   s = tile_staging(c, 2, bufs);
   if (s) return s;
@@ -1502,8 +1544,7 @@ pnpula_status pnpula_load_checkpoint(pnpula_ctx *c, const void *buf, uint64_t by
   if (!buf || bytes < sizeof(CkptHeader)) { set_error("checkpoint buffer too small"); return PNPULA_E_INVALID_ARG; }
   CkptHeader h;
   memcpy(&h, buf, sizeof(h));
-  c->cur = 0;   // the restored x^t goes to buffer 0
-  const uint64_t need = ckpt_bytes(c);
+  const uint64_t need = ckpt_bytes(c);   // independent of c->cur
   if (h.magic != kCkptMagic || h.ny != c->ny || h.nx != c->nx || h.tiles_y != c->tiles_y || h.tiles_x != c->tiles_x ||
       h.rank != c->rank || h.world != c->world || h.n_local != c->n_local ||
       h.elems_total != (need - sizeof(CkptHeader)) / sizeof(float) ||
@@ -1513,6 +1554,10 @@ pnpula_status pnpula_load_checkpoint(pnpula_ctx *c, const void *buf, uint64_t by
   }
   if (bytes < need) { set_error("checkpoint truncated"); return PNPULA_E_INVALID_ARG; }
   CU(c, cudaSetDevice(c->device));
+  // every check passed: only now switch the live context (the restored x^t goes to buffer 0);
+  // a rejected blob leaves the chain exactly as it was
+  drop_graphs(c);
+  c->cur = 0;
   const float *src = reinterpret_cast<const float *>(static_cast<const char *>(buf) + sizeof(h));
   for (auto &td : c->tiles) {
     const size_t n = geom_elems(td.g) * c->nc;
@@ -1522,7 +1567,6 @@ pnpula_status pnpula_load_checkpoint(pnpula_ctx *c, const void *buf, uint64_t by
     }
   }
   CU(c, cudaStreamSynchronize(c->stream));
-  drop_graphs(c);
   c->t = h.t;
   c->burn_in = h.burn_in;
   c->seed = h.seed;
@@ -1691,6 +1735,33 @@ pnpula_status pnpula_kernel_time(pnpula_ctx *c, const char *name, double *ms, in
   return PNPULA_OK;
 }
 
+pnpula_status pnpula_debug_philox(int32_t device, uint64_t seed, const uint32_t *counters, int64_t n,
+                                  uint32_t *words, float *normals) {
+  if (!counters || !words || !normals || n < 0) { set_error("null argument / negative n"); return PNPULA_E_INVALID_ARG; }
+  if (n == 0) return PNPULA_OK;
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return fail_cuda(nullptr, e, "cudaSetDevice", __LINE__);
+  uint32_t *dc = nullptr, *dw = nullptr;
+  float *dn = nullptr;
+  int *dbad = nullptr;
+  const size_t b4 = (size_t)n * 4 * sizeof(uint32_t);
+  int bad = 0;
+  e = cudaMalloc(&dc, b4);
+  if (e == cudaSuccess) e = cudaMalloc(&dw, b4);
+  if (e == cudaSuccess) e = cudaMalloc(&dn, b4);
+  if (e == cudaSuccess) e = cudaMalloc(&dbad, sizeof(int));
+  if (e == cudaSuccess) e = cudaMemset(dbad, 0, sizeof(int));
+  if (e == cudaSuccess) e = cudaMemcpy(dc, counters, b4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = launch_debug_philox(seed, dc, n, dw, dn, dbad, nullptr);
+  if (e == cudaSuccess) e = cudaMemcpy(words, dw, b4, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(normals, dn, b4, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(&bad, dbad, sizeof(int), cudaMemcpyDeviceToHost);
+  cudaFree(dc); cudaFree(dw); cudaFree(dn); cudaFree(dbad);
+  if (e != cudaSuccess) return fail_cuda(nullptr, e, "pnpula_debug_philox", __LINE__);
+  if (bad) { set_error("normals4 and normals4x2 differ on %d counters", bad); return PNPULA_E_STATE; }
+  return PNPULA_OK;
+}
+
 pnpula_status pnpula_release_memory(int32_t device) {
   cudaMemPool_t p = device_pool(device);
   if (!p) { set_error("no memory pool for device %d", device); return PNPULA_E_INVALID_ARG; }
@@ -1712,6 +1783,7 @@ pnpula_status pnpula_destroy(pnpula_ctx *c) {
   for (auto p : c->d_w) cudaFree(p);
   for (auto p : c->d_b) cudaFree(p);
   dfree(c, c->scratch);
+  dfree(c, c->gather_buf);
   if (c->pool && c->stream) cudaStreamSynchronize(c->stream);
   cudaFree(c->ddfb_u0); cudaFree(c->ddfb_fin);
   for (auto p : c->ddfb_t) cudaFree(p);

@@ -1120,6 +1120,38 @@ cudaError_t launch_copy_jobs(const CopyJob *d_jobs, int njobs, int max_elems, cu
   return cudaGetLastError();
 }
 
+// Test hook (pnpula_debug_philox): the raw Philox4x32-10 words and the four Box-Muller normals of
+// counters ctr[i] = (column quad, row, t+1, stream) under key `seed`, computed by the very device
+// functions the update kernels call (normals4 / normals4x2); bad[0] counts counters whose
+// normals4 and normals4x2 results differ in any bit (they must not).
+__global__ void debug_philox_kernel(uint32_t seed_lo, uint32_t seed_hi, const uint4 *ctr, int64_t n, uint4 *words,
+                                    float4 *normals, int *bad) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 c = ctr[i];
+    words[i] = philox4x32_10(c, seed_lo, seed_hi);
+    float a[4], b[2][4];
+    normals4(seed_lo, seed_hi, c.x, c.y, c.z, c.w, a);
+    normals4x2(seed_lo, seed_hi, c.x, c.y, c.z, c.w, b);
+    normals[i] = make_float4(a[0], a[1], a[2], a[3]);
+    bool same = true;
+#pragma unroll
+    for (int l = 0; l < 4; ++l) same = same && __float_as_uint(a[l]) == __float_as_uint(b[0][l]);
+    if (!same) atomicAdd(bad, 1);
+  }
+}
+
+cudaError_t launch_debug_philox(uint64_t seed, const uint32_t *d_ctr, int64_t n, uint32_t *d_words, float *d_normals,
+                                int *d_bad, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  debug_philox_kernel<<<(unsigned)blocks, 256, 0, s>>>((uint32_t)seed, (uint32_t)(seed >> 32),
+                                                       reinterpret_cast<const uint4 *>(d_ctr), n,
+                                                       reinterpret_cast<uint4 *>(d_words),
+                                                       reinterpret_cast<float4 *>(d_normals), d_bad);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_fill(float *ptr, float v, size_t n, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   size_t blocks = (n + 255) / 256;

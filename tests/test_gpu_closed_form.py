@@ -74,3 +74,105 @@ def test_blur_chain_matches_the_closed_form():
     assert 0.5 < np.mean(z ** 2) < 1.6
     ratio = var.ravel() / Sigma_diag
     assert abs(ratio.mean() - 1) < 0.03
+
+
+# ---------------------------------------------------------------- BASELINE configs[3] at its own size
+def _probes_c4(n):
+    """~64 probe pixels of the 2048^2 C4 image: the 4 corners, 4 edge midpoints, both sides of the
+    7 seams of an 8 x 1 row-strip tiling (at 4 columns: 56), the centre -- in groups whose members
+    are >= 128 px apart (Chebyshev), so one linear solve per group gives every member's diagonal
+    entry (the inverse operators decay like 0.3^(d/4) here: < 1e-9 at 128 px)."""
+    pts = [(0, 0), (0, n - 1), (n - 1, 0), (n - 1, n - 1), (0, n // 2), (n - 1, n // 2), (n // 2, 0),
+           (n // 2, n - 1), (n // 2 + 64, n // 2 + 64)]
+    for k in range(1, 8):
+        r = k * n // 8
+        for col in (3, n // 3, 2 * n // 3, n - 4):
+            pts += [(r - 1, col), (r, col)]
+    groups = []
+    for p in pts:
+        for g in groups:
+            if all(max(abs(p[0] - q[0]), abs(p[1] - q[1])) >= 128 for q in g):
+                g.append(p)
+                break
+        else:
+            groups.append([p])
+    return pts, groups
+
+
+def test_c4_2048_blur_chain_matches_the_closed_form():
+    """BASELINE.json configs[3] / SURVEY 8(c) C4 row: 2048^2, 9 x 9 Gaussian blur (sigma_b = 2),
+    sigma^2 = 1e-2, lambda = 0.05, c = 0.5, gamma = 0.99/120, x0 = 0, burn-in 200, T = 5000, 4 seeds,
+    on one GPU in 8 x 1 row strips (the tiling of the 8-GPU run).  Closed forms by conjugate gradients
+    on the zero-boundary convolution (scipy.ndimage, no oracle): mu = P^-1 b over the whole image,
+    and at 65 probe pixels (corners, edges, both sides of every strip seam, centre)
+    var_i = e_i^T (P - gamma P^2 / 2)^-1 e_i and Var(mean_i) = (2 / (gamma T)) ||P^-1 e_i||^2."""
+    from scipy.ndimage import convolve1d, correlate1d
+    from scipy.sparse.linalg import LinearOperator, cg
+
+    n = 2048
+    ky, kx = synth.gaussian_factors(9, 2.0)
+    k2 = synth.outer(ky, kx)
+    s2, lam, c, gamma = 1e-2, 0.05, 0.5, 0.99 / 120
+    y = synth.observe_blur(n, n, k2, s2)
+    kyd, kxd = ky.astype(np.float64), kx.astype(np.float64)
+
+    def H(v):
+        return convolve1d(convolve1d(v, kyd, axis=0, mode="constant"), kxd, axis=1, mode="constant")
+
+    def Ht(v):
+        return correlate1d(correlate1d(v, kyd, axis=0, mode="constant"), kxd, axis=1, mode="constant")
+
+    def Pm(v):
+        v = v.reshape(n, n)
+        return (Ht(H(v)) / s2 + v / lam).ravel()
+
+    def Am(v):
+        pv = Pm(v)
+        return pv - gamma / 2 * Pm(pv)
+
+    P_op = LinearOperator((n * n, n * n), matvec=Pm, dtype=np.float64)
+    A_op = LinearOperator((n * n, n * n), matvec=Am, dtype=np.float64)
+    b = (Ht(y.astype(np.float64)) / s2 + c / lam).ravel()
+    mu, info = cg(P_op, b, rtol=1e-11, maxiter=500)
+    assert info == 0
+    mu = mu.reshape(n, n)
+    pts, groups = _probes_c4(n)
+    var_true, se_mean = {}, {}
+    for g in groups:
+        e = np.zeros(n * n)
+        for (i, j) in g:
+            e[i * n + j] = 1.0
+        w, info = cg(A_op, e, rtol=1e-11, maxiter=500)
+        assert info == 0
+        u, info = cg(P_op, e, rtol=1e-11, maxiter=500)
+        assert info == 0
+        w, u = w.reshape(n, n), u.reshape(n, n)
+        for (i, j) in g:
+            var_true[(i, j)] = w[i, j]
+            win = u[max(i - 64, 0):i + 65, max(j - 64, 0):j + 65]   # P^-1 e_i, separated from the others
+            se_mean[(i, j)] = np.sqrt(2 / (gamma * 5000) * np.sum(win ** 2))
+
+    T, burn = 5000, 200
+    zm, zv, ratio = [], [], []
+    for seed in (870, 871, 872, 873):
+        s = Sampler(ny=n, nx=n, y=y, kernel_sep=(ky, kx), sigma2=s2, gamma=gamma, lam=lam, c_lo=c, c_hi=c,
+                    tiles=(8, 1))
+        try:
+            s.run(T + burn, burn, seed)
+            mean, var, cnt = s.moments()
+        finally:
+            s.close()
+        assert cnt == T
+        # MMSE mean at every pixel: the chain mean is exactly mu in law (linear Gaussian ULA)
+        assert np.sqrt(np.mean((mean - mu) ** 2)) < 4 * np.mean(list(se_mean.values()))
+        for p in pts:
+            zm.append((mean[p] - mu[p]) / se_mean[p])
+            ratio.append(var[p] / var_true[p])
+    zm, ratio = np.array(zm), np.array(ratio)
+    # pooled z-test of the probe means (4 x 65 draws) and of the probe variances: the sample
+    # variance of a chain with integrated autocorrelation ~ 1/(gamma p_min) ~ 6 has relative
+    # standard error ~ sqrt(2 * 6 / T) = 5 %; the pooled mean of 260 ratios is within 1 +- 1 %
+    assert abs(zm.mean()) < 4 / np.sqrt(zm.size)
+    assert 0.7 < np.mean(zm ** 2) < 1.4
+    assert abs(ratio.mean() - 1) < 0.015, ratio.mean()
+    assert np.all(np.abs(ratio - 1) < 0.3)
