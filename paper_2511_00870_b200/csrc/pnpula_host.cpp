@@ -98,6 +98,7 @@ struct pnpula_ctx {
 
   // CNN
   std::vector<CnnChunk> chunks;
+  uint32_t w5_mask = 0;             // bit k-1: layer k uses the W5 accumulator scheme
   std::vector<uint16_t *> d_w;      // per layer packed weights
   std::vector<float *> d_b;         // per layer biases
   std::vector<std::vector<float>> h_b;   // host copies (passed to the CNN kernel as parameters)
@@ -334,6 +335,7 @@ pnpula_status run_cnn(pnpula_ctx *c, int buf) {
       p.nl = ch.nl;
       p.first_is_input = ch.l0 == 1;
       p.last_is_output = ch.l0 + ch.nl - 1 == c->n_layers;
+      p.w5_mask = (int)((c->w5_mask >> (ch.l0 - 1)) & ((1u << ch.nl) - 1u));
       for (int l = 0; l < ch.nl; ++l) {
         p.w[l] = c->d_w[ch.l0 - 1 + l];
         const std::vector<float> &hb = c->h_b[ch.l0 - 1 + l];
@@ -717,17 +719,33 @@ pnpula_status build_halo_plan(pnpula_ctx *c) {
   return PNPULA_OK;
 }
 
-// CNN chunking: greedy, as many consecutive layers per launch as shared memory allows.
+// Which layers accumulate in the W5 TMEM scheme (cnn_kernels.cu w5_slots): the windowed 3x3
+// layers 2..K-1 of a P = 32 net -- for colour nets (N = 48 folded last layer) all but the last two,
+// so that a 4-layer chain ending the net fits 512 TMEM columns.  A function of (K, P, C) only, so
+// every chunking (fused, layer-wise) and every tiling rounds each layer identically.  Env
+// PNPULA_W5=0 (read at create): the ring-4 scheme everywhere (kernel experiments).
+uint32_t w5_layers(const pnpula_ctx *c) {
+  const char *e = getenv("PNPULA_W5");
+  if ((e && atoi(e) == 0) || c->channels != 32) return 0;
+  uint32_t m = 0;
+  const int K = c->n_layers, hi = c->nc > 1 ? K - 3 : K - 1;
+  for (int k = 2; k <= hi; ++k) m |= 1u << (k - 1);
+  return m;
+}
+
+// CNN chunking: greedy, as many consecutive layers per launch as shared memory and TMEM allow.
 void plan_cnn_chunks(pnpula_ctx *c) {
   c->chunks.clear();
   const int K = c->n_layers;
   const size_t budget = 227 * 1024;
+  c->w5_mask = w5_layers(c);
   int l = 1;
   while (l <= K) {
     int best = 1;
     const int maxnl = (c->flags & PNPULA_FLAG_CNN_LAYERWISE) ? 1 : kMaxChunk;
     for (int nl = 1; nl <= std::min(maxnl, K - l + 1); ++nl) {
-      if (cnn_chunk_smem_bytes(c->channels, nl, l == 1, l + nl - 1 == K, c->nc) <= budget) best = nl;
+      const int wm = (int)((c->w5_mask >> (l - 1)) & ((1u << nl) - 1u));
+      if (cnn_chunk_smem_bytes(c->channels, nl, l == 1, l + nl - 1 == K, c->nc, wm) <= budget) best = nl;
     }
     c->chunks.push_back({l, best, K - (l + best - 1)});
     l += best;

@@ -94,7 +94,7 @@ def test_graph_replay_matches_oracle_and_survives_checkpoint_and_timing():
     np.testing.assert_array_equal(x_a, x_b)
     np.testing.assert_array_equal(z_a, z_b)
     o = oracle.run(pb, 9, 3, 77)
-    assert rel_l2(x_b, o["x"]) <= 1e-5 and rel_l2(mean, o["mean"]) <= 1e-5 and rel_l2(var, o["var"]) <= 1e-4
+    assert rel_l2(x_b, o["x"]) <= 1e-5 and rel_l2(mean, o["mean"]) <= 1e-5 and rel_l2(var, o["var"]) <= 1e-5  # R44
 
 
 def test_long_chain_graph_replay_and_overlap_agree():
@@ -110,3 +110,55 @@ def test_long_chain_graph_replay_and_overlap_agree():
     for k in ("x", "z", "mean", "var"):
         assert np.isfinite(a[0][k]).all(), k
     assert (a[0]["var"] > 0).all()
+
+
+@pytest.mark.parametrize("tiles", [(2, 1), (3, 1), (2, 2)])
+def test_graph_with_captured_nccl_halo_group_bitwise(tiles):
+    """The NCCL halo group captured inside the iteration graph (FLAG_HALO_VIA_NCCL: NCCL self
+    send/recv on one GPU, the code path of a multi-rank run), with the comm-stream fork/join of the
+    overlapped exchange on row strips: bitwise equal to direct launches and to the untiled chain,
+    across a reset with a new seed and burn-in."""
+    from paper_2511_00870_b200 import FLAG_HALO_VIA_NCCL
+    kw, _ = make_problem(96, 70, kernel="gauss9", cnn=(8, 32), z=True)
+    plan = ((7, 2, 11), (10, 4, 12))
+    g = _chain(kw, FLAG_HALO_VIA_NCCL, tiles=tiles, plan=plan)
+    d = _chain(kw, FLAG_HALO_VIA_NCCL | FLAG_NO_GRAPH, tiles=tiles, plan=plan)
+    _assert_same(g, d)
+    assert g[2] == d[2]
+    _assert_same(g, _chain(kw, 0, plan=plan))
+
+
+@pytest.mark.parametrize("corrupt", ["magic", "truncated", "geometry"])
+def test_rejected_checkpoint_leaves_the_chain_untouched(corrupt):
+    """A blob that pnpula_load_checkpoint rejects (wrong magic / truncated / another geometry) must
+    not switch the live context's buffers: the chain continues bit for bit as if the
+    call had not happened, also when the current x^t lives in buffer 1 (odd t) and graphs replay."""
+    kw, _ = make_problem(45, 52, kernel="gauss5", cnn=(4, 16), z=True)
+    ref = Sampler(**kw)
+    ref.run(9, 2, 5)
+    want = ref.state()
+    ref.close()
+    s = Sampler(**kw)
+    try:
+        s.reset(2, 5)
+        s.advance(5)                 # odd t: x^t in buffer 1
+        blob = bytearray(s.save_checkpoint())
+        if corrupt == "magic":
+            blob[0] ^= 0xFF
+        elif corrupt == "truncated":
+            blob = blob[:-4]
+        else:
+            kw2, _ = make_problem(45, 60, kernel="gauss5", cnn=(4, 16), z=True)
+            other = Sampler(**kw2)
+            other.reset(2, 5)
+            blob = bytearray(other.save_checkpoint())
+            other.close()
+        with pytest.raises(Exception):
+            s.load_checkpoint(bytes(blob))
+        s.advance(4)
+        got = s.state()
+    finally:
+        s.close()
+    np.testing.assert_array_equal(got[0], want[0])
+    np.testing.assert_array_equal(got[1], want[1])
+    assert got[2] == want[2] == 9

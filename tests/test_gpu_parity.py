@@ -22,10 +22,14 @@ def test_noise_matches_oracle():
         for seed, t in [(870, 1), (2 ** 40 + 3, 3)]:
             s.run(t, 0, seed)
             x, _, _ = s.state()
-            # x^1 = sqrt(2*0.5) xi^1 exactly; x^t = sum of t normals
-            want = sum(oracle.normal_field(seed, k, ny, nx, 0) for k in range(1, t + 1))
+            # x^1 = sqrt(2*0.5) xi^1 exactly; x^t = sum of t normals.  Bound: reading R45 per normal
+            # (1.2e-6 rho + 1e-7, rho = the Box-Muller radius of the lane pair) + fp32 summation
+            fields = [oracle.normal_field(seed, k, ny, nx + 2, 0) for k in range(1, t + 1)]
+            want = sum(f[:, :nx] for f in fields)
+            rho = [np.sqrt(f[:, (np.arange(nx) & ~1)] ** 2 + f[:, (np.arange(nx) | 1)] ** 2) for f in fields]
+            bound = sum(1.2e-6 * r + 1e-7 for r in rho) + t * 6e-8 * sum(np.abs(f[:, :nx]) for f in fields)
             err = np.abs(x - want)
-            assert np.all(err <= 4e-6 * t + 2e-6 * np.abs(want)), err.max()
+            assert np.all(err <= bound), (err / bound).max()
     finally:
         s.close()
 
@@ -46,7 +50,7 @@ def test_chain_50_fp32(kernel, z):
     o = oracle.run(pb, 50, 10, 870)
     assert rel_l2(g["x"], o["x"]) <= 1e-5
     assert rel_l2(g["mean"], o["mean"]) <= 1e-5
-    assert rel_l2(g["var"], o["var"]) <= 1e-4
+    assert rel_l2(g["var"], o["var"]) <= 1e-5   # SURVEY A16; conditioning: DESIGN.md R44
     if z:
         assert rel_l2(g["z"], o["z"]) <= 1e-5
 

@@ -63,7 +63,7 @@ def test_poisson_chain_fp32_path_vs_oracle(kernel, shape):
     assert rel_l2(g["z"], o["z"]) <= 1e-5
     assert rel_l2(g["z1"], o["z1"]) <= 1e-5
     assert rel_l2(g["mean"], o["mean"]) <= 1e-5
-    assert rel_l2(g["var"], o["var"]) <= 1e-4
+    assert rel_l2(g["var"], o["var"]) <= 1e-5   # SURVEY A16; conditioning: DESIGN.md R44
     assert np.all(g["z1"] >= 0) and np.all(g["z"] >= 0)
 
 

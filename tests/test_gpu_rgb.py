@@ -103,7 +103,7 @@ def test_colour_chain_fp32_path(op, kernel):
     for k in keys:
         assert g[k].shape == (3, 53, 61)
         assert rel_l2(g[k], o[k]) <= 1e-5, k
-    assert rel_l2(g["var"], o["var"]) <= 1e-4
+    assert rel_l2(g["var"], o["var"]) <= 1e-5   # SURVEY A16; conditioning: DESIGN.md R44
 
 
 def test_colour_chain_with_cnn():

@@ -62,7 +62,7 @@ def test_tv_chain_fp32_path_vs_oracle(op, kernel, shape):
     o = oracle.run(pb, 50, 10, seed=872)
     for k in ("x", "z", "zh", "mean"):
         assert rel_l2(g[k], o[k]) <= 1e-5, k
-    assert rel_l2(g["var"], o["var"]) <= 1e-4
+    assert rel_l2(g["var"], o["var"]) <= 1e-5   # SURVEY A16; conditioning: DESIGN.md R44
     assert np.all(g["x"] >= 0)
 
 
