@@ -95,6 +95,8 @@ def _load():
         _lib.or_prox_l21.argtypes = [d, d, d, C.POINTER(d), C.POINTER(d)]
         _lib.or_ddfb_residual.argtypes = [vp, i32, i32, i32, i32, vp, vp, d, i32, vp]
         _lib.or_ddfb_residual.restype = C.c_int
+        _lib.or_ddfb_residual_c.argtypes = [vp, i32, i32, i32, i32, i32, vp, vp, d, i32, vp]
+        _lib.or_ddfb_residual_c.restype = C.c_int
         _lib.or_ddfb_param_count.argtypes = [i32, i32, i32]
         _lib.or_ddfb_param_count.restype = i64
     return _lib
@@ -176,12 +178,14 @@ def dncnn_residual(x, weights, biases, n_layers: int, channels: int, bf16_emulat
 
 
 def ddfb_residual(x, weights, gammas, n_layers: int, channels: int, ht_eps: float, bf16_emulate: bool = False):
-    """G = v - D(v) for the DDFB denoiser (eq:ddfb_operator, eq:dfb_operator:T; readings R39-R42)."""
+    """G = v - D(v) for the DDFB denoiser (eq:ddfb_operator, eq:dfb_operator:T; readings R39-R42);
+    x: [ny][nx], or [C][ny][nx] with weights [K][P][C][3][3] (colour, P:387)."""
     x = _f64(x)
     w, g = _f32(weights), _f32(gammas)
     G = np.zeros_like(x)
-    e = _load().or_ddfb_residual(x.ctypes.data, x.shape[0], x.shape[1], n_layers, channels, w.ctypes.data,
-                                 g.ctypes.data, ht_eps, int(bf16_emulate), G.ctypes.data)
+    nc = x.shape[0] if x.ndim == 3 else 1
+    e = _load().or_ddfb_residual_c(x.ctypes.data, x.shape[-2], x.shape[-1], nc, n_layers, channels,
+                                   w.ctypes.data, g.ctypes.data, ht_eps, int(bf16_emulate), G.ctypes.data)
     if e:
         raise ValueError("or_ddfb_residual failed")
     return G

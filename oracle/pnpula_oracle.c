@@ -25,8 +25,11 @@
  *                       z-update eq:sgs_pnp_ula_psgla:psgla, online moments
  *   or_run (tiles>1)    same chain, every tile computed from its own padded copy S_b x
  *                       (Def. prop:localselection P:135-152, ghost regions P:494-498)
- *   or_ddfb_residual    DDFB denoiser G = v - D(v) (Example sec:denoiser:cnn:ddfb, eq:ddfb_operator
- *                       P:382-385, eq:dfb_operator:T P:390-393), C = 1 (readings R39-R42)
+ *   or_ddfb_residual_c  DDFB denoiser G = v - D(v) (Example sec:denoiser:cnn:ddfb, eq:ddfb_operator
+ *                       P:382-385, eq:dfb_operator:T P:390-393) for C image channels: W_k : C -> P,
+ *                       W_k^* : P -> C (readings R39-R42, R43)
+ *   or_run (C = 3)      colour images (reading R43): planes; H / mask / box / z blocks / TV per
+ *                       channel (TV: channel-wise isotropic ||.||_{2,1}, D acting per plane)
  *   or_check_stepsizes  eq:stepsize_cond P:581-587 (reading R11: ||H2||^2 -> ||H2||^2/rho)
  *   or_prox_kl          prox of kappa KL(y || .) for the Poisson likelihood (eq:poisson:f2 P:737-741;
  *                       closed form = the positive root of u^2 - (v - kappa) u - kappa y = 0, reading R31)
@@ -255,74 +258,84 @@ int or_dncnn_residual(const double *x, int32_t ny, int32_t nx, int32_t n_layers,
  * bf16_emulate rounds at the GPU's points (R41): the conv weights as bf16(w_K) in u0 = W_K v,
  * bf16(gamma_k w_k) in T_k, bf16(w_k) in W_k^* (k < K), bf16(gamma_K w_K) in the final adjoint;
  * v and p at every W_k input; u after u0 and after every T_k.  Accumulation stays fp64. */
-static void or_ddfb_w(const double *v, int ny, int nx, int P, const float *w, double scale, int emul, double *out) {
+static void or_ddfb_w(const double *v, int ny, int nx, int C, int P, const float *w, double scale, int emul,
+                      double *out) {
+  /* (W v)_p[i,j] = sum_c sum_{u,q=-1..1} w[p][c][u+1][q+1] v_c[i+u][j+q]   (C -> P) */
   int64_t npx = (int64_t)ny * nx;
   OR_PARALLEL_ROWS2
   for (int c = 0; c < P; c++)
     for (int i = 0; i < ny; i++)
       for (int j = 0; j < nx; j++) {
         double s = 0.0;
-        for (int u = -1; u <= 1; u++)
-          for (int q = -1; q <= 1; q++) {
-            int ii = i + u, jj = j + q;
-            if (ii < 0 || ii >= ny || jj < 0 || jj >= nx) continue;
-            double wt = scale * (double)w[(c * 3 + (u + 1)) * 3 + (q + 1)];
-            if (emul) wt = or_bf16(wt);
-            double a = v[(int64_t)ii * nx + jj];
-            if (emul) a = or_bf16(a);
-            s += wt * a;
-          }
+        for (int ci = 0; ci < C; ci++)
+          for (int u = -1; u <= 1; u++)
+            for (int q = -1; q <= 1; q++) {
+              int ii = i + u, jj = j + q;
+              if (ii < 0 || ii >= ny || jj < 0 || jj >= nx) continue;
+              double wt = scale * (double)w[((c * C + ci) * 3 + (u + 1)) * 3 + (q + 1)];
+              if (emul) wt = or_bf16(wt);
+              double a = v[(int64_t)ci * npx + (int64_t)ii * nx + jj];
+              if (emul) a = or_bf16(a);
+              s += wt * a;
+            }
         out[(int64_t)c * npx + (int64_t)i * nx + j] = s;
       }
 }
 
-static void or_ddfb_wadj(const double *a, int ny, int nx, int P, const float *w, double scale, int emul, double *out) {
+static void or_ddfb_wadj(const double *a, int ny, int nx, int C, int P, const float *w, double scale, int emul,
+                         double *out) {
+  /* (W^* a)_c[i,j] = sum_p sum_{u,q} w[p][c][u+1][q+1] a_p[i-u][j-q]   (P -> C, the adjoint) */
   int64_t npx = (int64_t)ny * nx;
-  OR_PARALLEL_ROWS
-  for (int i = 0; i < ny; i++)
-    for (int j = 0; j < nx; j++) {
-      double s = 0.0;
-      for (int c = 0; c < P; c++)
-        for (int u = -1; u <= 1; u++)
-          for (int q = -1; q <= 1; q++) {
-            int ii = i - u, jj = j - q;
-            if (ii < 0 || ii >= ny || jj < 0 || jj >= nx) continue;
-            double wt = scale * (double)w[(c * 3 + (u + 1)) * 3 + (q + 1)];
-            if (emul) wt = or_bf16(wt);
-            s += wt * a[(int64_t)c * npx + (int64_t)ii * nx + jj];
-          }
-      out[(int64_t)i * nx + j] = s;
-    }
+  OR_PARALLEL_ROWS2
+  for (int ci = 0; ci < C; ci++)
+    for (int i = 0; i < ny; i++)
+      for (int j = 0; j < nx; j++) {
+        double s = 0.0;
+        for (int c = 0; c < P; c++)
+          for (int u = -1; u <= 1; u++)
+            for (int q = -1; q <= 1; q++) {
+              int ii = i - u, jj = j - q;
+              if (ii < 0 || ii >= ny || jj < 0 || jj >= nx) continue;
+              double wt = scale * (double)w[((c * C + ci) * 3 + (u + 1)) * 3 + (q + 1)];
+              if (emul) wt = or_bf16(wt);
+              s += wt * a[(int64_t)c * npx + (int64_t)ii * nx + jj];
+            }
+        out[(int64_t)ci * npx + (int64_t)i * nx + j] = s;
+      }
 }
 
 int64_t or_ddfb_param_count(int32_t K, int32_t P, int32_t C) { return (int64_t)K * P * C * 9; }
 
-/* in != NULL: only pixels with in[n] != 0 belong to the image (a worker's padded crop, reading
- * R8): u and p are zero elsewhere, exactly as the global image's zero boundary. */
-static int or_ddfb_masked(const double *v, int32_t ny, int32_t nx, int32_t K, int32_t P, const float *weights,
-                          const float *gammas, double ht_eps, int32_t emul, const uint8_t *in, double *G) {
-  if (K < 1 || P < 1) return OR_E_INVALID;
+/* C image channels (the colour DDFB of P:387: W_k : C -> P, W_k^* : P -> C; weights per layer
+ * [P][C][3][3], layers concatenated).  in != NULL: only pixels with in[n] != 0 belong to the
+ * image (a worker's padded crop, reading R8): u and p are zero elsewhere, exactly as the global
+ * image's zero boundary. */
+static int or_ddfb_masked(const double *v, int32_t ny, int32_t nx, int32_t C, int32_t K, int32_t P,
+                          const float *weights, const float *gammas, double ht_eps, int32_t emul, const uint8_t *in,
+                          double *G) {
+  if (K < 1 || P < 1 || C < 1) return OR_E_INVALID;
   int64_t npx = (int64_t)ny * nx;
+  int64_t lw = (int64_t)P * C * 9;   /* weights per layer */
   double *u = (double *)calloc((size_t)(npx * P), sizeof(double));
   double *t = (double *)calloc((size_t)(npx * P), sizeof(double));
-  double *a = (double *)calloc((size_t)npx, sizeof(double));
-  double *pp = (double *)calloc((size_t)npx, sizeof(double));
+  double *a = (double *)calloc((size_t)(npx * C), sizeof(double));
+  double *pp = (double *)calloc((size_t)(npx * C), sizeof(double));
   if (!u || !t || !a || !pp) { free(u); free(t); free(a); free(pp); return OR_E_INVALID; }
-  const float *wK = weights + (int64_t)(K - 1) * P * 9;
-  or_ddfb_w(v, ny, nx, P, wK, 1.0, emul, u);                      /* u0 = W_K v */
+  const float *wK = weights + (int64_t)(K - 1) * lw;
+  or_ddfb_w(v, ny, nx, C, P, wK, 1.0, emul, u);                   /* u0 = W_K v */
   for (int64_t n = 0; n < npx * P; n++) {
     if (emul) u[n] = or_bf16(u[n]);
     if (in && !in[n % npx]) u[n] = 0.0;
   }
   for (int k = 1; k <= K - 1; k++) {                               /* u <- T_k(u) */
-    const float *wk = weights + (int64_t)(k - 1) * P * 9;
-    or_ddfb_wadj(u, ny, nx, P, wk, 1.0, emul, a);
-    for (int64_t n = 0; n < npx; n++) {
+    const float *wk = weights + (int64_t)(k - 1) * lw;
+    or_ddfb_wadj(u, ny, nx, C, P, wk, 1.0, emul, a);
+    for (int64_t n = 0; n < npx * C; n++) {
       double q = v[n] - a[n];
       pp[n] = q < 0.0 ? 0.0 : (q > 1.0 ? 1.0 : q);                 /* proj_[0,1] */
-      if (in && !in[n]) pp[n] = 0.0;
+      if (in && !in[n % npx]) pp[n] = 0.0;
     }
-    or_ddfb_w(pp, ny, nx, P, wk, (double)gammas[k - 1], emul, t);
+    or_ddfb_w(pp, ny, nx, C, P, wk, (double)gammas[k - 1], emul, t);
     for (int64_t n = 0; n < npx * P; n++) {
       double q = u[n] + t[n];
       q = q < -ht_eps ? -ht_eps : (q > ht_eps ? ht_eps : q);      /* HT_eps */
@@ -330,8 +343,8 @@ static int or_ddfb_masked(const double *v, int32_t ny, int32_t nx, int32_t K, in
       if (in && !in[n % npx]) u[n] = 0.0;
     }
   }
-  or_ddfb_wadj(u, ny, nx, P, wK, (double)gammas[K - 1], emul, a);  /* gamma_K W_K^* u */
-  for (int64_t n = 0; n < npx; n++) {
+  or_ddfb_wadj(u, ny, nx, C, P, wK, (double)gammas[K - 1], emul, a);  /* gamma_K W_K^* u */
+  for (int64_t n = 0; n < npx * C; n++) {
     double q = v[n] - a[n];
     double d = q < 0.0 ? 0.0 : (q > 1.0 ? 1.0 : q);
     G[n] = v[n] - d;
@@ -340,9 +353,14 @@ static int or_ddfb_masked(const double *v, int32_t ny, int32_t nx, int32_t K, in
   return OR_OK;
 }
 
+int or_ddfb_residual_c(const double *v, int32_t ny, int32_t nx, int32_t C, int32_t K, int32_t P,
+                       const float *weights, const float *gammas, double ht_eps, int32_t emul, double *G) {
+  return or_ddfb_masked(v, ny, nx, C, K, P, weights, gammas, ht_eps, emul, NULL, G);
+}
+
 int or_ddfb_residual(const double *v, int32_t ny, int32_t nx, int32_t K, int32_t P, const float *weights,
                      const float *gammas, double ht_eps, int32_t emul, double *G) {
-  return or_ddfb_masked(v, ny, nx, K, P, weights, gammas, ht_eps, emul, NULL, G);
+  return or_ddfb_masked(v, ny, nx, 1, K, P, weights, gammas, ht_eps, emul, NULL, G);
 }
 
 /* ------------------------------------------------------------------ */
@@ -569,8 +587,8 @@ static int or_step_global(const or_config *c, const double *k, const double *yd,
   const int64_t npx = (int64_t)c->ny * c->nx;
   if (c->n_layers > 0 && c->alpha != 0.0) {
     int e = c->den_kind == 1
-                ? or_ddfb_residual(x, c->ny, c->nx, c->n_layers, c->channels, c->weights, c->ddfb_gammas,
-                                   c->ht_eps, c->bf16_emulate, G)
+                ? or_ddfb_residual_c(x, c->ny, c->nx, nc, c->n_layers, c->channels, c->weights, c->ddfb_gammas,
+                                     c->ht_eps, c->bf16_emulate, G)
                 : or_dncnn_residual_c(x, c->ny, c->nx, nc, c->n_layers, c->channels, c->weights, c->biases,
                                       c->bf16_emulate, G);
     if (e) return e;
@@ -666,7 +684,7 @@ static int or_step_tiled(const or_config *c, const double *k, const double *yd, 
             int64_t gi = i0 - h + a, gj = j0 - h + b;
             inm[(int64_t)a * pw + b] = (gi >= 0 && gi < ny && gj >= 0 && gj < nx) ? 1 : 0;
           }
-        int e = or_ddfb_masked(xp, ph, pw, c->n_layers, c->channels, c->weights, c->ddfb_gammas, c->ht_eps,
+        int e = or_ddfb_masked(xp, ph, pw, 1, c->n_layers, c->channels, c->weights, c->ddfb_gammas, c->ht_eps,
                                c->bf16_emulate, inm, Gp);
         for (int a = 0; a < th; a++)
           for (int b = 0; b < tw; b++) Gl[(int64_t)a * tw + b] = Gp[(int64_t)(a + h) * pw + (b + h)];
@@ -834,7 +852,7 @@ int or_run_ex(const or_config *c, double *x_out, double *z_out, double *z1_out, 
   if (c->tv_beta > 0.0 && (!(c->rho > 0.0) || (c->n_layers > 0 && c->alpha != 0.0) || c->lambda > 0.0))
     return OR_E_INVALID;   /* TV: z block on (the TV block), no CNN, no box term; any likelihood */
   const int nc = or_nchan(c);
-  if (nc > 1 && (c->tiles_y > 1 || c->tiles_x > 1 || c->tv_beta > 0.0 || c->den_kind == 1)) return OR_E_INVALID;
+  if (nc > 1 && (c->tiles_y > 1 || c->tiles_x > 1)) return OR_E_INVALID;   /* tiled mode: C = 1 */
   int64_t npx = (int64_t)c->ny * c->nx * nc;   /* all C planes */
   double *k = (double *)calloc((size_t)(c->kh > 0 ? c->kh * c->kw : 1), sizeof(double));
   double *yd = (double *)malloc(sizeof(double) * (size_t)npx);

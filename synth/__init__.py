@@ -280,14 +280,16 @@ def linear_cnn_weights(n_layers: int, channels: int, theta: float, shift: float 
     return np.concatenate(ws), np.concatenate(bs)
 
 
-def ddfb_weights(n_layers: int, channels: int, seed: int = WEIGHT_SEED + 1, ht_eps: float = 0.05):
-    """Random-init DDFB weights (Example sec:denoiser:cnn:ddfb, C = 1): K operators W_k : 1 -> P
-    (3x3, fp32 [P][1][3][3] concatenated), steps gamma_k = 1.8 / ||W_k||^2 inside (0, 2/||W_k||^2)
-    (SPEC S:327), and the hard-tanh level."""
+def ddfb_weights(n_layers: int, channels: int, seed: int = WEIGHT_SEED + 1, ht_eps: float = 0.05,
+                 image_channels: int = 1):
+    """Random-init DDFB weights (Example sec:denoiser:cnn:ddfb): K operators W_k : C -> P
+    (3x3, fp32 [P][C][3][3] concatenated; C = image_channels), steps gamma_k = 1.8 / ||W_k||^2
+    inside (0, 2/||W_k||^2), and the hard-tanh level."""
     rng = np.random.default_rng(seed)
     ws, gs = [], []
+    bound = 1.0 / np.sqrt(9.0 * image_channels)
     for _ in range(n_layers):
-        w = rng.uniform(-1.0 / 3.0, 1.0 / 3.0, size=(channels, 1, 3, 3))
+        w = rng.uniform(-bound, bound, size=(channels, image_channels, 3, 3))
         nrm = _conv_spectral_norm(w)
         ws.append(w.astype(np.float32).ravel())
         gs.append(np.float32(1.8 / nrm ** 2))

@@ -127,7 +127,7 @@ def test_rgb_poisson_z1_block_per_channel():
         np.testing.assert_allclose(out["z1"][c], z1, rtol=0, atol=1e-11)
 
 
-def test_rgb_rejects_tiles_and_tv():
+def test_rgb_rejects_tiles():
     pb, _ = _rgb_problem(12, 12)
     with pytest.raises(ValueError):
         oracle.run(pb, 1, 0, 1, tiles=(2, 1))
