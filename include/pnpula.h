@@ -95,7 +95,8 @@ typedef struct {
   int32_t channels;      /* P, one of 16, 32, 64 */
   const float *weights;  /* host; DnCNN: OIHW per layer, layers concatenated:
                             [P][1][3][3], (K-2) x [P][P][3][3], [1][P][3][3];
-                            DDFB: K x [P][1][3][3] (W_k : 1 -> P, PyTorch conv2d convention) */
+                            DDFB: K x [P][C][3][3] (W_k : C -> P, PyTorch conv2d convention;
+                            C = img_channels) */
   const float *biases;   /* host; DnCNN: P per layer for layers 1..K-1, then 1; DDFB: unused */
   int32_t kind;          /* PNPULA_DEN_DNCNN (0) or PNPULA_DEN_DDFB */
   const float *ddfb_gammas;  /* DDFB: K steps gamma_k in (0, 2/||W_k||^2) */
@@ -163,7 +164,8 @@ typedef struct {
    * the mask is one plane shared by the channels.  H, the box and the z blocks act on each
    * channel; the DnCNN's first layer is C -> P and its last P -> C (weights OIHW as for C = 1,
    * with I = C / O = C; needs channels P >= 32).  Channel c draws Philox streams 4c + s.
-   * Not with the TV prior or the DDFB denoiser (E_UNSUPPORTED). */
+   * DDFB: W_k : C -> P and W_k^* : P -> C (P = 32 or 64).  TV: channel-wise isotropic
+   * ||.||_{2,1} (D acts on every plane), z_v / z_h have C planes. */
   int32_t img_channels;
 } pnpula_config;
 
@@ -228,7 +230,7 @@ pnpula_status pnpula_get_state(pnpula_ctx *ctx, float *x, float *z, int64_t *t, 
 pnpula_status pnpula_get_z1(pnpula_ctx *ctx, float *z1, int32_t scope);
 
 /* [collective for GLOBAL scope] TV prior: the horizontal component z_h of z ~ D x (z_v is the z of
- * pnpula_get_state). */
+ * pnpula_get_state); C planes for colour images, like every per-pixel output. */
 pnpula_status pnpula_get_tv_zh(pnpula_ctx *ctx, float *zh, int32_t scope);
 
 /* Checkpoint / resume.  The blob holds this rank's complete chain state:

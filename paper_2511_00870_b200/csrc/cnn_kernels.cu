@@ -129,28 +129,28 @@ __host__ __device__ inline SmemLayout make_layout(int P, int nl, int first, int 
 }
 
 // TMEM accumulator plan of one chain (columns of the 512-column allocation).  Per layer:
-//  * im2col layer (C -> P, one N = P MMA per row, accumulate = 0): S slots of P columns, S = 1..4
-//    (whatever TMEM the other layers leave; the result does not depend on S);
+//  * im2col layer (C -> P, one N = P MMA per row, accumulate = 0): S slots of P columns, S = 1, 2
+//    or 4 (whatever TMEM the other layers leave; the result does not depend on S);
 //  * windowed 3x3 layer, "ring-4" scheme: 4 row slots of P columns (slot = row mod 4); a fill whose
 //    three output rows wrap the ring issues two MMAs (N = 2P + P or P + 2P);
-//  * windowed layer, "W5" scheme (bit l of w5_mask): 5 slots of P columns, never split -- see
-//    w5_slots() below;
+//  * windowed layer, "wide" scheme (bit l of wmask): W = 5 or 6 slots of P columns, never split --
+//    see wide_slots() below;
 //  * folded P -> C last layer: 2 per-fill slots of 16 C columns.
 // Returns the total columns (> 512: the chain does not fit), fills base[] / nslots[].
-__host__ __device__ inline uint32_t tmem_plan(int P, int nl, int first, int last, int nc, int w5_mask,
+__host__ __device__ inline uint32_t tmem_plan(int P, int nl, int first, int last, int nc, int wmask, int W,
                                               uint32_t *base, uint32_t *nslots) {
   uint32_t other = 0;
   for (int l = 0; l < nl; ++l) {
     const bool im2col = l == 0 && first, netlast = l == nl - 1 && last && !im2col;
     if (im2col) continue;
-    other += netlast ? 32u * (uint32_t)nc : ((w5_mask >> l) & 1) ? 5u * P : 4u * P;
+    other += netlast ? 32u * (uint32_t)nc : ((wmask >> l) & 1) ? (uint32_t)W * P : 4u * P;
   }
   uint32_t s_im = other >= 512u ? 1u : (512u - other) / (uint32_t)P;
-  s_im = s_im < 1u ? 1u : s_im > 4u ? 4u : s_im;
+  s_im = s_im >= 4u ? 4u : s_im >= 2u ? 2u : 1u;   // a power of two: slot = row & (S - 1)
   uint32_t off = 0;
   for (int l = 0; l < nl; ++l) {
     const bool im2col = l == 0 && first, netlast = l == nl - 1 && last && !im2col;
-    const uint32_t ns = im2col ? s_im : netlast ? 2u : ((w5_mask >> l) & 1) ? 5u : 4u;
+    const uint32_t ns = im2col ? s_im : netlast ? 2u : ((wmask >> l) & 1) ? (uint32_t)W : 4u;
     if (base) base[l] = off;
     if (nslots) nslots[l] = ns;
     off += netlast ? 32u * (uint32_t)nc : ns * (uint32_t)P;
@@ -158,21 +158,24 @@ __host__ __device__ inline uint32_t tmem_plan(int P, int nl, int first, int last
   return off;
 }
 
-// W5 scheme (a windowed layer whose output rows o accumulate in 5 TMEM slots without ever
-// splitting an MMA): the fill whose fresh output row is o (first contribution, dy = -1) writes
-// the three contiguous slots b, b+1, b+2, b = o mod 3, receiving the dy = +1 / 0 / -1 sums of
-// rows o-2, o-1, o.  A row o therefore accumulates in slot(s) fixed by o mod 3 alone:
-//   o = 0 mod 3: slot 2 (all three fills);
-//   o = 1 mod 3: slot 3 (dy = -1, 0) + slot 0 (dy = +1), summed by the epilogue;
-//   o = 2 mod 3: slot 4 (dy = -1) + slot 1 (dy = 0, +1), summed by the epilogue.
+// Wide scheme (a windowed layer whose output rows o accumulate in W = T + 2 TMEM slots without
+// ever splitting an MMA; T = 3 or 4): the fill whose fresh output row is o (its first
+// contribution, dy = -1) writes the three contiguous slots b, b+1, b+2 with b = o mod T, which
+// receive the dy = +1 / 0 / -1 sums of rows o-2, o-1, o.  Row o's three contributions therefore
+// land in slots fixed by o mod T alone: dy = -1 in (o mod T) + 2, dy = 0 in ((o+1) mod T) + 1,
+// dy = +1 in (o+2) mod T -- one slot, or two summed by the epilogue:
+//   T = 3 (W5): o = 0: {2};  o = 1: {3 (dy -1, 0), 0 (dy +1)};  o = 2: {4 (dy -1), 1 (dy 0, +1)}
+//   T = 4 (W6): o = 0: {2};  o = 1: {3};  o = 2: {4 (dy -1, 0), 0 (dy +1)};  o = 3: {5 (dy -1), 1}
 // The rounding of every output row is a function of its global row only, so results stay
-// bitwise independent of the strip / unit / tile decomposition.  A slot is re-used by the row
-// three rows later, one fill after its previous owner completed (the MMA warp waits until the
-// epilogue has drained it); at a unit start every row of the previous unit must be drained.
-__host__ __device__ inline void w5_slots(int o, int *main_slot, int *second_slot) {
-  const int m = ((o % 3) + 3) % 3;
-  *main_slot = 2 + m;
-  *second_slot = m == 0 ? -1 : m - 1;
+// bitwise independent of the strip / unit / tile decomposition (R46).  A slot is re-used
+// by the row T rows later, T - 2 fills after its previous owner completed (W5: one fill, W6:
+// two); the MMA warp waits until the epilogue has drained it (at a unit start: every row of the
+// previous unit).  tests/test_cnn_w5_schedule.py checks these invariants.
+__host__ __device__ inline void wide_slots(int o, int T, int *main_slot, int *second_slot) {
+  const int m = ((o % T) + T) % T;
+  const int q2 = m + 2, q0 = (m + 2) % T;
+  *main_slot = q2;
+  *second_slot = q0 == q2 ? -1 : q0;
 }
 
 // ---------------------------------------------------------------- PTX wrappers
@@ -358,7 +361,7 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
   const bool last = p.last_is_output != 0;
   const SmemLayout L = make_layout(P, NL, first, last, NC);
   constexpr int K0 = im2col_k(NC);      // im2col K (9 NC taps, zero padded)
-  constexpr bool kDdfb = NC == 1 && NL <= 2;   // DDFB operator modes compiled in (R39-R42)
+  constexpr bool kDdfb = NL <= 2;   // DDFB operator modes compiled in (R39-R42; C = 1 or 3)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t sbase = smem_u32(smem);
   const uint32_t bar0 = sbase + L.bar_off;
@@ -371,7 +374,7 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
   volatile int *abort_flag = reinterpret_cast<volatile int *>(smem + L.misc_off + 4);
   const uint32_t bar_done = sbase + L.misc_off + 8;
   // TMEM: per-layer column ranges from tmem_plan (kept in the layer table: {base, slots}); the
-  // allocation is sized for the ring-4 layout of the chain, or all 512 columns for P = 32 (W5)
+  // allocation is sized for the ring-4 layout of the chain, or all 512 columns for P = 32 (wide)
   constexpr uint32_t tmem_old = (uint32_t)NL * kAcc * P;
   static_assert(tmem_old <= 512 || P == 32, "TMEM columns");
   constexpr uint32_t tmem_need = P == 32 ? 512u : tmem_old;
@@ -408,11 +411,13 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
     *abort_flag = 0;
     uint4 *tab = reinterpret_cast<uint4 *>(smem + L.misc_off + 16);
     uint32_t tb[kMaxChunk], tn[kMaxChunk];
-    tmem_plan(P, NL, first, last, NC, p.w5_mask, tb, tn);
-    // .w = TMEM column base | slots << 16 | W5 << 24
+    tmem_plan(P, NL, first, last, NC, p.wide_mask, p.wide_slots, tb, tn);
+    // .w = TMEM column base | log2(slots) << 16 (ring-4 / im2col; 1, 2 or 4 slots) | T << 24 (wide
+    // scheme: T = W - 2 = 3 or 4; 0 otherwise)
     for (int l = 0; l < NL; ++l)
       tab[l] = make_uint4(L.ring_off[l], L.slot_bytes[l], L.w_off[l],
-                          tb[l] | (tn[l] << 16) | ((uint32_t)((p.w5_mask >> l) & 1) << 24));
+                          tb[l] | ((tn[l] >= 4u ? 2u : tn[l] >= 2u ? 1u : 0u) << 16) |
+                              (((p.wide_mask >> l) & 1) ? (uint32_t)(p.wide_slots - 2) << 24 : 0u));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == kMma0) {
@@ -601,18 +606,21 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
           const uint32_t O0 = Ocnt(l);
           const uint32_t Ig = O0 + (uint32_t)f;
           const uint4 lt = ltab[l];
-          const uint32_t nsl = (lt.w >> 16) & 0xffu;   // accumulator slots of this layer
-          const bool w5 = (lt.w >> 24) != 0;
+          const uint32_t lgs = (lt.w >> 16) & 0xffu;   // log2 of the accumulator slots (non-W5)
+          const uint32_t nsl = 1u << lgs, msk = nsl - 1u;
+          const int T = (int)(lt.w >> 24);              // wide scheme period (0: ring-4 / im2col)
+          const bool w5 = T != 0;
           if (netlast) {   // 2-slot ring of per-fill accumulators: fill Fg-2 must have been read
             if (ok && Fg >= 2u) ok = mbar_wait(bar_tempty(l, Fg & 1), ((Fg >> 1) - 1) & 1, abort_flag, p.err, 3);
           } else if (w5) {
             // every row drained whose slot this fill may re-use: at a unit start all rows of the
-            // previous unit, later the row three rows back (completed one fill ago); single
-            // barrier, one phase per drained row (the epilogue drains rows in order)
-            const uint32_t need = O0 + (uint32_t)(f > 2 ? f - 2 : 0);
-            if (ok && need > 0u) ok = mbar_wait(bar_tempty(l, 0), (need - 1u) & 1u, abort_flag, p.err, 3);
+            // previous unit, later the row T rows back (completed T - 2 fills ago).  Two barriers
+            // (row parity), one phase per drained row; the epilogue drains rows in order
+            const uint32_t need = O0 + (uint32_t)(f > T - 1 ? f - (T - 1) : 0);
+            if (ok && need > 0u)
+              ok = mbar_wait(bar_tempty(l, (need - 1u) & 1u), ((need - 1u) >> 1) & 1u, abort_flag, p.err, 3);
           } else if (ok && f < no && Ig >= nsl)
-            ok = mbar_wait(bar_tempty(l, Ig % nsl), ((Ig / nsl) - 1) & 1, abort_flag, p.err, 3);
+            ok = mbar_wait(bar_tempty(l, Ig & msk), ((Ig >> lgs) - 1) & 1, abort_flag, p.err, 3);
           ok = __shfl_sync(0xffffffffu, ok ? 1 : 0, 0) != 0;
           trace_ev(p.trace, tr_on && lane == 0, 4, s, l);
           if (!ok) return false;
@@ -626,7 +634,7 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
             if (elect_one()) {
 #pragma unroll
               for (int ks = 0; ks < K0 / 16; ++ks)   // K step = 2 core-matrix groups of A and B
-                mma_bf16(acc0 + (Ig % nsl) * P, ad + (uint64_t)(ks * 256), bd + (uint64_t)(ks * 2 * P),
+                mma_bf16(acc0 + (Ig & msk) * P, ad + (uint64_t)(ks * 256), bd + (uint64_t)(ks * 2 * P),
                          make_idesc(P), ks > 0 ? 1u : 0u);
             }
           } else if (netlast) {
@@ -644,14 +652,14 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
                          bd0 + (uint64_t)(ks * 32 * NC), make_idesc(16 * NC), ks > 0 ? 1u : 0u);
             }
           } else if (w5) {
-            // W5 (see w5_slots): the rows f-2, f-1, f of this fill sit in the contiguous slots
-            // b, b+1, b+2 (b = global row of row f, mod 3); rows outside [0, no) are skipped, which
+            // wide scheme (see wide_slots): the rows f-2, f-1, f of this fill sit in the contiguous
+            // slots b, b+1, b+2 (b = global row of row f, mod T); rows outside [0, no) are skipped, which
             // leaves a contiguous sub-window: one MMA per (dx, K step), never split.
             const uint32_t Cb = (uint32_t)P;
             const int ilo = f - 2 > 0 ? f - 2 : 0;
             const int ihi = f < no - 1 ? f : no - 1;
             const int of = r_lo - (NL - 1 - l) + f;                 // global row of row f
-            const uint32_t b = (uint32_t)(((of % 3) + 3) % 3);
+            const uint32_t b = (uint32_t)(((of % T) + T) % T);
             const uint32_t q0 = (uint32_t)(ilo - (f - 2));
             const uint32_t d = acc0 + (b + q0) * Cb;
             const uint32_t id = make_idesc((int)((uint32_t)(ihi - ilo + 1) * Cb));
@@ -705,7 +713,7 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
               mma_commit(bar_tfull(l, Fg & 1));          // this fill's tap sums
             } else {
               const int ic = im2col ? f : f - 2;         // output row completed by this group
-              if (ic >= 0 && ic < no) mma_commit(bar_tfull(l, w5 ? 0u : (O0 + (uint32_t)ic) % nsl));
+              if (ic >= 0 && ic < no) mma_commit(bar_tfull(l, w5 ? (O0 + (uint32_t)ic) & 1u : (O0 + (uint32_t)ic) & msk));
             }
           }
           __syncwarp();
@@ -806,11 +814,11 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
               if (!kDdfb || p.mode < 2) {   // DDFB modes exist for 1- and 2-operator launches only
                 p.G[(int64_t)co * p.gcs + gidx] = row_done + p.bias[l][co];
               } else if (o >= 0 && o < p.ny && cm >= 0 && cm < p.nx) {
-                // DDFB adjoint step (R39): q = proj_[0,1](v - W_k^* u); final: G = v - q
+                // DDFB adjoint step (R39): q = proj_[0,1](v - W_k^* u); final: G = v - q (channel co)
                 const TileGeom &xg = p.xg;
-                const float v = p.xv[(int64_t)(o - (xg.i0 - xg.h)) * xg.pitch + (cm - (xg.j0 - xg.hx))];
+                const float v = p.xv[(int64_t)co * p.xcs + (int64_t)(o - (xg.i0 - xg.h)) * xg.pitch + (cm - (xg.j0 - xg.hx))];
                 const float q = fminf(fmaxf(v - row_done, 0.f), 1.f);
-                p.G[gidx] = p.mode == 4 ? v - q : q;
+                p.G[(int64_t)co * p.gcs + gidx] = p.mode == 4 ? v - q : q;
               }
             }
           }
@@ -840,10 +848,11 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
           const int s = (im2col ? ic : ic + 2) + kLag * l;
           const uint32_t Ig = Ocnt(l) + (uint32_t)ic;
           const uint32_t ltw = ltab[l].w;
-          const uint32_t nsl = (ltw >> 16) & 0xffu;
-          const bool w5 = (ltw >> 24) != 0;
-          // W5: one full barrier per layer, one phase per completed row (rows complete in order)
-          const uint32_t fslot = w5 ? 0u : Ig % nsl, fphase = w5 ? Ig : Ig / nsl;
+          const uint32_t lgs = (ltw >> 16) & 0xffu, msk = (1u << lgs) - 1u;
+          const int T = (int)(ltw >> 24);
+          const bool w5 = T != 0;
+          // wide scheme: two full barriers (row parity), one phase per completed row
+          const uint32_t fslot = w5 ? Ig & 1u : Ig & msk, fphase = w5 ? Ig >> 1 : Ig >> lgs;
           if (!mbar_wait(bar_tfull(l, fslot), fphase & 1, abort_flag, p.err, 4)) return false;
           trace_ev(p.trace, trw, 6, s, l);
           tc_fence_after();
@@ -853,25 +862,25 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
           if ((l == NL - 1) && last) {
             // network output G (no ReLU), column 0 of the slot
             float v[1];
-            const uint32_t ta = taddr + (Ig % nsl) * (uint32_t)P;
+            const uint32_t ta = taddr + (Ig & msk) * (uint32_t)P;
             tmem_load<1>(ta, v);
             tmem_wait_ld();
             tmem_zero<1>(ta);
             tmem_wait_st();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(bar_tempty(l, Ig % nsl));
+            if (lane == 0) mbar_arrive(bar_tempty(l, Ig & msk));
             if (col_valid) {
               const TileGeom &g = p.gg;
               p.G[(int64_t)(o - (g.i0 - g.h)) * g.pitch + (cm - (g.j0 - g.hx))] = v[0] + p.bias[l][0];
             }
             return true;
           }
-          uint32_t ta = taddr + (Ig % nsl) * (uint32_t)P;   // ring-4 / im2col slot
+          uint32_t ta = taddr + (Ig & msk) * (uint32_t)P;   // ring-4 / im2col slot
           int w5s = -1;                                     // W5: second slot (-1: none)
           if (w5) {
             int ms;
-            w5_slots(o, &ms, &w5s);
+            wide_slots(o, T, &ms, &w5s);
             ta = taddr + (uint32_t)ms * P;
           }
           uint32_t w[P / 2];
@@ -937,7 +946,7 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
           }
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(bar_tempty(l, w5 ? 0u : Ig % nsl));
+          if (lane == 0) mbar_arrive(bar_tempty(l, w5 ? Ig & 1u : Ig & msk));
           trace_ev(p.trace, trw, 7, s, l);
           if (l < NL - 1) {
             // next layer's input fill = this layer's output row index ic
@@ -1081,12 +1090,12 @@ cudaError_t dispatch_nl(const CnnChunkParams &p, int num_sms, cudaStream_t s) {
 
 }  // namespace
 
-size_t cnn_chunk_smem_bytes(int P, int nl, int first, int last, int nc, int w5_mask) {
+size_t cnn_chunk_smem_bytes(int P, int nl, int first, int last, int nc, int wide_mask, int wide_slots) {
   if (nl < 1 || nl > kMaxChunk) return SIZE_MAX;
   if (nl > max_nl(P)) return SIZE_MAX;
   if (nc != 1 && (nc != 3 || P < 32)) return SIZE_MAX;   // C = 3: N = 48 columns of the folded last layer
-  if (w5_mask && P != 32) return SIZE_MAX;                // the W5 layout is compiled for P = 32
-  if (tmem_plan(P, nl, first, last, nc, w5_mask, nullptr, nullptr) > 512u) return SIZE_MAX;
+  if (wide_mask && (P != 32 || (wide_slots != 5 && wide_slots != 6))) return SIZE_MAX;   // compiled for P = 32
+  if (tmem_plan(P, nl, first, last, nc, wide_mask, wide_slots, nullptr, nullptr) > 512u) return SIZE_MAX;
   return make_layout(P, nl, first, last, nc).total;
 }
 

@@ -98,7 +98,8 @@ struct pnpula_ctx {
 
   // CNN
   std::vector<CnnChunk> chunks;
-  uint32_t w5_mask = 0;             // bit k-1: layer k uses the W5 accumulator scheme
+  uint32_t wide_mask = 0;           // bit k-1: layer k uses the wide accumulator scheme (cnn_kernels.cu)
+  int wide_slots = 0;               // its slot count W (5 or 6)
   std::vector<uint16_t *> d_w;      // per layer packed weights
   std::vector<float *> d_b;         // per layer biases
   std::vector<std::vector<float>> h_b;   // host copies (passed to the CNN kernel as parameters)
@@ -287,7 +288,8 @@ pnpula_status run_ddfb(pnpula_ctx *c, int buf) {
       CnnChunkParams p{};
       p.P = P;
       p.nl = 2;
-      p.nc = 1;
+      p.nc = c->nc;                                        // colour: W_k C -> P, W_k^* P -> C
+      p.xcs = p.gcs = (int64_t)geom_elems(g);
       p.first_is_input = 1;
       p.last_is_output = 1;
       p.mode0 = j == 0 ? 1 : 3;
@@ -335,7 +337,8 @@ pnpula_status run_cnn(pnpula_ctx *c, int buf) {
       p.nl = ch.nl;
       p.first_is_input = ch.l0 == 1;
       p.last_is_output = ch.l0 + ch.nl - 1 == c->n_layers;
-      p.w5_mask = (int)((c->w5_mask >> (ch.l0 - 1)) & ((1u << ch.nl) - 1u));
+      p.wide_mask = (int)((c->wide_mask >> (ch.l0 - 1)) & ((1u << ch.nl) - 1u));
+      p.wide_slots = c->wide_slots;
       for (int l = 0; l < ch.nl; ++l) {
         p.w[l] = c->d_w[ch.l0 - 1 + l];
         const std::vector<float> &hb = c->h_b[ch.l0 - 1 + l];
@@ -494,6 +497,8 @@ pnpula_status enqueue_step(pnpula_ctx *c, int buf, const IterState *it) {
         p.x += o; p.xn += o; p.y += o; p.mean += o; p.m2 += o;
         if (p.G) p.G += o;
         if (p.z) p.z += o;
+        if (p.zv) p.zv += o;   // TV (colour: channel-wise)
+        if (p.zh) p.zh += o;
         p.sb = 4u * (uint32_t)ch;
       }
       const int h = td.g.h, th = td.g.th;
@@ -522,12 +527,16 @@ pnpula_status enqueue_step(pnpula_ctx *c, int buf, const IterState *it) {
     if ((s = exchange(c, buf ^ 1))) return s;
   }
   if (c->tv_beta > 0) {
-    // TV z block (R37, R38): x^{t+1} (halo now valid) -> z = (z_v, z_h) on tile (+) 1
-    for (auto &td : c->tiles) {
+    // TV z block (R37, R38): x^{t+1} (halo now valid) -> z = (z_v, z_h) on tile (+) 1, per
+    // channel plane for colour images (channel-wise isotropic TV; streams 4 c + 1 / 3)
+    for (auto &td : c->tiles)
+    for (int ch = 0; ch < c->nc; ++ch) {
+      const size_t o = (size_t)ch * geom_elems(td.g);
       TvZParams q{};
-      q.x = td.x[buf ^ 1];
-      q.zv = td.z;
-      q.zh = td.zh;
+      q.x = td.x[buf ^ 1] + o;
+      q.zv = td.z + o;
+      q.zh = td.zh + o;
+      q.sb = 4u * (uint32_t)ch;
       q.g = td.g;
       q.ny = c->ny; q.nx = c->nx;
       q.b = (float)(c->kappa / c->rho);
@@ -719,17 +728,19 @@ pnpula_status build_halo_plan(pnpula_ctx *c) {
   return PNPULA_OK;
 }
 
-// Which layers accumulate in the W5 TMEM scheme (cnn_kernels.cu w5_slots): the windowed 3x3
-// layers 2..K-1 of a P = 32 net -- for colour nets (N = 48 folded last layer) all but the last two,
-// so that a 4-layer chain ending the net fits 512 TMEM columns.  A function of (K, P, C) only, so
-// every chunking (fused, layer-wise) and every tiling rounds each layer identically.  Env
-// PNPULA_W5=0 (read at create): the ring-4 scheme everywhere (kernel experiments).
-uint32_t w5_layers(const pnpula_ctx *c) {
-  const char *e = getenv("PNPULA_W5");
-  if ((e && atoi(e) == 0) || c->channels != 32) return 0;
+// Which layers accumulate in the wide TMEM scheme (cnn_kernels.cu wide_slots) and with how many
+// slots: the windowed 3x3 layers 2..K-1 of a P = 32 net.  A function of (K, P) only, so every
+// chunking (fused, layer-wise) and every tiling rounds each layer identically (R46).  Env (read
+// at create; kernel experiments): PNPULA_WSLOTS=4 (ring-4 everywhere) / 5 / 6 (default),
+// PNPULA_W5_MASK=<hex> (bit k-1 = layer k) restricts the wide layers.
+uint32_t wide_layers(const pnpula_ctx *c, int *slots) {
+  const char *e = getenv("PNPULA_WSLOTS");
+  *slots = e ? atoi(e) : 6;
+  if ((*slots != 5 && *slots != 6) || c->channels != 32) { *slots = 0; return 0; }
   uint32_t m = 0;
-  const int K = c->n_layers, hi = c->nc > 1 ? K - 3 : K - 1;
-  for (int k = 2; k <= hi; ++k) m |= 1u << (k - 1);
+  const int K = c->n_layers;
+  for (int k = 2; k <= K - 1; ++k) m |= 1u << (k - 1);
+  if (const char *em = getenv("PNPULA_W5_MASK")) m &= (uint32_t)strtoul(em, nullptr, 16);
   return m;
 }
 
@@ -738,14 +749,15 @@ void plan_cnn_chunks(pnpula_ctx *c) {
   c->chunks.clear();
   const int K = c->n_layers;
   const size_t budget = 227 * 1024;
-  c->w5_mask = w5_layers(c);
+  c->wide_mask = wide_layers(c, &c->wide_slots);
   int l = 1;
   while (l <= K) {
     int best = 1;
     const int maxnl = (c->flags & PNPULA_FLAG_CNN_LAYERWISE) ? 1 : kMaxChunk;
     for (int nl = 1; nl <= std::min(maxnl, K - l + 1); ++nl) {
-      const int wm = (int)((c->w5_mask >> (l - 1)) & ((1u << nl) - 1u));
-      if (cnn_chunk_smem_bytes(c->channels, nl, l == 1, l + nl - 1 == K, c->nc, wm) <= budget) best = nl;
+      const int wm = (int)((c->wide_mask >> (l - 1)) & ((1u << nl) - 1u));
+      if (cnn_chunk_smem_bytes(c->channels, nl, l == 1, l + nl - 1 == K, c->nc, wm, c->wide_slots) <= budget)
+        best = nl;
     }
     c->chunks.push_back({l, best, K - (l + best - 1)});
     l += best;
@@ -880,7 +892,9 @@ pnpula_status pnpula_create(const pnpula_config *cfg, pnpula_ctx **out) {
   }
   const int nc = f.img_channels > 1 ? f.img_channels : 1;
   if (nc != 1 && nc != 3) { set_error("img_channels must be 1 or 3"); return PNPULA_E_UNSUPPORTED; }
-  if (nc > 1 && (tv || ddfb)) { set_error("colour images: TV prior and DDFB denoiser not supported"); return PNPULA_E_UNSUPPORTED; }
+  if (nc > 1 && ddfb && f.den->channels != 32 && f.den->channels != 64) {
+    set_error("colour DDFB needs P = 32 or 64 (N = 48 folded adjoint columns)"); return PNPULA_E_UNSUPPORTED;
+  }
   if (nc > 1 && use_cnn && f.den->channels < 32) {
     set_error("colour DnCNN needs channels >= 32 (N = 48 folded output columns)"); return PNPULA_E_UNSUPPORTED;
   }
@@ -1097,35 +1111,38 @@ pnpula_status pnpula_create(const pnpula_config *cfg, pnpula_ctx **out) {
       if (e2 != cudaSuccess) { fail_cuda(nullptr, e2, "DDFB weights", __LINE__); return PNPULA_E_CUDA; }
       return PNPULA_OK;
     };
-    // W_k as a 1 -> P conv [P][1][3][3] (scaled), and W_k^* as a P -> 1 conv [1][P][3][3]:
-    // w'[0][c][a][b] = s * w_k[c][0][2-a][2-b] (the adjoint of a cross-correlation)
+    // W_k as a C -> P conv [P][C][3][3] (scaled), and W_k^* as a P -> C conv [C][P][3][3]:
+    // w'[c][p][a][b] = s * w_k[p][c][2-a][2-b] (the adjoint of a cross-correlation; C = 1 or 3)
+    const size_t lw = (size_t)P * nc * 9;   // weights per DDFB layer
     auto wk = [&](int k, double sc) {
-      std::vector<float> o((size_t)P * 9);
-      for (size_t i = 0; i < o.size(); ++i) o[i] = (float)(sc * f.den->weights[(size_t)(k - 1) * P * 9 + i]);
+      std::vector<float> o(lw);
+      for (size_t i = 0; i < o.size(); ++i) o[i] = (float)(sc * f.den->weights[(size_t)(k - 1) * lw + i]);
       return o;
     };
     auto wadj = [&](int k, double sc) {
-      std::vector<float> o((size_t)P * 9);
-      for (int ch = 0; ch < P; ++ch)
-        for (int a = 0; a < 3; ++a)
-          for (int b = 0; b < 3; ++b)
-            o[((size_t)ch * 3 + a) * 3 + b] = (float)(sc * f.den->weights[(size_t)(k - 1) * P * 9 + ((size_t)ch * 3 + (2 - a)) * 3 + (2 - b)]);
+      std::vector<float> o(lw);
+      for (int ci = 0; ci < nc; ++ci)
+        for (int ch = 0; ch < P; ++ch)
+          for (int a = 0; a < 3; ++a)
+            for (int b = 0; b < 3; ++b)
+              o[(((size_t)ci * P + ch) * 3 + a) * 3 + b] =
+                  (float)(sc * f.den->weights[(size_t)(k - 1) * lw + (((size_t)ch * nc + ci) * 3 + (2 - a)) * 3 + (2 - b)]);
       return o;
     };
-    pnpula_status s = upload(wk(K, 1.0), P, 1, &c->ddfb_u0);
+    pnpula_status s = upload(wk(K, 1.0), P, nc, &c->ddfb_u0);
     if (s) return bail(s);
     for (int k = 1; k < K; ++k) {
       uint16_t *t = nullptr, *a = nullptr;
-      s = upload(wk(k, f.den->ddfb_gammas[k - 1]), P, 1, &t);
-      if (!s) s = upload(wadj(k, 1.0), 1, P, &a);
+      s = upload(wk(k, f.den->ddfb_gammas[k - 1]), P, nc, &t);
+      if (!s) s = upload(wadj(k, 1.0), nc, P, &a);
       c->ddfb_t.push_back(t);
       c->ddfb_adj.push_back(a);
       if (s) return bail(s);
     }
-    s = upload(wadj(K, f.den->ddfb_gammas[K - 1]), 1, P, &c->ddfb_fin);
+    s = upload(wadj(K, f.den->ddfb_gammas[K - 1]), nc, P, &c->ddfb_fin);
     if (s) return bail(s);
     for (auto &td : c->tiles) {
-      const size_t n = geom_elems(td.g);
+      const size_t n = geom_elems(td.g) * (size_t)nc;   // p = proj(v - W^* u): C planes
       CUB(dmalloc(c, &td.pbuf, n * sizeof(float)));
       CUB(cudaMemsetAsync(td.pbuf, 0, n * sizeof(float), c->stream));
       CUB(dmalloc(c, &td.pbuf2, n * sizeof(float)));

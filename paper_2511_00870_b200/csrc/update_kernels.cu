@@ -792,8 +792,8 @@ __global__ void __launch_bounds__(NTHREADS) tv_z_kernel(const __grid_constant__ 
     const int gi = r0 + (int)qr;
     const int gj4 = 4 * (q0 + (int)(e - qr * (uint32_t)nq));
     float zev[4], zeh[4];
-    normals4(p.seed_lo, p.seed_hi, (uint32_t)gj4 >> 2, (uint32_t)gi, t1, 1u, zev);
-    normals4(p.seed_lo, p.seed_hi, (uint32_t)gj4 >> 2, (uint32_t)gi, t1, 3u, zeh);
+    normals4(p.seed_lo, p.seed_hi, (uint32_t)gj4 >> 2, (uint32_t)gi, t1, p.sb + 1u, zev);
+    normals4(p.seed_lo, p.seed_hi, (uint32_t)gj4 >> 2, (uint32_t)gi, t1, p.sb + 3u, zeh);
     const int64_t n0 = pidx(g, gi, gj4);   // 16-byte aligned
     if (gj4 >= c0 && gj4 + 4 <= c1) {
       // whole quad inside: 4 float4 loads + 1 scalar (x right of the quad), 2 float4 stores

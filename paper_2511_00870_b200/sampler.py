@@ -155,8 +155,8 @@ class Sampler:
         return out
 
     def tv_zh(self, scope: int = L.SCOPE_LOCAL):
-        """TV prior: the horizontal component z_h of z ~ D x."""
-        shp = self._out_shape(scope, planes=1)
+        """TV prior: the horizontal component z_h of z ~ D x (C planes for colour images)."""
+        shp = self._out_shape(scope)
         out = np.zeros(shp, np.float32) if shp else None
         L.check(self._lib.pnpula_get_tv_zh(self._h, L._ptr(out), scope))
         return out

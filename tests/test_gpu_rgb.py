@@ -159,6 +159,95 @@ def test_colour_rejections():
     kw, _ = rgb_problem(32, 32, cnn=(4, 16))
     with pytest.raises(Exception):
         Sampler(**kw)          # the colour DnCNN needs P >= 32
-    kw, _ = rgb_problem(32, 32, z=True, box=False)
-    with pytest.raises(Exception):
-        Sampler(**kw, tv_beta=1.0)
+    kw, _ = rgb_problem(32, 32, z=False)
+    w, g, ht = synth.ddfb_weights(2, 16, seed=3, image_channels=3)
+    with pytest.raises(Exception):   # the colour DDFB adjoint (N = 48 folded columns) needs P >= 32
+        Sampler(**kw, weights=w, n_layers=2, channels=16, alpha=1.0, eps=0.1, den_kind="ddfb", ddfb_gammas=g,
+                ht_eps=ht)
+
+
+# ---------------------------------------------------------------- colour DDFB and colour TV
+def ddfb_rgb_problem(ny, nx, K=4, P=32):
+    kw, pb = rgb_problem(ny, nx, kernel="gauss9", z=False)
+    w, g, ht = synth.ddfb_weights(K, P, seed=7, image_channels=3)
+    extra = dict(weights=w, n_layers=K, channels=P, alpha=1.0, eps=0.1, den_kind="ddfb", ddfb_gammas=g, ht_eps=ht)
+    kw.update(extra)
+    pb = oracle.Problem(**{**pb.__dict__, **extra})
+    return kw, pb
+
+
+def tv_rgb_problem(ny, nx, op="conv"):
+    kw, pb = rgb_problem(ny, nx, op=op, kernel="gauss9", z=False, box=False)
+    hp = params.tv_gaussian(kw["sigma2"], rho=1e-3)
+    extra = dict(gamma=hp["gamma"], rho=hp["rho"], kappa=hp["kappa"], tv_beta=hp["tv_beta"])
+    kw.update(extra)
+    pb = oracle.Problem(**{**pb.__dict__, **extra})
+    return kw, pb
+
+
+@pytest.mark.parametrize("K,P,shape", [(1, 32, (40, 70)), (2, 64, (33, 140)), (4, 32, (45, 130)), (4, 64, (37, 61))])
+def test_colour_ddfb_residual(K, P, shape):
+    kw, _ = ddfb_rgb_problem(*shape, K=K, P=P)
+    s = Sampler(**kw)
+    try:
+        s.reset(0, 1)
+        G = s.denoiser_residual()
+    finally:
+        s.close()
+    assert G.shape == (3,) + shape
+    args = (kw["x0"], kw["weights"], kw["ddfb_gammas"], K, P, kw["ht_eps"])
+    ref, ref16 = oracle.ddfb_residual(*args), oracle.ddfb_residual(*args, bf16_emulate=True)
+    assert rel_l2(G, ref) <= 2e-2
+    for c in range(3):
+        assert rel_l2(G[c], ref16[c]) <= 2e-3, c
+
+
+def test_colour_ddfb_chain_vs_oracle():
+    kw, pb = ddfb_rgb_problem(45, 70)
+    g = run(kw, 20, 4, 873)
+    o16 = oracle.run(pb, 20, 4, 873, bf16_emulate=True)
+    o = oracle.run(pb, 20, 4, 873)
+    for k in ("x", "mean"):
+        assert rel_l2(g[k], o16[k]) <= 2e-3, k
+        assert rel_l2(g[k], o[k]) <= 2e-2, k
+
+
+@pytest.mark.parametrize("op", ["conv", "mask"])
+def test_colour_tv_chain_fp32_path(op):
+    kw, pb = tv_rgb_problem(53, 61, op=op)
+    s = Sampler(**kw)
+    try:
+        s.run(30, 5, 874)
+        x, zv, _ = s.state()
+        zh = s.tv_zh()
+        mean, var, _ = s.moments()
+    finally:
+        s.close()
+    o = oracle.run(pb, 30, 5, 874)
+    for k, v in (("x", x), ("z", zv), ("zh", zh), ("mean", mean)):
+        assert v.shape == (3, 53, 61)
+        assert rel_l2(v, o[k]) <= 1e-5, k
+    assert rel_l2(var, o["var"]) <= 1e-5   # R44
+    assert np.all(x >= 0)
+
+
+@pytest.mark.parametrize("case,tiles,flags", [("tv", (2, 2), 0), ("tv", (3, 1), FLAG_HALO_VIA_NCCL),
+                                              ("ddfb", (2, 2), 0), ("ddfb", (3, 1), FLAG_HALO_VIA_NCCL)])
+def test_colour_ddfb_tv_tiled_bitwise(case, tiles, flags):
+    kw, _ = tv_rgb_problem(60, 66) if case == "tv" else ddfb_rgb_problem(60, 66)
+
+    def go(t, f):
+        s = Sampler(**kw, tiles=t, flags=f)
+        try:
+            s.run(10, 3, 55)
+            x, z, _ = s.state()
+            mean, var, _ = s.moments()
+            out = dict(x=x, z=z, mean=mean, var=var)
+            if case == "tv":
+                out["zh"] = s.tv_zh()
+            return out
+        finally:
+            s.close()
+    a, b = go((1, 1), 0), go(tiles, flags)
+    for k in a:
+        np.testing.assert_array_equal(a[k], b[k], err_msg=k)
