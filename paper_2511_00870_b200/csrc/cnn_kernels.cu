@@ -128,56 +128,6 @@ __host__ __device__ inline SmemLayout make_layout(int P, int nl, int first, int 
   return L;
 }
 
-// TMEM accumulator plan of one chain (columns of the 512-column allocation).  Per layer:
-//  * im2col layer (C -> P, one N = P MMA per row, accumulate = 0): S slots of P columns, S = 1, 2
-//    or 4 (whatever TMEM the other layers leave; the result does not depend on S);
-//  * windowed 3x3 layer, "ring-4" scheme: 4 row slots of P columns (slot = row mod 4); a fill whose
-//    three output rows wrap the ring issues two MMAs (N = 2P + P or P + 2P);
-//  * windowed layer, "wide" scheme (bit l of wmask): W = 5 or 6 slots of P columns, never split --
-//    see wide_slots() below;
-//  * folded P -> C last layer: 2 per-fill slots of 16 C columns.
-// Returns the total columns (> 512: the chain does not fit), fills base[] / nslots[].
-__host__ __device__ inline uint32_t tmem_plan(int P, int nl, int first, int last, int nc, int wmask, int W,
-                                              uint32_t *base, uint32_t *nslots) {
-  uint32_t other = 0;
-  for (int l = 0; l < nl; ++l) {
-    const bool im2col = l == 0 && first, netlast = l == nl - 1 && last && !im2col;
-    if (im2col) continue;
-    other += netlast ? 32u * (uint32_t)nc : ((wmask >> l) & 1) ? (uint32_t)W * P : 4u * P;
-  }
-  uint32_t s_im = other >= 512u ? 1u : (512u - other) / (uint32_t)P;
-  s_im = s_im >= 4u ? 4u : s_im >= 2u ? 2u : 1u;   // a power of two: slot = row & (S - 1)
-  uint32_t off = 0;
-  for (int l = 0; l < nl; ++l) {
-    const bool im2col = l == 0 && first, netlast = l == nl - 1 && last && !im2col;
-    const uint32_t ns = im2col ? s_im : netlast ? 2u : ((wmask >> l) & 1) ? (uint32_t)W : 4u;
-    if (base) base[l] = off;
-    if (nslots) nslots[l] = ns;
-    off += netlast ? 32u * (uint32_t)nc : ns * (uint32_t)P;
-  }
-  return off;
-}
-
-// Wide scheme (a windowed layer whose output rows o accumulate in W = T + 2 TMEM slots without
-// ever splitting an MMA; T = 3 or 4): the fill whose fresh output row is o (its first
-// contribution, dy = -1) writes the three contiguous slots b, b+1, b+2 with b = o mod T, which
-// receive the dy = +1 / 0 / -1 sums of rows o-2, o-1, o.  Row o's three contributions therefore
-// land in slots fixed by o mod T alone: dy = -1 in (o mod T) + 2, dy = 0 in ((o+1) mod T) + 1,
-// dy = +1 in (o+2) mod T -- one slot, or two summed by the epilogue:
-//   T = 3 (W5): o = 0: {2};  o = 1: {3 (dy -1, 0), 0 (dy +1)};  o = 2: {4 (dy -1), 1 (dy 0, +1)}
-//   T = 4 (W6): o = 0: {2};  o = 1: {3};  o = 2: {4 (dy -1, 0), 0 (dy +1)};  o = 3: {5 (dy -1), 1}
-// The rounding of every output row is a function of its global row only, so results stay
-// bitwise independent of the strip / unit / tile decomposition (R46).  A slot is re-used
-// by the row T rows later, T - 2 fills after its previous owner completed (W5: one fill, W6:
-// two); the MMA warp waits until the epilogue has drained it (at a unit start: every row of the
-// previous unit).  tests/test_cnn_w5_schedule.py checks these invariants.
-__host__ __device__ inline void wide_slots(int o, int T, int *main_slot, int *second_slot) {
-  const int m = ((o % T) + T) % T;
-  const int q2 = m + 2, q0 = (m + 2) % T;
-  *main_slot = q2;
-  *second_slot = q0 == q2 ? -1 : q0;
-}
-
 // ---------------------------------------------------------------- PTX wrappers
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -213,10 +163,15 @@ __device__ __forceinline__ bool mbar_test_sleep(uint32_t bar, uint32_t parity) {
 }
 // Bounded wait: gives up (sets the CTA abort flag and the device error flag) after
 // ~4e9 cycles so a pipeline bug cannot hang the GPU.
+#ifndef PNPULA_POLL_BATCH
+#define PNPULA_POLL_BATCH 32   // tries between two watchdog checks (profiles/r02_cnn_schemes.md)
+#endif
 __device__ __noinline__ bool mbar_wait_slow(uint32_t bar, uint32_t parity, volatile int *abort, int *err, int code) {
   const long long t0 = clock64();
   while (true) {
-    if (mbar_test_sleep(bar, parity)) return true;
+#pragma unroll 1
+    for (int i = 0; i < PNPULA_POLL_BATCH; ++i)
+      if (mbar_test_sleep(bar, parity)) return true;
     if (*abort) return false;
     if (clock64() - t0 > (1ll << 32)) {
       *abort = 1;
@@ -327,6 +282,16 @@ __device__ __forceinline__ void tmem_zero<16>(uint32_t taddr) {
 }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
+// ReLU + round-to-nearest bf16 of a pair, packed (lo in the low half): one instruction
+__device__ __forceinline__ uint32_t relu_pack_bf16(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.relu.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+#ifndef PNPULA_EPI_CVT
+#define PNPULA_EPI_CVT 1   // 1: bias add + cvt.rn.relu.bf16x2 per pair, outside-image zeroing behind a vote
+#endif
+
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t *>(&v);
@@ -373,11 +338,9 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + L.misc_off);
   volatile int *abort_flag = reinterpret_cast<volatile int *>(smem + L.misc_off + 4);
   const uint32_t bar_done = sbase + L.misc_off + 8;
-  // TMEM: per-layer column ranges from tmem_plan (kept in the layer table: {base, slots}); the
-  // allocation is sized for the ring-4 layout of the chain, or all 512 columns for P = 32 (wide)
-  constexpr uint32_t tmem_old = (uint32_t)NL * kAcc * P;
-  static_assert(tmem_old <= 512 || P == 32, "TMEM columns");
-  constexpr uint32_t tmem_need = P == 32 ? 512u : tmem_old;
+  // TMEM: layer l owns columns [l*4P, l*4P + 4*Cb): accumulator-row slot q at l*4P + q*Cb
+  constexpr uint32_t tmem_need = (uint32_t)NL * kAcc * P;
+  static_assert(tmem_need <= 512, "TMEM columns");
   constexpr uint32_t tmem_cols = tmem_need <= 32 ? 32 : tmem_need <= 64 ? 64 : tmem_need <= 128 ? 128
                                  : tmem_need <= 256 ? 256 : 512;
 
@@ -410,14 +373,7 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
       for (int w = 0; w < kProdWarps; ++w) mbar_init(sbase + L.xs_off + (uint32_t)(kProdWarps * 3 * NC * kXS) * 4u + w * 8u, 1);
     *abort_flag = 0;
     uint4 *tab = reinterpret_cast<uint4 *>(smem + L.misc_off + 16);
-    uint32_t tb[kMaxChunk], tn[kMaxChunk];
-    tmem_plan(P, NL, first, last, NC, p.wide_mask, p.wide_slots, tb, tn);
-    // .w = TMEM column base | log2(slots) << 16 (ring-4 / im2col; 1, 2 or 4 slots) | T << 24 (wide
-    // scheme: T = W - 2 = 3 or 4; 0 otherwise)
-    for (int l = 0; l < NL; ++l)
-      tab[l] = make_uint4(L.ring_off[l], L.slot_bytes[l], L.w_off[l],
-                          tb[l] | ((tn[l] >= 4u ? 2u : tn[l] >= 2u ? 1u : 0u) << 16) |
-                              (((p.wide_mask >> l) & 1) ? (uint32_t)(p.wide_slots - 2) << 24 : 0u));
+    for (int l = 0; l < NL; ++l) tab[l] = make_uint4(L.ring_off[l], L.slot_bytes[l], L.w_off[l], 0u);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == kMma0) {
@@ -605,27 +561,16 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
           // output row that receives its first contribution (im2col: the only one)
           const uint32_t O0 = Ocnt(l);
           const uint32_t Ig = O0 + (uint32_t)f;
-          const uint4 lt = ltab[l];
-          const uint32_t lgs = (lt.w >> 16) & 0xffu;   // log2 of the accumulator slots (non-W5)
-          const uint32_t nsl = 1u << lgs, msk = nsl - 1u;
-          const int T = (int)(lt.w >> 24);              // wide scheme period (0: ring-4 / im2col)
-          const bool w5 = T != 0;
           if (netlast) {   // 2-slot ring of per-fill accumulators: fill Fg-2 must have been read
             if (ok && Fg >= 2u) ok = mbar_wait(bar_tempty(l, Fg & 1), ((Fg >> 1) - 1) & 1, abort_flag, p.err, 3);
-          } else if (w5) {
-            // every row drained whose slot this fill may re-use: at a unit start all rows of the
-            // previous unit, later the row T rows back (completed T - 2 fills ago).  Two barriers
-            // (row parity), one phase per drained row; the epilogue drains rows in order
-            const uint32_t need = O0 + (uint32_t)(f > T - 1 ? f - (T - 1) : 0);
-            if (ok && need > 0u)
-              ok = mbar_wait(bar_tempty(l, (need - 1u) & 1u), ((need - 1u) >> 1) & 1u, abort_flag, p.err, 3);
-          } else if (ok && f < no && Ig >= nsl)
-            ok = mbar_wait(bar_tempty(l, Ig & msk), ((Ig >> lgs) - 1) & 1, abort_flag, p.err, 3);
+          } else if (ok && f < no && Ig >= (uint32_t)kAcc)
+            ok = mbar_wait(bar_tempty(l, Ig & 3), ((Ig >> 2) - 1) & 1, abort_flag, p.err, 3);
           ok = __shfl_sync(0xffffffffu, ok ? 1 : 0, 0) != 0;
           trace_ev(p.trace, tr_on && lane == 0, 4, s, l);
           if (!ok) return false;
           tc_fence_after();
-          const uint32_t acc0 = tmem_base + (lt.w & 0xffffu);
+          const uint4 lt = ltab[l];
+          const uint32_t acc0 = tmem_base + (uint32_t)(l * kAcc * P);
           const uint32_t wbase = sbase + lt.z;
           const uint32_t slot = sbase + lt.x + rs * lt.y;
           if (im2col) {
@@ -634,7 +579,7 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
             if (elect_one()) {
 #pragma unroll
               for (int ks = 0; ks < K0 / 16; ++ks)   // K step = 2 core-matrix groups of A and B
-                mma_bf16(acc0 + (Ig & msk) * P, ad + (uint64_t)(ks * 256), bd + (uint64_t)(ks * 2 * P),
+                mma_bf16(acc0 + (Ig & 3) * P, ad + (uint64_t)(ks * 256), bd + (uint64_t)(ks * 2 * P),
                          make_idesc(P), ks > 0 ? 1u : 0u);
             }
           } else if (netlast) {
@@ -650,32 +595,6 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
               for (int ks = 0; ks < KS; ++ks)
                 mma_bf16(acc0 + (Fg & 1) * 16u * NC, ad0 + (uint64_t)((2 * ks * GS) >> 4),
                          bd0 + (uint64_t)(ks * 32 * NC), make_idesc(16 * NC), ks > 0 ? 1u : 0u);
-            }
-          } else if (w5) {
-            // wide scheme (see wide_slots): the rows f-2, f-1, f of this fill sit in the contiguous
-            // slots b, b+1, b+2 (b = global row of row f, mod T); rows outside [0, no) are skipped, which
-            // leaves a contiguous sub-window: one MMA per (dx, K step), never split.
-            const uint32_t Cb = (uint32_t)P;
-            const int ilo = f - 2 > 0 ? f - 2 : 0;
-            const int ihi = f < no - 1 ? f : no - 1;
-            const int of = r_lo - (NL - 1 - l) + f;                 // global row of row f
-            const uint32_t b = (uint32_t)(((of % T) + T) % T);
-            const uint32_t q0 = (uint32_t)(ilo - (f - 2));
-            const uint32_t d = acc0 + (b + q0) * Cb;
-            const uint32_t id = make_idesc((int)((uint32_t)(ihi - ilo + 1) * Cb));
-            const uint64_t ad0 = make_desc(slot, GS, 128);
-            const uint64_t bd0 = make_desc(wbase, 3u * Cb * 16u, 128);
-            const uint32_t bstep = 3u * Cb * 2u;
-            if (elect_one()) {
-#pragma unroll
-              for (int dx = 0; dx < 3; ++dx) {
-#pragma unroll
-                for (int ks = 0; ks < KS; ++ks) {
-                  const uint64_t ad = ad0 + (uint64_t)((2 * ks * GS + dx * 16) >> 4);
-                  const uint64_t bd = bd0 + (uint64_t)((dx * KS + ks) * bstep);
-                  mma_bf16(d, ad, bd + (uint64_t)(q0 * Cb), id, 1);
-                }
-              }
             }
           } else {
             // input row f contributes to output rows f-2 (dy=+1), f-1 (dy=0), f (dy=-1): B block q=0,1,2.
@@ -713,7 +632,7 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
               mma_commit(bar_tfull(l, Fg & 1));          // this fill's tap sums
             } else {
               const int ic = im2col ? f : f - 2;         // output row completed by this group
-              if (ic >= 0 && ic < no) mma_commit(bar_tfull(l, w5 ? (O0 + (uint32_t)ic) & 1u : (O0 + (uint32_t)ic) & msk));
+              if (ic >= 0 && ic < no) mma_commit(bar_tfull(l, (O0 + (uint32_t)ic) & 3));
             }
           }
           __syncwarp();
@@ -763,7 +682,7 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
           float d[NC][16];
 #pragma unroll
           for (int co = 0; co < NC; ++co)
-            tmem_load<16>(tmem_base + lane_base + (ltab[l].w & 0xffffu) + (Fg & 1) * 16u * NC + co * 16u, d[co]);
+            tmem_load<16>(tmem_base + lane_base + (uint32_t)(l * kAcc * P) + (Fg & 1) * 16u * NC + co * 16u, d[co]);
           tmem_wait_ld();
           tc_fence_before();
           __syncwarp();
@@ -847,42 +766,30 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
           const bool im2col = is_im2col(l);
           const int s = (im2col ? ic : ic + 2) + kLag * l;
           const uint32_t Ig = Ocnt(l) + (uint32_t)ic;
-          const uint32_t ltw = ltab[l].w;
-          const uint32_t lgs = (ltw >> 16) & 0xffu, msk = (1u << lgs) - 1u;
-          const int T = (int)(ltw >> 24);
-          const bool w5 = T != 0;
-          // wide scheme: two full barriers (row parity), one phase per completed row
-          const uint32_t fslot = w5 ? Ig & 1u : Ig & msk, fphase = w5 ? Ig >> 1 : Ig >> lgs;
-          if (!mbar_wait(bar_tfull(l, fslot), fphase & 1, abort_flag, p.err, 4)) return false;
+          if (!mbar_wait(bar_tfull(l, Ig & 3), (Ig >> 2) & 1, abort_flag, p.err, 4)) return false;
           trace_ev(p.trace, trw, 6, s, l);
           tc_fence_after();
-          const uint32_t taddr = tmem_base + lane_base + (ltw & 0xffffu);
+          const uint32_t taddr = tmem_base + lane_base + (uint32_t)(l * kAcc * P);
           const int o = r_lo - (NL - 1 - l) + ic;      // global output row
           const bool inside = col_in && o >= 0 && o < p.ny;
           if ((l == NL - 1) && last) {
-            // network output G (no ReLU), column 0 of the slot
+            // network output G (no ReLU), column 0 of the 16-column slot
             float v[1];
-            const uint32_t ta = taddr + (Ig & msk) * (uint32_t)P;
+            const uint32_t ta = taddr + (Ig & 3) * 16u;
             tmem_load<1>(ta, v);
             tmem_wait_ld();
             tmem_zero<1>(ta);
             tmem_wait_st();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(bar_tempty(l, Ig & msk));
+            if (lane == 0) mbar_arrive(bar_tempty(l, Ig & 3));
             if (col_valid) {
               const TileGeom &g = p.gg;
               p.G[(int64_t)(o - (g.i0 - g.h)) * g.pitch + (cm - (g.j0 - g.hx))] = v[0] + p.bias[l][0];
             }
             return true;
           }
-          uint32_t ta = taddr + (Ig & msk) * (uint32_t)P;   // ring-4 / im2col slot
-          int w5s = -1;                                     // W5: second slot (-1: none)
-          if (w5) {
-            int ms;
-            wide_slots(o, T, &ms, &w5s);
-            ta = taddr + (uint32_t)ms * P;
-          }
+          const uint32_t ta = taddr + (Ig & 3) * (uint32_t)P;
           uint32_t w[P / 2];
           const int m0 = NL == 1 ? p.mode : p.mode0;   // DDFB mode of the im2col layer
           if (kDdfb && is_im2col(l) && (m0 == 1 || m0 == 3)) {
@@ -919,34 +826,32 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
           for (int h = 0; h < P; h += 16) {
             float v[16];
             tmem_load<16>(ta + h, v);
-            if (w5s >= 0) {   // W5 row in two slots: (dy -1 [, 0] partial) + ([0,] +1 partial)
-              float v2[16];
-              tmem_load<16>(taddr + (uint32_t)w5s * P + h, v2);
-              tmem_wait_ld();
-#pragma unroll
-              for (int c = 0; c < 16; ++c) v[c] += v2[c];
-            }
             tmem_wait_ld();
 #pragma unroll
             for (int c = 0; c < 16; c += 4) {
               const float4 b4 = *reinterpret_cast<const float4 *>(&p.bias[l][h + c]);   // constant cache
-              w[(h + c) / 2] = pack_bf16(inside ? fmaxf(v[c] + b4.x, 0.f) : 0.f, inside ? fmaxf(v[c + 1] + b4.y, 0.f) : 0.f);
-              w[(h + c) / 2 + 1] = pack_bf16(inside ? fmaxf(v[c + 2] + b4.z, 0.f) : 0.f, inside ? fmaxf(v[c + 3] + b4.w, 0.f) : 0.f);
+              if (PNPULA_EPI_CVT) {
+                w[(h + c) / 2] = relu_pack_bf16(v[c] + b4.x, v[c + 1] + b4.y);
+                w[(h + c) / 2 + 1] = relu_pack_bf16(v[c + 2] + b4.z, v[c + 3] + b4.w);
+              } else {
+                w[(h + c) / 2] = pack_bf16(inside ? fmaxf(v[c] + b4.x, 0.f) : 0.f, inside ? fmaxf(v[c + 1] + b4.y, 0.f) : 0.f);
+                w[(h + c) / 2 + 1] = pack_bf16(inside ? fmaxf(v[c + 2] + b4.z, 0.f) : 0.f, inside ? fmaxf(v[c + 3] + b4.w, 0.f) : 0.f);
+              }
             }
+          }
+          if (PNPULA_EPI_CVT && __any_sync(0xffffffffu, !inside)) {
+#pragma unroll
+            for (int k = 0; k < P / 2; ++k) w[k] = inside ? w[k] : 0u;
           }
           }
           if (!im2col) {       // im2col MMAs overwrite (accumulate = 0): no re-zeroing needed
 #pragma unroll
             for (int c = 0; c < P; c += 16) tmem_zero<16>(ta + c);
-            if (w5s >= 0) {
-#pragma unroll
-              for (int c = 0; c < P; c += 16) tmem_zero<16>(taddr + (uint32_t)w5s * P + c);
-            }
             tmem_wait_st();
           }
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(bar_tempty(l, w5 ? Ig & 1u : Ig & msk));
+          if (lane == 0) mbar_arrive(bar_tempty(l, Ig & 3));
           trace_ev(p.trace, trw, 7, s, l);
           if (l < NL - 1) {
             // next layer's input fill = this layer's output row index ic
@@ -1090,12 +995,11 @@ cudaError_t dispatch_nl(const CnnChunkParams &p, int num_sms, cudaStream_t s) {
 
 }  // namespace
 
-size_t cnn_chunk_smem_bytes(int P, int nl, int first, int last, int nc, int wide_mask, int wide_slots) {
+size_t cnn_chunk_smem_bytes(int P, int nl, int first, int last, int nc) {
+  // (TMEM: nl * 4 P <= 512 columns holds for every chain max_nl admits)
   if (nl < 1 || nl > kMaxChunk) return SIZE_MAX;
   if (nl > max_nl(P)) return SIZE_MAX;
   if (nc != 1 && (nc != 3 || P < 32)) return SIZE_MAX;   // C = 3: N = 48 columns of the folded last layer
-  if (wide_mask && (P != 32 || (wide_slots != 5 && wide_slots != 6))) return SIZE_MAX;   // compiled for P = 32
-  if (tmem_plan(P, nl, first, last, nc, wide_mask, wide_slots, nullptr, nullptr) > 512u) return SIZE_MAX;
   return make_layout(P, nl, first, last, nc).total;
 }
 

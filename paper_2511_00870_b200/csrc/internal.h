@@ -142,9 +142,6 @@ struct CnnChunkParams {
   const float *xv;       // DDFB: v (padded, geometry xg) for modes 2 / 4
   int nc;                // image channels C (1, or 3 with P >= 32; reading R43): planes of x / G
   int64_t xcs, gcs;      // floats between the channel planes of x and of G
-  int wide_mask;         // bit l: layer l of this chunk accumulates in the wide TMEM scheme (cnn_kernels.cu);
-                         // a function of the net and the layer's global index only (bitwise tiling invariance)
-  int wide_slots;        // W = 5 or 6 slots of the wide scheme
 };
 
 // Launchers (return cudaGetLastError()).
@@ -171,9 +168,8 @@ cudaError_t launch_finalize(const FinalizeParams &p, cudaStream_t s);
 cudaError_t launch_debug_philox(uint64_t seed, const uint32_t *d_ctr, int64_t n, uint32_t *d_words, float *d_normals,
                                 int *d_bad, cudaStream_t s);
 cudaError_t launch_cnn_chunk(const CnnChunkParams &p, int num_sms, cudaStream_t s);
-// shared-memory bytes of a chain, or SIZE_MAX if it does not fit (shared memory / TMEM columns)
-size_t cnn_chunk_smem_bytes(int P, int nl, int first_is_input, int last_is_output, int nc, int wide_mask,
-                            int wide_slots);
+// shared-memory bytes of a chain, or SIZE_MAX if it does not fit
+size_t cnn_chunk_smem_bytes(int P, int nl, int first_is_input, int last_is_output, int nc);
 // Pack host fp32 OIHW weights of one layer into the device B-operand image (host side).
 void cnn_pack_layer(const float *w, int cout, int cin, uint16_t *out);
 size_t cnn_packed_layer_elems(int cout, int cin);

@@ -98,8 +98,6 @@ struct pnpula_ctx {
 
   // CNN
   std::vector<CnnChunk> chunks;
-  uint32_t wide_mask = 0;           // bit k-1: layer k uses the wide accumulator scheme (cnn_kernels.cu)
-  int wide_slots = 0;               // its slot count W (5 or 6)
   std::vector<uint16_t *> d_w;      // per layer packed weights
   std::vector<float *> d_b;         // per layer biases
   std::vector<std::vector<float>> h_b;   // host copies (passed to the CNN kernel as parameters)
@@ -337,8 +335,6 @@ pnpula_status run_cnn(pnpula_ctx *c, int buf) {
       p.nl = ch.nl;
       p.first_is_input = ch.l0 == 1;
       p.last_is_output = ch.l0 + ch.nl - 1 == c->n_layers;
-      p.wide_mask = (int)((c->wide_mask >> (ch.l0 - 1)) & ((1u << ch.nl) - 1u));
-      p.wide_slots = c->wide_slots;
       for (int l = 0; l < ch.nl; ++l) {
         p.w[l] = c->d_w[ch.l0 - 1 + l];
         const std::vector<float> &hb = c->h_b[ch.l0 - 1 + l];
@@ -728,36 +724,17 @@ pnpula_status build_halo_plan(pnpula_ctx *c) {
   return PNPULA_OK;
 }
 
-// Which layers accumulate in the wide TMEM scheme (cnn_kernels.cu wide_slots) and with how many
-// slots: the windowed 3x3 layers 2..K-1 of a P = 32 net.  A function of (K, P) only, so every
-// chunking (fused, layer-wise) and every tiling rounds each layer identically (R46).  Env (read
-// at create; kernel experiments): PNPULA_WSLOTS=4 (ring-4 everywhere) / 5 / 6 (default),
-// PNPULA_W5_MASK=<hex> (bit k-1 = layer k) restricts the wide layers.
-uint32_t wide_layers(const pnpula_ctx *c, int *slots) {
-  const char *e = getenv("PNPULA_WSLOTS");
-  *slots = e ? atoi(e) : 6;
-  if ((*slots != 5 && *slots != 6) || c->channels != 32) { *slots = 0; return 0; }
-  uint32_t m = 0;
-  const int K = c->n_layers;
-  for (int k = 2; k <= K - 1; ++k) m |= 1u << (k - 1);
-  if (const char *em = getenv("PNPULA_W5_MASK")) m &= (uint32_t)strtoul(em, nullptr, 16);
-  return m;
-}
-
-// CNN chunking: greedy, as many consecutive layers per launch as shared memory and TMEM allow.
+// CNN chunking: greedy, as many consecutive layers per launch as shared memory allows.
 void plan_cnn_chunks(pnpula_ctx *c) {
   c->chunks.clear();
   const int K = c->n_layers;
   const size_t budget = 227 * 1024;
-  c->wide_mask = wide_layers(c, &c->wide_slots);
   int l = 1;
   while (l <= K) {
     int best = 1;
     const int maxnl = (c->flags & PNPULA_FLAG_CNN_LAYERWISE) ? 1 : kMaxChunk;
     for (int nl = 1; nl <= std::min(maxnl, K - l + 1); ++nl) {
-      const int wm = (int)((c->wide_mask >> (l - 1)) & ((1u << nl) - 1u));
-      if (cnn_chunk_smem_bytes(c->channels, nl, l == 1, l + nl - 1 == K, c->nc, wm, c->wide_slots) <= budget)
-        best = nl;
+      if (cnn_chunk_smem_bytes(c->channels, nl, l == 1, l + nl - 1 == K, c->nc) <= budget) best = nl;
     }
     c->chunks.push_back({l, best, K - (l + best - 1)});
     l += best;
