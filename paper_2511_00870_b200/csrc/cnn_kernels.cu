@@ -344,7 +344,8 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
   constexpr uint32_t tmem_cols = tmem_need <= 32 ? 32 : tmem_need <= 64 ? 64 : tmem_need <= 128 ? 128
                                  : tmem_need <= 256 ? 256 : 512;
 
-  // ---- one-time setup: weights, biases, zero rings, barriers, TMEM
+  pdl_trigger();   // the next kernel's CTAs may start their own prologue as SMs free up
+  // ---- one-time setup: weights, biases, zero rings, barriers, TMEM (nothing the previous kernel wrote)
 #pragma unroll
   for (int l = 0; l < NL; ++l) {
     const int cin = (l == 0 && first) ? NC : P;
@@ -396,6 +397,7 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  pdl_wait();      // programmatic dependent launch: the previous kernel's writes are visible from here
 
   // valid output columns per strip: each fused layer costs one column per side; the folded
   // P -> 1 layer needs its MMA rows m +- 1, so a 1-layer chunk ending the net counts as 2
@@ -975,7 +977,18 @@ cudaError_t launch_pn(const CnnChunkParams &p0, int num_sms, cudaStream_t s) {
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
   if (e != cudaSuccess) return e;
   const int grid = p.units < num_sms ? p.units : num_sms;
-  kfn<<<grid, block_threads(NL), L.total, s>>>(p);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block_threads(NL));
+  cfg.dynamicSmemBytes = L.total;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = p.pdl ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, kfn, p);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

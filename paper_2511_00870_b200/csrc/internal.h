@@ -142,7 +142,18 @@ struct CnnChunkParams {
   const float *xv;       // DDFB: v (padded, geometry xg) for modes 2 / 4
   int nc;                // image channels C (1, or 3 with P >= 32; reading R43): planes of x / G
   int64_t xcs, gcs;      // floats between the channel planes of x and of G
+  int pdl;               // launch as a programmatic dependent of the previous kernel (see pdl_wait)
 };
+
+// Programmatic dependent launch (PDL): the CNN chain kernels are launched as dependents of the
+// kernel before them, so their prologue (weights to shared memory, barriers, TMEM) runs on the SMs
+// the previous kernel's CTAs have left while its last CTAs finish; they execute griddepcontrol.wait
+// before touching anything the previous kernel wrote.  Every kernel that can precede a CNN launch
+// signals griddepcontrol.launch_dependents at its start.  Env PNPULA_PDL=0 at create: plain launches.
+#if defined(__CUDACC__)
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+#endif
 
 // Launchers (return cudaGetLastError()).
 cudaError_t launch_update(const UpdateParams &p, cudaStream_t s);

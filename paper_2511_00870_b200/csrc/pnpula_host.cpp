@@ -142,6 +142,7 @@ struct pnpula_ctx {
   // halo-exchange overlap (row-strip tiles with NCCL messages): boundary bands first, then the
   // exchange on comm_stream concurrently with the interior update
   bool overlap = false;
+  int pdl = 1;                     // CNN launches as programmatic dependents (internal.h pdl_wait)
   cudaMemPool_t pool = nullptr;    // stream-ordered pool of the per-tile buffers (see dmalloc)
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t ev_bands = nullptr, ev_halo = nullptr;
@@ -313,6 +314,7 @@ pnpula_status run_ddfb(pnpula_ctx *c, int buf) {
       p.gg = g;
       p.ny = c->ny; p.nx = c->nx;
       p.err = c->d_err;
+      p.pdl = c->pdl;
       cudaEvent_t end;
       timer_begin(c, c->tm_cnn, &end);
       CU(c, launch_cnn_chunk(p, c->num_sms, c->stream));
@@ -362,6 +364,7 @@ pnpula_status run_cnn(pnpula_ctx *c, int buf) {
       p.nc = c->nc;
       p.xcs = p.gcs = (int64_t)geom_elems(g);
       p.err = c->d_err;
+      p.pdl = c->pdl;
       // optional pipeline trace of the first evaluation (diagnostics; env PNPULA_CNN_TRACE=<path prefix>)
       const char *trace_path = getenv("PNPULA_CNN_TRACE");
       unsigned long long *d_trace = nullptr;
@@ -1008,6 +1011,10 @@ pnpula_status pnpula_create(const pnpula_config *cfg, pnpula_ctx **out) {
   {
     const char *pe = getenv("PNPULA_POOL");
     if (!(pe && atoi(pe) == 0)) c->pool = device_pool(f.device);
+  }
+  {
+    const char *pe2 = getenv("PNPULA_PDL");
+    c->pdl = (pe2 && atoi(pe2) == 0) ? 0 : 1;
   }
   {
     const char *ge = getenv("PNPULA_GRAPHS");

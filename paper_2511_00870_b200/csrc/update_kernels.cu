@@ -305,6 +305,7 @@ __device__ __forceinline__ void ula_quad(const UpdateParams &p, const IterScalar
 template <int RY_, int RX_, bool SEP>
 __global__ void __launch_bounds__(NTHREADS)
 update_conv_kernel(const __grid_constant__ UpdateParams p) {
+  pdl_trigger();
   extern __shared__ float smem[];
   it_advance(p);
   const IterScalars is = iter_scalars(p);
@@ -466,6 +467,7 @@ template <int R, int TVM>
 __global__ void __launch_bounds__(NTHREADS, 2)
 update_sep_kernel(const __grid_constant__ UpdateParams p, const __grid_constant__ CUtensorMap tmx,
                   const __grid_constant__ CUtensorMap tmy, int nbx, int nblk) {
+  pdl_trigger();
   using Gm = SepGeom<R>;
   constexpr int XR = Gm::XR, XC = Gm::XC, RR = Gm::RR, RC = Gm::RC, NW = Gm::NW;
   static_assert(RC % 4 == 0 && XC % 4 == 0 && NW % 4 == 0, "R must be even");
@@ -640,6 +642,7 @@ update_sep_kernel(const __grid_constant__ UpdateParams p, const __grid_constant_
 // so the Philox call is shared exactly as in the x-update), 2-D stencil of x+ read through L1.
 // Pixels outside tile (+) r_H or the image are skipped (z1 stays 0 outside the image).
 __global__ void __launch_bounds__(NTHREADS) z1_update_kernel(const __grid_constant__ Z1Params p) {
+  pdl_trigger();
   const uint32_t t1 = iter_t1(p);
   const TileGeom &g = p.g;
   const int ry = p.ry, rx = p.rx, kw = 2 * rx + 1;
@@ -681,6 +684,7 @@ template <int R>
 __global__ void __launch_bounds__(NTHREADS) z1_sep_kernel(const __grid_constant__ Z1Params p,
                                                         const __grid_constant__ CUtensorMap tmx, int r0, int q0,
                                                         int nbx) {
+  pdl_trigger();
   const uint32_t t1 = iter_t1(p);
   // the staged columns start 16-B aligned (XL = R rounded up to 4): TMA tile loads need a
   // 16-B aligned inner start coordinate
@@ -781,6 +785,7 @@ __global__ void __launch_bounds__(NTHREADS) z1_sep_kernel(const __grid_constant_
 // One thread per column quad of tile (+) 1 (global quads: the Philox calls match the oracle's
 // (stream, pixel) counters); D x+ from the padded x+ (halo >= 2), block soft threshold per pixel.
 __global__ void __launch_bounds__(NTHREADS) tv_z_kernel(const __grid_constant__ TvZParams p) {
+  pdl_trigger();
   const uint32_t t1 = iter_t1(p);
   const TileGeom &g = p.g;
   const int r0 = max(g.i0 - 1, 0), r1 = min(g.i0 + g.th + 1, p.ny);
@@ -928,6 +933,7 @@ __global__ void opnorm_init_kernel(const __grid_constant__ OpNormParams p) {
 
 // ---------------------------------------------------------------- mask K7 (no stencil)
 __global__ void __launch_bounds__(NTHREADS) update_mask_kernel(const __grid_constant__ UpdateParams p) {
+  pdl_trigger();
   it_advance(p);
   const IterScalars is = iter_scalars(p);
   const TileGeom &g = p.g;
@@ -948,6 +954,7 @@ __global__ void __launch_bounds__(NTHREADS) update_mask_kernel(const __grid_cons
 }
 
 __global__ void copy_jobs_kernel(const CopyJob *__restrict__ jobs) {
+  pdl_trigger();
   const CopyJob j = jobs[blockIdx.y];
   const int64_t n = (int64_t)j.rows * j.cols;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
