@@ -45,6 +45,17 @@ namespace {
 #define PNPULA_EPI_GROUPS 4
 #endif
 constexpr int kRowPos = 130;                    // positions per ring row (128 MMA rows + 1 each side)
+// Shared-memory alignment of the activation rings (r02, exp/mma_align.cu): a tcgen05 operand whose
+// core matrices (8 rows x 16 B) do not start on a 128-B boundary costs about 1.3x the fetch of an
+// aligned one (N = 96: ~90 vs ~69 cycles).  The dx taps shift A by 16 B, so at most one of the
+// three can be aligned: the channel-group stride is padded to 136 positions (2,176 B = 17 x 128)
+// and each ring starts 16 B before a 128-B boundary, so position 1 -- the centre tap of a windowed
+// layer and the unshifted A of the folded last layer -- is aligned in every channel group.
+#ifndef PNPULA_RING_ALIGN
+#define PNPULA_RING_ALIGN 0   // measured neutral on c5 (profiles/r02_cnn_schemes.md): off, 6 KB less smem
+#endif
+constexpr int kRowStride = PNPULA_RING_ALIGN ? 136 : kRowPos;   // positions between channel groups
+constexpr uint32_t kRingPad = PNPULA_RING_ALIGN ? 112u : 0u;      // ring base = 128 k + 112
 constexpr int kEpiGroups = PNPULA_EPI_GROUPS;   // max epilogue groups (each: 4 warps = 4 TMEM lane quarters)
 #ifndef PNPULA_MMA_WARPS
 #define PNPULA_MMA_WARPS 4
@@ -103,9 +114,11 @@ __host__ __device__ inline uint32_t packed_layer_elems(int cout, int cin) {
 __host__ __device__ inline SmemLayout make_layout(int P, int nl, int first, int last, int nc) {
   SmemLayout L{};
   uint32_t off = 0;
-  const uint32_t act_slot = (uint32_t)(P / 8) * kRowPos * 16u;
+  const uint32_t act_slot = (uint32_t)(P / 8) * kRowStride * 16u;
   for (int l = 0; l < nl; ++l) {
-    L.slot_bytes[l] = (l == 0 && first) ? (uint32_t)(im2col_k(nc) / 8) * 128u * 16u : act_slot;
+    const bool im = l == 0 && first;
+    L.slot_bytes[l] = im ? (uint32_t)(im2col_k(nc) / 8) * 128u * 16u : act_slot;
+    if (!im) off += kRingPad;   // position 1 of every activation row on a 128-B boundary
     L.ring_off[l] = off;
     off = align_up(off + ring_slots(l) * L.slot_bytes[l], 128);
   }
@@ -321,7 +334,7 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr int G = P / 8;              // channel groups of 8
   constexpr int KS = P / 16;            // K steps per tap
-  constexpr uint32_t GS = kRowPos * 16; // bytes between channel groups in a ring row
+  constexpr uint32_t GS = kRowStride * 16; // bytes between channel groups in a ring row
   const bool first = p.first_is_input != 0;
   const bool last = p.last_is_output != 0;
   const SmemLayout L = make_layout(P, NL, first, last, NC);
