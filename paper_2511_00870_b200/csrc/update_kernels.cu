@@ -453,18 +453,27 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map
       : "memory");
 }
 
+// PNPULA_UPD_CTAS (kernel experiment): CTAs per SM of update_sep_kernel.  3 keeps the residual
+// H x - y in place of the staged y it is formed from (each phase-2 item reads its own 4 y values
+// and writes its 4 residuals at the same addresses), so a CTA needs ~70 KB of shared memory.
+#ifndef PNPULA_UPD_CTAS
+#define PNPULA_UPD_CTAS 2
+#endif
+constexpr int kUpdCtas = PNPULA_UPD_CTAS;
 template <int R>
 struct SepGeom {
   static constexpr int XR = TY + 4 * R, XC = TX + 4 * R;   // x region
   static constexpr int RR = TY + 2 * R, RC = TX + 2 * R;   // residual region (y staged RR x XC)
   static constexpr int NW = 2 * R + 4;                     // inputs of a 4-wide output block
-  static constexpr size_t floats = 2 * (size_t)XR * XC + 2 * (size_t)RR * XC + (size_t)XR * RC + (size_t)RR * RC;
+  static constexpr bool kRsInY = kUpdCtas >= 3 && R % 4 == 0;   // float4-aligned in-place residual
+  static constexpr size_t floats = 2 * (size_t)XR * XC + 2 * (size_t)RR * XC + (size_t)XR * RC +
+                                   (kRsInY ? 0 : (size_t)RR * RC);
   static_assert((XR * XC * 4) % 128 == 0 && (RR * XC * 4) % 128 == 0, "TMA destinations 128-B aligned");
   static constexpr size_t bytes = floats * sizeof(float) + 16;   // + 2 mbarriers
 };
 
 template <int R, int TVM>
-__global__ void __launch_bounds__(NTHREADS, 2)
+__global__ void __launch_bounds__(NTHREADS, kUpdCtas)
 update_sep_kernel(const __grid_constant__ UpdateParams p, const __grid_constant__ CUtensorMap tmx,
                   const __grid_constant__ CUtensorMap tmy, int nbx, int nblk) {
   pdl_trigger();
@@ -479,7 +488,9 @@ update_sep_kernel(const __grid_constant__ UpdateParams p, const __grid_constant_
   // memory: the dynamic region then starts 1024-B aligned, as the TMA destinations need)
   uint64_t *const full_bar = reinterpret_cast<uint64_t *>(sm + Gm::floats);
   float *const T1 = sm + 2 * XR * XC + 2 * RR * XC;   // horizontal forward pass, XR x RC
-  float *const Rs = T1 + XR * RC;                     // residual H x - y, RR x RC
+  // residual H x - y, RR x RC (Gm::kRsInY: in place of the staged y of this block, row pitch XC)
+  float *const Rs0 = T1 + XR * RC;
+  constexpr int RP = Gm::kRsInY ? XC : RC;
   const TileGeom &g = p.g;
   const int tid = threadIdx.x;
   const float *ky = p.ky, *kx = p.kx;   // parameter space: FFMA constant-bank operands
@@ -513,7 +524,9 @@ update_sep_kernel(const __grid_constant__ UpdateParams p, const __grid_constant_
     const int bi0 = g.i0 + (blk / nbx) * TY;
     const int bj0 = (g.j0 & ~3) + (blk - (blk / nbx) * nbx) * TX;
     float *const X = sm + buf * XR * XC;
-    const float *const Y = sm + 2 * XR * XC + buf * RR * XC;
+    float *const Yw = sm + 2 * XR * XC + buf * RR * XC;
+    const float *const Y = Yw;
+    float *const Rs = Gm::kRsInY ? Yw + R : Rs0;
     float *const T2 = X;
 
     // the update's own operands (x, G, z, mean, M2 of this thread's 2 rows x 1 quad) are
@@ -586,7 +599,7 @@ update_sep_kernel(const __grid_constant__ UpdateParams p, const __grid_constant_
         const bool rin = gi >= 0 && gi < p.ny;
 #pragma unroll
         for (int j = 0; j < 4; ++j) o[j] = (rin && gj + j >= 0 && gj + j < p.nx) ? p.eta * o[j] - yv[j] : 0.f;
-        *reinterpret_cast<float4 *>(Rs + a * RC + 4 * k4) = make_float4(o[0], o[1], o[2], o[3]);
+        *reinterpret_cast<float4 *>(Rs + a * RP + 4 * k4) = make_float4(o[0], o[1], o[2], o[3]);
       }
     }
     __syncthreads();
@@ -596,7 +609,7 @@ update_sep_kernel(const __grid_constant__ UpdateParams p, const __grid_constant_
       float rs[NW];
 #pragma unroll
       for (int i = 0; i < NW; i += 4) {
-        const float4 t = *reinterpret_cast<const float4 *>(Rs + a * RC + 4 * k4 + i);
+        const float4 t = *reinterpret_cast<const float4 *>(Rs + a * RP + 4 * k4 + i);
         rs[i] = t.x; rs[i + 1] = t.y; rs[i + 2] = t.z; rs[i + 3] = t.w;
       }
       float o[4];
@@ -1061,7 +1074,7 @@ cudaError_t launch_update(const UpdateParams &p, cudaStream_t s) {
       const int XC = TX + 4 * R;
       if (!encode_padded_2d(&tmx, p.x, p.g, XC, TY + 4 * R) || !encode_padded_2d(&tmy, p.y, p.g, XC, TY + 2 * R))
         return cudaErrorInvalidValue;
-      const int grid = nblk < 2 * num_sms ? nblk : 2 * num_sms;
+      const int grid = nblk < kUpdCtas * num_sms ? nblk : kUpdCtas * num_sms;
       kfn<<<grid, NTHREADS, smem, s>>>(p, tmx, tmy, nbx, nblk);
       return cudaGetLastError();
     }
