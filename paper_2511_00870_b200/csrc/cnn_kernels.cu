@@ -246,6 +246,22 @@ __device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t adesc, uint64
       : "memory");
 }
 
+// A-operand collector reuse (kernel experiment PNPULA_COLLECTOR_A): the first MMA of a ring-wrap
+// split pair keeps its A tile in the tensor core's operand collector, the second reuses it.
+__device__ __forceinline__ void mma_bf16_afill(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc) {
+  asm volatile("tcgen05.mma.cta_group::1.kind::f16.collector::a::fill [%0], %1, %2, %3, 1;" ::"r"(d_tmem), "l"(adesc),
+               "l"(bdesc), "r"(idesc)
+               : "memory");
+}
+__device__ __forceinline__ void mma_bf16_alast(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc) {
+  asm volatile("tcgen05.mma.cta_group::1.kind::f16.collector::a::lastuse [%0], %1, %2, %3, 1;" ::"r"(d_tmem), "l"(adesc),
+               "l"(bdesc), "r"(idesc)
+               : "memory");
+}
+#ifndef PNPULA_COLLECTOR_A
+#define PNPULA_COLLECTOR_A 0
+#endif
+
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
                : "memory");
@@ -634,8 +650,13 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
                 for (int ks = 0; ks < KS; ++ks) {
                   const uint64_t ad = ad0 + (uint64_t)((2 * ks * GS + dx * 16) >> 4);
                   const uint64_t bd = bd0 + (uint64_t)((dx * KS + ks) * bstep);
-                  mma_bf16(d1, ad, bd + (uint64_t)(q0 * Cb), id1, 1);
-                  if (n2 > 0) mma_bf16(d2, ad, bd + (uint64_t)((q0 + n1) * Cb), id2, 1);
+                  if (PNPULA_COLLECTOR_A && n2 > 0) {
+                    mma_bf16_afill(d1, ad, bd + (uint64_t)(q0 * Cb), id1);
+                    mma_bf16_alast(d2, ad, bd + (uint64_t)((q0 + n1) * Cb), id2);
+                  } else {
+                    mma_bf16(d1, ad, bd + (uint64_t)(q0 * Cb), id1, 1);
+                    if (n2 > 0) mma_bf16(d2, ad, bd + (uint64_t)((q0 + n1) * Cb), id2, 1);
+                  }
                 }
               }
             }
