@@ -122,3 +122,19 @@ def test_create_validates_before_touching_the_gpu():
         pk.Sampler(ny=16, nx=16, y=y, sigma2=0.1, gamma=0.01, op="mask", mask=np.ones((16, 16), np.uint8),
                    weights=w, biases=w, n_layers=3, channels=24, alpha=1.0, eps=0.1)
     assert e.value.status == 10          # unsupported channel count
+
+
+def test_create_validates_colour_and_prior_combinations():
+    y3 = np.zeros((3, 16, 16), np.float32)
+    m = np.ones((16, 16), np.uint8)
+    w = np.zeros(4 * 16 * 3 * 9, np.float32)
+    with pytest.raises(pk.PnpulaError) as e:   # colour DDFB needs P = 32 / 64 (N = 48 folded adjoint)
+        pk.Sampler(ny=16, nx=16, y=y3, sigma2=0.1, gamma=0.01, op="mask", mask=m, weights=w, n_layers=4,
+                   channels=16, alpha=1.0, eps=0.1, den_kind="ddfb", ddfb_gammas=np.ones(4, np.float32), ht_eps=0.05)
+    assert e.value.status == 10
+    with pytest.raises(pk.PnpulaError) as e:   # img_channels other than 1 / 3
+        pk.Sampler(ny=16, nx=16, y=np.zeros((2, 16, 16), np.float32), sigma2=0.1, gamma=0.01, op="mask", mask=m)
+    assert e.value.status == 10
+    with pytest.raises(pk.PnpulaError) as e:   # TV needs its z block (rho > 0) and no box term
+        pk.Sampler(ny=16, nx=16, y=y3, sigma2=0.1, gamma=0.01, op="mask", mask=m, tv_beta=1.0)
+    assert e.value.status == 1
