@@ -82,48 +82,6 @@ constexpr int kRingAct = PNPULA_RING_ACT;       // ring slots of the epilogue-fe
 static_assert(kRingAct >= 3 && kRingAct <= 8, "input ring slots");
 __host__ __device__ constexpr uint32_t ring_slots(int l) { return l == 0 ? (uint32_t)kRing : (uint32_t)kRingAct; }
 constexpr int kAcc = 4;                         // accumulator-row slots per layer (TMEM)
-// "Shadow-5" accumulator layout (r02; P = 32 single-channel chains of 3-4 layers, PNPULA_SHADOW).
-// Ring-4 keeps output row o in slot o mod 4; a fill (input row f: output rows f-2, f-1, f) whose
-// three slots wrap the ring is issued as two MMAs (N = 64 + 32), and every tcgen05.mma costs at
-// least ~44 cycles whatever its N (exp/mma_ts.cu: N = 96 48-56, N = 32 44, a split pair 88), so the
-// wrapping half of the fills cost ~1.6x.  Shadow-5 gives a windowed layer a fifth 32-column
-// position (4) that shadows slot 0: a slot-0 row accumulates its first two fills (dy = -1, 0) at
-// position 4 and its last fill (dy = +1) at position 0, and the epilogue adds the two.  Windows
-// (2,3,0) become positions 2,3,4 (one MMA); only (3,0,1) -> 3,4 | 1 still splits: 1 fill in 4.
-// The slot is the GLOBAL output row mod 4 (not a per-CTA row counter) so that which rows sum two
-// partials -- the only rounding difference -- is a function of the pixel, and results stay bitwise
-// independent of the tile grid; per-slot mbarrier phases are tracked as parity bits.  TMEM:
-// 3 windowed layers x 160 + the im2col layer (1 slot) or the folded last layer (32) = 512.
-#ifndef PNPULA_SHADOW
-#define PNPULA_SHADOW 0   // measured slower on c5 (profiles/r02_cnn_schemes.md): off
-#endif
-#ifndef PNPULA_SHADOW_NOPOS
-#define PNPULA_SHADOW_NOPOS 0   // experiment: shadow TMEM plan and global-row slots, ring-4 positions
-#endif
-#ifndef PNPULA_SHADOW_MIN_IM
-#define PNPULA_SHADOW_MIN_IM 0   // log2 of the fewest im2col accumulator slots a shadow plan may use
-#endif
-__host__ __device__ constexpr bool shadow_ok(int P, int NL, int NC) {
-  return PNPULA_SHADOW && P == 32 && NC == 1 && NL >= 3 && NL <= 4;
-}
-// TMEM plan of a chain.  w[l] = first column | shadow << 16 | log2(im2col slots) << 20.  Returns
-// the columns used.  Legacy (ring-4) plan: layer l at 4 P l, im2col 4 slots.
-__host__ __device__ inline uint32_t tmem_plan(int P, int nl, int first, int last, int nc, bool sh, uint32_t *w) {
-  if (sh) {
-    for (int lg = 2; lg >= PNPULA_SHADOW_MIN_IM; --lg) {
-      uint32_t tot = 0;
-      for (int l = 0; l < nl; ++l) {
-        const bool im = l == 0 && first, nlst = l == nl - 1 && last && !im;
-        if (w) w[l] = tot | ((im || nlst) ? 0u : 1u << 16) | ((uint32_t)lg << 20);
-        tot += im ? ((uint32_t)P << lg) : nlst ? 32u * (uint32_t)nc : 5u * (uint32_t)P;
-      }
-      if (tot <= 512u) return tot;
-    }
-  }
-  for (int l = 0; l < nl; ++l)
-    if (w) w[l] = (uint32_t)(l * kAcc * P) | (2u << 20);
-  return (uint32_t)(nl * kAcc * P);
-}
 constexpr int kXS = 136;                        // staged floats per x row (130 ring positions + alignment)
 #ifndef PNPULA_LAG
 #define PNPULA_LAG 3
@@ -278,12 +236,8 @@ __host__ __device__ constexpr uint32_t make_idesc(int N) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
 }
 
-#ifndef PNPULA_ABL
-#define PNPULA_ABL 0   // timing ablations (results garbage): 1 no MMAs, 2 no epilogue TMEM ld / zero, 4 no ring STS
-#endif
 __device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                          uint32_t accumulate) {
-  if (PNPULA_ABL & 1) return;
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
@@ -413,12 +367,11 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + L.misc_off);
   volatile int *abort_flag = reinterpret_cast<volatile int *>(smem + L.misc_off + 4);
   const uint32_t bar_done = sbase + L.misc_off + 8;
-  // TMEM: per-layer column ranges from tmem_plan (ring-4: layer l owns [4Pl, 4Pl + 4P), slot q at
-  // 4Pl + qP; shadow-5: see tmem_plan), kept in the layer table's .w
-  constexpr bool kSh = shadow_ok(P, NL, NC);
-  const uint32_t tmem_need = tmem_plan(P, NL, first, last, NC, kSh, nullptr);
-  const uint32_t tmem_cols = tmem_need <= 32 ? 32 : tmem_need <= 64 ? 64 : tmem_need <= 128 ? 128
-                             : tmem_need <= 256 ? 256 : 512;
+  // TMEM: layer l owns columns [l*4P, l*4P + 4*Cb): accumulator-row slot q at l*4P + q*Cb
+  constexpr uint32_t tmem_need = (uint32_t)NL * kAcc * P;
+  static_assert(tmem_need <= 512, "TMEM columns");
+  constexpr uint32_t tmem_cols = tmem_need <= 32 ? 32 : tmem_need <= 64 ? 64 : tmem_need <= 128 ? 128
+                                 : tmem_need <= 256 ? 256 : 512;
 
   pdl_trigger();   // the next kernel's CTAs may start their own prologue as SMs free up
   // ---- one-time setup: weights, biases, zero rings, barriers, TMEM (nothing the previous kernel wrote)
@@ -450,9 +403,7 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
       for (int w = 0; w < kProdWarps; ++w) mbar_init(sbase + L.xs_off + (uint32_t)(kProdWarps * 3 * NC * kXS) * 4u + w * 8u, 1);
     *abort_flag = 0;
     uint4 *tab = reinterpret_cast<uint4 *>(smem + L.misc_off + 16);
-    uint32_t tw[NL];
-    tmem_plan(P, NL, first, last, NC, kSh, tw);
-    for (int l = 0; l < NL; ++l) tab[l] = make_uint4(L.ring_off[l], L.slot_bytes[l], L.w_off[l], tw[l]);
+    for (int l = 0; l < NL; ++l) tab[l] = make_uint4(L.ring_off[l], L.slot_bytes[l], L.w_off[l], 0u);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == kMma0) {
@@ -498,10 +449,6 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
   auto Ocnt = [&](int l) { return sumRn + kdone * (uint32_t)(2 * (NL - 1 - l)); };
 
   uint32_t xphase = 0;   // im2col producers: phase of this warp's x-staging mbarrier
-  // shadow-5 windowed layers (kSh): per-slot (global row mod 4) mbarrier state as bits -- MMA
-  // warp: slot used / tempty use parity; epilogue: tfull parity.  In every shadow-capable chain a
-  // warp owns exactly one layer (NL <= 4 MMA warps and epilogue groups).
-  uint32_t sh_used = 0, sh_par = 0, sh_epar = 0;
   for (int u = blockIdx.x; u < units; u += gridDim.x) {
     if (*abort_flag) break;
     const int rb = u / strips, strip = u - (u / strips) * strips;
@@ -645,75 +592,26 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
           // output row that receives its first contribution (im2col: the only one)
           const uint32_t O0 = Ocnt(l);
           const uint32_t Ig = O0 + (uint32_t)f;
-          const uint4 lt = ltab[l];
-          const uint32_t lgim = (lt.w >> 20) & 7u;               // log2 of the im2col slots
-          const int ofirst = r_lo - (NL - 1 - l);                // global row of output row 0
           if (netlast) {   // 2-slot ring of per-fill accumulators: fill Fg-2 must have been read
             if (ok && Fg >= 2u) ok = mbar_wait(bar_tempty(l, Fg & 1), ((Fg >> 1) - 1) & 1, abort_flag, p.err, 3);
-          } else if (kSh && !im2col) {
-            if (ok && f < no) {   // row f's slot: wait until its previous occupant was drained
-              const uint32_t sl = (uint32_t)(ofirst + f) & 3u;
-              if ((sh_used >> sl) & 1u) ok = mbar_wait(bar_tempty(l, sl), ((sh_par >> sl) & 1u) ^ 1u, abort_flag, p.err, 3);
-              sh_used |= 1u << sl;
-              sh_par ^= 1u << sl;
-            }
-          } else if (kSh) {       // im2col layer with 2^lgim slots
-            if (ok && f < no && Ig >= (1u << lgim))
-              ok = mbar_wait(bar_tempty(l, Ig & ((1u << lgim) - 1u)), ((Ig >> lgim) - 1) & 1, abort_flag, p.err, 3);
           } else if (ok && f < no && Ig >= (uint32_t)kAcc)
             ok = mbar_wait(bar_tempty(l, Ig & 3), ((Ig >> 2) - 1) & 1, abort_flag, p.err, 3);
           ok = __shfl_sync(0xffffffffu, ok ? 1 : 0, 0) != 0;
           trace_ev(p.trace, tr_on && lane == 0, 4, s, l);
           if (!ok) return false;
           tc_fence_after();
-          const uint32_t acc0 = tmem_base + (kSh ? (lt.w & 0xffffu) : (uint32_t)(l * kAcc * P));
+          const uint4 lt = ltab[l];
+          const uint32_t acc0 = tmem_base + (uint32_t)(l * kAcc * P);
           const uint32_t wbase = sbase + lt.z;
           const uint32_t slot = sbase + lt.x + rs * lt.y;
           if (im2col) {
             const uint64_t ad = make_desc(slot, 2048, 128);
             const uint64_t bd = make_desc(wbase, (uint32_t)P * 16, 128);
-            const uint32_t isl = kSh ? (Ig & ((1u << lgim) - 1u)) : (Ig & 3);
             if (elect_one()) {
 #pragma unroll
               for (int ks = 0; ks < K0 / 16; ++ks)   // K step = 2 core-matrix groups of A and B
-                mma_bf16(acc0 + isl * P, ad + (uint64_t)(ks * 256), bd + (uint64_t)(ks * 2 * P),
+                mma_bf16(acc0 + (Ig & 3) * P, ad + (uint64_t)(ks * 256), bd + (uint64_t)(ks * 2 * P),
                          make_idesc(P), ks > 0 ? 1u : 0u);
-            }
-          } else if (kSh && !netlast) {
-            // windowed layer, global-row slots; rows ilo..ihi of this fill at positions pos(i):
-            // slot (o mod 4), or 4 for a slot-0 row that is not the fill's dy = +1 row (i != f-2)
-            // when the layer is shadowed.  At most two contiguous runs (one split).
-            const uint32_t Cb = (uint32_t)P;
-            const bool shl = !PNPULA_SHADOW_NOPOS && ((lt.w >> 16) & 1u) != 0;
-            const int ilo = f - 2 > 0 ? f - 2 : 0;
-            const int ihi = f < no - 1 ? f : no - 1;
-            auto pos = [&](int i) -> uint32_t {
-              const uint32_t sl = (uint32_t)(ofirst + i) & 3u;
-              return (shl && sl == 0u && i != f - 2) ? 4u : sl;
-            };
-            const int n = ihi - ilo + 1;
-            const uint32_t p0 = pos(ilo);
-            int n1 = 1;
-            if (n >= 2 && pos(ilo + 1) == p0 + 1u) n1 = (n >= 3 && pos(ilo + 2) == p0 + 2u) ? 3 : 2;
-            const int n2 = n - n1;
-            const uint32_t p2 = n2 > 0 ? pos(ilo + n1) : 0u;
-            const uint64_t ad0 = make_desc(slot, GS, 128);
-            const uint64_t bd0 = make_desc(wbase, 3u * Cb * 16u, 128);
-            const uint32_t bstep = 3u * Cb * 2u;
-            const uint32_t q0 = (uint32_t)(ilo - (f - 2));
-            const uint32_t d1 = acc0 + p0 * Cb, d2 = acc0 + p2 * Cb;
-            const uint32_t id1 = make_idesc((int)(n1 * Cb)), id2 = make_idesc((int)((n2 > 0 ? n2 : 1) * Cb));
-            if (n > 0 && elect_one()) {
-#pragma unroll
-              for (int dx = 0; dx < 3; ++dx) {
-#pragma unroll
-                for (int ks = 0; ks < KS; ++ks) {
-                  const uint64_t ad = ad0 + (uint64_t)((2 * ks * GS + dx * 16) >> 4);
-                  const uint64_t bd = bd0 + (uint64_t)((dx * KS + ks) * bstep);
-                  mma_bf16(d1, ad, bd + (uint64_t)(q0 * Cb), id1, 1);
-                  if (n2 > 0) mma_bf16(d2, ad, bd + (uint64_t)((q0 + n1) * Cb), id2, 1);
-                }
-              }
             }
           } else if (netlast) {
             // P -> 1 layer: all nine taps folded into N = 16 (column n = q*3 + dxi, q = 1 - dy),
@@ -770,11 +668,7 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
               mma_commit(bar_tfull(l, Fg & 1));          // this fill's tap sums
             } else {
               const int ic = im2col ? f : f - 2;         // output row completed by this group
-              if (ic >= 0 && ic < no) {
-                uint32_t sl = (O0 + (uint32_t)ic) & 3;
-                if (kSh) sl = im2col ? ((O0 + (uint32_t)ic) & ((1u << lgim) - 1u)) : ((uint32_t)(ofirst + ic) & 3u);
-                mma_commit(bar_tfull(l, sl));
-              }
+              if (ic >= 0 && ic < no) mma_commit(bar_tfull(l, (O0 + (uint32_t)ic) & 3));
             }
           }
           __syncwarp();
@@ -824,7 +718,7 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
           float d[NC][16];
 #pragma unroll
           for (int co = 0; co < NC; ++co)
-            tmem_load<16>(tmem_base + lane_base + (kSh ? (ltab[l].w & 0xffffu) : (uint32_t)(l * kAcc * P)) + (Fg & 1) * 16u * NC + co * 16u, d[co]);
+            tmem_load<16>(tmem_base + lane_base + (uint32_t)(l * kAcc * P) + (Fg & 1) * 16u * NC + co * 16u, d[co]);
           tmem_wait_ld();
           tc_fence_before();
           __syncwarp();
@@ -908,22 +802,11 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
           const bool im2col = is_im2col(l);
           const int s = (im2col ? ic : ic + 2) + kLag * l;
           const uint32_t Ig = Ocnt(l) + (uint32_t)ic;
-          const int o = r_lo - (NL - 1 - l) + ic;      // global output row
-          // accumulator slot of this row and the tfull phase (ring-4: Ig mod 4; shadow-capable
-          // chains: im2col Ig mod 2^lgim, windowed layers the global row mod 4 with tracked parity)
-          const uint32_t ltw = kSh ? ltab[l].w : 0u;
-          const uint32_t lgim = (ltw >> 20) & 7u;
-          uint32_t esl = Ig & 3, eph = (Ig >> 2) & 1;
-          if (kSh) {
-            if (im2col) { esl = Ig & ((1u << lgim) - 1u); eph = (Ig >> lgim) & 1u; }
-            else { esl = (uint32_t)o & 3u; eph = (sh_epar >> esl) & 1u; sh_epar ^= 1u << esl; }
-          }
-          if (!mbar_wait(bar_tfull(l, esl), eph, abort_flag, p.err, 4)) return false;
+          if (!mbar_wait(bar_tfull(l, Ig & 3), (Ig >> 2) & 1, abort_flag, p.err, 4)) return false;
           trace_ev(p.trace, trw, 6, s, l);
           tc_fence_after();
-          const uint32_t taddr = tmem_base + lane_base + (kSh ? (ltw & 0xffffu) : (uint32_t)(l * kAcc * P));
-          // shadow-5 slot-0 row: its dy = -1 / 0 partial sits at position 4 (see tmem_plan)
-          const bool two = !PNPULA_SHADOW_NOPOS && kSh && !im2col && ((ltw >> 16) & 1u) && esl == 0u;
+          const uint32_t taddr = tmem_base + lane_base + (uint32_t)(l * kAcc * P);
+          const int o = r_lo - (NL - 1 - l) + ic;      // global output row
           const bool inside = col_in && o >= 0 && o < p.ny;
           if ((l == NL - 1) && last) {
             // network output G (no ReLU), column 0 of the 16-column slot
@@ -942,8 +825,7 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
             }
             return true;
           }
-          const uint32_t ta = taddr + esl * (uint32_t)P;
-          const uint32_t ta4 = taddr + 4u * (uint32_t)P;
+          const uint32_t ta = taddr + (Ig & 3) * (uint32_t)P;
           uint32_t w[P / 2];
           const int m0 = NL == 1 ? p.mode : p.mode0;   // DDFB mode of the im2col layer
           if (kDdfb && is_im2col(l) && (m0 == 1 || m0 == 3)) {
@@ -979,18 +861,7 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
 #pragma unroll
           for (int h = 0; h < P; h += 16) {
             float v[16];
-            if (PNPULA_ABL & 2) {
-#pragma unroll
-              for (int c = 0; c < 16; ++c) v[c] = (float)(c + h);
-            } else
             tmem_load<16>(ta + h, v);
-            if (two) {
-              float v4[16];
-              tmem_load<16>(ta4 + h, v4);
-              tmem_wait_ld();
-#pragma unroll
-              for (int c = 0; c < 16; ++c) v[c] += v4[c];
-            }
             tmem_wait_ld();
 #pragma unroll
             for (int c = 0; c < 16; c += 4) {
@@ -1009,18 +880,14 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
             for (int k = 0; k < P / 2; ++k) w[k] = inside ? w[k] : 0u;
           }
           }
-          if (!im2col && !(PNPULA_ABL & 2)) {   // im2col MMAs overwrite (accumulate = 0): no re-zeroing
+          if (!im2col) {       // im2col MMAs overwrite (accumulate = 0): no re-zeroing needed
 #pragma unroll
             for (int c = 0; c < P; c += 16) tmem_zero<16>(ta + c);
-            if (two) {
-#pragma unroll
-              for (int c = 0; c < P; c += 16) tmem_zero<16>(ta4 + c);
-            }
             tmem_wait_st();
           }
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(bar_tempty(l, esl));
+          if (lane == 0) mbar_arrive(bar_tempty(l, Ig & 3));
           trace_ev(p.trace, trw, 7, s, l);
           if (l < NL - 1) {
             // next layer's input fill = this layer's output row index ic
@@ -1032,7 +899,6 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
             uint8_t *slot = smem + lt.x + (Fg % kRingAct) * lt.y + (m + 1) * 16;
 #pragma unroll
             for (int gq = 0; gq < G; ++gq)
-              if (!(PNPULA_ABL & 4))
               *reinterpret_cast<uint4 *>(slot + gq * GS) = make_uint4(w[4 * gq], w[4 * gq + 1], w[4 * gq + 2], w[4 * gq + 3]);
             fence_proxy_async();
             __syncwarp();
