@@ -33,7 +33,7 @@ def _nccl_dirs():
 
 def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cpp")) +
-                  glob.glob(os.path.join(CSRC, "*.h")) + [os.path.join(ROOT, "include", "pnpula.h")])
+                  glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(ROOT, "include", "pnpula.h")])
 
 
 def needs_build() -> bool:

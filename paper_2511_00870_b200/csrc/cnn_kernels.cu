@@ -36,6 +36,7 @@
 #include <cuda_runtime.h>
 
 #include "internal.h"
+#include "update_math.cuh"
 
 namespace pnpula {
 
@@ -96,8 +97,12 @@ struct SmemLayout {
   uint32_t xs_off;      // first-layer x staging: [producer warp][3 C rows][kXS] fp32, then one mbarrier per warp
   uint32_t bar_off;
   uint32_t misc_off;
+  uint32_t fu_off;      // fused update (last chunk): x rows [2][144], T1 ring [9][136], Rs rows [2][136], T2 ring [9][128]
   uint32_t total;
 };
+// fused-update stencil buffers (floats): strip columns <= 126 valid + 2 R (R <= 4), 2 R + 1 <= 9 ring rows
+constexpr int kFuXS = 144, kFuT1 = 136, kFuT2 = 128;
+constexpr uint32_t kFuFloats = 2 * kFuXS + 9 * kFuT1 + 2 * kFuT1 + 9 * kFuT2;
 
 __host__ __device__ inline uint32_t align_up(uint32_t v, uint32_t a) { return (v + a - 1) / a * a; }
 
@@ -111,7 +116,7 @@ __host__ __device__ inline uint32_t packed_layer_elems(int cout, int cin) {
   return 9u * (uint32_t)cin * (uint32_t)cout;
 }
 
-__host__ __device__ inline SmemLayout make_layout(int P, int nl, int first, int last, int nc) {
+__host__ __device__ inline SmemLayout make_layout(int P, int nl, int first, int last, int nc, int fuse = 0) {
   SmemLayout L{};
   uint32_t off = 0;
   const uint32_t act_slot = (uint32_t)(P / 8) * kRowStride * 16u;
@@ -137,6 +142,11 @@ __host__ __device__ inline SmemLayout make_layout(int P, int nl, int first, int 
   L.misc_off = off;  // tmem address, abort flag, drain barrier, per-layer table {ring, slot, w, 0},
                      // folded last layer's warp-edge exchange [2][C][4 warps][6] floats
   off += 16 + 16u * (uint32_t)nl + 192u * (uint32_t)nc;
+  if (fuse) {
+    off = align_up(off, 16);
+    L.fu_off = off;
+    off += kFuFloats * 4u;
+  }
   L.total = align_up(off, 128);
   return L;
 }
@@ -343,7 +353,7 @@ __device__ __forceinline__ void trace_ev(unsigned long long *tr, bool on, int co
 }
 
 // ---------------------------------------------------------------- the kernel
-template <int P, int NL, int NC>
+template <int P, int NL, int NC, bool FU>
 __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const __grid_constant__ CnnChunkParams p) {
   constexpr int kMmaWarps = mma_warps(NL), kEpiGroups = epi_groups(NL), kEpi0 = epi0(NL);
   constexpr int kThreads = block_threads(NL);
@@ -353,7 +363,8 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
   constexpr uint32_t GS = kRowStride * 16; // bytes between channel groups in a ring row
   const bool first = p.first_is_input != 0;
   const bool last = p.last_is_output != 0;
-  const SmemLayout L = make_layout(P, NL, first, last, NC);
+  const bool fuse = FU && last && p.fuse != 0;   // fused x / z / moment update in the folded layer's epilogue
+  const SmemLayout L = make_layout(P, NL, first, last, NC, fuse ? 1 : 0);
   constexpr int K0 = im2col_k(NC);      // im2col K (9 NC taps, zero padded)
   constexpr bool kDdfb = NL <= 2;   // DDFB operator modes compiled in (R39-R42; C = 1 or 3)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -427,6 +438,24 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
   __syncthreads();
   tc_fence_after();
   pdl_wait();      // programmatic dependent launch: the previous kernel's writes are visible from here
+  // fused update: iteration scalars (by value, or the device IterState of a graph replay), and the
+  // next iteration's scalars written once (as the first update launch of an unfused step does)
+  uint32_t fu_t1 = 0;
+  int fu_acc = 0;
+  float fu_invn = 0.f;
+  if (FU && fuse) {
+    const UpdateParams &U = p.up;
+    if (U.it) { fu_t1 = (uint32_t)U.it->t1; fu_acc = U.it->accumulate; fu_invn = U.it->inv_n; }
+    else { fu_t1 = U.t1; fu_acc = U.accumulate; fu_invn = U.inv_n; }
+    if (U.it_next && blockIdx.x == 0 && threadIdx.x == 0) {
+      const long long t1n = U.it->t1 + 1, b = U.it->burn_in;
+      const bool acc = t1n > b;
+      U.it_next->t1 = t1n;
+      U.it_next->burn_in = b;
+      U.it_next->accumulate = acc;
+      U.it_next->inv_n = (float)(1.0 / (acc ? (double)(t1n - b) : 1.0));
+    }
+  }
 
   // valid output columns per strip: each fused layer costs one column per side; the folded
   // P -> 1 layer needs its MMA rows m +- 1, so a 1-layer chunk ending the net counts as 2
@@ -709,9 +738,94 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
 #pragma unroll
       for (int co = 0; co < NC; ++co) { nacc0[co] = 0.f; nacc1[co] = 0.f; }
       float *const xch = reinterpret_cast<float *>(smem + L.misc_off + 16 + 16 * NL);
+      // ---- fused update (FU && fuse; the folded layer's group, C = 1).  g = H^T(eta H x - y) at the
+      // strip's pixels in the order of update_sep_kernel, streamed row by row through shared memory:
+      //   T1(r, c) = sum_q kx[q+R] x(r, c - q)                 (Rs / T1 columns c = fcT + k, k < fKW)
+      //   Rs(r, c) = eta sum_q ky[q+R] T1(r - q, c) - y(r, c)  (0 outside the image)
+      //   T2(r, c) = sum_q kx[q+R] Rs(r, c + q)                (the strip's valid columns)
+      //   g(o, c)  = sum_q ky[q+R] T2(o + q, c)                (q = -R .. R, fma chains from 0)
+      // Output row o needs T2 rows o-R..o+R, hence T1 rows up to o+2R: rows are produced ahead as
+      // the group completes output rows (fnt1 / fnt2: next T1 / Rs-T2 row of this unit).  A lane
+      // owns T1 / Rs columns m, m + 128 and the T2 column of its pixel, so the rings need no
+      // barrier; the x and Rs rows other lanes read are double-buffered behind one group barrier.
+      const UpdateParams &U = p.up;
+      const int fR = (FU && fuse && U.op != 1) ? U.ry : 0;
+      const int fKW = Wv + 2 * fR;
+      const int fcT = c_strip0 - fR;
+      int fnt1 = r_lo - 2 * fR, fnt2 = r_lo - fR;
+      float fu_gr = 0.f;
+      float *const fu_xs = reinterpret_cast<float *>(smem + L.fu_off);   // [2][kFuXS] x rows
+      float *const fT1 = fu_xs + 2 * kFuXS;                            // [9][kFuT1] T1 ring
+      float *const fRS = fT1 + 9 * kFuT1;                            // [2][kFuT1] Rs rows
+      float *const fT2 = fRS + 2 * kFuT1;                            // [9][kFuT2] T2 ring (by lane)
+      const bool fu_lane = cm >= c_strip0 && cm < c_strip0 + Wv;         // this lane's pixel is in the strip
+      auto fu_bar = [&]() { asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory"); };
+      // padded-buffer read, zero outside the buffer (the TMA staging of update_sep_kernel)
+      auto fu_ld = [&](const float *b, int row, int col) -> float {
+        const TileGeom &g = U.g;
+        const int pr = row - (g.i0 - g.h), pc = col - (g.j0 - g.hx);
+        return (pr >= 0 && pr < g.ph && pc >= 0 && pc < g.pitch) ? b[(int64_t)pr * g.pitch + pc] : 0.f;
+      };
+      auto fu_slot = [](int row) { return (row + 18) % 9; };   // rows >= -2R >= -8
+      auto fu_t1_row = [&](int row) {
+        float *const xs = fu_xs + (row & 1) * kFuXS;
+        for (int u2 = m; u2 < fKW + 2 * fR; u2 += 128) xs[u2] = fu_ld(U.x, row, fcT - fR + u2);
+        fu_bar();
+        float *const t1 = fT1 + fu_slot(row) * kFuT1;
+        for (int k = m; k < fKW; k += 128) {
+          float sa = 0.f;
+          for (int q = -fR; q <= fR; ++q) sa = fmaf(U.kx[q + fR], xs[k + fR - q], sa);
+          t1[k] = sa;
+        }
+      };
+      auto fu_rs_t2_row = [&](int row) {
+        float *const rs = fRS + (row & 1) * kFuT1;
+        const bool rin = row >= 0 && row < p.ny;
+        for (int k = m; k < fKW; k += 128) {
+          float sa = 0.f;
+          for (int q = -fR; q <= fR; ++q) sa = fmaf(U.ky[q + fR], fT1[fu_slot(row - q) * kFuT1 + k], sa);
+          const int c = fcT + k;
+          rs[k] = (rin && c >= 0 && c < p.nx) ? U.eta * sa - fu_ld(U.y, row, c) : 0.f;
+        }
+        fu_bar();
+        if (fu_lane) {
+          const int k0 = cm - fcT;
+          float sa = 0.f;
+          for (int q = -fR; q <= fR; ++q) sa = fmaf(U.kx[q + fR], rs[k0 + q], sa);
+          fT2[fu_slot(row) * kFuT2 + m] = sa;
+        }
+      };
+      auto fu_advance = [&](int o) {
+        while (fnt2 <= o + fR) {
+          while (fnt1 <= fnt2 + fR) { fu_t1_row(fnt1); ++fnt1; }
+          fu_rs_t2_row(fnt2); ++fnt2;
+        }
+        float sa = 0.f;
+        if (fu_lane)
+          for (int q = -fR; q <= fR; ++q) sa = fmaf(U.ky[q + fR], fT2[fu_slot(o + q) * kFuT2 + m], sa);
+        fu_gr = sa;
+      };
       auto netlast_fill = [&](const int l, const int f) -> bool {
           const int s = f + kLag * l;
           const uint32_t Fg = Fcnt(l) + (uint32_t)f;
+          // fused update: g at this row (independent of the CNN) and the pixel's own operands,
+          // requested before the wait for the accumulators so their latency overlaps it
+          float fx = 0.f, fz = 0.f, fm = 0.f, fs = 0.f;
+          int64_t fidx = 0;
+          if constexpr (FU) {
+            const int icf = f - 2;
+            if (fuse && icf >= 0 && icf < nout(l)) {
+              const int of = r_lo - (NL - 1 - l) + icf;
+              if (U.op != 1) fu_advance(of);
+              if (col_valid) {
+                const TileGeom &g = U.g;
+                fidx = (int64_t)(of - (g.i0 - g.h)) * g.pitch + (cm - (g.j0 - g.hx));
+                fx = U.x[fidx];
+                if (U.has_z) fz = U.z[fidx];
+                if (fu_acc) { fm = U.mean[fidx]; fs = U.m2[fidx]; }
+              }
+            }
+          }
           if (!mbar_wait(bar_tfull(l, Fg & 1), (Fg >> 1) & 1, abort_flag, p.err, 4)) return false;
           trace_ev(p.trace, trw, 6, s, l);
           tc_fence_after();
@@ -766,7 +880,27 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
             nacc0[co] = nacc1[co] + c[1];
             nacc1[co] = c[2];
             if (store) {
-              if (!kDdfb || p.mode < 2) {   // DDFB modes exist for 1- and 2-operator launches only
+              if (FU && fuse) {
+                // fused K7 tail at (o, cm): the per-pixel arithmetic of ula_finish (update_math.cuh)
+                const float Gv = row_done + p.bias[l][co];
+                float gr = fu_gr;
+                if (U.op == 1) {
+                  const float mk = U.mask[fidx] ? 1.f : 0.f;
+                  gr = mk * (mk * fx - U.y[fidx]);
+                }
+                const float xi = upd::normal1(U.seed_lo, U.seed_hi, (uint32_t)cm >> 2, (uint32_t)o, fu_t1, U.sb + 0u, cm & 3);
+                const float xn = upd::x_step<0>(U, false, fx, gr, Gv, fz, 0.f, xi);
+                U.xn[fidx] = xn;
+                if (U.has_z) {
+                  const float ze = upd::normal1(U.seed_lo, U.seed_hi, (uint32_t)cm >> 2, (uint32_t)o, fu_t1, U.sb + 1u, cm & 3);
+                  U.z[fidx] = upd::z_step(U, fz, xn, ze);
+                }
+                if (fu_acc) {
+                  upd::welford(xn, fu_invn, fm, fs);
+                  U.mean[fidx] = fm;
+                  U.m2[fidx] = fs;
+                }
+              } else if (!kDdfb || p.mode < 2) {   // DDFB modes exist for 1- and 2-operator launches only
                 p.G[(int64_t)co * p.gcs + gidx] = row_done + p.bias[l][co];
               } else if (o >= 0 && o < p.ny && cm >= 0 && cm < p.nx) {
                 // DDFB adjoint step (R39): q = proj_[0,1](v - W_k^* u); final: G = v - q (channel co)
@@ -986,10 +1120,10 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
   }
 }
 
-template <int P, int NL, int NC>
+template <int P, int NL, int NC, bool FU>
 cudaError_t launch_pn(const CnnChunkParams &p0, int num_sms, cudaStream_t s) {
   CnnChunkParams p = p0;
-  const SmemLayout L = make_layout(P, NL, p.first_is_input, p.last_is_output, NC);
+  const SmemLayout L = make_layout(P, NL, p.first_is_input, p.last_is_output, NC, FU && p.last_is_output && p.fuse);
   const int Wv = kRowPos - 2 * ((p.last_is_output && NL < 2) ? 2 : NL);   // as in the kernel
   const int strips = (p.ow + Wv - 1) / Wv;
   // rows per unit: minimise (waves) x (rows per unit + pipeline fill) over row-block counts
@@ -1007,7 +1141,7 @@ cudaError_t launch_pn(const CnnChunkParams &p0, int num_sms, cudaStream_t s) {
   p.strips = strips;
   p.rows_per_unit = R;
   p.units = strips * ((p.oh + R - 1) / R);
-  auto kfn = cnn_chunk_kernel<P, NL, NC>;
+  auto kfn = cnn_chunk_kernel<P, NL, NC, FU>;
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
   if (e != cudaSuccess) return e;
   const int grid = p.units < num_sms ? p.units : num_sms;
@@ -1029,25 +1163,31 @@ cudaError_t launch_pn(const CnnChunkParams &p0, int num_sms, cudaStream_t s) {
 // compile-time chain lengths: TMEM (NL * 4 * P <= 512 columns) and 227 KB of shared memory
 constexpr int max_nl(int P) { return P == 16 ? 8 : P == 32 ? 4 : 2; }
 
-template <int P, int NL, int NC>
+template <int P, int NL, int NC, bool FU = false>
 cudaError_t dispatch_nl(const CnnChunkParams &p, int num_sms, cudaStream_t s) {
   if constexpr (NL > max_nl(P)) {
     return cudaErrorInvalidValue;
   } else {
-    if (p.nl == NL) return launch_pn<P, NL, NC>(p, num_sms, s);
-    if constexpr (NL < kMaxChunk) return dispatch_nl<P, NL + 1, NC>(p, num_sms, s);
+    if (p.nl == NL) return launch_pn<P, NL, NC, FU>(p, num_sms, s);
+    if constexpr (NL < kMaxChunk) return dispatch_nl<P, NL + 1, NC, FU>(p, num_sms, s);
     return cudaErrorInvalidValue;
   }
 }
 
 }  // namespace
 
-size_t cnn_chunk_smem_bytes(int P, int nl, int first, int last, int nc) {
+size_t cnn_chunk_smem_bytes(int P, int nl, int first, int last, int nc, int fuse) {
   // (TMEM: nl * 4 P <= 512 columns holds for every chain max_nl admits)
   if (nl < 1 || nl > kMaxChunk) return SIZE_MAX;
   if (nl > max_nl(P)) return SIZE_MAX;
   if (nc != 1 && (nc != 3 || P < 32)) return SIZE_MAX;   // C = 3: N = 48 columns of the folded last layer
-  return make_layout(P, nl, first, last, nc).total;
+  return make_layout(P, nl, first, last, nc, fuse && last).total;
+}
+
+bool cnn_fused_update_supported(int P, int nc, const UpdateParams &u) {
+  if (P != 32 || nc != 1 || u.has_tv) return false;
+  if (u.op == 1) return true;                                         // mask: no stencil
+  return u.op == 0 && u.separable && u.ry == u.rx && (u.ry == 2 || u.ry == 4);   // update_sep_kernel's cases
 }
 
 size_t cnn_packed_layer_elems(int cout, int cin) { return packed_layer_elems(cout, cin); }
@@ -1123,6 +1263,10 @@ cudaError_t launch_cnn_chunk(const CnnChunkParams &p, int num_sms, cudaStream_t 
     }
   }
   if (nc != 1) return cudaErrorInvalidValue;
+  if (p.fuse && p.last_is_output) {   // fused update: compiled for P = 32 (cnn_fused_update_supported)
+    if (p.P != 32) return cudaErrorInvalidValue;
+    return dispatch_nl<32, 1, 1, true>(p, num_sms, s);
+  }
   switch (p.P) {
     case 16: return dispatch_nl<16, 1, 1>(p, num_sms, s);
     case 32: return dispatch_nl<32, 1, 1>(p, num_sms, s);

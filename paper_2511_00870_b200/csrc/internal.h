@@ -143,6 +143,13 @@ struct CnnChunkParams {
   int nc;                // image channels C (1, or 3 with P >= 32; reading R43): planes of x / G
   int64_t xcs, gcs;      // floats between the channel planes of x and of G
   int pdl;               // launch as a programmatic dependent of the previous kernel (see pdl_wait)
+  // Fused x / z / moment update (the chain's last layer, C = 1, P = 32): instead of storing G, the
+  // folded layer's epilogue evaluates H^T(eta H x - y) in a streaming separable stencil (or the mask
+  // term) and the K7 tail of `up` for every tile pixel it completes -- the same per-pixel
+  // arithmetic as update_sep_kernel / update_mask_kernel (update_math.cuh), so results are bitwise
+  // those of the unfused iteration.  up.G is unused.
+  int fuse;
+  UpdateParams up;
 };
 
 // Programmatic dependent launch (PDL): the CNN chain kernels are launched as dependents of the
@@ -180,7 +187,9 @@ cudaError_t launch_debug_philox(uint64_t seed, const uint32_t *d_ctr, int64_t n,
                                 int *d_bad, cudaStream_t s);
 cudaError_t launch_cnn_chunk(const CnnChunkParams &p, int num_sms, cudaStream_t s);
 // shared-memory bytes of a chain, or SIZE_MAX if it does not fit
-size_t cnn_chunk_smem_bytes(int P, int nl, int first_is_input, int last_is_output, int nc);
+size_t cnn_chunk_smem_bytes(int P, int nl, int first_is_input, int last_is_output, int nc, int fuse = 0);
+// the fused update is compiled for P = 32, C = 1 chains; conv: separable with ry = rx in {2, 4}, or mask
+bool cnn_fused_update_supported(int P, int nc, const UpdateParams &u);
 // Pack host fp32 OIHW weights of one layer into the device B-operand image (host side).
 void cnn_pack_layer(const float *w, int cout, int cin, uint16_t *out);
 size_t cnn_packed_layer_elems(int cout, int cin);

@@ -142,6 +142,11 @@ struct pnpula_ctx {
   // halo-exchange overlap (row-strip tiles with NCCL messages): boundary bands first, then the
   // exchange on comm_stream concurrently with the interior update
   bool overlap = false;
+  // x / z / moment update fused into the last CNN chunk (cnn_kernels.cu, FU): DnCNN, C = 1,
+  // P = 32, separable 5x5 / 9x9 conv (or Poisson's x step) or mask.  Opt-in (env PNPULA_FUSE=1 at
+  // create): bitwise equal to the unfused step but measured slower -- the folded layer's epilogue
+  // group is latency-bound and paces the chunk (profiles/r02_fused_update.md).
+  bool fuse = false;
   int pdl = 1;                     // CNN launches as programmatic dependents (internal.h pdl_wait)
   cudaMemPool_t pool = nullptr;    // stream-ordered pool of the per-tile buffers (see dmalloc)
   cudaStream_t comm_stream = nullptr;
@@ -327,7 +332,12 @@ pnpula_status run_ddfb(pnpula_ctx *c, int buf) {
   return PNPULA_OK;
 }
 
-pnpula_status run_cnn(pnpula_ctx *c, int buf) {
+UpdateParams make_update_params(pnpula_ctx *c, TileDev &td, int buf);
+
+// fused: the last chunk also performs the x / z / moment update of the step reading x[buf]
+// (FU, c->fuse; iteration scalars as enqueue_step's update_rows: t1 by value or `it`), and G is
+// not stored.  Not fused: G for the update kernels (or pnpula_get_denoiser_residual).
+pnpula_status run_cnn(pnpula_ctx *c, int buf, bool fused = false, const IterState *it = nullptr) {
   if (c->den_kind == PNPULA_DEN_DDFB) return run_ddfb(c, buf);
   for (auto &td : c->tiles) {
     for (size_t ci = 0; ci < c->chunks.size(); ++ci) {
@@ -359,6 +369,18 @@ pnpula_status run_cnn(pnpula_ctx *c, int buf) {
       } else {
         p.G = td.G;
         p.gg = g;
+        if (fused) {
+          const uint64_t t1 = (uint64_t)c->t + 1;
+          const bool acc = (int64_t)t1 > c->burn_in;
+          const double k = acc ? (double)((int64_t)t1 - c->burn_in) : 1.0;
+          p.fuse = 1;
+          p.up = make_update_params(c, td, buf);
+          p.up.t1 = (uint32_t)t1;
+          p.up.accumulate = acc;
+          p.up.inv_n = (float)(1.0 / k);
+          p.up.it = it;
+          p.up.it_next = (it && &td == &c->tiles[0]) ? c->d_iter + (buf ^ 1) : nullptr;
+        }
       }
       p.ny = c->ny; p.nx = c->nx;
       p.nc = c->nc;
@@ -474,8 +496,9 @@ UpdateParams make_update_params(pnpula_ctx *c, TileDev &td, int buf) {
 // (t1 = c->t + 1); otherwise every kernel reads them from it = d_iter[buf] and the first
 // update launch writes the next iteration's into d_iter[buf ^ 1] (graph capture).
 pnpula_status enqueue_step(pnpula_ctx *c, int buf, const IterState *it) {
+  const bool fused = c->fuse && c->n_layers > 0;
   if (c->n_layers > 0) {
-    pnpula_status s = run_cnn(c, buf);
+    pnpula_status s = run_cnn(c, buf, fused, it);
     if (s) return s;
   }
   const uint64_t t1 = (uint64_t)c->t + 1;
@@ -511,7 +534,9 @@ pnpula_status enqueue_step(pnpula_ctx *c, int buf, const IterState *it) {
     return PNPULA_OK;
   };
   pnpula_status s;
-  if (c->overlap) {
+  if (fused) {
+    if ((s = exchange(c, buf ^ 1))) return s;   // x^{t+1} was written by the fused last CNN chunk
+  } else if (c->overlap) {
     // boundary bands (the rows neighbours receive) first, then the exchange on the comm stream
     // while the interior rows update (SURVEY 8(e) overlap); the next kernels wait for both
     if ((s = update_rows(false, true, false)) || (s = update_rows(false, false, false))) return s;
@@ -737,7 +762,7 @@ void plan_cnn_chunks(pnpula_ctx *c) {
     int best = 1;
     const int maxnl = (c->flags & PNPULA_FLAG_CNN_LAYERWISE) ? 1 : kMaxChunk;
     for (int nl = 1; nl <= std::min(maxnl, K - l + 1); ++nl) {
-      if (cnn_chunk_smem_bytes(c->channels, nl, l == 1, l + nl - 1 == K, c->nc) <= budget) best = nl;
+      if (cnn_chunk_smem_bytes(c->channels, nl, l == 1, l + nl - 1 == K, c->nc, c->fuse) <= budget) best = nl;
     }
     c->chunks.push_back({l, best, K - (l + best - 1)});
     l += best;
@@ -1141,6 +1166,15 @@ pnpula_status pnpula_create(const pnpula_config *cfg, pnpula_ctx **out) {
   // CNN weights
   phase("ddfb");
   if (c->n_layers > 0 && !ddfb) {
+    {
+      const char *fe = getenv("PNPULA_FUSE");
+      UpdateParams u{};
+      u.op = c->op == PNPULA_OP_MASK ? 1 : 0;   // Poisson's x step runs the conv path (R32)
+      u.separable = c->separable;
+      u.ry = c->ry; u.rx = c->rx;
+      u.has_tv = c->tv_beta > 0;
+      c->fuse = (fe && atoi(fe) == 1) && cnn_fused_update_supported(c->channels, nc, u);
+    }
     plan_cnn_chunks(c);
     const int K = c->n_layers, P = c->channels;
     const float *w = f.den->weights;
@@ -1189,7 +1223,8 @@ pnpula_status pnpula_create(const pnpula_config *cfg, pnpula_ctx **out) {
   // the h top / bottom rows of a tile) whose tiles have interior rows (env PNPULA_OVERLAP=0: off)
   {
     const char *oe = getenv("PNPULA_OVERLAP");
-    bool ok = !(oe && atoi(oe) == 0) && (!c->sends.empty() || !c->recvs.empty()) && c->tiles_x == 1 && c->h > 0;
+    bool ok = !(oe && atoi(oe) == 0) && (!c->sends.empty() || !c->recvs.empty()) && c->tiles_x == 1 && c->h > 0 &&
+              !c->fuse;   // fused: the update runs inside the CNN, the exchange follows it
     for (auto &td : c->tiles) ok = ok && td.g.th > 2 * td.g.h;
     if (ok) {
       CUB(cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));

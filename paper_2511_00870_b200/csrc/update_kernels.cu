@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 
 #include "internal.h"
+#include "update_math.cuh"
 
 namespace pnpula {
 
@@ -32,85 +33,9 @@ constexpr int TY = 32;            // output rows per block
 constexpr int TX = 64;            // output columns per block (16 quads)
 constexpr int NTHREADS = 256;
 
-// ---------------------------------------------------------------- Philox4x32-10
-__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1) {
-#pragma unroll
-  for (int r = 0; r < 10; ++r) {
-    const uint32_t lo0 = 0xD2511F53u * c.x;
-    const uint32_t hi0 = __umulhi(0xD2511F53u, c.x);
-    const uint32_t lo1 = 0xCD9E8D57u * c.z;
-    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z);
-    c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
-    k0 += 0x9E3779B9u;
-    k1 += 0xBB67AE85u;
-  }
-  return c;
-}
-
-// ln(u), u = (U + 0.5) 2^-32, accurate for u near 0 and near 1, without a data-dependent branch
-// (both halves are evaluated and selected, so a warp never runs two paths):
-//  * u <= 1/2: the hardware log2 (abs. error ~2^-22 on |log2 u| >= 1, i.e. relative 2^-22);
-//  * u > 1/2: ln(1 - v) = -2 atanh(z), z = v / (2 - v) in (0, 1/3], with v = 1 - u formed
-//    exactly from the integer; atanh(z) = z (1 + w/3 + w^2/5 + ... + w^7/15), w = z^2 <= 1/9
-//    (truncation < w^8/17 ~ 1e-9 relative; a few ulp of rounding).
-__device__ __forceinline__ float log_unit(uint32_t U) {
-  const float lo = __log2f(fmaf((float)U, 0x1p-32f, 0x1p-33f)) * 0.69314718055994531f;
-  const float v = fmaf((float)(~U), 0x1p-32f, 0x1p-33f);   // 1 - u
-  const float z = __fdividef(v, 2.0f - v);
-  const float w = z * z;
-  float a = 1.0f / 15.0f;
-  a = fmaf(a, w, 1.0f / 13.0f);
-  a = fmaf(a, w, 1.0f / 11.0f);
-  a = fmaf(a, w, 1.0f / 9.0f);
-  a = fmaf(a, w, 1.0f / 7.0f);
-  a = fmaf(a, w, 1.0f / 5.0f);
-  a = fmaf(a, w, 1.0f / 3.0f);
-  a = fmaf(a, w, 1.0f);
-  const float hi = -2.0f * z * a;
-  return U < 0x80000000u ? lo : hi;
-}
-
-// Box-Muller pair from (Ua, Ub): (rho cos theta, rho sin theta), theta = 2 pi (Ub+0.5) 2^-32,
-// evaluated as pi * x with x = ((int)Ub + 0.5) 2^-31 in (-1, 1) (same angle mod 2 pi) with
-// the hardware sin/cos (abs. error ~2^-21 on [-pi, pi]).
-__device__ __forceinline__ float2 box_muller(uint32_t Ua, uint32_t Ub) {
-  const float rho = sqrtf(-2.0f * log_unit(Ua));
-  const float xs = fmaf((float)(int32_t)Ub, 0x1p-31f, 0x1p-32f);
-  float s, c;
-  __sincosf(3.14159265358979323846f * xs, &s, &c);
-  return make_float2(rho * c, rho * s);
-}
-
-__device__ __forceinline__ void normals4(uint32_t seed_lo, uint32_t seed_hi, uint32_t quad,
-                                         uint32_t row, uint32_t t1, uint32_t stream, float out[4]) {
-  const uint4 w = philox4x32_10(make_uint4(quad, row, t1, stream), seed_lo, seed_hi);
-  const float2 a = box_muller(w.x, w.y);
-  const float2 b = box_muller(w.z, w.w);
-  out[0] = a.x; out[1] = a.y; out[2] = b.x; out[3] = b.y;
-}
-
-// normals4 for rows `row` and `row + 1` of the same quad, the two Philox chains advanced in one
-// loop (independent chains interleave: twice the instruction-level parallelism of two calls)
-__device__ __forceinline__ void normals4x2(uint32_t seed_lo, uint32_t seed_hi, uint32_t quad, uint32_t row,
-                                           uint32_t t1, uint32_t stream, float out[2][4]) {
-  uint4 c0 = make_uint4(quad, row, t1, stream), c1 = make_uint4(quad, row + 1u, t1, stream);
-  uint32_t k0 = seed_lo, k1 = seed_hi;
-#pragma unroll
-  for (int r = 0; r < 10; ++r) {
-    const uint32_t lo0 = 0xD2511F53u * c0.x, hi0 = __umulhi(0xD2511F53u, c0.x);
-    const uint32_t lo1 = 0xCD9E8D57u * c0.z, hi1 = __umulhi(0xCD9E8D57u, c0.z);
-    const uint32_t lo2 = 0xD2511F53u * c1.x, hi2 = __umulhi(0xD2511F53u, c1.x);
-    const uint32_t lo3 = 0xCD9E8D57u * c1.z, hi3 = __umulhi(0xCD9E8D57u, c1.z);
-    c0 = make_uint4(hi1 ^ c0.y ^ k0, lo1, hi0 ^ c0.w ^ k1, lo0);
-    c1 = make_uint4(hi3 ^ c1.y ^ k0, lo3, hi2 ^ c1.w ^ k1, lo2);
-    k0 += 0x9E3779B9u;
-    k1 += 0xBB67AE85u;
-  }
-  const float2 a0 = box_muller(c0.x, c0.y), b0 = box_muller(c0.z, c0.w);
-  const float2 a1 = box_muller(c1.x, c1.y), b1 = box_muller(c1.z, c1.w);
-  out[0][0] = a0.x; out[0][1] = a0.y; out[0][2] = b0.x; out[0][3] = b0.y;
-  out[1][0] = a1.x; out[1][1] = a1.y; out[1][2] = b1.x; out[1][3] = b1.y;
-}
+// Philox4x32-10 + Box-Muller noise and the per-pixel tail: update_math.cuh (shared with the update
+// fused into the last CNN chunk)
+using namespace upd;
 
 // Iteration scalars: by value (direct launches) or from the device IterState (CUDA-graph
 // replays; see IterState), read once per thread at kernel entry.
@@ -247,32 +172,17 @@ __device__ __forceinline__ void ula_finish(const UpdateParams &p, const IterScal
   if (has_tv) tv_term(p, gi, gj4, xv, dtv);
   float xn[4];
 #pragma unroll
-  for (int l = 0; l < 4; ++l) {
-    float v = xv[l] - p.a_g * gr[l];
-    if (TVM != 2 && p.has_z) v -= p.a_rho * (xv[l] - zv[l]);
-    if (TVM != 2 && p.has_G) v += p.a_d * (-Gv[l]);
-    if (TVM != 2 && p.has_box) v += p.a_lam * (fminf(fmaxf(xv[l], p.c_lo), p.c_hi) - xv[l]);
-    if (has_tv) v -= p.a_tv * dtv[l];
-    v += p.a_xi * xi[l];
-    xn[l] = has_tv ? fmaxf(v, 0.f) : v;   // TV: PSGLA projection onto R+ after the step (R37)
-  }
+  for (int l = 0; l < 4; ++l) xn[l] = x_step<TVM>(p, has_tv, xv[l], gr[l], Gv[l], zv[l], dtv[l], xi[l]);
   float zn[4];
   if (TVM != 2 && p.has_z) {
     float ze[4];
     normals4(p.seed_lo, p.seed_hi, (uint32_t)gj4 >> 2, (uint32_t)gi, is.t1, p.sb + 1u, ze);
 #pragma unroll
-    for (int l = 0; l < 4; ++l) {
-      const float v = zv[l] - p.b_rho * (zv[l] - xn[l]) + p.b_zeta * ze[l];
-      zn[l] = fminf(fmaxf(v, p.z_lo), p.z_hi);
-    }
+    for (int l = 0; l < 4; ++l) zn[l] = z_step(p, zv[l], xn[l], ze[l]);
   }
   if (is.acc) {
 #pragma unroll
-    for (int l = 0; l < 4; ++l) {
-      const float d = xn[l] - mv[l];
-      mv[l] = mv[l] + d * is.inv_n;
-      sv[l] = sv[l] + d * (xn[l] - mv[l]);
-    }
+    for (int l = 0; l < 4; ++l) welford(xn[l], is.inv_n, mv[l], sv[l]);
   }
   if (full) {
     *reinterpret_cast<float4 *>(p.xn + base) = make_float4(xn[0], xn[1], xn[2], xn[3]);
