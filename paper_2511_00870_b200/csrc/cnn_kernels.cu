@@ -97,12 +97,14 @@ struct SmemLayout {
   uint32_t xs_off;      // first-layer x staging: [producer warp][3 C rows][kXS] fp32, then one mbarrier per warp
   uint32_t bar_off;
   uint32_t misc_off;
-  uint32_t fu_off;      // fused update (last chunk): x rows [2][144], T1 ring [9][136], Rs rows [2][136], T2 ring [9][128]
+  uint32_t fu_off;      // fused update (last chunk): x rows [2][144], T1 ring [16][136], Rs rows [2][136],
+                        // T2 ring [16][128], G ring [8][128]; then mbarriers gfull[8], gempty[8], sync[2]
   uint32_t total;
 };
-// fused-update stencil buffers (floats): strip columns <= 126 valid + 2 R (R <= 4), 2 R + 1 <= 9 ring rows
-constexpr int kFuXS = 144, kFuT1 = 136, kFuT2 = 128;
-constexpr uint32_t kFuFloats = 2 * kFuXS + 9 * kFuT1 + 2 * kFuT1 + 9 * kFuT2;
+// fused-update buffers (floats): strip columns <= 126 valid + 2 R (R <= 4); T1 / T2 rings of 16 rows
+// (2 R + 1 <= 9 live), G ring of 8 rows handed from the folded layer's epilogue to the producers
+constexpr int kFuXS = 144, kFuT1 = 136, kFuT2 = 128, kFuRing = 16, kFuG = 8;
+constexpr uint32_t kFuFloats = 2 * kFuXS + kFuRing * kFuT1 + 2 * kFuT1 + kFuRing * kFuT2 + kFuG * 128;
 
 __host__ __device__ inline uint32_t align_up(uint32_t v, uint32_t a) { return (v + a - 1) / a * a; }
 
@@ -145,7 +147,7 @@ __host__ __device__ inline SmemLayout make_layout(int P, int nl, int first, int 
   if (fuse) {
     off = align_up(off, 16);
     L.fu_off = off;
-    off += kFuFloats * 4u;
+    off += kFuFloats * 4u + (2u * kFuG + 2u) * 8u;   // + the producers' row barriers sync[2]
   }
   L.total = align_up(off, 128);
   return L;
@@ -363,7 +365,8 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
   constexpr uint32_t GS = kRowStride * 16; // bytes between channel groups in a ring row
   const bool first = p.first_is_input != 0;
   const bool last = p.last_is_output != 0;
-  const bool fuse = FU && last && p.fuse != 0;   // fused x / z / moment update in the folded layer's epilogue
+  // fused x / z / moment update (chains whose layer 0 is fed by TMA: the producers have the time)
+  const bool fuse = FU && last && !first && p.fuse != 0;
   const SmemLayout L = make_layout(P, NL, first, last, NC, fuse ? 1 : 0);
   constexpr int K0 = im2col_k(NC);      // im2col K (9 NC taps, zero padded)
   constexpr bool kDdfb = NL <= 2;   // DDFB operator modes compiled in (R39-R42; C = 1 or 3)
@@ -410,6 +413,12 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
       }
     }
     mbar_init(bar_done, kMmaWarps);
+    if (FU && fuse)
+      for (int g2 = 0; g2 < kFuG; ++g2) {
+        mbar_init(sbase + L.fu_off + kFuFloats * 4u + (uint32_t)g2 * 8u, 4);            // G row full: 4 epilogue warps
+        mbar_init(sbase + L.fu_off + kFuFloats * 4u + (uint32_t)(kFuG + g2) * 8u, 4);   // G row read: 4 producer warps
+        if (g2 < 2) mbar_init(sbase + L.fu_off + kFuFloats * 4u + (uint32_t)(2 * kFuG + g2) * 8u, 4);   // stencil rows
+      }
     if (first)
       for (int w = 0; w < kProdWarps; ++w) mbar_init(sbase + L.xs_off + (uint32_t)(kProdWarps * 3 * NC * kXS) * 4u + w * 8u, 1);
     *abort_flag = 0;
@@ -502,6 +511,140 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
       const uint32_t F0 = Fcnt(0);
       const uint32_t ring0 = ltab[0].x, slot0 = ltab[0].y;
       const int f0 = (kProdWarps == 1) ? 0 : (int)(((uint32_t)warp - F0) & 3u);
+      // ---- fused update (FU && fuse): the 4 producer warps (one pixel per lane: m = 32 w + lane,
+      // the folded layer's lane mapping) also run the x / z / moment update of every completed
+      // output row.  g = H^T(eta H x - y) is streamed row by row in the order of update_sep_kernel:
+      //   T1(r, c) = sum_q kx[q+R] x(r, c - q)                 (columns c = fcT + k, k < fKW)
+      //   Rs(r, c) = eta sum_q ky[q+R] T1(r - q, c) - y(r, c)  (0 outside the image)
+      //   T2(r, c) = sum_q kx[q+R] Rs(r, c + q)                (the strip's valid columns)
+      //   g(o, c)  = sum_q ky[q+R] T2(o + q, c)                (q = -R .. R, fma chains from 0)
+      // (T1 / Rs columns k = m, m + 128 and the T2 column of a lane's pixel are its own: the rings
+      // need no barrier; the x and Rs rows read across lanes are double-buffered behind one named
+      // barrier of the 128 producer threads per row.)  G arrives through the G ring.  A warp
+      // finishes output row ic only after issuing its layer-0 fills up to ic + 2 + kLag (NL-1) + 4,
+      // so a row it waits for never depends on a fill it has not issued (no deadlock).
+      [[maybe_unused]] int fu_done = 0, fnt1 = 0, fnt2 = 0;
+      [[maybe_unused]] uint32_t fu_nsync = 0;   // stencil row barriers passed (all 4 warps pass the same sequence)
+      [[maybe_unused]] const int fu_lag = 2 + kLag * (NL - 1) + 4;
+      auto fu_rows_upto = [&](int icmax) -> bool {
+        if constexpr (FU) {
+          if (!fuse) return true;
+          const UpdateParams &U = p.up;
+          const int l = NL - 1;
+          const int no = nout(l);
+          const int fR = U.op != 1 ? U.ry : 0;
+          const int fKW = Wv + 2 * fR;
+          const int fcT = c_strip0 - fR;
+          const int m = warp * 32 + lane;
+          const int cm = col0 + m;
+          const bool fu_lane = cm >= c_strip0 && cm < c_strip0 + Wv;
+          const bool cvalid = fu_lane && cm < p.oj0 + p.ow;
+          float *const fxs = reinterpret_cast<float *>(smem + L.fu_off);
+          float *const fT1 = fxs + 2 * kFuXS;
+          float *const fRS = fT1 + kFuRing * kFuT1;
+          float *const fT2 = fRS + 2 * kFuT1;
+          float *const fG = fT2 + kFuRing * kFuT2;
+          const uint32_t gb = sbase + L.fu_off + kFuFloats * 4u;
+          const TileGeom &g = U.g;
+          auto ldpad = [&](const float *b, int row, int col) -> float {   // 0 outside the buffer (TMA)
+            const int pr = row - (g.i0 - g.h), pc = col - (g.j0 - g.hx);
+            return (pr >= 0 && pr < g.ph && pc >= 0 && pc < g.pitch) ? b[(int64_t)pr * g.pitch + pc] : 0.f;
+          };
+          // barrier of the 4 producer warps (two mbarriers used alternately, one arrival per warp; the
+          // bounded wait keeps an aborted CTA from hanging here, unlike a named barrier)
+          auto pbar = [&]() -> bool {
+            const uint32_t b = gb + (2u * kFuG + (fu_nsync & 1u)) * 8u;
+            const uint32_t ph = (fu_nsync >> 1) & 1u;
+            ++fu_nsync;
+            __syncwarp();
+            if (lane == 0) mbar_arrive(b);
+            return mbar_wait(b, ph, abort_flag, p.err, 11);
+          };
+          auto t1_row = [&](int row) -> bool {
+            float *const xs = fxs + (row & 1) * kFuXS;
+            for (int u2 = m; u2 < fKW + 2 * fR; u2 += 128) xs[u2] = ldpad(U.x, row, fcT - fR + u2);
+            if (!pbar()) return false;
+            float *const t1 = fT1 + (row & (kFuRing - 1)) * kFuT1;
+            for (int k = m; k < fKW; k += 128) {
+              float sa = 0.f;
+              for (int q = -fR; q <= fR; ++q) sa = fmaf(U.kx[q + fR], xs[k + fR - q], sa);
+              t1[k] = sa;
+            }
+            return true;
+          };
+          auto rs_t2_row = [&](int row) -> bool {
+            float *const rs = fRS + (row & 1) * kFuT1;
+            const bool rin = row >= 0 && row < p.ny;
+            for (int k = m; k < fKW; k += 128) {
+              float sa = 0.f;
+              for (int q = -fR; q <= fR; ++q) sa = fmaf(U.ky[q + fR], fT1[((row - q) & (kFuRing - 1)) * kFuT1 + k], sa);
+              const int c = fcT + k;
+              rs[k] = (rin && c >= 0 && c < p.nx) ? U.eta * sa - ldpad(U.y, row, c) : 0.f;
+            }
+            if (!pbar()) return false;
+            if (fu_lane) {
+              const int k0 = cm - fcT;
+              float sa = 0.f;
+              for (int q = -fR; q <= fR; ++q) sa = fmaf(U.kx[q + fR], rs[k0 + q], sa);
+              fT2[(row & (kFuRing - 1)) * kFuT2 + m] = sa;
+            }
+            return true;
+          };
+          if (fu_done == 0) { fnt1 = r_lo - 2 * fR; fnt2 = r_lo - fR; }
+          const int last_ic = icmax < no - 1 ? icmax : no - 1;
+          for (; fu_done <= last_ic; ++fu_done) {
+            const int ic = fu_done;
+            const int o = r_lo + ic;
+            float gr = 0.f;
+            if (U.op != 1) {
+              while (fnt2 <= o + fR) {
+                while (fnt1 <= fnt2 + fR) {
+                  if (!t1_row(fnt1)) return false;
+                  ++fnt1;
+                }
+                if (!rs_t2_row(fnt2)) return false;
+                ++fnt2;
+              }
+              if (fu_lane)
+                for (int q = -fR; q <= fR; ++q) gr = fmaf(U.ky[q + fR], fT2[((o + q) & (kFuRing - 1)) * kFuT2 + m], gr);
+            }
+            float fx = 0.f, fz = 0.f, fm = 0.f, fs = 0.f;
+            int64_t idx = 0;
+            if (cvalid) {
+              idx = (int64_t)(o - (g.i0 - g.h)) * g.pitch + (cm - (g.j0 - g.hx));
+              fx = U.x[idx];
+              if (U.has_z) fz = U.z[idx];
+              if (fu_acc) { fm = U.mean[idx]; fs = U.m2[idx]; }
+              if (U.op == 1) {
+                const float mk = U.mask[idx] ? 1.f : 0.f;
+                gr = mk * (mk * fx - U.y[idx]);
+              }
+            }
+            const uint32_t Ig = Ocnt(l) + (uint32_t)ic;
+            const uint32_t gs = Ig & (kFuG - 1);
+            if (!mbar_wait(gb + gs * 8u, (Ig / kFuG) & 1, abort_flag, p.err, 10)) return false;
+            const float Gv = fG[gs * 128 + m];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(gb + (kFuG + gs) * 8u);
+            if (cvalid) {
+              // the K7 tail of ula_finish for this pixel (update_math.cuh)
+              const float xi = upd::normal1(U.seed_lo, U.seed_hi, (uint32_t)cm >> 2, (uint32_t)o, fu_t1, U.sb + 0u, cm & 3);
+              const float xn = upd::x_step<0>(U, false, fx, gr, Gv, fz, 0.f, xi);
+              U.xn[idx] = xn;
+              if (U.has_z) {
+                const float ze = upd::normal1(U.seed_lo, U.seed_hi, (uint32_t)cm >> 2, (uint32_t)o, fu_t1, U.sb + 1u, cm & 3);
+                U.z[idx] = upd::z_step(U, fz, xn, ze);
+              }
+              if (fu_acc) {
+                upd::welford(xn, fu_invn, fm, fs);
+                U.mean[idx] = fm;
+                U.m2[idx] = fs;
+              }
+            }
+          }
+        }
+        return true;
+      };
       for (int f = f0; f < nf; f += kProdWarps) {
         const uint32_t Fg = F0 + f;
         if (Fg >= 4 && !mbar_wait(bar_empty(0, Fg & 3), ((Fg >> 2) - 1) & 1, abort_flag, p.err, 1)) break;
@@ -600,7 +743,9 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
           }
         }
         trace_ev(p.trace, tr_on && lane == 0, 2, f, 0);
+        if (FU && fuse && !fu_rows_upto(f - fu_lag)) break;
       }
+      if (FU && fuse && !*abort_flag) fu_rows_upto(nout(NL - 1) - 1);
     } else if (warp < kEpi0) {
       // ================= MMA issuers (whole warp walks the schedule; one elected lane issues).
       // MMA warp w owns the layers l % kMmaWarps == w, so one warp's barrier waits overlap the
@@ -738,94 +883,10 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
 #pragma unroll
       for (int co = 0; co < NC; ++co) { nacc0[co] = 0.f; nacc1[co] = 0.f; }
       float *const xch = reinterpret_cast<float *>(smem + L.misc_off + 16 + 16 * NL);
-      // ---- fused update (FU && fuse; the folded layer's group, C = 1).  g = H^T(eta H x - y) at the
-      // strip's pixels in the order of update_sep_kernel, streamed row by row through shared memory:
-      //   T1(r, c) = sum_q kx[q+R] x(r, c - q)                 (Rs / T1 columns c = fcT + k, k < fKW)
-      //   Rs(r, c) = eta sum_q ky[q+R] T1(r - q, c) - y(r, c)  (0 outside the image)
-      //   T2(r, c) = sum_q kx[q+R] Rs(r, c + q)                (the strip's valid columns)
-      //   g(o, c)  = sum_q ky[q+R] T2(o + q, c)                (q = -R .. R, fma chains from 0)
-      // Output row o needs T2 rows o-R..o+R, hence T1 rows up to o+2R: rows are produced ahead as
-      // the group completes output rows (fnt1 / fnt2: next T1 / Rs-T2 row of this unit).  A lane
-      // owns T1 / Rs columns m, m + 128 and the T2 column of its pixel, so the rings need no
-      // barrier; the x and Rs rows other lanes read are double-buffered behind one group barrier.
-      const UpdateParams &U = p.up;
-      const int fR = (FU && fuse && U.op != 1) ? U.ry : 0;
-      const int fKW = Wv + 2 * fR;
-      const int fcT = c_strip0 - fR;
-      int fnt1 = r_lo - 2 * fR, fnt2 = r_lo - fR;
-      float fu_gr = 0.f;
-      float *const fu_xs = reinterpret_cast<float *>(smem + L.fu_off);   // [2][kFuXS] x rows
-      float *const fT1 = fu_xs + 2 * kFuXS;                            // [9][kFuT1] T1 ring
-      float *const fRS = fT1 + 9 * kFuT1;                            // [2][kFuT1] Rs rows
-      float *const fT2 = fRS + 2 * kFuT1;                            // [9][kFuT2] T2 ring (by lane)
-      const bool fu_lane = cm >= c_strip0 && cm < c_strip0 + Wv;         // this lane's pixel is in the strip
-      auto fu_bar = [&]() { asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory"); };
-      // padded-buffer read, zero outside the buffer (the TMA staging of update_sep_kernel)
-      auto fu_ld = [&](const float *b, int row, int col) -> float {
-        const TileGeom &g = U.g;
-        const int pr = row - (g.i0 - g.h), pc = col - (g.j0 - g.hx);
-        return (pr >= 0 && pr < g.ph && pc >= 0 && pc < g.pitch) ? b[(int64_t)pr * g.pitch + pc] : 0.f;
-      };
-      auto fu_slot = [](int row) { return (row + 18) % 9; };   // rows >= -2R >= -8
-      auto fu_t1_row = [&](int row) {
-        float *const xs = fu_xs + (row & 1) * kFuXS;
-        for (int u2 = m; u2 < fKW + 2 * fR; u2 += 128) xs[u2] = fu_ld(U.x, row, fcT - fR + u2);
-        fu_bar();
-        float *const t1 = fT1 + fu_slot(row) * kFuT1;
-        for (int k = m; k < fKW; k += 128) {
-          float sa = 0.f;
-          for (int q = -fR; q <= fR; ++q) sa = fmaf(U.kx[q + fR], xs[k + fR - q], sa);
-          t1[k] = sa;
-        }
-      };
-      auto fu_rs_t2_row = [&](int row) {
-        float *const rs = fRS + (row & 1) * kFuT1;
-        const bool rin = row >= 0 && row < p.ny;
-        for (int k = m; k < fKW; k += 128) {
-          float sa = 0.f;
-          for (int q = -fR; q <= fR; ++q) sa = fmaf(U.ky[q + fR], fT1[fu_slot(row - q) * kFuT1 + k], sa);
-          const int c = fcT + k;
-          rs[k] = (rin && c >= 0 && c < p.nx) ? U.eta * sa - fu_ld(U.y, row, c) : 0.f;
-        }
-        fu_bar();
-        if (fu_lane) {
-          const int k0 = cm - fcT;
-          float sa = 0.f;
-          for (int q = -fR; q <= fR; ++q) sa = fmaf(U.kx[q + fR], rs[k0 + q], sa);
-          fT2[fu_slot(row) * kFuT2 + m] = sa;
-        }
-      };
-      auto fu_advance = [&](int o) {
-        while (fnt2 <= o + fR) {
-          while (fnt1 <= fnt2 + fR) { fu_t1_row(fnt1); ++fnt1; }
-          fu_rs_t2_row(fnt2); ++fnt2;
-        }
-        float sa = 0.f;
-        if (fu_lane)
-          for (int q = -fR; q <= fR; ++q) sa = fmaf(U.ky[q + fR], fT2[fu_slot(o + q) * kFuT2 + m], sa);
-        fu_gr = sa;
-      };
       auto netlast_fill = [&](const int l, const int f) -> bool {
           const int s = f + kLag * l;
           const uint32_t Fg = Fcnt(l) + (uint32_t)f;
-          // fused update: g at this row (independent of the CNN) and the pixel's own operands,
-          // requested before the wait for the accumulators so their latency overlaps it
-          float fx = 0.f, fz = 0.f, fm = 0.f, fs = 0.f;
-          int64_t fidx = 0;
-          if constexpr (FU) {
-            const int icf = f - 2;
-            if (fuse && icf >= 0 && icf < nout(l)) {
-              const int of = r_lo - (NL - 1 - l) + icf;
-              if (U.op != 1) fu_advance(of);
-              if (col_valid) {
-                const TileGeom &g = U.g;
-                fidx = (int64_t)(of - (g.i0 - g.h)) * g.pitch + (cm - (g.j0 - g.hx));
-                fx = U.x[fidx];
-                if (U.has_z) fz = U.z[fidx];
-                if (fu_acc) { fm = U.mean[fidx]; fs = U.m2[fidx]; }
-              }
-            }
-          }
+          float fu_g = 0.f;   // fused update: this lane's G value of the completed row
           if (!mbar_wait(bar_tfull(l, Fg & 1), (Fg >> 1) & 1, abort_flag, p.err, 4)) return false;
           trace_ev(p.trace, trw, 6, s, l);
           tc_fence_after();
@@ -881,25 +942,7 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
             nacc1[co] = c[2];
             if (store) {
               if (FU && fuse) {
-                // fused K7 tail at (o, cm): the per-pixel arithmetic of ula_finish (update_math.cuh)
-                const float Gv = row_done + p.bias[l][co];
-                float gr = fu_gr;
-                if (U.op == 1) {
-                  const float mk = U.mask[fidx] ? 1.f : 0.f;
-                  gr = mk * (mk * fx - U.y[fidx]);
-                }
-                const float xi = upd::normal1(U.seed_lo, U.seed_hi, (uint32_t)cm >> 2, (uint32_t)o, fu_t1, U.sb + 0u, cm & 3);
-                const float xn = upd::x_step<0>(U, false, fx, gr, Gv, fz, 0.f, xi);
-                U.xn[fidx] = xn;
-                if (U.has_z) {
-                  const float ze = upd::normal1(U.seed_lo, U.seed_hi, (uint32_t)cm >> 2, (uint32_t)o, fu_t1, U.sb + 1u, cm & 3);
-                  U.z[fidx] = upd::z_step(U, fz, xn, ze);
-                }
-                if (fu_acc) {
-                  upd::welford(xn, fu_invn, fm, fs);
-                  U.mean[fidx] = fm;
-                  U.m2[fidx] = fs;
-                }
+                fu_g = row_done + p.bias[l][co];   // handed to the producers below (no G store)
               } else if (!kDdfb || p.mode < 2) {   // DDFB modes exist for 1- and 2-operator launches only
                 p.G[(int64_t)co * p.gcs + gidx] = row_done + p.bias[l][co];
               } else if (o >= 0 && o < p.ny && cm >= 0 && cm < p.nx) {
@@ -909,6 +952,23 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
                 const float q = fminf(fmaxf(v - row_done, 0.f), 1.f);
                 p.G[(int64_t)co * p.gcs + gidx] = p.mode == 4 ? v - q : q;
               }
+            }
+          }
+          if constexpr (FU) {
+            // fused update: the completed G row goes to the G ring the producer warps read
+            // (slot = running output-row count mod 8; a slot is re-filled once the 4 producer
+            // warps have read it)
+            if (fuse && ic >= 0 && ic < nout(l)) {
+              const uint32_t Ig = Ocnt(l) + (uint32_t)ic;
+              const uint32_t gs = Ig & (kFuG - 1);
+              const uint32_t gb = sbase + L.fu_off + kFuFloats * 4u;
+              if (Ig >= (uint32_t)kFuG &&
+                  !mbar_wait(gb + (kFuG + gs) * 8u, ((Ig / kFuG) - 1) & 1, abort_flag, p.err, 9))
+                return false;
+              float *const fG = reinterpret_cast<float *>(smem + L.fu_off) + (kFuFloats - kFuG * 128);
+              fG[gs * 128 + m] = fu_g;
+              __syncwarp();
+              if (lane == 0) mbar_arrive(gb + gs * 8u);
             }
           }
           trace_ev(p.trace, trw, 8, s, l);

@@ -143,9 +143,8 @@ struct pnpula_ctx {
   // exchange on comm_stream concurrently with the interior update
   bool overlap = false;
   // x / z / moment update fused into the last CNN chunk (cnn_kernels.cu, FU): DnCNN, C = 1,
-  // P = 32, separable 5x5 / 9x9 conv (or Poisson's x step) or mask.  Opt-in (env PNPULA_FUSE=1 at
-  // create): bitwise equal to the unfused step but measured slower -- the folded layer's epilogue
-  // group is latency-bound and paces the chunk (profiles/r02_fused_update.md).
+  // P = 32, separable 5x5 / 9x9 conv (or Poisson's x step) or mask, nets of more than one chunk
+  // (the last chunk's producer warps run the update).  Env PNPULA_FUSE=1 at create.
   bool fuse = false;
   int pdl = 1;                     // CNN launches as programmatic dependents (internal.h pdl_wait)
   cudaMemPool_t pool = nullptr;    // stream-ordered pool of the per-tile buffers (see dmalloc)
@@ -1176,6 +1175,10 @@ pnpula_status pnpula_create(const pnpula_config *cfg, pnpula_ctx **out) {
       c->fuse = (fe && atoi(fe) == 1) && cnn_fused_update_supported(c->channels, nc, u);
     }
     plan_cnn_chunks(c);
+    if (c->fuse && c->chunks.back().l0 == 1) {   // one chunk: its producers build im2col rows (no time to spare)
+      c->fuse = false;
+      plan_cnn_chunks(c);
+    }
     const int K = c->n_layers, P = c->channels;
     const float *w = f.den->weights;
     const float *b = f.den->biases;

@@ -1,7 +1,7 @@
 """The x / z / moment update fused into the last CNN chunk (cnn_kernels.cu, FU):
-the folded layer's epilogue evaluates g = H^T(eta H x - y) in a streaming separable stencil (or the
-mask term) and the K7 tail for every tile pixel it completes, in the per-pixel order of
-update_sep_kernel / update_mask_kernel.  The fused chain must therefore equal the unfused one
+the folded layer's epilogue hands every completed G row to the chunk's producer warps, which
+evaluate g = H^T(eta H x - y) in a streaming separable stencil (or the mask term) and the K7 tail
+ for every tile pixel, in the per-pixel order of update_sep_kernel / update_mask_kernel.  The fused chain must therefore equal the unfused one
 (PNPULA_FUSE=0 at create: G stored, then the update kernel) BIT FOR BIT -- over 3x3 / 5x5 / 9x9
 stencils, the mask operator, Poisson's x step, the AXDA z block, box prox, several column strips
 and row units per CTA, tiled grids, graph replays and the layer-wise chain -- and the fused run
