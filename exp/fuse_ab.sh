@@ -1,5 +1,5 @@
 # fused update (PNPULA_FUSE=1) vs unfused (PNPULA_FUSE=0): tests, then c5 / c3 / c2 bench A/B
-true
+timeout 900 python -m pytest tests/test_gpu_fused_update.py -q -x > gpurun_out/fu_tests.log 2>&1; echo "fused tests rc=$?"; tail -3 gpurun_out/fu_tests.log
 for rep in a b; do for v in "fused:PNPULA_FUSE=1" "unfused:PNPULA_FUSE=0"; do
   n=${v%%:*}; e=${v#*:}
   for w in c5 c3; do

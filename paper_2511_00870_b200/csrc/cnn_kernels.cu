@@ -32,6 +32,7 @@
 // strip/tile it falls in, so results are bitwise identical for every tile grid.
 #include <cstdint>
 #include <cstring>
+#include <type_traits>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -487,6 +488,9 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
   auto Ocnt = [&](int l) { return sumRn + kdone * (uint32_t)(2 * (NL - 1 - l)); };
 
   uint32_t xphase = 0;   // im2col producers: phase of this warp's x-staging mbarrier
+  // fused update: stencil row barriers this producer warp has passed -- across units, as the
+  // mbarrier phases persist (all 4 producer warps pass the same sequence)
+  [[maybe_unused]] uint32_t fu_nsync = 0;
   for (int u = blockIdx.x; u < units; u += gridDim.x) {
     if (*abort_flag) break;
     const int rb = u / strips, strip = u - (u / strips) * strips;
@@ -523,125 +527,181 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
       // barrier of the 128 producer threads per row.)  G arrives through the G ring.  A warp
       // finishes output row ic only after issuing its layer-0 fills up to ic + 2 + kLag (NL-1) + 4,
       // so a row it waits for never depends on a fill it has not issued (no deadlock).
-      [[maybe_unused]] int fu_done = 0, fnt1 = 0, fnt2 = 0;
-      [[maybe_unused]] uint32_t fu_nsync = 0;   // stencil row barriers passed (all 4 warps pass the same sequence)
+      [[maybe_unused]] int fu_done = 0;
+      // the next row's global operands, loaded one row ahead (valid when fu_pf == fu_done)
+      [[maybe_unused]] int fu_pf = -1;
+      [[maybe_unused]] float pf_x = 0.f, pf_z = 0.f, pf_m = 0.f, pf_s = 0.f, pf_y = 0.f;
+      [[maybe_unused]] float pf_xa = 0.f, pf_xb = 0.f, pf_ya = 0.f, pf_yb = 0.f;
+      [[maybe_unused]] uint8_t pf_mk = 0;
       [[maybe_unused]] const int fu_lag = 2 + kLag * (NL - 1) + 4;
+      [[maybe_unused]] bool fu_warm = false;
+      // rows [fu_done, icmax] of this unit, for a compile-time stencil radius R (0: mask, no stencil)
+      auto fu_rows_R = [&](auto Rc, int icmax) -> bool {
+        constexpr int R = decltype(Rc)::value;
+        const UpdateParams &U = p.up;
+        const int l = NL - 1;
+        const int no = nout(l);
+        constexpr int KX = 2 * R;
+        const int fKW = Wv + KX;            // T1 / Rs columns c = fcT + k
+        const int fcT = c_strip0 - R;
+        const int m = warp * 32 + lane;
+        const int cm = col0 + m;
+        const bool fu_lane = cm >= c_strip0 && cm < c_strip0 + Wv;
+        const bool cvalid = fu_lane && cm < p.oj0 + p.ow;
+        const bool k2 = m + 128 < fKW;      // this lane also owns T1 / Rs column m + 128
+        const bool x2 = m + 128 < fKW + KX; // ... and x staging column m + 128
+        float *const fxs = reinterpret_cast<float *>(smem + L.fu_off);
+        float *const fT1 = fxs + 2 * kFuXS;
+        float *const fRS = fT1 + kFuRing * kFuT1;
+        float *const fT2 = fRS + 2 * kFuT1;
+        float *const fG = fT2 + kFuRing * kFuT2;
+        const uint32_t gb = sbase + L.fu_off + kFuFloats * 4u;
+        const TileGeom &g = U.g;
+        auto ldpad = [&](const float *b, int row, int col) -> float {   // 0 outside the buffer (TMA)
+          const int pr = row - (g.i0 - g.h), pc = col - (g.j0 - g.hx);
+          return (pr >= 0 && pr < g.ph && pc >= 0 && pc < g.pitch) ? b[(int64_t)pr * g.pitch + pc] : 0.f;
+        };
+        // barrier of the 4 producer warps (two mbarriers used alternately, one arrival per warp; the
+        // bounded wait keeps an aborted CTA from hanging, unlike a named barrier)
+        auto pbar = [&]() -> bool {
+          const uint32_t b = gb + (2u * kFuG + (fu_nsync & 1u)) * 8u;
+          const uint32_t ph = (fu_nsync >> 1) & 1u;
+          ++fu_nsync;
+          __syncwarp();
+          if (lane == 0) mbar_arrive(b);
+          return mbar_wait(b, ph, abort_flag, p.err, 11);
+        };
+        auto stage_x = [&](int row, float a0, float a1) {   // x row `row`, columns fcT - R + u
+          float *const xs = fxs + (row & 1) * kFuXS;
+          xs[m] = a0;
+          if (x2) xs[m + 128] = a1;
+        };
+        auto t1_at = [&](int row, int k) {                   // T1(row, fcT + k) = sum_q kx[q+R] x(row, c - q)
+          const float *const xs = fxs + (row & 1) * kFuXS;
+          float sa = 0.f;
+#pragma unroll
+          for (int q = -R; q <= R; ++q) sa = fmaf(U.kx[q + R], xs[k + R - q], sa);
+          fT1[(row & (kFuRing - 1)) * kFuT1 + k] = sa;
+        };
+        auto rs_at = [&](int row, int k, float yv) {         // Rs(row, c) = eta sum_q ky[q+R] T1(row - q, c) - y
+          float sa = 0.f;
+#pragma unroll
+          for (int q = -R; q <= R; ++q) sa = fmaf(U.ky[q + R], fT1[((row - q) & (kFuRing - 1)) * kFuT1 + k], sa);
+          const int c = fcT + k;
+          fRS[(row & 1) * kFuT1 + k] = (row >= 0 && row < p.ny && c >= 0 && c < p.nx) ? U.eta * sa - yv : 0.f;
+        };
+        auto t2_own = [&](int row) {                         // T2(row, cm) = sum_q kx[q+R] Rs(row, cm + q)
+          if (!fu_lane) return;
+          const float *const rs = fRS + (row & 1) * kFuT1 + (cm - fcT);
+          float sa = 0.f;
+#pragma unroll
+          for (int q = -R; q <= R; ++q) sa = fmaf(U.kx[q + R], rs[q], sa);
+          fT2[(row & (kFuRing - 1)) * kFuT2 + m] = sa;
+        };
+        if constexpr (R > 0) {
+          if (!fu_warm) {   // unit start: T1 rows r_lo-2R .. r_lo+2R-1, Rs / T2 rows r_lo-R .. r_lo+R-1
+            for (int t = r_lo - 2 * R; t < r_lo + 2 * R; ++t) {
+              stage_x(t, ldpad(U.x, t, fcT - R + m), x2 ? ldpad(U.x, t, fcT - R + m + 128) : 0.f);
+              if (!pbar()) return false;
+              t1_at(t, m);
+              if (k2) t1_at(t, m + 128);
+            }
+            for (int t = r_lo - R; t < r_lo + R; ++t) {
+              rs_at(t, m, ldpad(U.y, t, fcT + m));
+              if (k2) rs_at(t, m + 128, ldpad(U.y, t, fcT + m + 128));
+              if (!pbar()) return false;
+              t2_own(t);
+            }
+            const int t = r_lo + 2 * R;
+            stage_x(t, ldpad(U.x, t, fcT - R + m), x2 ? ldpad(U.x, t, fcT - R + m + 128) : 0.f);
+            if (!pbar()) return false;
+          }
+        }
+        fu_warm = true;
+        const int last_ic = icmax < no - 1 ? icmax : no - 1;
+        // global operands of row ic (pixel: x, z, mean, M2 [, mask, y]; stencil: x row o + 2R + 1 and
+        // y row o + R at this lane's staging / Rs columns) into the pf_ registers
+        auto prefetch = [&](int ic) {
+          const int o = r_lo + ic;
+          if (cvalid) {
+            const int64_t idx = (int64_t)(o - (g.i0 - g.h)) * g.pitch + (cm - (g.j0 - g.hx));
+            pf_x = U.x[idx];
+            if (U.has_z) pf_z = U.z[idx];
+            if (fu_acc) { pf_m = U.mean[idx]; pf_s = U.m2[idx]; }
+            if (R == 0) { pf_mk = U.mask[idx]; pf_y = U.y[idx]; }
+          }
+          if constexpr (R > 0) {
+            const int tx = o + 2 * R + 1, ty = o + R;
+            pf_xa = ldpad(U.x, tx, fcT - R + m);
+            pf_xb = x2 ? ldpad(U.x, tx, fcT - R + m + 128) : 0.f;
+            pf_ya = ldpad(U.y, ty, fcT + m);
+            pf_yb = k2 ? ldpad(U.y, ty, fcT + m + 128) : 0.f;
+          }
+          fu_pf = ic;
+        };
+        for (; fu_done <= last_ic; ++fu_done) {
+          const int ic = fu_done;
+          const int o = r_lo + ic;
+          // A. this row's operands (loaded one row ahead), then the next row's requested
+          if (fu_pf != ic) prefetch(ic);
+          const float fx = pf_x, fz = pf_z, fm0 = pf_m, fs0 = pf_s, fy = pf_y;
+          const uint8_t fmk = pf_mk;
+          const float xa = pf_xa, xb = pf_xb, ya = pf_ya, yb = pf_yb;
+          const int64_t idx = (int64_t)(o - (g.i0 - g.h)) * g.pitch + (cm - (g.j0 - g.hx));
+          if (ic + 1 < no) prefetch(ic + 1);
+          // the noise does not depend on the stencil or G: computed while the loads are in flight
+          float xi = 0.f, ze = 0.f;
+          if (cvalid) {
+            xi = upd::normal1(U.seed_lo, U.seed_hi, (uint32_t)cm >> 2, (uint32_t)o, fu_t1, U.sb + 0u, cm & 3);
+            if (U.has_z) ze = upd::normal1(U.seed_lo, U.seed_hi, (uint32_t)cm >> 2, (uint32_t)o, fu_t1, U.sb + 1u, cm & 3);
+          }
+          float fm = fm0, fs = fs0;
+          float gr = 0.f;
+          if constexpr (R > 0) {
+            const int tx = o + 2 * R + 1, ty = o + R;
+            // B. T1(o + 2R) (x row staged last iteration); C. Rs(o + R); D. stage x(o + 2R + 1)
+            t1_at(o + 2 * R, m);
+            if (k2) t1_at(o + 2 * R, m + 128);
+            rs_at(ty, m, ya);
+            if (k2) rs_at(ty, m + 128, yb);
+            stage_x(tx, xa, xb);
+            if (!pbar()) return false;   // E. one barrier per row
+            t2_own(ty);                  // F. T2(o + R)
+            if (fu_lane) {               // G. g(o) = sum_q ky[q+R] T2(o + q, cm)
+#pragma unroll
+              for (int q = -R; q <= R; ++q) gr = fmaf(U.ky[q + R], fT2[((o + q) & (kFuRing - 1)) * kFuT2 + m], gr);
+            }
+          } else if (cvalid) {
+            const float mk = fmk ? 1.f : 0.f;
+            gr = mk * (mk * fx - fy);
+          }
+          // H. G from the ring, then the K7 tail (update_math.cuh)
+          const uint32_t Ig = Ocnt(l) + (uint32_t)ic;
+          const uint32_t gs = Ig & (kFuG - 1);
+          if (!mbar_wait(gb + gs * 8u, (Ig / kFuG) & 1, abort_flag, p.err, 10)) return false;
+          const float Gv = fG[gs * 128 + m];
+          __syncwarp();
+          if (lane == 0) mbar_arrive(gb + (kFuG + gs) * 8u);
+          if (cvalid) {
+            const float xn = upd::x_step<0>(U, false, fx, gr, Gv, fz, 0.f, xi);
+            U.xn[idx] = xn;
+            if (U.has_z) U.z[idx] = upd::z_step(U, fz, xn, ze);
+            if (fu_acc) {
+              upd::welford(xn, fu_invn, fm, fs);
+              U.mean[idx] = fm;
+              U.m2[idx] = fs;
+            }
+          }
+        }
+        return true;
+      };
       auto fu_rows_upto = [&](int icmax) -> bool {
         if constexpr (FU) {
           if (!fuse) return true;
-          const UpdateParams &U = p.up;
-          const int l = NL - 1;
-          const int no = nout(l);
-          const int fR = U.op != 1 ? U.ry : 0;
-          const int fKW = Wv + 2 * fR;
-          const int fcT = c_strip0 - fR;
-          const int m = warp * 32 + lane;
-          const int cm = col0 + m;
-          const bool fu_lane = cm >= c_strip0 && cm < c_strip0 + Wv;
-          const bool cvalid = fu_lane && cm < p.oj0 + p.ow;
-          float *const fxs = reinterpret_cast<float *>(smem + L.fu_off);
-          float *const fT1 = fxs + 2 * kFuXS;
-          float *const fRS = fT1 + kFuRing * kFuT1;
-          float *const fT2 = fRS + 2 * kFuT1;
-          float *const fG = fT2 + kFuRing * kFuT2;
-          const uint32_t gb = sbase + L.fu_off + kFuFloats * 4u;
-          const TileGeom &g = U.g;
-          auto ldpad = [&](const float *b, int row, int col) -> float {   // 0 outside the buffer (TMA)
-            const int pr = row - (g.i0 - g.h), pc = col - (g.j0 - g.hx);
-            return (pr >= 0 && pr < g.ph && pc >= 0 && pc < g.pitch) ? b[(int64_t)pr * g.pitch + pc] : 0.f;
-          };
-          // barrier of the 4 producer warps (two mbarriers used alternately, one arrival per warp; the
-          // bounded wait keeps an aborted CTA from hanging here, unlike a named barrier)
-          auto pbar = [&]() -> bool {
-            const uint32_t b = gb + (2u * kFuG + (fu_nsync & 1u)) * 8u;
-            const uint32_t ph = (fu_nsync >> 1) & 1u;
-            ++fu_nsync;
-            __syncwarp();
-            if (lane == 0) mbar_arrive(b);
-            return mbar_wait(b, ph, abort_flag, p.err, 11);
-          };
-          auto t1_row = [&](int row) -> bool {
-            float *const xs = fxs + (row & 1) * kFuXS;
-            for (int u2 = m; u2 < fKW + 2 * fR; u2 += 128) xs[u2] = ldpad(U.x, row, fcT - fR + u2);
-            if (!pbar()) return false;
-            float *const t1 = fT1 + (row & (kFuRing - 1)) * kFuT1;
-            for (int k = m; k < fKW; k += 128) {
-              float sa = 0.f;
-              for (int q = -fR; q <= fR; ++q) sa = fmaf(U.kx[q + fR], xs[k + fR - q], sa);
-              t1[k] = sa;
-            }
-            return true;
-          };
-          auto rs_t2_row = [&](int row) -> bool {
-            float *const rs = fRS + (row & 1) * kFuT1;
-            const bool rin = row >= 0 && row < p.ny;
-            for (int k = m; k < fKW; k += 128) {
-              float sa = 0.f;
-              for (int q = -fR; q <= fR; ++q) sa = fmaf(U.ky[q + fR], fT1[((row - q) & (kFuRing - 1)) * kFuT1 + k], sa);
-              const int c = fcT + k;
-              rs[k] = (rin && c >= 0 && c < p.nx) ? U.eta * sa - ldpad(U.y, row, c) : 0.f;
-            }
-            if (!pbar()) return false;
-            if (fu_lane) {
-              const int k0 = cm - fcT;
-              float sa = 0.f;
-              for (int q = -fR; q <= fR; ++q) sa = fmaf(U.kx[q + fR], rs[k0 + q], sa);
-              fT2[(row & (kFuRing - 1)) * kFuT2 + m] = sa;
-            }
-            return true;
-          };
-          if (fu_done == 0) { fnt1 = r_lo - 2 * fR; fnt2 = r_lo - fR; }
-          const int last_ic = icmax < no - 1 ? icmax : no - 1;
-          for (; fu_done <= last_ic; ++fu_done) {
-            const int ic = fu_done;
-            const int o = r_lo + ic;
-            float gr = 0.f;
-            if (U.op != 1) {
-              while (fnt2 <= o + fR) {
-                while (fnt1 <= fnt2 + fR) {
-                  if (!t1_row(fnt1)) return false;
-                  ++fnt1;
-                }
-                if (!rs_t2_row(fnt2)) return false;
-                ++fnt2;
-              }
-              if (fu_lane)
-                for (int q = -fR; q <= fR; ++q) gr = fmaf(U.ky[q + fR], fT2[((o + q) & (kFuRing - 1)) * kFuT2 + m], gr);
-            }
-            float fx = 0.f, fz = 0.f, fm = 0.f, fs = 0.f;
-            int64_t idx = 0;
-            if (cvalid) {
-              idx = (int64_t)(o - (g.i0 - g.h)) * g.pitch + (cm - (g.j0 - g.hx));
-              fx = U.x[idx];
-              if (U.has_z) fz = U.z[idx];
-              if (fu_acc) { fm = U.mean[idx]; fs = U.m2[idx]; }
-              if (U.op == 1) {
-                const float mk = U.mask[idx] ? 1.f : 0.f;
-                gr = mk * (mk * fx - U.y[idx]);
-              }
-            }
-            const uint32_t Ig = Ocnt(l) + (uint32_t)ic;
-            const uint32_t gs = Ig & (kFuG - 1);
-            if (!mbar_wait(gb + gs * 8u, (Ig / kFuG) & 1, abort_flag, p.err, 10)) return false;
-            const float Gv = fG[gs * 128 + m];
-            __syncwarp();
-            if (lane == 0) mbar_arrive(gb + (kFuG + gs) * 8u);
-            if (cvalid) {
-              // the K7 tail of ula_finish for this pixel (update_math.cuh)
-              const float xi = upd::normal1(U.seed_lo, U.seed_hi, (uint32_t)cm >> 2, (uint32_t)o, fu_t1, U.sb + 0u, cm & 3);
-              const float xn = upd::x_step<0>(U, false, fx, gr, Gv, fz, 0.f, xi);
-              U.xn[idx] = xn;
-              if (U.has_z) {
-                const float ze = upd::normal1(U.seed_lo, U.seed_hi, (uint32_t)cm >> 2, (uint32_t)o, fu_t1, U.sb + 1u, cm & 3);
-                U.z[idx] = upd::z_step(U, fz, xn, ze);
-              }
-              if (fu_acc) {
-                upd::welford(xn, fu_invn, fm, fs);
-                U.mean[idx] = fm;
-                U.m2[idx] = fs;
-              }
-            }
-          }
+          const int fR = p.up.op != 1 ? p.up.ry : 0;
+          if (fR == 4) return fu_rows_R(std::integral_constant<int, 4>{}, icmax);
+          if (fR == 2) return fu_rows_R(std::integral_constant<int, 2>{}, icmax);
+          return fu_rows_R(std::integral_constant<int, 0>{}, icmax);
         }
         return true;
       };
