@@ -30,6 +30,7 @@
 //  * fp32 accumulation in TMEM.
 // Every output pixel's arithmetic (K order, rounding points) is independent of the
 // strip/tile it falls in, so results are bitwise identical for every tile grid.
+#include <algorithm>
 #include <cstdint>
 #include <cstring>
 #include <type_traits>
@@ -491,15 +492,36 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
   // fused update: stencil row barriers this producer warp has passed -- across units, as the
   // mbarrier phases persist (all 4 producer warps pass the same sequence)
   [[maybe_unused]] uint32_t fu_nsync = 0;
-  for (int u = blockIdx.x; u < units; u += gridDim.x) {
+  // Work units.  Row blocks (rows_per_cta == 0): unit u = (row block u / strips, strip u % strips),
+  // CTAs take units round-robin.  Contiguous (rows_per_cta = T > 0): CTA b owns the strip-major
+  // output rows [b T, (b+1) T) of the strips x oh grid, one unit per strip it touches -- every unit
+  // pays the pipeline's fill once, so a CTA pays it once or twice instead of once per row block.
+  const int Tc = p.rows_per_cta;
+  int64_t cpos = (int64_t)blockIdx.x * Tc;
+  const int64_t cend = Tc > 0 ? min((int64_t)(blockIdx.x + 1) * Tc, (int64_t)strips * p.oh) : 0;
+  bool first_unit = true;
+  for (int u = blockIdx.x;;) {
+    int strip, r_lo, r_hi;
+    if (Tc > 0) {
+      if (cpos >= cend) break;
+      strip = (int)(cpos / p.oh);
+      const int64_t segend = min(cend, (int64_t)(strip + 1) * p.oh);
+      r_lo = p.oi0 + (int)(cpos - (int64_t)strip * p.oh);
+      r_hi = r_lo + (int)(segend - cpos);
+      cpos = segend;
+    } else {
+      if (u >= units) break;
+      const int rb = u / strips;
+      strip = u - rb * strips;
+      r_lo = p.oi0 + rb * R;
+      r_hi = min(r_lo + R, p.oi0 + p.oh);
+      u += gridDim.x;
+    }
     if (*abort_flag) break;
-    const int rb = u / strips, strip = u - (u / strips) * strips;
-    const int r_lo = p.oi0 + rb * R;
-    const int r_hi = min(r_lo + R, p.oi0 + p.oh);
     const int Rn = r_hi - r_lo;
     const int c_strip0 = p.oj0 + strip * Wv;         // first valid output column of the strip
     const int col0 = c_strip0 - NLg + 1;             // column of MMA row 0 (ring position 1)
-    const bool tr_on = p.trace != nullptr && blockIdx.x == 0 && u == (int)blockIdx.x;
+    const bool tr_on = p.trace != nullptr && blockIdx.x == 0 && first_unit;
     // layer l: nout(l) = Rn + 2 (NL-1-l) output rows starting at global row r_lo-(NL-1-l);
     // its input fills are rows r0(l)-1 .. (nout+2 fills), or nout im2col rows for an im2col layer.
     auto nout = [&](int l) { return Rn + 2 * (NL - 1 - l); };
@@ -1223,6 +1245,7 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
     }
     sumRn += (uint32_t)Rn;
     ++kdone;
+    first_unit = false;
   }
 
   // ---- teardown: make sure every tcgen05 op (and its mbarrier arrivals) has retired
@@ -1261,10 +1284,25 @@ cudaError_t launch_pn(const CnnChunkParams &p0, int num_sms, cudaStream_t s) {
   p.strips = strips;
   p.rows_per_unit = R;
   p.units = strips * ((p.oh + R - 1) / R);
+  p.rows_per_cta = 0;
+  int grid = p.units < num_sms ? p.units : num_sms;
+  if (p.contig) {
+    // contiguous strip-major ranges of T rows per CTA: a CTA touches <= ceil(T / oh) + 1 strips, each
+    // a unit with one pipeline fill; use them when that model beats the row blocks' waves x (R + fill)
+    const int64_t total = (int64_t)strips * p.oh;
+    const int g2 = (int)std::min<int64_t>(num_sms, total);
+    const int64_t T = (total + g2 - 1) / g2;
+    const double cost_c = (double)T + 3.0 * NL * (double)((T + p.oh - 1) / p.oh + 1);
+    const int nrb = (p.oh + R - 1) / R;
+    const double cost_b = (double)((strips * nrb + num_sms - 1) / num_sms) * (R + 3.0 * NL);
+    if (cost_c < cost_b) {
+      p.rows_per_cta = (int)T;
+      grid = (int)((total + T - 1) / T);
+    }
+  }
   auto kfn = cnn_chunk_kernel<P, NL, NC, FU>;
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
   if (e != cudaSuccess) return e;
-  const int grid = p.units < num_sms ? p.units : num_sms;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(block_threads(NL));

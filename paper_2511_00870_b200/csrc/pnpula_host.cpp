@@ -146,6 +146,7 @@ struct pnpula_ctx {
   // P = 32, separable 5x5 / 9x9 conv (or Poisson's x step) or mask, nets of more than one chunk
   // (the last chunk's producer warps run the update).  Env PNPULA_FUSE=1 at create.
   bool fuse = false;
+  int cnn_contig = 1;              // contiguous CNN work ranges where the cost model prefers them (PNPULA_CNN_CONTIG=0: off)
   int pdl = 1;                     // CNN launches as programmatic dependents (internal.h pdl_wait)
   cudaMemPool_t pool = nullptr;    // stream-ordered pool of the per-tile buffers (see dmalloc)
   cudaStream_t comm_stream = nullptr;
@@ -386,6 +387,7 @@ pnpula_status run_cnn(pnpula_ctx *c, int buf, bool fused = false, const IterStat
       p.xcs = p.gcs = (int64_t)geom_elems(g);
       p.err = c->d_err;
       p.pdl = c->pdl;
+      p.contig = c->cnn_contig;
       // optional pipeline trace of the first evaluation (diagnostics; env PNPULA_CNN_TRACE=<path prefix>)
       const char *trace_path = getenv("PNPULA_CNN_TRACE");
       unsigned long long *d_trace = nullptr;
@@ -1039,6 +1041,8 @@ pnpula_status pnpula_create(const pnpula_config *cfg, pnpula_ctx **out) {
   {
     const char *pe2 = getenv("PNPULA_PDL");
     c->pdl = (pe2 && atoi(pe2) == 0) ? 0 : 1;
+    const char *pe3 = getenv("PNPULA_CNN_CONTIG");
+    c->cnn_contig = (pe3 && atoi(pe3) == 0) ? 0 : 1;
   }
   {
     const char *ge = getenv("PNPULA_GRAPHS");
