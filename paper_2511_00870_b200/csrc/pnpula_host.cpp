@@ -319,7 +319,7 @@ pnpula_status run_ddfb(pnpula_ctx *c, int buf) {
       p.gg = g;
       p.ny = c->ny; p.nx = c->nx;
       p.err = c->d_err;
-      p.pdl = c->pdl;
+      p.pdl = c->pdl;   // (row-block units: the contiguous ranges measured 1 % slower for DDFB, d5)
       cudaEvent_t end;
       timer_begin(c, c->tm_cnn, &end);
       CU(c, launch_cnn_chunk(p, c->num_sms, c->stream));
