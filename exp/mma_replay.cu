@@ -60,6 +60,54 @@ __global__ void __launch_bounds__(128, 1) kern(int rows, long long *cyc) {
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tb = tslot, sb = smem_u32(smem);
+  if (mode == 4) {   // warp w issues layer w only (run-time descriptors, as the kernel's MMA warps)
+    const uint32_t ring[4] = {RING0, RING1, RING2, RING3};
+    const uint32_t wo[4] = {W0, W1, W2, W3};
+    __shared__ __align__(8) uint64_t fin[4];
+    if (threadIdx.x == 0) for (int w = 0; w < 4; ++w) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&fin[w])));
+    __syncthreads();
+    const long long t0 = clock64();
+    const int l = warp;
+    for (int r = 0; r < rows; ++r) {
+      if (l == 0) {
+        const uint64_t ad = make_desc(sb + RING0 + (r & 3) * SLOT_IM, 2048, 128);
+        const uint64_t bd = make_desc(sb + W0, P * 16, 128);
+        if (elect_one()) mma(tb + (r & 3) * P, ad, bd, make_idesc(P), 0);
+        __syncwarp();
+      } else {
+        const uint32_t acc0 = tb + l * 4 * P;
+        const uint32_t slot = sb + ring[l] + (r & 3) * SLOT_ACT;
+        const uint32_t wb = sb + wo[l];
+        const uint32_t Ilo = (uint32_t)(r + 2);
+        const int n1 = (int)min(3u, 4u - (Ilo & 3));
+        const int n2 = 3 - n1;
+        const uint64_t ad0 = make_desc(slot, GS, 128), bd0 = make_desc(wb, 3 * P * 16, 128);
+        const uint32_t d1 = acc0 + (Ilo & 3) * P, d2 = acc0;
+        const uint32_t id1 = make_idesc(n1 * P), id2 = make_idesc(n2 > 0 ? n2 * P : P);
+        if (elect_one()) {
+#pragma unroll
+          for (int dx = 0; dx < 3; ++dx)
+#pragma unroll
+            for (int ks = 0; ks < 2; ++ks) {
+              const uint64_t ad = ad0 + (uint64_t)((2 * ks * GS + dx * 16) >> 4);
+              const uint64_t bd = bd0 + (uint64_t)((dx * 2 + ks) * 3 * P * 2);
+              mma(d1, ad, bd, id1, 1);
+              if (n2 > 0) mma(d2, ad, bd + (uint64_t)(n1 * P), id2, 1);
+            }
+        }
+        __syncwarp();
+      }
+    }
+    if (elect_one())
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&fin[warp])));
+    __syncwarp();
+    uint32_t ok = 0;
+    while (!ok)
+      asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\tselp.u32 %0,1,0,p;\n\t}"
+                   : "=r"(ok) : "r"(smem_u32(&fin[warp])));
+    __syncthreads();
+    if (threadIdx.x == 0) cyc[blockIdx.x] = clock64() - t0;
+  } else
   if (warp == 0) {   // the whole warp walks the stream (warp-uniform descriptors), one elected lane issues
     const uint32_t ring[4] = {RING0, RING1, RING2, RING3};
     const uint32_t wo[4] = {W0, W1, W2, W3};
@@ -137,7 +185,6 @@ int main() {
   run<0>("kernel chunk-1 MMA stream (ring-4 splits)", 2000);
   run<2>("windowed layers, no splits (N = 96 only)", 2000);
   run<3>("as mode 0, one weight block for all layers", 2000);
-  run<0>("kernel chunk-1 MMA stream, long (~1 s)", 600000);
-  run<0>("kernel chunk-1 MMA stream (after the long run)", 2000);
+  run<4>("chunk-1 stream, 4 warps (one layer each), run-time descriptors", 2000);
   return 0;
 }
