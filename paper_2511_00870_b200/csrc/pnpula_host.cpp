@@ -761,7 +761,8 @@ void plan_cnn_chunks(pnpula_ctx *c) {
   int l = 1;
   while (l <= K) {
     int best = 1;
-    const int maxnl = (c->flags & PNPULA_FLAG_CNN_LAYERWISE) ? 1 : kMaxChunk;
+    const char *mnl = getenv("PNPULA_MAX_NL");   // experiment: cap the layers per launch
+    const int maxnl = (c->flags & PNPULA_FLAG_CNN_LAYERWISE) ? 1 : (mnl && atoi(mnl) > 0) ? std::min(atoi(mnl), kMaxChunk) : kMaxChunk;
     for (int nl = 1; nl <= std::min(maxnl, K - l + 1); ++nl) {
       if (cnn_chunk_smem_bytes(c->channels, nl, l == 1, l + nl - 1 == K, c->nc, c->fuse) <= budget) best = nl;
     }
