@@ -428,11 +428,17 @@ update_sep_kernel(const __grid_constant__ UpdateParams p, const __grid_constant_
   __syncthreads();
   int blk = blockIdx.x;
   if (tid == 0 && blk < nblk) stage(blk, 0);
+  // block coordinates advanced incrementally (one run-time division at entry, not one per block)
+  const int gq = (int)gridDim.x / nbx, gr_ = (int)gridDim.x - gq * nbx;
+  int bby = blk / nbx, bbx = blk - bby * nbx;
   for (int k = 0; blk < nblk; blk += gridDim.x, ++k) {
     const int buf = k & 1;
     const int nxt = blk + gridDim.x;
-    const int bi0 = g.i0 + (blk / nbx) * TY;
-    const int bj0 = (g.j0 & ~3) + (blk - (blk / nbx) * nbx) * TX;
+    const int bi0 = g.i0 + bby * TY;
+    const int bj0 = (g.j0 & ~3) + bbx * TX;
+    bbx += gr_;
+    bby += gq;
+    if (bbx >= nbx) { bbx -= nbx; ++bby; }
     float *const X = sm + buf * XR * XC;
     float *const Yw = sm + 2 * XR * XC + buf * RR * XC;
     const float *const Y = Yw;
@@ -476,6 +482,7 @@ update_sep_kernel(const __grid_constant__ UpdateParams p, const __grid_constant_
     // this barrier, so the next block's prefetch is issued here (no end-of-block barrier)
     if (tid == 0 && nxt < nblk) stage(nxt, buf ^ 1);
     // phase 2: Rs[a][b] = sum_p ky[p+R] T1[a+R-p][b] - y, zero outside the image (4x4 per item)
+    const bool rs_inside = bi0 - R >= 0 && bi0 - R + RR <= p.ny && bj0 - R >= 0 && bj0 - R + RC <= p.nx;
     for (int e = tid; e < (RR / 4) * (RC / 4); e += NTHREADS) {
       const int a4 = e / (RC / 4), k4 = e - a4 * (RC / 4);
       float col[NW][4];
@@ -506,9 +513,14 @@ update_sep_kernel(const __grid_constant__ UpdateParams p, const __grid_constant_
           const float2 t0 = *reinterpret_cast<const float2 *>(yr), t1 = *reinterpret_cast<const float2 *>(yr + 2);
           yv[0] = t0.x; yv[1] = t0.y; yv[2] = t1.x; yv[3] = t1.y;
         }
-        const bool rin = gi >= 0 && gi < p.ny;
+        if (rs_inside) {   // the block's whole residual region lies in the image: no per-element test
 #pragma unroll
-        for (int j = 0; j < 4; ++j) o[j] = (rin && gj + j >= 0 && gj + j < p.nx) ? p.eta * o[j] - yv[j] : 0.f;
+          for (int j = 0; j < 4; ++j) o[j] = p.eta * o[j] - yv[j];
+        } else {
+          const bool rin = gi >= 0 && gi < p.ny;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) o[j] = (rin && gj + j >= 0 && gj + j < p.nx) ? p.eta * o[j] - yv[j] : 0.f;
+        }
         *reinterpret_cast<float4 *>(Rs + a * RP + 4 * k4) = make_float4(o[0], o[1], o[2], o[3]);
       }
     }
