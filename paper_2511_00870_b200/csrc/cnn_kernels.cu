@@ -842,8 +842,11 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
           const bool netlast = (l == NL - 1) && last && !im2col;
           const uint32_t Fg = Fcnt(l) + (uint32_t)f;
           trace_ev(p.trace, tr_on && lane == 0, 3, s, l);
-          const uint32_t nring = ring_slots(l), rs = Fg % nring;
-          ok = mbar_wait(bar_full(l, rs), (Fg / nring) & 1, abort_flag, p.err, 2);
+          // ring slot and phase of this input row: compile-time divisors on both branches (a ring
+          // size selected at run time would put an integer division on the issue path)
+          const uint32_t rs = l == 0 ? Fg % (uint32_t)kRing : Fg % (uint32_t)kRingAct;
+          const uint32_t rph = l == 0 ? (Fg / (uint32_t)kRing) & 1u : (Fg / (uint32_t)kRingAct) & 1u;
+          ok = mbar_wait(bar_full(l, rs), rph, abort_flag, p.err, 2);
           trace_ev(p.trace, tr_on && lane == 0, 14, s, l);
           // output row that receives its first contribution (im2col: the only one)
           const uint32_t O0 = Ocnt(l);
