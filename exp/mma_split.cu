@@ -33,7 +33,7 @@ __device__ __forceinline__ void mma(uint32_t d, uint64_t ad, uint64_t bd, uint32
 constexpr int P = 32, GS = 130 * 16;
 constexpr uint32_t AOFF = 0, BOFF = 4 * 4 * GS, TOTAL0 = BOFF + 6 * 96 * 32;
 // chunk layout: 3 windowed layers, each 4 ring rows (4 x 8,320 B) + 18 KB weights; im2col ring 4 x 4 KB + 1 KB
-constexpr uint32_t LSTRIDE = 4 * 4 * GS + 6 * 96 * 32, IMOFF = 3 * LSTRIDE, TOTAL = IMOFF + 4 * 4096 + 1024;
+constexpr uint32_t LSTRIDE = 4 * 4 * GS + 6 * 96 * 32, IMOFF = 3 * LSTRIDE, TOTAL = 190 * 1024;
 
 // one fill at ring phase S: rows at slots S, S+1, S+2 (mod 4); SPLITMODE 0 ring-4 split, 1 always
 // N = 32 x 3 (three MMAs), 2 never split (D window at S even past slot 3: TMEM 0..191)
@@ -120,6 +120,28 @@ __global__ void __launch_bounds__(128, 1) kern(int iters, long long *cyc) {
         if constexpr (PAT == 4) { F(3, 0, 0); F(3, 0, 1); F(3, 0, 2); F(3, 0, 3); }        // phase 3 (32 | 64)
         if constexpr (PAT == 5) { F(0, 1, 0); F(1, 1, 1); F(2, 1, 2); F(3, 1, 3); }        // three N = 32 per position
         if constexpr (PAT == 6) { F(0, 2, 0); F(1, 2, 1); F(2, 2, 2); F(3, 2, 3); }        // never split (D up to 191)
+        if constexpr (PAT == 9) {   // chunk 1 with cnn_kernels.cu make_layout(32, 4, 1, 0, 1) offsets
+          // rings: im2col 4 x 4,096 at 0; layers 1-3: 4 x 8,320 at 16,384 / 49,664 / 82,944;
+          // weights: im2col 1,024 at 116,224; layers 1-3 18,432 at 117,248 / 135,680 / 154,112
+#define G(S, R)                                                                                              \
+  mma(tb + (R) * P, make_desc(sb + (R) * 4096, 2048, 128), make_desc(sb + 116224, P * 16, 128), make_idesc(32)); \
+  fill<S, 0>(tb + 128, sb + 16384 + (R) * 4 * GS, sb + 117248);                                               \
+  fill<S, 0>(tb + 256, sb + 49664 + (R) * 4 * GS, sb + 135680);                                               \
+  fill<S, 0>(tb + 384, sb + 82944 + (R) * 4 * GS, sb + 154112);
+          G(0, 0) G(1, 1) G(2, 2) G(3, 3)
+#undef G
+        }
+        if constexpr (PAT == 10) {  // chunk 2 with make_layout(32, 4, 0, 1, 1): rings 4 x 8,320 at 0 / 33,280 /
+          // 66,560 / 99,840; weights 18,432 at 133,120 / 151,552 / 169,984, folded 1,024 at 188,416
+#define G(S, R)                                                                                              \
+  fill<S, 0>(tb + 0, sb + 0 + (R) * 4 * GS, sb + 133120);                                                     \
+  fill<S, 0>(tb + 128, sb + 33280 + (R) * 4 * GS, sb + 151552);                                               \
+  fill<S, 0>(tb + 256, sb + 66560 + (R) * 4 * GS, sb + 169984);                                               \
+  mma(tb + 384 + ((R) & 1) * 16, make_desc(sb + 99840 + (R) * 4 * GS + 16, GS, 128), make_desc(sb + 188416, 256, 128), make_idesc(16)); \
+  mma(tb + 384 + ((R) & 1) * 16, make_desc(sb + 99840 + (R) * 4 * GS + 16 + 2 * GS, GS, 128), make_desc(sb + 188416 + 512, 256, 128), make_idesc(16));
+          G(0, 0) G(1, 1) G(2, 2) G(3, 3)
+#undef G
+        }
         if constexpr (PAT == 7) {   // chunk stream from one warp: per row step im2col + 3 layers
 #define G(S, R)                                                                                              \
   mma(tb + (R) * P, make_desc(sb + IMOFF + (R) * 4096, 2048, 128), make_desc(sb + IMOFF + 4 * 4096, P * 16, 128), \
@@ -175,5 +197,7 @@ int main() {
   run<6>("never split (D window from slot S, up to col 191)");
   run<7>("chunk stream, 1 warp (per ROW STEP = 4 fills... /4)");
   run<8>("chunk stream, 4 warps (1 per layer)");
+  run<9>("chunk 1 stream, kernel smem layout, 1 warp");
+  run<10>("chunk 2 stream, kernel smem layout, 1 warp");
   return 0;
 }
