@@ -1298,7 +1298,7 @@ cudaError_t launch_pn(const CnnChunkParams &p0, int num_sms, cudaStream_t s) {
     const double cost_c = (double)T + 3.0 * NL * (double)((T + p.oh - 1) / p.oh + 1);
     const int nrb = (p.oh + R - 1) / R;
     const double cost_b = (double)((strips * nrb + num_sms - 1) / num_sms) * (R + 3.0 * NL);
-    if (cost_c < cost_b) {
+    if (cost_c < cost_b || p.contig == 2) {   // 2: forced (tests)
       p.rows_per_cta = (int)T;
       grid = (int)((total + T - 1) / T);
     }

@@ -133,7 +133,7 @@ struct CnnChunkParams {
   int rows_per_unit;     // output rows per work unit
   int units;             // strips * row blocks
   int rows_per_cta;      // > 0: CTA b owns strip-major output rows [b T, (b+1) T) instead (set by the launcher)
-  int contig;            // allow the contiguous decomposition when the launcher's cost model prefers it
+  int contig;            // 1: contiguous decomposition when the launcher's cost model prefers it; 2: always
   int *err;              // device error flag (watchdog)
   unsigned long long *trace;   // optional pipeline trace (CTA 0, first unit): [0] = count, then records
   int mode;              // 0 DnCNN; DDFB (R39-R42): 1 u0 = W_K v, 2 p = proj(v - W^* u), 3 u = HT(u + gamma W p),

@@ -1043,7 +1043,7 @@ pnpula_status pnpula_create(const pnpula_config *cfg, pnpula_ctx **out) {
     const char *pe2 = getenv("PNPULA_PDL");
     c->pdl = (pe2 && atoi(pe2) == 0) ? 0 : 1;
     const char *pe3 = getenv("PNPULA_CNN_CONTIG");
-    c->cnn_contig = (pe3 && atoi(pe3) == 0) ? 0 : 1;
+    c->cnn_contig = (pe3 && atoi(pe3) == 0) ? 0 : (pe3 && atoi(pe3) == 2) ? 2 : 1;   // 2: always (tests)
   }
   {
     const char *ge = getenv("PNPULA_GRAPHS");
