@@ -78,7 +78,12 @@ __global__ void __launch_bounds__(128, 1) kern(int iters, long long *cyc) {
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tb = tslot, sb = smem_u32(smem);
-  if constexpr (PAT == 8) {
+  if constexpr (PAT == 8 || PAT == 11 || PAT == 12 || PAT == 13) {
+    __shared__ __align__(8) uint64_t junk2[4][2];
+    if (threadIdx.x == 0)
+      for (int w = 0; w < 4; ++w)
+        for (int j = 0; j < 2; ++j) asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&junk2[w][j])), "r"(1 << 20));
+    __syncthreads();
     const long long t0 = clock64();
     for (int it = 0; it < iters; ++it) {
       if (elect_one()) {
@@ -88,8 +93,14 @@ __global__ void __launch_bounds__(128, 1) kern(int iters, long long *cyc) {
             mma(tb + R * P, make_desc(sb + IMOFF + R * 4096, 2048, 128), make_desc(sb + IMOFF + 4 * 4096, P * 16, 128), make_idesc(32));
         } else {
           const uint32_t L0 = sb + (uint32_t)warp * LSTRIDE, acc = tb + 128u * (uint32_t)(warp + 1);
-          fill<0, 0>(acc, L0 + 0 * 4 * GS, L0 + 4 * 4 * GS); fill<1, 0>(acc, L0 + 1 * 4 * GS, L0 + 4 * 4 * GS);
-          fill<2, 0>(acc, L0 + 2 * 4 * GS, L0 + 4 * 4 * GS); fill<3, 0>(acc, L0 + 3 * 4 * GS, L0 + 4 * 4 * GS);
+#define FF(S) \
+          if (PAT == 11 || PAT == 13) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); \
+          fill<S, 0>(acc, L0 + S * 4 * GS, L0 + 4 * 4 * GS); \
+          if (PAT == 11 || PAT == 12) { \
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&junk2[warp][0]))); \
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&junk2[warp][1]))); }
+          FF(0) FF(1) FF(2) FF(3)
+#undef FF
         }
       }
       __syncwarp();
@@ -199,5 +210,8 @@ int main() {
   run<8>("chunk stream, 4 warps (1 per layer)");
   run<9>("chunk 1 stream, kernel smem layout, 1 warp");
   run<10>("chunk 2 stream, kernel smem layout, 1 warp");
+  run<11>("4 warps + tcgen05.fence::after_thread_sync + 2 commits per fill");
+  run<12>("4 warps + 2 commits per fill");
+  run<13>("4 warps + tcgen05.fence::after_thread_sync per fill");
   return 0;
 }

@@ -1,0 +1,11 @@
+# one commit per fill also for the folded last layer; tests + c5 / c3 / c2 against the two-commit build
+L=paper_2511_00870_b200
+timeout 1500 python -m pytest tests/test_gpu_parity.py tests/test_gpu_tiling_fuzz.py tests/test_gpu_c3_chain.py tests/test_gpu_ddfb.py tests/test_gpu_cnn_decomposition.py tests/test_gpu_fused_update.py tests/test_gpu_rgb.py tests/test_gpu_fullsize.py -q -x > gpurun_out/oc_tests.log 2>&1; echo "tests rc=$?"; tail -1 gpurun_out/oc_tests.log
+for rep in a b; do for v in "one:PNPULA_X=0" "two:PNPULA_LIB=$L/libpnpula_2c.so"; do
+  n=${v%%:*}; e=${v#*:}
+  for w in c5 c3 c2; do
+  st=30; [ $w = c2 ] && st=50
+  env $e timeout 300 python bench.py --workload $w --steps $st --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/oc_${w}_$n.json 2>/dev/null
+  python -c "import json;d=json.loads(open('gpurun_out/oc_${w}_$n.json').read().strip().splitlines()[-1]);print('$w $n $rep',round(d['value']),'cnn',round(d['kernel_ms_per_step']['cnn'],4))"
+  done
+done; done

@@ -190,6 +190,9 @@ __device__ __forceinline__ bool mbar_test_sleep(uint32_t bar, uint32_t parity) {
 }
 // Bounded wait: gives up (sets the CTA abort flag and the device error flag) after
 // ~4e9 cycles so a pipeline bug cannot hang the GPU.
+#ifndef PNPULA_ONE_COMMIT
+#define PNPULA_ONE_COMMIT 1   // one tcgen05.commit per fill (see epi_step)
+#endif
 #ifndef PNPULA_POLL_BATCH
 #define PNPULA_POLL_BATCH 32   // tries between two watchdog checks (profiles/r02_cnn_schemes.md)
 #endif
@@ -924,10 +927,12 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
           if (elect_one()) {
             mma_commit(bar_empty(l, rs));                // input row consumed
             if (netlast) {
-              mma_commit(bar_tfull(l, Fg & 1));          // this fill's tap sums
+              if (!PNPULA_ONE_COMMIT) mma_commit(bar_tfull(l, Fg & 1));   // this fill's tap sums
             } else {
               const int ic = im2col ? f : f - 2;         // output row completed by this group
-              if (ic >= 0 && ic < no) mma_commit(bar_tfull(l, (O0 + (uint32_t)ic) & 3));
+              // (PNPULA_ONE_COMMIT: the epilogue waits on the input ring's empty barrier of this fill
+              // instead -- the same completion, one commit fewer per fill)
+              if (!PNPULA_ONE_COMMIT && ic >= 0 && ic < no) mma_commit(bar_tfull(l, (O0 + (uint32_t)ic) & 3));
             }
           }
           __syncwarp();
@@ -972,7 +977,13 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
           const int s = f + kLag * l;
           const uint32_t Fg = Fcnt(l) + (uint32_t)f;
           float fu_g = 0.f;   // fused update: this lane's G value of the completed row
-          if (!mbar_wait(bar_tfull(l, Fg & 1), (Fg >> 1) & 1, abort_flag, p.err, 4)) return false;
+          if (PNPULA_ONE_COMMIT) {
+            // this fill's tap sums are complete with its MMAs: its input-ring empty barrier (the slot is
+            // re-used by fill Fg + ring size, whose MMAs need fill Fg + 2's accumulators read first)
+            const uint32_t rsc = l == 0 ? Fg % (uint32_t)kRing : Fg % (uint32_t)kRingAct;
+            const uint32_t phc = l == 0 ? (Fg / (uint32_t)kRing) & 1u : (Fg / (uint32_t)kRingAct) & 1u;
+            if (!mbar_wait(bar_empty(l, rsc), phc, abort_flag, p.err, 4)) return false;
+          } else if (!mbar_wait(bar_tfull(l, Fg & 1), (Fg >> 1) & 1, abort_flag, p.err, 4)) return false;
           trace_ev(p.trace, trw, 6, s, l);
           tc_fence_after();
           float d[NC][16];
@@ -1081,7 +1092,16 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
           const bool im2col = is_im2col(l);
           const int s = (im2col ? ic : ic + 2) + kLag * l;
           const uint32_t Ig = Ocnt(l) + (uint32_t)ic;
-          if (!mbar_wait(bar_tfull(l, Ig & 3), (Ig >> 2) & 1, abort_flag, p.err, 4)) return false;
+          if (PNPULA_ONE_COMMIT) {
+            // row ic is complete when the MMAs of the fill that finishes it (im2col: fill ic; windowed:
+            // fill ic + 2) have completed -- the commit to that fill's input-ring empty barrier.  The
+            // slot is re-used (and its barrier completes again) only by fill + ring size, whose MMAs
+            // need this row's accumulator slot drained first: the parity cannot alias.
+            const uint32_t Fgc = Fcnt(l) + (uint32_t)(im2col ? ic : ic + 2);
+            const uint32_t rsc = l == 0 ? Fgc % (uint32_t)kRing : Fgc % (uint32_t)kRingAct;
+            const uint32_t phc = l == 0 ? (Fgc / (uint32_t)kRing) & 1u : (Fgc / (uint32_t)kRingAct) & 1u;
+            if (!mbar_wait(bar_empty(l, rsc), phc, abort_flag, p.err, 4)) return false;
+          } else if (!mbar_wait(bar_tfull(l, Ig & 3), (Ig >> 2) & 1, abort_flag, p.err, 4)) return false;
           trace_ev(p.trace, trw, 6, s, l);
           tc_fence_after();
           const uint32_t taddr = tmem_base + lane_base + (uint32_t)(l * kAcc * P);
