@@ -499,7 +499,9 @@ __global__ void __launch_bounds__(block_threads(NL), 1) cnn_chunk_kernel(const _
   // CTAs take units round-robin.  Contiguous (rows_per_cta = T > 0): CTA b owns the strip-major
   // output rows [b T, (b+1) T) of the strips x oh grid, one unit per strip it touches -- every unit
   // pays the pipeline's fill once, so a CTA pays it once or twice instead of once per row block.
-  const int Tc = p.rows_per_cta;
+  // (2-layer chains -- DDFB operator pairs -- always use row blocks: their kernel keeps the plain
+  // round-robin loop, whose code generation the ranges' bookkeeping measurably perturbed)
+  const int Tc = NL <= 2 ? 0 : p.rows_per_cta;
   int64_t cpos = (int64_t)blockIdx.x * Tc;
   const int64_t cend = Tc > 0 ? min((int64_t)(blockIdx.x + 1) * Tc, (int64_t)strips * p.oh) : 0;
   bool first_unit = true;
@@ -1309,7 +1311,7 @@ cudaError_t launch_pn(const CnnChunkParams &p0, int num_sms, cudaStream_t s) {
   p.units = strips * ((p.oh + R - 1) / R);
   p.rows_per_cta = 0;
   int grid = p.units < num_sms ? p.units : num_sms;
-  if (p.contig) {
+  if (p.contig && NL > 2) {
     // contiguous strip-major ranges of T rows per CTA: a CTA touches <= ceil(T / oh) + 1 strips, each
     // a unit with one pipeline fill; use them when that model beats the row blocks' waves x (R + fill)
     const int64_t total = (int64_t)strips * p.oh;
